@@ -1,0 +1,25 @@
+import os
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a CUDA device (B200, sm_100a)")
+    config.addinivalue_line("markers", "slow: takes more than ~30 s")
+
+
+@pytest.fixture(scope="session")
+def tiny_scene():
+    import scenes
+    return scenes.make_scene("tiny")
+
+
+@pytest.fixture(scope="session")
+def tiny_data(tiny_scene):
+    import scenes
+    return scenes.synthesize_cpu(tiny_scene)
