@@ -1,0 +1,316 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 reconstruction path (BASELINE.json metric:
+"ms per 3-D image; Gsamples/s; achieved HBM GB/s vs B200 peak").
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config large]
+    python bench.py --impl reference ...      # the fp64 CPU oracle arm
+
+A step is one sar_reconstruct call over the whole workload (all 5 kernels:
+correction+x-FFT, y-FFT, filter+Stolt+z-IFFT, y-IFFT, x-IFFT+magnitude) with
+the input already resident in HBM.  The default workload is Large
+(BASELINE.json configs[3], the config the north-star roofline target is
+quoted on; 12 GiB of raw samples, larger than the 126 MB L2, so no flush is
+needed between steps).  Under torchrun every rank reconstructs its own replica
+(the path is one GPU per image: "replicas only") and rank 0
+prints one JSON line with the max-over-ranks device time.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+import dataclasses  # noqa: E402
+
+import numpy as np  # noqa: E402
+
+METRIC = "Gsamples/s (raw complex64 samples reconstructed into 3-D images per second)"
+UNIT = "Gsamples/s"
+FALLBACK_HBM_GBS = 6650.0
+
+
+def _peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+def stage_alg_bytes(sc):
+    """Algorithmic bytes per launch of each kernel: the
+    compulsory read of its input and write of its output, 8 B per complex64
+    element, 4 B per float32 voxel."""
+    F, ny, nx, nk, nz = sc.n_frames, sc.ny, sc.nx, sc.n_k, sc.nz
+    planar = 8 * F * ny * nx * nk
+    vol = 8 * F * ny * nx * nz
+    img = 4 * F * nz * ny * nx
+    return [sc.raw_bytes() + planar, 2 * planar, planar + vol, 2 * vol, vol + img]
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled every 100 ms during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100", "-f", self.path],
+                                         stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.path or not os.path.exists(self.path):
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = float(f[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[4:8]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        os.unlink(self.path)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def _dist():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def oracle_sample(sc, s_host, max_pairs=1):
+    """Time the fp64 oracle (as it stands) on a bounded sample of the workload:
+    the first Tx/Rx channel(s) through the whole O1..O7 pipeline (the full-size
+    3-D RMA included).  Returns (seconds, samples processed, cores)."""
+    import oracle
+    sub = s_host[:, :1, :max_pairs]
+    geo = oracle.decompose(sc.tx[:1], sc.rx[:max_pairs], sc.scan, sc.npx, sc.npy, sc.x0, sc.y0, sc.dx, sc.dy,
+                           sc.z0, sc.k, sc.nx, sc.ny, sc.nz, sc.dz_img, sc.z_ref)
+    t0 = time.perf_counter()
+    oracle.reconstruct(sub, geo)
+    dt = time.perf_counter() - t0
+    return dt, int(np.prod(sub.shape)), os.cpu_count()
+
+
+def run_reference(args):
+    """--impl reference: the oracle arm (fp64 CPU), rank 0 only."""
+    rank, world, _ = _dist()
+    if rank != 0:
+        return
+    import scenes
+    sc = scenes.make_scene(args.config)
+    # a one-channel sample needs only that channel's echo: synthesise it on the
+    # CPU when feasible, else on the GPU
+    sub = dataclasses.replace(sc, tx=sc.tx[:1], rx=sc.rx[:1])
+    if sub.n_samples * max(len(q) for q in sub.scat_pos) <= 5e8:
+        s = scenes.synthesize_cpu(sub)
+    else:
+        import scenes.gpu
+        scenes.gpu.build()
+        s = scenes.gpu.synthesize_gpu(sub).cpu().numpy()
+    for _ in range(args.warmup):
+        oracle_sample(sub, s)
+    times = []
+    n = 0
+    for _ in range(args.steps):
+        dt, n, cores = oracle_sample(sub, s)
+        times.append(dt)
+    t = float(np.sum(times))
+    val = n * args.steps / t / 1e9
+    sample = (f"{args.config}: Tx/Rx channel (0,0) only ({n} of {sc.n_samples} samples) through the full "
+              f"oracle O1..O7 incl. the {sc.nx}x{sc.ny}x{sc.nz} RMA, per step")
+    line = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": args.config, "sample": sample},
+            "cpu_baseline": {"value": val, "unit": UNIT, "cores": os.cpu_count(), "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args):
+    import torch
+    import scenes
+    import scenes.gpu
+    import paper_2305_02064_b200 as sar
+    from paper_2305_02064_b200 import build as sbuild
+
+    rank, world, local = _dist()
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if rank == 0:
+        sbuild.build()
+        scenes.gpu.build()
+    if world > 1:
+        dist.barrier()
+
+    sc = scenes.make_scene(args.config)
+    data = scenes.gpu.synthesize_gpu(sc, device=local)
+    plan = sar.Plan.from_scene(sc, flags=sar.SAR_PROFILE_STAGES, device=local)
+    out = torch.empty(sc.image_shape, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    for _ in range(args.warmup):
+        plan.reconstruct(data, out, stream)
+    torch.cuda.synchronize(dev)
+    plan.profile_reset()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+        ev0.record(stream)
+        for _ in range(args.steps):
+            plan.reconstruct(data, out, stream)
+        ev1.record(stream)
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+    ms_total = ev0.elapsed_time(ev1)
+    stage_ms, ncalls = plan.profile_read()
+    if world > 1:
+        t = torch.tensor([ms_total], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_total = float(t.item())
+    ms_step = ms_total / args.steps
+    samples = sc.n_samples
+    value = samples * world / (ms_step * 1e-3) / 1e9
+
+    # roofline of the dominant kernel (largest share of the step)
+    peak, peak_src = _peaks()
+    avg = [m / max(ncalls, 1) for m in stage_ms]
+    share = [a / max(sum(avg), 1e-12) for a in avg]
+    dom = int(np.argmax(avg))
+    alg = stage_alg_bytes(sc)
+    ach = alg[dom] / (avg[dom] * 1e-3) / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", f"{args.config}_traffic.json")
+    if os.path.exists(tp):
+        traffic = json.load(open(tp)).get(str(dom))
+    path_gbs = sc.alg_bytes() / (ms_step * 1e-3) / 1e9
+
+    # end-to-end through the public API with host buffers (pinned)
+    e2e = None
+    if not args.no_e2e:
+        h_in = torch.empty(sc.data_shape, dtype=torch.complex64, pin_memory=True)
+        h_in.copy_(data)
+        h_out = torch.empty(sc.image_shape, dtype=torch.float32, pin_memory=True)
+        plan2 = sar.Plan.from_scene(sc, device=local)
+        plan2.reconstruct_host(h_in, h_out, stream)  # warm-up (allocates staging)
+        ke = max(1, min(args.steps, args.e2e_steps))
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(ke):
+            plan2.reconstruct_host(h_in, h_out, stream)
+        dt = (time.perf_counter() - t0) / ke
+        if world > 1:
+            t = torch.tensor([dt], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            dt = float(t.item())
+        e2e = {"value": samples * world / dt / 1e9, "unit": UNIT, "ms_per_step": dt * 1e3,
+               "h2d_bytes_per_step": sc.raw_bytes(), "d2h_bytes_per_step": sc.image_bytes(), "steps": ke}
+        plan2.close()
+        del h_in, h_out
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        s_host = data[:, :1, :1].cpu().numpy()
+        sub = dataclasses.replace(sc, tx=sc.tx[:1], rx=sc.rx[:1])
+        dt, n, cores = oracle_sample(sub, s_host)
+        cpu = {"value": n / dt / 1e9, "unit": UNIT, "cores": cores, "kind": "oracle",
+               "sample": f"Tx/Rx channel (0,0) of {args.config} ({n} of {samples} samples) through the full "
+                         f"fp64 oracle O1..O7 incl. the {sc.nx}x{sc.ny}x{sc.nz} RMA: {dt:.1f} s"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded scenes, GPU-synthesised Eq. (9) echo)",
+            "config": {"workload": args.config, "frames": sc.n_frames, "tx": sc.n_tx, "rx": sc.n_rx,
+                       "poses": sc.n_pos, "n_k": sc.n_k, "image": [sc.nx, sc.ny, sc.nz],
+                       "samples_per_step": samples * world, "raw_GiB_per_gpu": sc.raw_bytes() / 2**30,
+                       "l2": "inputs larger than L2 (no flush)" if sc.raw_bytes() > 126e6 else "L2 not flushed",
+                       "parallelism": f"replicas x{world}"},
+            "ms_per_image": ms_step / sc.n_frames,
+            "path": {"alg_bytes": sc.alg_bytes(), "achieved_GBps": path_gbs, "peak_GBps": peak,
+                     "frac": path_gbs / peak},
+            "roofline": {"bound": "hbm", "kernel": sar.STAGE_NAMES[dom], "achieved": ach, "peak": peak,
+                         "unit": "GB/s", "frac": ach / peak, "traffic": traffic, "alg_bytes": alg[dom],
+                         "ms": avg[dom], "peak_source": peak_src},
+            "stages": {n: {"ms": a, "share": s_, "alg_GBps": b / (a * 1e-3) / 1e9}
+                       for n, a, s_, b in zip(sar.STAGE_NAMES, avg, share, alg)},
+            "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": plan.launches_per_call() * args.steps,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    plan.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="large", choices=["tiny", "small", "freehand", "large", "realtime"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        print("warning: --warmup < 3 is below the timing rules", file=sys.stderr)
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

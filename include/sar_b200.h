@@ -1,0 +1,189 @@
+/*
+ * sar_b200.h -- C ABI of the B200-native reconstruction path of
+ * arXiv 2305.02064 ("efficient near-field MIMO-SAR imaging for irregular
+ * scanning geometries").  Citation keys: P:n = PAPER.md line n.
+ *
+ * The library reconstructs a 3-D reflectivity image o(x,y,z) from multistatic,
+ * multi-planar frequency-domain samples s[f][tx][rx][pos][k] in four steps
+ * (Fig. 3):
+ *   1. multistatic->monostatic / multi-planar->planar phase correction
+ *      s_hat = s * exp(+j k beta) (Eqs. (11)-(12)) accumulated on
+ *      the virtual planar lambda/4 lattice (Eqs. (3)-(4));
+ *   2. forward 2-D spatial FFT (FT_2D of Eq. (14));
+ *   3. RMA filter k_z/P(f) e^{-j k_z Z0} and Stolt resampling onto a uniform
+ *      k_z grid (Eqs. (13)-(14));
+ *   4. inverse 3-D FFT and magnitude (IFT_3D of Eq. (14)).
+ * Readings where the paper is silent are DESIGN.md section 3 (R1..R17).
+ *
+ * Conventions (all entry points):
+ *  - Every function returns an int status (enum sar_status); nothing throws
+ *    across the ABI.  On failure sar_last_error() returns a thread-local
+ *    human-readable message.
+ *  - "device pointer" = CUDA global memory on the plan's device; "host
+ *    pointer" = ordinary (preferably pinned) host memory.
+ *  - Array layouts are C order (last index fastest); complex64 is interleaved
+ *    (re, im) float32.
+ *  - Asynchronous CUDA faults surface as SAR_ERR_CUDA on a later call.
+ */
+#ifndef SAR_B200_H
+#define SAR_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SAR_B200_VERSION 1
+
+typedef struct sar_plan sar_plan;       /* opaque */
+typedef struct CUstream_st *sar_stream; /* == cudaStream_t; NULL = legacy default stream */
+
+enum sar_status {
+  SAR_OK = 0,
+  SAR_ERR_INVALID_ARG = 1, /* null pointer, bad size, not a power of two, ... */
+  SAR_ERR_GEOMETRY = 2,    /* non-uniform k, off-lattice Tx/Rx midpoint, R_ref <= 0, Tx/Rx planes differ */
+  SAR_ERR_UNSUPPORTED = 3, /* device is not sm_100 (B200), size above the compiled limits */
+  SAR_ERR_OOM = 4,         /* device allocation failed */
+  SAR_ERR_CUDA = 5         /* a CUDA runtime error (launch, copy, asynchronous fault) */
+};
+
+enum sar_flags {
+  SAR_NO_COMPENSATION = 1u << 0, /* beta == 0: plain RMA on the raw samples (the paper's
+                                    failure baseline) */
+  SAR_OUTPUT_COMPLEX = 1u << 1,  /* image is complex64 o (scaled, rolled) instead of |o| */
+  SAR_PROFILE_STAGES = 1u << 2   /* record CUDA events around every kernel (sar_plan_profile_read) */
+};
+
+/* Limits of this build. */
+#define SAR_MAX_FFT 1024  /* nx, ny, nz <= 1024 (powers of two >= 2) */
+#define SAR_MAX_PAIRS 64  /* n_tx * n_rx <= 64 */
+
+/* Acquisition geometry (host memory; copied by sar_plan_create, so the caller
+ * may free every array as soon as the call returns). */
+typedef struct {
+  int32_t n_frames;        /* F >= 0 independent frames (F = 0: every call is a no-op) */
+  int32_t n_tx, n_rx;      /* >= 1 each, n_tx*n_rx <= SAR_MAX_PAIRS */
+  const double *tx_xyz;    /* [n_tx][3] Tx positions in the radar body frame (m) */
+  const double *rx_xyz;    /* [n_rx][3] Rx positions in the radar body frame (m); tx.z == rx.z */
+  int32_t npx, npy;        /* nominal raster: pose p = iy*npx + ix, 1 <= npx <= nx, 1 <= npy <= ny */
+  double x0, y0;           /* nominal world position of pose (0,0) (m); only the output axes use it */
+  double dx, dy;           /* raster = virtual-lattice pitch (m), lambda/4 in the paper */
+  const double *scan_xyz;  /* [F][npy*npx][3] actual radar positions, world frame (m); the z
+                              coordinate gives the plane displacement d_z (Eq. (4)); x,y are
+                              not used in RASTER placement (reading R7) */
+  const double *z0;        /* [F] reference plane Z_0 per frame (m), or NULL = mean of scan z */
+  int32_t n_k;             /* >= 2 frequency samples */
+  const double *k;         /* [n_k] wavenumbers 2*pi*f/c (rad/m), uniform (1e-9 rel.), ascending */
+  const double *pulse;     /* [n_k][2] complex P(f) (re,im) or NULL for P == 1 (Eq. (14)) */
+  int32_t device;          /* CUDA device ordinal */
+} sar_geom_desc;
+
+/* Image grid. */
+typedef struct {
+  int32_t nx, ny;  /* spatial FFT size = image x/y size; powers of two in [2, SAR_MAX_FFT] */
+  int32_t nz;      /* Stolt bins = image z size; power of two in [2, SAR_MAX_FFT] */
+  double dz;       /* image z pitch (m); k_z grid spacing 2*pi/(nz*dz) (reading R5) */
+  double z_ref;    /* reference depth (m): centre of the z window and R_ref = z_ref - Z_0 > 0 */
+} sar_image_desc;
+
+/* Host-side result of the geometry decomposition (no device needed). */
+typedef struct {
+  int32_t n_pairs;           /* n_tx * n_rx */
+  int32_t jx_min, jy_min;    /* minima of rint(midpoint/pitch) over the pairs (subtracted) */
+  int32_t nvx, nvy;          /* virtual aperture extent in nodes: npx + max jx, npy + max jy */
+  int32_t roll_x, roll_y;    /* output rolls floor(nv/2) - n/2 (reading R8) */
+  double axes[6];            /* as sar_plan_get_axes */
+  double k0, dk;             /* k[0] and (k[n_k-1]-k[0])/(n_k-1) */
+  size_t workspace_bytes;    /* device workspace a plan would allocate */
+} sar_plan_info;
+
+/* Validate and decompose a geometry on the host only (no CUDA device is
+ * touched): the same checks and fp64 tables sar_plan_create computes.  Any
+ * of the optional outputs may be NULL; sizes: jx, jy [n_tx*n_rx] (offsets
+ * after min-subtraction, row-major [n_tx][n_rx]); kx [nx], ky [ny], kz [nz]
+ * (rad/m, the tables the Stolt step uses); apose [F*P] (-2 d_z, float32) and
+ * bpair [F*n_tx*n_rx] ((d_x^2+d_y^2)/(4 R_ref), float32), both zero with
+ * SAR_NO_COMPENSATION.  Errors: INVALID_ARG, GEOMETRY, UNSUPPORTED. */
+int sar_plan_describe(const sar_geom_desc *g, const sar_image_desc *im, uint32_t flags,
+                      sar_plan_info *info, int32_t *jx, int32_t *jy, double *kx, double *ky,
+                      double *kz, float *apose, float *bpair);
+
+/* Create a plan: validates the geometry, runs the fp64 decomposition of
+ * Eqs. (3),(4),(7),(12) on the host (virtual-node offsets j_tr, beta terms,
+ * k_x/k_y/k_z tables), allocates the device workspace
+ * (F*ny*nx*(n_k+nz)*8 bytes) and uploads the tables.  *out receives the plan
+ * (NULL on failure).  Errors: INVALID_ARG, GEOMETRY, UNSUPPORTED, OOM, CUDA. */
+int sar_plan_create(sar_plan **out, const sar_geom_desc *g, const sar_image_desc *im,
+                    uint32_t flags);
+
+/* Reconstruct.  d_data: device, complex64 [F][n_tx][n_rx][npy*npx][n_k],
+ * 8-byte aligned, read only, caller-owned.  d_image: device, float32
+ * [F][nz][ny][nx] (complex64 with SAR_OUTPUT_COMPLEX), caller-owned, fully
+ * overwritten.  Voxel (m,iy,ix) is at world (x_first+ix*dx, y_first+iy*dy,
+ * z_first+m*dz), see sar_plan_get_axes.  Enqueues 5 kernels on `stream` and
+ * returns without synchronising; no allocation.  Not re-entrant per plan (the
+ * workspace is shared): use one plan per concurrent stream.
+ * Errors: INVALID_ARG (null pointers), CUDA. */
+int sar_reconstruct(sar_plan *p, const void *d_data, void *d_image, sar_stream stream);
+
+/* End-to-end variant with HOST buffers: copies h_data (same layout as d_data)
+ * host->device, reconstructs, copies the image device->host and synchronises
+ * `stream` before returning.  Device staging buffers are allocated on first
+ * use and owned by the plan.  Pinned host memory gives full PCIe bandwidth.
+ * Errors: INVALID_ARG, OOM, CUDA. */
+int sar_reconstruct_host(sar_plan *p, const void *h_data, void *h_image, sar_stream stream);
+
+/* Synchronise the plan's last stream and free everything.  NULL is a no-op. */
+int sar_plan_destroy(sar_plan *p);
+
+/* out[6] = {x_first, y_first, z_first, dx, dy, dz} of the output voxel grid
+ * (each axis periodic with period n*pitch; reading R8). */
+int sar_plan_get_axes(const sar_plan *p, double out[6]);
+
+/* Bytes of device workspace owned by the plan (excluding staging buffers). */
+int sar_plan_workspace_bytes(const sar_plan *p, size_t *bytes);
+
+/* Stage profiling (plan created with SAR_PROFILE_STAGES): sum of the CUDA-event
+ * durations (ms) of each of the 5 kernels over all calls since the last reset.
+ * Synchronises the recorded events.  ms_out[5] = {K1 correct+x-FFT, K2 y-FFT,
+ * K3 filter+Stolt+z-IFFT, K4a y-IFFT, K4b x-IFFT+magnitude}; *n_calls
+ * receives the number of calls summed (at most 1024 since the last reset). */
+int sar_plan_profile_read(sar_plan *p, float ms_out[5], int32_t *n_calls);
+int sar_plan_profile_reset(sar_plan *p);
+
+/* Number of kernel launches one sar_reconstruct call enqueues (5; 0 if F = 0). */
+int sar_plan_launches_per_call(const sar_plan *p, int32_t *n);
+
+/* ---- debug / parity entry points (same kernels as sar_reconstruct) ---- */
+
+/* Run the path up to `stage` and copy that stage's result to d_out (device):
+ *   1: planar lattice after correction, complex64 [F][ny][nx][n_k]
+ *   2: spatial spectrum after the 2-D FFT, complex64 [F][ny][nx][n_k]
+ *   3: Stolt output before the z-IFFT, complex64 [F][ny][nx][nz]
+ *   4: rolled complex image, complex64 [F][nz][ny][nx] (scaled 1/(nx ny nz))
+ * Errors: INVALID_ARG (stage outside 1..4, null pointers), CUDA. */
+int sar_debug_stage(sar_plan *p, int32_t stage, const void *d_data, void *d_out,
+                    sar_stream stream);
+
+/* Host copies of the integer virtual-node offsets of every (tx,rx) pair after
+ * min-subtraction (row-major [n_tx][n_rx]) and the minima subtracted. */
+int sar_debug_node_offsets(const sar_plan *p, int32_t *jx, int32_t *jy, int32_t *jx_min,
+                           int32_t *jy_min);
+
+/* Stolt pull indices computed by the device code of step 3 for n columns
+ * (d_cols: device int32 [n][2] = (a, b) spectral indices):
+ * d_i0[n][nz] = floor index or -1 (zero bin), d_tau[n][nz] = weight (float32).
+ * Errors: INVALID_ARG, CUDA. */
+int sar_debug_stolt_index(sar_plan *p, const int32_t *d_cols, int32_t n, int32_t *d_i0,
+                          float *d_tau, sar_stream stream);
+
+const char *sar_status_string(int status);
+const char *sar_last_error(void);
+int sar_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SAR_B200_H */

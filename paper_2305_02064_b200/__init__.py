@@ -1,0 +1,12 @@
+"""B200-native (sm_100a) reconstruction path of arXiv 2305.02064.
+
+Public API: :class:`Plan` (``sar_plan_create`` / ``sar_reconstruct`` /
+``sar_plan_destroy`` of ``include/sar_b200.h``).  All compute runs in the
+in-tree CUDA library ``libsar_b200.so``; PyTorch provides device memory and
+streams only.  There is no CPU fallback.
+"""
+from .sar import (Plan, SarError, describe, describe_scene, load_library, LIB_PATH, SAR_NO_COMPENSATION,  # noqa: F401
+                  SAR_OUTPUT_COMPLEX, SAR_PROFILE_STAGES, STAGE_NAMES)
+
+__all__ = ["Plan", "SarError", "describe", "describe_scene", "load_library", "LIB_PATH", "SAR_NO_COMPENSATION",
+           "SAR_OUTPUT_COMPLEX", "SAR_PROFILE_STAGES", "STAGE_NAMES"]

@@ -1,0 +1,512 @@
+// plan.cpp -- host side of the C ABI (include/sar_b200.h): argument
+// validation, the fp64 geometry decomposition of Eqs. (3), (4), (7), (12)
+// (P:123-153), table upload, workspace ownership, stage profiling.
+// Compiled with -ffp-contract=off so that every table entry is the same IEEE
+// expression the oracle evaluates (k_x, k_y, k_z, dk feed the bit-exact Stolt
+// index decisions, reading R9).
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+#include <string.h>
+
+#include <algorithm>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "plan_internal.h"
+
+namespace {
+thread_local std::string g_last_error;
+
+bool pow2_in_range(int n) { return n >= 2 && n <= SAR_MAX_FFT && (n & (n - 1)) == 0; }
+
+int fail(int status, const std::string &msg) {
+  g_last_error = msg;
+  return status;
+}
+
+int cuda_fail(cudaError_t e, const char *what) {
+  g_last_error = std::string("CUDA: ") + cudaGetErrorString(e) + " (" + what + ")";
+  return SAR_ERR_CUDA;
+}
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+void free_plan(sar_plan *p) {
+  if (!p) return;
+  DeviceGuard g(p->device);
+  if (p->last_stream) cudaStreamSynchronize(p->last_stream);
+  cudaDeviceSynchronize();
+  if (p->prof_events)
+    for (int i = 0; i < SAR_PROFILE_RING; ++i)
+      for (int j = 0; j <= SAR_N_STAGES; ++j) cudaEventDestroy(p->ev[i][j]);
+  cudaFree(p->d_tables);
+  cudaFree(p->d_w0);
+  cudaFree(p->d_w1);
+  cudaFree(p->d_in);
+  cudaFree(p->d_img);
+  delete p;
+}
+
+// twiddle table exp(-2 pi i m / n), fp64 -> fp32
+void twiddles(std::vector<float> &dst, int n) {
+  for (int m = 0; m < n; ++m) {
+    const double a = -2.0 * M_PI * (double)m / (double)n;
+    dst.push_back((float)cos(a));
+    dst.push_back((float)sin(a));
+  }
+}
+}  // namespace
+
+void sar_set_error(const std::string &msg) { g_last_error = msg; }
+
+extern "C" {
+
+const char *sar_last_error(void) { return g_last_error.c_str(); }
+
+int sar_version(void) { return SAR_B200_VERSION; }
+
+const char *sar_status_string(int s) {
+  switch (s) {
+    case SAR_OK: return "SAR_OK";
+    case SAR_ERR_INVALID_ARG: return "SAR_ERR_INVALID_ARG";
+    case SAR_ERR_GEOMETRY: return "SAR_ERR_GEOMETRY";
+    case SAR_ERR_UNSUPPORTED: return "SAR_ERR_UNSUPPORTED";
+    case SAR_ERR_OOM: return "SAR_ERR_OOM";
+    case SAR_ERR_CUDA: return "SAR_ERR_CUDA";
+    default: return "SAR_ERR_UNKNOWN";
+  }
+}
+
+}  // extern "C"
+
+namespace {
+
+// Host tables produced by the fp64 decomposition (uploaded by sar_plan_create).
+struct HostTables {
+  std::vector<float> apose, bpair, kturn, pinv, tw;
+  std::vector<double> kx, ky, kz, kd, rref;
+  size_t tw_y_off = 0, tw_z_off = 0;
+  int roll_x = 0, roll_y = 0;
+  double k0 = 0, dk = 0;
+};
+
+// Validation + Eqs. (3),(4),(7),(12) decomposition, no device involved.
+int host_decompose(const sar_geom_desc *g, const sar_image_desc *im, uint32_t flags, sar_plan *p,
+                   HostTables &T) {
+  if (!g || !im) return fail(SAR_ERR_INVALID_ARG, "geometry or image descriptor is NULL");
+  if (g->n_frames < 0) return fail(SAR_ERR_INVALID_ARG, "n_frames < 0");
+  if (g->n_tx < 1 || g->n_rx < 1) return fail(SAR_ERR_INVALID_ARG, "n_tx and n_rx must be >= 1");
+  if (g->n_tx * g->n_rx > SAR_MAX_PAIRS) return fail(SAR_ERR_UNSUPPORTED, "n_tx*n_rx > SAR_MAX_PAIRS");
+  if (!g->tx_xyz || !g->rx_xyz || !g->k) return fail(SAR_ERR_INVALID_ARG, "tx_xyz, rx_xyz or k is NULL");
+  if (g->n_frames > 0 && !g->scan_xyz) return fail(SAR_ERR_INVALID_ARG, "scan_xyz is NULL");
+  if (g->npx < 1 || g->npy < 1) return fail(SAR_ERR_INVALID_ARG, "npx, npy must be >= 1");
+  if (g->n_k < 2) return fail(SAR_ERR_INVALID_ARG, "n_k must be >= 2");
+  if (!pow2_in_range(im->nx) || !pow2_in_range(im->ny) || !pow2_in_range(im->nz))
+    return fail(SAR_ERR_INVALID_ARG, "nx, ny, nz must be powers of two in [2, SAR_MAX_FFT]");
+  if (g->npx > im->nx || g->npy > im->ny) return fail(SAR_ERR_INVALID_ARG, "raster larger than the FFT grid");
+  if (!(g->dx > 0) || !(g->dy > 0) || !(im->dz > 0)) return fail(SAR_ERR_INVALID_ARG, "pitches must be > 0");
+  if ((long long)g->n_frames * g->npx * g->npy > (1LL << 31)) return fail(SAR_ERR_UNSUPPORTED, "too many poses");
+  if (g->n_frames > 65535) return fail(SAR_ERR_UNSUPPORTED, "n_frames > 65535");
+
+  const int F = g->n_frames, nt = g->n_tx, nr = g->n_rx, nk = g->n_k;
+  const int P = g->npx * g->npy;
+  // O0: uniform wavenumber grid
+  T.k0 = g->k[0];
+  T.dk = (g->k[nk - 1] - g->k[0]) / (double)(nk - 1);
+  if (!(T.dk > 0)) return fail(SAR_ERR_GEOMETRY, "k must be ascending");
+  for (int i = 0; i < nk; ++i)
+    if (fabs(g->k[i] - (T.k0 + (double)i * T.dk)) > 1e-9 * T.k0) return fail(SAR_ERR_GEOMETRY, "k grid not uniform");
+
+  p->F = F; p->nt = nt; p->nr = nr; p->npair = nt * nr; p->npx = g->npx; p->npy = g->npy; p->P = P;
+  p->nk = nk; p->nx = im->nx; p->ny = im->ny; p->nz = im->nz; p->flags = flags; p->device = g->device;
+  p->dx = g->dx; p->dy = g->dy; p->dz = im->dz; p->z_ref = im->z_ref;
+
+  // Eq. (3): virtual element at the Tx/Rx midpoint; lattice offset j = rint(m/pitch)
+  std::vector<double> bm(p->npair);
+  p->jx.assign(p->npair, 0);
+  p->jy.assign(p->npair, 0);
+  const double mz = g->tx_xyz[2];
+  for (int t = 0; t < nt; ++t)
+    for (int r = 0; r < nr; ++r) {
+      const double *tx = g->tx_xyz + 3 * t, *rx = g->rx_xyz + 3 * r;
+      if (tx[2] != rx[2] || tx[2] != mz) return fail(SAR_ERR_GEOMETRY, "Tx and Rx must share one z plane (P:111)");
+      const double mx = (tx[0] + rx[0]) / 2.0, my = (tx[1] + rx[1]) / 2.0;
+      const double bx = rx[0] - tx[0], by = rx[1] - tx[1];
+      const double fx = mx / g->dx, fy = my / g->dy;
+      const double jxr = nearbyint(fx), jyr = nearbyint(fy);
+      if (fabs(fx - jxr) > 1e-6 || fabs(fy - jyr) > 1e-6)
+        return fail(SAR_ERR_GEOMETRY, "Tx/Rx midpoints are not on the virtual lattice");
+      p->jx[t * nr + r] = (int)jxr;
+      p->jy[t * nr + r] = (int)jyr;
+      bm[t * nr + r] = bx * bx + by * by;
+    }
+  p->jx_min = *std::min_element(p->jx.begin(), p->jx.end());
+  p->jy_min = *std::min_element(p->jy.begin(), p->jy.end());
+  int jxmax = 0, jymax = 0;
+  for (int i = 0; i < p->npair; ++i) {
+    p->jx[i] -= p->jx_min;
+    p->jy[i] -= p->jy_min;
+    jxmax = std::max(jxmax, p->jx[i]);
+    jymax = std::max(jymax, p->jy[i]);
+  }
+  p->nvx = p->npx + jxmax;
+  p->nvy = p->npy + jymax;
+
+  // Eq. (4): Z_0, R_ref and the per-pose beta term -2 d_z (reading R1)
+  std::vector<double> z0(F);
+  T.rref.assign(F, 0.0);
+  for (int f = 0; f < F; ++f) {
+    if (g->z0) {
+      z0[f] = g->z0[f];
+    } else {
+      double acc = 0;
+      for (int q = 0; q < P; ++q) acc += g->scan_xyz[((size_t)f * P + q) * 3 + 2];
+      z0[f] = acc / (double)P;
+    }
+    T.rref[f] = im->z_ref - z0[f];
+    if (!(T.rref[f] > 0)) return fail(SAR_ERR_GEOMETRY, "z_ref must lie beyond the reference plane (R_ref > 0)");
+  }
+  const bool nocomp = (flags & SAR_NO_COMPENSATION) != 0;
+  T.apose.assign((size_t)F * P, 0.f);
+  T.bpair.assign((size_t)F * p->npair, 0.f);
+  for (int f = 0; f < F; ++f) {
+    for (int q = 0; q < P; ++q) {
+      const double dzp = g->scan_xyz[((size_t)f * P + q) * 3 + 2] + mz - z0[f];
+      T.apose[(size_t)f * P + q] = nocomp ? 0.f : (float)(-2.0 * dzp);
+    }
+    for (int i = 0; i < p->npair; ++i)
+      T.bpair[(size_t)f * p->npair + i] = nocomp ? 0.f : (float)(bm[i] / (4.0 * T.rref[f]));
+  }
+  // wavenumber tables (reading R2) and the k_z grid (reading R5)
+  T.kx.resize(p->nx);
+  T.ky.resize(p->ny);
+  T.kz.resize(p->nz);
+  T.kd.assign(g->k, g->k + nk);
+  for (int a = 0; a < p->nx; ++a) {
+    const int as = a < p->nx / 2 ? a : a - p->nx;
+    T.kx[a] = 2.0 * M_PI * (double)as / ((double)p->nx * g->dx);
+  }
+  for (int b = 0; b < p->ny; ++b) {
+    const int bs = b < p->ny / 2 ? b : b - p->ny;
+    T.ky[b] = 2.0 * M_PI * (double)bs / ((double)p->ny * g->dy);
+  }
+  const double dkz = 2.0 * M_PI / ((double)p->nz * im->dz);
+  for (int j = 0; j < p->nz; ++j) T.kz[j] = 2.0 * g->k[nk - 1] - (double)(p->nz - 1 - j) * dkz;
+  T.kturn.resize(nk);
+  for (int i = 0; i < nk; ++i) T.kturn[i] = (float)(g->k[i] / (2.0 * M_PI));
+  T.pinv.clear();
+  if (g->pulse) {
+    for (int i = 0; i < nk; ++i) {
+      const double re = g->pulse[2 * i], im_ = g->pulse[2 * i + 1];
+      const double d = re * re + im_ * im_;
+      if (!(d > 0)) return fail(SAR_ERR_INVALID_ARG, "pulse spectrum has a zero");
+      T.pinv.push_back((float)(re / d));
+      T.pinv.push_back((float)(-im_ / d));
+    }
+  }
+  T.tw.clear();
+  twiddles(T.tw, p->nx);
+  T.tw_y_off = T.tw.size() / 2;
+  twiddles(T.tw, p->ny);
+  T.tw_z_off = T.tw.size() / 2;
+  twiddles(T.tw, p->nz);
+
+  // O7 rolls and axes (reading R8)
+  T.roll_x = p->nvx / 2 - p->nx / 2;
+  T.roll_y = p->nvy / 2 - p->ny / 2;
+  p->axes[0] = g->x0 + (double)(p->jx_min + T.roll_x) * g->dx;
+  p->axes[1] = g->y0 + (double)(p->jy_min + T.roll_y) * g->dy;
+  p->axes[2] = im->z_ref - (double)(p->nz / 2) * im->dz;
+  p->axes[3] = g->dx;
+  p->axes[4] = g->dy;
+  p->axes[5] = im->dz;
+  p->ws_bytes = ((size_t)F * p->ny * p->nx * ((size_t)nk + p->nz)) * sizeof(float2);
+  return SAR_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int sar_plan_describe(const sar_geom_desc *g, const sar_image_desc *im, uint32_t flags, sar_plan_info *info,
+                      int32_t *jx, int32_t *jy, double *kx, double *ky, double *kz, float *apose, float *bpair) {
+  if (!info) return fail(SAR_ERR_INVALID_ARG, "info is NULL");
+  sar_plan tmp;
+  HostTables T;
+  int st = host_decompose(g, im, flags, &tmp, T);
+  if (st != SAR_OK) return st;
+  info->n_pairs = tmp.npair;
+  info->jx_min = tmp.jx_min;
+  info->jy_min = tmp.jy_min;
+  info->nvx = tmp.nvx;
+  info->nvy = tmp.nvy;
+  info->roll_x = T.roll_x;
+  info->roll_y = T.roll_y;
+  memcpy(info->axes, tmp.axes, sizeof(tmp.axes));
+  info->k0 = T.k0;
+  info->dk = T.dk;
+  info->workspace_bytes = tmp.ws_bytes;
+  for (int i = 0; i < tmp.npair; ++i) {
+    if (jx) jx[i] = tmp.jx[i];
+    if (jy) jy[i] = tmp.jy[i];
+  }
+  if (kx) memcpy(kx, T.kx.data(), T.kx.size() * sizeof(double));
+  if (ky) memcpy(ky, T.ky.data(), T.ky.size() * sizeof(double));
+  if (kz) memcpy(kz, T.kz.data(), T.kz.size() * sizeof(double));
+  if (apose) memcpy(apose, T.apose.data(), T.apose.size() * sizeof(float));
+  if (bpair) memcpy(bpair, T.bpair.data(), T.bpair.size() * sizeof(float));
+  return SAR_OK;
+}
+
+int sar_plan_create(sar_plan **out, const sar_geom_desc *g, const sar_image_desc *im, uint32_t flags) {
+  if (!out) return fail(SAR_ERR_INVALID_ARG, "out is NULL");
+  *out = nullptr;
+  sar_plan *p = new (std::nothrow) sar_plan();
+  if (!p) return fail(SAR_ERR_OOM, "host allocation failed");
+  HostTables T;
+  int st = host_decompose(g, im, flags, p, T);
+  if (st != SAR_OK) {
+    delete p;
+    return st;
+  }
+  int ndev = 0;
+  cudaError_t ce = cudaGetDeviceCount(&ndev);
+  if (ce != cudaSuccess || ndev == 0) {
+    delete p;
+    return fail(SAR_ERR_UNSUPPORTED, "no CUDA device");
+  }
+  if (g->device < 0 || g->device >= ndev) {
+    delete p;
+    return fail(SAR_ERR_INVALID_ARG, "device ordinal out of range");
+  }
+  cudaDeviceProp prop;
+  ce = cudaGetDeviceProperties(&prop, g->device);
+  if (ce != cudaSuccess) {
+    delete p;
+    return cuda_fail(ce, "cudaGetDeviceProperties");
+  }
+  if (prop.major != 10 || prop.minor != 0) {
+    delete p;
+    return fail(SAR_ERR_UNSUPPORTED, "this build targets sm_100a (B200) only; device is sm_" +
+                                         std::to_string(prop.major) + std::to_string(prop.minor));
+  }
+  const int F = p->F, nk = p->nk, P = p->P;
+
+  // one device allocation for all tables (256-byte aligned sections)
+  DeviceGuard guard(p->device);
+  auto al = [](size_t n) { return (n + 255) & ~(size_t)255; };
+  size_t off = 0;
+  const size_t o_ap = off; off += al(T.apose.size() * 4);
+  const size_t o_bp = off; off += al(T.bpair.size() * 4);
+  const size_t o_kt = off; off += al(T.kturn.size() * 4);
+  const size_t o_k = off; off += al(T.kd.size() * 8);
+  const size_t o_kx = off; off += al(T.kx.size() * 8);
+  const size_t o_ky = off; off += al(T.ky.size() * 8);
+  const size_t o_kz = off; off += al(T.kz.size() * 8);
+  const size_t o_rr = off; off += al(T.rref.size() * 8 + 8);
+  const size_t o_pi = off; off += al(T.pinv.size() * 4);
+  const size_t o_tw = off; off += al(T.tw.size() * 4);
+  ce = cudaMalloc(&p->d_tables, off);
+  if (ce != cudaSuccess) {
+    cudaGetLastError();
+    free_plan(p);
+    return fail(SAR_ERR_OOM, "table allocation failed");
+  }
+  char *base = (char *)p->d_tables;
+  auto up = [&](size_t o, const void *src, size_t n) {
+    return n ? cudaMemcpy(base + o, src, n, cudaMemcpyHostToDevice) : cudaSuccess;
+  };
+  if ((ce = up(o_ap, T.apose.data(), T.apose.size() * 4)) != cudaSuccess ||
+      (ce = up(o_bp, T.bpair.data(), T.bpair.size() * 4)) != cudaSuccess ||
+      (ce = up(o_kt, T.kturn.data(), T.kturn.size() * 4)) != cudaSuccess ||
+      (ce = up(o_k, T.kd.data(), T.kd.size() * 8)) != cudaSuccess ||
+      (ce = up(o_kx, T.kx.data(), T.kx.size() * 8)) != cudaSuccess ||
+      (ce = up(o_ky, T.ky.data(), T.ky.size() * 8)) != cudaSuccess ||
+      (ce = up(o_kz, T.kz.data(), T.kz.size() * 8)) != cudaSuccess ||
+      (ce = up(o_rr, T.rref.data(), T.rref.size() * 8)) != cudaSuccess ||
+      (ce = up(o_pi, T.pinv.data(), T.pinv.size() * 4)) != cudaSuccess ||
+      (ce = up(o_tw, T.tw.data(), T.tw.size() * 4)) != cudaSuccess) {
+    free_plan(p);
+    return cuda_fail(ce, "table upload");
+  }
+  const size_t n0 = (size_t)F * p->ny * p->nx * nk, n1 = (size_t)F * p->ny * p->nx * p->nz;
+  if (F > 0) {
+    if (cudaMalloc(&p->d_w0, n0 * sizeof(float2)) != cudaSuccess ||
+        cudaMalloc(&p->d_w1, n1 * sizeof(float2)) != cudaSuccess) {
+      cudaGetLastError();
+      free_plan(p);
+      return fail(SAR_ERR_OOM, "workspace allocation failed");
+    }
+  }
+  SarDeviceView &v = p->v;
+  v.F = F; v.nt = p->nt; v.nr = p->nr; v.npair = p->npair; v.npx = p->npx; v.npy = p->npy; v.P = P;
+  v.nk = nk; v.nx = p->nx; v.ny = p->ny; v.nz = p->nz;
+  v.roll_x = T.roll_x; v.roll_y = T.roll_y;
+  v.no_comp = (flags & SAR_NO_COMPENSATION) ? 1 : 0;
+  for (int i = 0; i < p->npair; ++i) {
+    v.jx[i] = p->jx[i] % p->nx;  // placement mod the FFT grid (reading R6)
+    v.jy[i] = p->jy[i] % p->ny;
+  }
+  v.apose = (const float *)(base + o_ap);
+  v.bpair = (const float *)(base + o_bp);
+  v.kturn = (const float *)(base + o_kt);
+  v.k = (const double *)(base + o_k);
+  v.kx = (const double *)(base + o_kx);
+  v.ky = (const double *)(base + o_ky);
+  v.kz = (const double *)(base + o_kz);
+  v.rref = (const double *)(base + o_rr);
+  v.pinv = T.pinv.empty() ? nullptr : (const float2 *)(base + o_pi);
+  v.tw_x = (const float2 *)(base + o_tw);
+  v.tw_y = (const float2 *)(base + o_tw) + T.tw_y_off;
+  v.tw_z = (const float2 *)(base + o_tw) + T.tw_z_off;
+  v.k0 = T.k0;
+  v.dk = T.dk;
+  v.img_scale = (float)(1.0 / ((double)p->nx * p->ny * p->nz));
+  v.w0 = p->d_w0;
+  v.w1 = p->d_w1;
+
+  if (flags & SAR_PROFILE_STAGES) {
+    for (int i = 0; i < SAR_PROFILE_RING; ++i)
+      for (int j = 0; j <= SAR_N_STAGES; ++j) cudaEventCreate(&p->ev[i][j]);
+    p->prof_events = true;
+  }
+  *out = p;
+  return SAR_OK;
+}
+
+int sar_reconstruct(sar_plan *p, const void *d_data, void *d_image, sar_stream stream) {
+  if (!p) return fail(SAR_ERR_INVALID_ARG, "plan is NULL");
+  if (p->F == 0) return SAR_OK;
+  if (!d_data || !d_image) return fail(SAR_ERR_INVALID_ARG, "data or image pointer is NULL");
+  DeviceGuard g(p->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  p->last_stream = s;
+  cudaEvent_t *ev = nullptr;
+  if (p->prof_events && p->n_prof < SAR_PROFILE_RING) ev = p->ev[p->n_prof++];
+  return sar_launch_pipeline(p, d_data, d_image, s, 0, (p->flags & SAR_OUTPUT_COMPLEX) ? 1 : 0, ev);
+}
+
+int sar_reconstruct_host(sar_plan *p, const void *h_data, void *h_image, sar_stream stream) {
+  if (!p) return fail(SAR_ERR_INVALID_ARG, "plan is NULL");
+  if (p->F == 0) return SAR_OK;
+  if (!h_data || !h_image) return fail(SAR_ERR_INVALID_ARG, "data or image pointer is NULL");
+  DeviceGuard g(p->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t in_b = (size_t)p->F * p->npair * p->P * p->nk * sizeof(float2);
+  const size_t img_b = (size_t)p->F * p->nz * p->ny * p->nx *
+                       ((p->flags & SAR_OUTPUT_COMPLEX) ? sizeof(float2) : sizeof(float));
+  if (!p->d_in) {
+    if (cudaMalloc(&p->d_in, in_b) != cudaSuccess || cudaMalloc(&p->d_img, img_b) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(SAR_ERR_OOM, "staging allocation failed");
+    }
+    p->in_bytes = in_b;
+    p->img_bytes = img_b;
+  }
+  cudaError_t e = cudaMemcpyAsync(p->d_in, h_data, in_b, cudaMemcpyHostToDevice, s);
+  if (e != cudaSuccess) return cuda_fail(e, "H2D");
+  int st = sar_reconstruct(p, p->d_in, p->d_img, stream);
+  if (st != SAR_OK) return st;
+  e = cudaMemcpyAsync(h_image, p->d_img, img_b, cudaMemcpyDeviceToHost, s);
+  if (e != cudaSuccess) return cuda_fail(e, "D2H");
+  e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return cuda_fail(e, "synchronize");
+  return SAR_OK;
+}
+
+int sar_plan_destroy(sar_plan *p) {
+  free_plan(p);
+  return SAR_OK;
+}
+
+int sar_plan_get_axes(const sar_plan *p, double out[6]) {
+  if (!p || !out) return fail(SAR_ERR_INVALID_ARG, "NULL argument");
+  memcpy(out, p->axes, sizeof(p->axes));
+  return SAR_OK;
+}
+
+int sar_plan_workspace_bytes(const sar_plan *p, size_t *bytes) {
+  if (!p || !bytes) return fail(SAR_ERR_INVALID_ARG, "NULL argument");
+  *bytes = p->ws_bytes;
+  return SAR_OK;
+}
+
+int sar_plan_launches_per_call(const sar_plan *p, int32_t *n) {
+  if (!p || !n) return fail(SAR_ERR_INVALID_ARG, "NULL argument");
+  *n = p->F > 0 ? SAR_N_STAGES : 0;
+  return SAR_OK;
+}
+
+int sar_plan_profile_reset(sar_plan *p) {
+  if (!p) return fail(SAR_ERR_INVALID_ARG, "plan is NULL");
+  p->n_prof = 0;
+  return SAR_OK;
+}
+
+int sar_plan_profile_read(sar_plan *p, float ms_out[5], int32_t *n_calls) {
+  if (!p || !ms_out) return fail(SAR_ERR_INVALID_ARG, "NULL argument");
+  if (!p->prof_events) return fail(SAR_ERR_INVALID_ARG, "plan was created without SAR_PROFILE_STAGES");
+  DeviceGuard g(p->device);
+  for (int j = 0; j < SAR_N_STAGES; ++j) ms_out[j] = 0.f;
+  for (int i = 0; i < p->n_prof; ++i) {
+    cudaError_t e = cudaEventSynchronize(p->ev[i][SAR_N_STAGES]);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaEventSynchronize");
+    for (int j = 0; j < SAR_N_STAGES; ++j) {
+      float ms = 0.f;
+      e = cudaEventElapsedTime(&ms, p->ev[i][j], p->ev[i][j + 1]);
+      if (e != cudaSuccess) return cuda_fail(e, "cudaEventElapsedTime");
+      ms_out[j] += ms;
+    }
+  }
+  if (n_calls) *n_calls = p->n_prof;
+  return SAR_OK;
+}
+
+int sar_debug_stage(sar_plan *p, int32_t stage, const void *d_data, void *d_out, sar_stream stream) {
+  if (!p) return fail(SAR_ERR_INVALID_ARG, "plan is NULL");
+  if (stage < 1 || stage > 4) return fail(SAR_ERR_INVALID_ARG, "stage must be 1..4");
+  if (p->F == 0) return SAR_OK;
+  if (!d_data || !d_out) return fail(SAR_ERR_INVALID_ARG, "NULL pointer");
+  DeviceGuard g(p->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  p->last_stream = s;
+  if (stage == 4) return sar_launch_pipeline(p, d_data, d_out, s, 0, 1, nullptr);
+  int st = sar_launch_pipeline(p, d_data, nullptr, s, stage, 0, nullptr);
+  if (st != SAR_OK) return st;
+  const size_t n = (size_t)p->F * p->ny * p->nx * (stage == 3 ? p->nz : p->nk);
+  cudaError_t e = cudaMemcpyAsync(d_out, stage == 3 ? p->d_w1 : p->d_w0, n * sizeof(float2),
+                                  cudaMemcpyDeviceToDevice, s);
+  if (e != cudaSuccess) return cuda_fail(e, "stage copy");
+  return SAR_OK;
+}
+
+int sar_debug_node_offsets(const sar_plan *p, int32_t *jx, int32_t *jy, int32_t *jx_min, int32_t *jy_min) {
+  if (!p || !jx || !jy) return fail(SAR_ERR_INVALID_ARG, "NULL argument");
+  for (int i = 0; i < p->npair; ++i) {
+    jx[i] = p->jx[i];
+    jy[i] = p->jy[i];
+  }
+  if (jx_min) *jx_min = p->jx_min;
+  if (jy_min) *jy_min = p->jy_min;
+  return SAR_OK;
+}
+
+int sar_debug_stolt_index(sar_plan *p, const int32_t *d_cols, int32_t n, int32_t *d_i0, float *d_tau,
+                          sar_stream stream) {
+  if (!p || n < 0 || (n > 0 && (!d_cols || !d_i0 || !d_tau))) return fail(SAR_ERR_INVALID_ARG, "bad argument");
+  DeviceGuard g(p->device);
+  return sar_launch_stolt_index(p, d_cols, n, d_i0, d_tau, (cudaStream_t)stream);
+}
+
+}  // extern "C"

@@ -1,0 +1,68 @@
+// plan_internal.h -- the plan object shared by the host C ABI (plan.cpp) and
+// the kernel launchers (kernels.cu).  Not part of the public ABI.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/sar_b200.h"
+
+#define SAR_PROFILE_RING 1024
+#define SAR_N_STAGES 5
+
+// Everything a kernel needs, passed by value (fits the 32 KB parameter space).
+struct SarDeviceView {
+  int F, nt, nr, npair, npx, npy, P, nk, nx, ny, nz;
+  int roll_x, roll_y;
+  int no_comp;
+  int jx[SAR_MAX_PAIRS], jy[SAR_MAX_PAIRS];  // virtual-node offsets, pair = t*nr + r
+  const float *apose;   // [F][P]      -2 d_z (m), fp32
+  const float *bpair;   // [F][npair]  (d_x^2+d_y^2)/(4 R_ref) (m), fp32
+  const float *kturn;   // [nk]        k_i / (2 pi) (turns per metre), fp32
+  const double *k;      // [nk]        k_i (rad/m)
+  const double *kx;     // [nx]
+  const double *ky;     // [ny]
+  const double *kz;     // [nz]        uniform Stolt grid (reading R5)
+  const double *rref;   // [F]         R_ref = z_ref - Z_0
+  const float2 *pinv;   // [nk] 1/P(f) or nullptr (P == 1)
+  const float2 *tw_x;   // [nx] exp(-2 pi i m/nx)
+  const float2 *tw_y;   // [ny]
+  const float2 *tw_z;   // [nz]
+  double k0, dk;
+  float img_scale;      // 1/(nx ny nz)
+  float2 *w0;           // [F][ny][nx][nk]  planar lattice -> spectrum
+  float2 *w1;           // [F][ny][nx][nz]  Stolt output -> partial inverse
+};
+
+struct sar_plan {
+  // sizes
+  int F = 0, nt = 0, nr = 0, npair = 0, npx = 0, npy = 0, P = 0, nk = 0, nx = 0, ny = 0, nz = 0;
+  uint32_t flags = 0;
+  int device = 0;
+  double dx = 0, dy = 0, dz = 0, z_ref = 0;
+  double axes[6] = {0, 0, 0, 0, 0, 0};
+  std::vector<int> jx, jy;
+  int jx_min = 0, jy_min = 0, nvx = 0, nvy = 0;
+  SarDeviceView v{};
+  // device allocations
+  void *d_tables = nullptr;
+  float2 *d_w0 = nullptr, *d_w1 = nullptr;
+  size_t ws_bytes = 0;
+  // host-buffer staging (sar_reconstruct_host)
+  void *d_in = nullptr, *d_img = nullptr;
+  size_t in_bytes = 0, img_bytes = 0;
+  // profiling
+  cudaEvent_t ev[SAR_PROFILE_RING][SAR_N_STAGES + 1];
+  int n_prof = 0;
+  bool prof_events = false;
+  cudaStream_t last_stream = nullptr;
+};
+
+// kernels.cu
+int sar_launch_pipeline(sar_plan *p, const void *d_data, void *d_image, cudaStream_t s,
+                        int stop_stage /*0 = full*/, int complex_out, cudaEvent_t *ev /*6 or null*/);
+int sar_launch_stolt_index(sar_plan *p, const int32_t *d_cols, int n, int32_t *d_i0, float *d_tau,
+                           cudaStream_t s);
+void sar_set_error(const std::string &msg);

@@ -1,0 +1,121 @@
+"""Host-side tests of the C ABI (no GPU): the library loads, exports every
+entry point include/sar_b200.h declares, validates its arguments, and its fp64
+host decomposition (sar_plan_describe) reproduces the oracle's integer tables
+and k tables bit for bit (the inputs of every index decision, reading R9)."""
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+import oracle
+import scenes
+import paper_2305_02064_b200 as sar
+from paper_2305_02064_b200 import sar as sarmod
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "sar_b200.h")
+
+
+@pytest.fixture(scope="module", autouse=True)
+def built():
+    import __graft_entry__
+    __graft_entry__.build()
+
+
+def _declared():
+    txt = open(HEADER).read()
+    txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+    return sorted(set(re.findall(r"\b(sar_[a-z_]+)\s*\(", txt)))
+
+
+def test_library_exports_every_declared_symbol():
+    declared = _declared()
+    assert len(declared) >= 15
+    out = subprocess.run(["nm", "-D", "--defined-only", sar.LIB_PATH], capture_output=True, text=True).stdout
+    exported = set(re.findall(r"\bT (sar_\w+)", out))
+    missing = [d for d in declared if d not in exported]
+    assert not missing, missing
+    lib = sar.load_library()
+    for d in declared:
+        assert hasattr(lib, d)
+    assert sorted(sarmod.exported_symbols()) == declared
+    assert lib.sar_version() == 1
+
+
+def test_no_oracle_in_product_path():
+    """The product package never imports the oracle (test infrastructure)."""
+    pkg = os.path.join(ROOT, "paper_2305_02064_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for fn in files:
+            if fn.endswith((".py", ".cu", ".cpp", ".cuh", ".h")):
+                txt = open(os.path.join(dirpath, fn)).read()
+                assert not re.search(r"^\s*(import|from)\s+oracle", txt, flags=re.M), fn
+                assert "scipy" not in txt, fn
+
+
+@pytest.mark.parametrize("name", ["tiny", "small", "freehand", "large", "realtime"])
+def test_describe_matches_oracle_bit_exact(name):
+    sc = scenes.make_scene(name)
+    d = sar.describe_scene(sc)
+    geo = oracle.rma.geometry_of(sc)
+    assert np.array_equal(d["jx"], geo.jx) and np.array_equal(d["jy"], geo.jy)
+    assert (d["jx_min"], d["jy_min"], d["nvx"], d["nvy"]) == (geo.jx_min, geo.jy_min, geo.nvx, geo.nvy)
+    assert (d["roll_x"], d["roll_y"]) == (geo.roll_x, geo.roll_y)
+    # bit-exact fp64 tables feeding the Stolt decisions
+    assert np.array_equal(d["kx"], geo.kx) and np.array_equal(d["ky"], geo.ky)
+    assert np.array_equal(d["kz"], geo.kz)
+    assert d["k0"] == geo.k0 and d["dk"] == geo.dk
+    assert d["axes"] == tuple(geo.axes)
+    # fp32 beta terms: the fp64 oracle values rounded once
+    bet = -2.0 * geo.d_z
+    assert np.array_equal(d["apose"], bet.astype(np.float32))
+    assert np.array_equal(d["bpair"], geo.beta_mimo.astype(np.float32))
+    assert d["workspace_bytes"] == sc.n_frames * sc.ny * sc.nx * (sc.n_k + sc.nz) * 8
+
+
+def test_describe_no_compensation_zero_beta():
+    sc = scenes.make_scene("tiny")
+    d = sar.describe_scene(sc, flags=sar.SAR_NO_COMPENSATION)
+    assert not d["apose"].any() and not d["bpair"].any()
+
+
+def _args(**over):
+    sc = scenes.make_scene("tiny")
+    a = dict(tx=sc.tx, rx=sc.rx, scan=sc.scan, npx=sc.npx, npy=sc.npy, x0=sc.x0, y0=sc.y0, dx=sc.dx,
+             dy=sc.dy, z0=sc.z0, k=sc.k, nx=sc.nx, ny=sc.ny, nz=sc.nz, dz=sc.dz_img, z_ref=sc.z_ref)
+    a.update(over)
+    return a
+
+
+@pytest.mark.parametrize("over,status", [
+    (dict(nx=48), 1), (dict(nz=1), 1), (dict(ny=2048), 1), (dict(npx=65, nx=64), 1),
+    (dict(k=scenes.wavenumbers(16)[:1]), 1), (dict(dz=0.0), 1),
+    (dict(k=np.sort(np.random.default_rng(0).uniform(1600, 1700, 16))), 2),
+    (dict(z_ref=-1.0), 2),
+    (dict(rx=np.array([[0.0, 0.3e-3, 0.0]] * 4)), 2),
+    (dict(rx=np.array([[0.0, 0.0, 1e-3]] * 4)), 2),
+    (dict(tx=np.zeros((9, 3)), rx=np.zeros((8, 3))), 3),
+])
+def test_validation_errors(over, status):
+    with pytest.raises(sar.SarError) as ei:
+        sar.describe(**_args(**over))
+    assert ei.value.status == status
+    assert sar.load_library().sar_last_error().decode()
+
+
+def test_empty_frames_describe_ok():
+    sc = scenes.make_scene("tiny")
+    d = sar.describe(**_args(scan=np.zeros((0, sc.n_pos, 3)), z0=np.zeros(0)))
+    assert d["workspace_bytes"] == 0
+
+
+def test_plan_create_without_gpu_fails_loudly():
+    """No CPU fallback: without a B200 the plan refuses (UNSUPPORTED)."""
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    with pytest.raises(sar.SarError) as ei:
+        sar.Plan.from_scene(scenes.make_scene("tiny"))
+    assert ei.value.status == 3

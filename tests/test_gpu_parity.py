@@ -1,0 +1,256 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 oracle on the
+same seeded complex64 inputs.
+
+Bar (BASELINE.json north_star): relative L2 <= 1e-4 and max normalised error
+<= 1e-3 on the magnitude image; integer/index work bit-exact.  Per-stage
+tolerances (fp32 FFTs of up to 512^2 points, fp32 phase in turns) are 2e-5
+relative L2, derived in DESIGN.md section 7.
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+import oracle  # noqa: E402
+import scenes  # noqa: E402
+import paper_2305_02064_b200 as sar  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+E2_BAR, EINF_BAR, STAGE_BAR = 1e-4, 1e-3, 2e-5
+
+
+@pytest.fixture(scope="module", autouse=True)
+def built():
+    import __graft_entry__
+    __graft_entry__.build()
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def errs(got, want):
+    got = np.asarray(got, dtype=np.complex128 if np.iscomplexobj(got) else np.float64)
+    d = got - want
+    e2 = np.linalg.norm(d.ravel()) / max(np.linalg.norm(np.ravel(want)), 1e-300)
+    einf = np.abs(d).max() / max(np.abs(want).max(), 1e-300)
+    return e2, einf
+
+
+def _data(sc, gpu_gen=None):
+    if gpu_gen is None:
+        gpu_gen = sc.n_samples * max(len(q) for q in sc.scat_pos) > 5e8
+    if gpu_gen:
+        import scenes.gpu
+        d = scenes.gpu.synthesize_gpu(sc)
+        return d, d.cpu().numpy()
+    s = scenes.synthesize_cpu(sc)
+    return torch.from_numpy(s).cuda(), s
+
+
+def test_gpu_generator_matches_cpu():
+    import scenes.gpu
+    for name in ("tiny", "small"):
+        sc = scenes.make_scene(name)
+        a = scenes.gpu.synthesize_gpu(sc).cpu().numpy()
+        b = scenes.synthesize_cpu(sc)
+        e2, _ = errs(a, b)
+        assert e2 < 2e-6, (name, e2)
+
+
+@pytest.mark.parametrize("name", ["tiny", "small"])
+def test_stage_parity(name):
+    sc = scenes.make_scene(name)
+    d, s = _data(sc)
+    img, geo, st = oracle.reconstruct(s, sc, complex_out=True, return_stages=True)
+    with sar.Plan.from_scene(sc) as plan:
+        g1 = plan.debug_stage(1, d).cpu().numpy()
+        g2 = plan.debug_stage(2, d).cpu().numpy()
+        g3 = plan.debug_stage(3, d).cpu().numpy()
+        g4 = plan.debug_stage(4, d).cpu().numpy()
+    e = {k: errs(g, w) for k, g, w in (("planar", g1, st["planar"]), ("spectrum", g2, st["spectrum"]),
+                                       ("stolt", g3, st["stolt"]), ("complex", g4, img))}
+    for k, (e2, einf) in e.items():
+        assert e2 <= STAGE_BAR, (k, e2, einf)
+
+
+def _check_e2e(sc, flags=0, gpu_gen=None, geo=None, pulse=None):
+    d, s = _data(sc, gpu_gen)
+    want, _ = oracle.reconstruct(s, geo if geo is not None else sc,
+                                 no_compensation=bool(flags & sar.SAR_NO_COMPENSATION))
+    with sar.Plan.from_scene(sc, flags=flags, pulse=pulse) as plan:
+        got = plan.reconstruct(d)
+        torch.cuda.synchronize()
+        got = got.cpu().numpy()
+    e2, einf = errs(got, want)
+    assert e2 <= E2_BAR and einf <= EINF_BAR, (sc.name, e2, einf)
+    return got, want, e2, einf
+
+
+@pytest.mark.parametrize("name", ["tiny", "small", "freehand", "realtime"])
+def test_end_to_end(name):
+    _check_e2e(scenes.make_scene(name))
+
+
+@pytest.mark.slow
+def test_end_to_end_large_bench_configuration():
+    """Large (configs[3]) at full size in the launch configuration bench.py
+    times (plan with SAR_PROFILE_STAGES), full oracle on the host."""
+    sc = scenes.make_scene("large")
+    _check_e2e(sc, flags=sar.SAR_PROFILE_STAGES, gpu_gen=True)
+
+
+def test_node_offsets_match_oracle():
+    for name in ("tiny", "large"):
+        sc = scenes.make_scene(name)
+        geo = oracle.rma.geometry_of(sc)
+        with sar.Plan.from_scene(sc) as plan:
+            jx, jy, mx, my = plan.node_offsets()
+            assert np.array_equal(jx, geo.jx) and np.array_equal(jy, geo.jy)
+            assert (mx, my) == (geo.jx_min, geo.jy_min)
+            assert plan.axes() == tuple(geo.axes)
+
+
+@pytest.mark.parametrize("name,n_sample", [("tiny", None), ("small", None), ("large", 8192)])
+def test_stolt_index_bit_exact(name, n_sample):
+    """Device Stolt decisions (the code K3 runs) == oracle table, bit for bit
+    in the index, to fp32 rounding in the weight.  Large: a random sample of
+    columns plus the DC row/column and the Nyquist corners."""
+    sc = scenes.make_scene(name)
+    geo = oracle.rma.geometry_of(sc)
+    b, a = np.meshgrid(np.arange(sc.ny), np.arange(sc.nx), indexing="ij")
+    cols = np.stack([a.ravel(), b.ravel()], axis=1)
+    if n_sample:
+        rng = np.random.default_rng(0)
+        pick = rng.choice(len(cols), n_sample, replace=False)
+        extra = np.array([[0, 0], [sc.nx // 2, 0], [0, sc.ny // 2], [sc.nx // 2, sc.ny // 2], [1, 0], [0, 1],
+                          [sc.nx - 1, sc.ny - 1]])
+        cols = np.concatenate([cols[pick], extra])
+    with sar.Plan.from_scene(sc) as plan:
+        i0, tau = plan.stolt_index(cols)
+        i0, tau = i0.cpu().numpy(), tau.cpu().numpy()
+    wi, wt = oracle.stolt_index_table(geo, cols[:, 0], cols[:, 1])
+    assert np.array_equal(i0, wi)
+    assert np.abs(tau - wt).max() <= 1e-7
+    assert (i0 >= 0).any() and (i0 < 0).any()
+
+
+def _custom(npx, npy, nx, ny, nk, nz, dz, z_ref, n_frames=1, monostatic=False, n_tx=2, nsc=4, seed=0):
+    sc = scenes.raster_scene(npx, npy, nx, ny, nk, nz, dz, z_ref, monostatic=monostatic, n_tx=n_tx,
+                             jitter_xy=0.5e-3, jitter_z=2e-3, n_frames=n_frames, seed=seed)
+    rng = np.random.default_rng(seed + 1)
+    pos, amp = [], []
+    cx = sc.x0 + npx * sc.dx / 2
+    cy = sc.y0 + npy * sc.dy / 2
+    for _ in range(n_frames):
+        q = np.stack([cx + rng.uniform(-0.01, 0.01, nsc), cy + rng.uniform(-0.01, 0.01, nsc),
+                      z_ref + rng.uniform(-0.02, 0.02, nsc)], axis=1)
+        pos.append(q)
+        amp.append(rng.normal(size=nsc) + 1j * rng.normal(size=nsc))
+    sc.scat_pos, sc.scat_amp = pos, amp
+    sc.noise_sigma = 1e-3
+    sc.name = f"custom{npx}x{npy}/{nx}x{ny}x{nz}/k{nk}/F{n_frames}"
+    return sc
+
+
+EDGE = [
+    # ragged k chunks (n_k not a multiple of 16), ragged raster, nz > n_k
+    dict(npx=20, npy=13, nx=32, ny=32, nk=20, nz=64, dz=4e-3, z_ref=0.2),
+    dict(npx=33, npy=7, nx=64, ny=16, nk=37, nz=16, dz=5e-3, z_ref=0.15),
+    # wrap: virtual aperture taller than the grid (npy + 7 > ny)
+    dict(npx=16, npy=16, nx=16, ny=16, nk=16, nz=8, dz=6e-3, z_ref=0.25),
+    # minimal sizes: 2-point FFTs, 2 frequencies, single pose
+    dict(npx=1, npy=1, nx=2, ny=2, nk=2, nz=2, dz=5e-3, z_ref=0.25, monostatic=True),
+    dict(npx=2, npy=1, nx=2, ny=4, nk=3, nz=4, dz=5e-3, z_ref=0.25),
+    # several frames with their own geometry; 3 Tx
+    dict(npx=24, npy=20, nx=32, ny=32, nk=32, nz=32, dz=5e-3, z_ref=0.2, n_frames=3, n_tx=3),
+    # maximum FFT size along x and z (1024), small elsewhere
+    dict(npx=600, npy=4, nx=1024, ny=16, nk=16, nz=1024, dz=1e-3, z_ref=0.3),
+    dict(npx=4, npy=700, nx=8, ny=1024, nk=24, nz=8, dz=5e-3, z_ref=0.3),
+]
+
+
+@pytest.mark.parametrize("kw", EDGE, ids=lambda kw: "x".join(str(kw[k]) for k in ("npx", "npy", "nx", "ny", "nk", "nz")))
+def test_edge_cases(kw):
+    _check_e2e(_custom(**kw), gpu_gen=False)
+
+
+def test_no_compensation_parity_and_contrast():
+    sc = scenes.make_scene("small")
+    a, _, _, _ = _check_e2e(sc, flags=sar.SAR_NO_COMPENSATION)
+    b, _, _, _ = _check_e2e(sc)
+    assert np.linalg.norm(a - b) / np.linalg.norm(b) > 0.05
+
+
+def test_pulse_spectrum_parity():
+    sc = scenes.make_scene("tiny")
+    pulse = np.exp(1j * np.linspace(0, 2, sc.n_k)) * np.linspace(1.0, 2.0, sc.n_k)
+    geo = oracle.decompose(sc.tx, sc.rx, sc.scan, sc.npx, sc.npy, sc.x0, sc.y0, sc.dx, sc.dy, sc.z0, sc.k,
+                           sc.nx, sc.ny, sc.nz, sc.dz_img, sc.z_ref, pulse=pulse)
+    _check_e2e(sc, geo=geo, pulse=pulse)
+
+
+def test_zero_input_zero_output_and_empty_frames():
+    sc = scenes.make_scene("tiny")
+    with sar.Plan.from_scene(sc) as plan:
+        out = plan.reconstruct(torch.zeros(sc.data_shape, dtype=torch.complex64, device="cuda"))
+        assert not out.any().item()
+    sc0 = scenes.make_scene("tiny")
+    sc0.scan = sc0.scan[:0]
+    sc0.z0 = sc0.z0[:0]
+    sc0.n_frames = 0
+    with sar.Plan.from_scene(sc0) as plan:
+        out = plan.reconstruct(torch.zeros(sc0.data_shape, dtype=torch.complex64, device="cuda"))
+        assert out.numel() == 0 and plan.launches_per_call() == 0
+
+
+def test_complex_output_linearity():
+    sc = scenes.make_scene("tiny")
+    d, _ = _data(sc)
+    rng = np.random.default_rng(1)
+    o = torch.from_numpy((rng.normal(size=sc.data_shape) + 1j * rng.normal(size=sc.data_shape)).astype(np.complex64)).cuda()
+    with sar.Plan.from_scene(sc, flags=sar.SAR_OUTPUT_COMPLEX) as plan:
+        A = plan.reconstruct(d).cpu().numpy()
+        B = plan.reconstruct(o).cpu().numpy()
+        Cc = plan.reconstruct(d + 2 * o).cpu().numpy()
+    e2, _ = errs(Cc, A + 2 * B)
+    assert e2 < 1e-5
+
+
+def test_host_api_matches_device_api():
+    sc = scenes.make_scene("small")
+    d, s = _data(sc)
+    with sar.Plan.from_scene(sc) as plan:
+        dev = plan.reconstruct(d).cpu().numpy()
+        host = plan.reconstruct_host(torch.from_numpy(s).pin_memory()).numpy()
+    assert np.array_equal(dev, host)
+
+
+def test_profiling_and_launch_count():
+    sc = scenes.make_scene("small")
+    d, _ = _data(sc)
+    with sar.Plan.from_scene(sc, flags=sar.SAR_PROFILE_STAGES) as plan:
+        assert plan.launches_per_call() == 5
+        for _ in range(3):
+            plan.reconstruct(d)
+        ms, n = plan.profile_read()
+        assert n == 3 and all(m > 0 for m in ms)
+        plan.profile_reset()
+        assert plan.profile_read()[1] == 0
+
+
+def test_deterministic():
+    sc = scenes.make_scene("small")
+    d, _ = _data(sc)
+    with sar.Plan.from_scene(sc) as plan:
+        a = plan.reconstruct(d).cpu().numpy()
+        b = plan.reconstruct(d).cpu().numpy()
+    assert np.array_equal(a, b)
+
+
+def test_bad_tensor_arguments():
+    sc = scenes.make_scene("tiny")
+    with sar.Plan.from_scene(sc) as plan:
+        with pytest.raises(ValueError):
+            plan.reconstruct(torch.zeros((1, 2, 4, 256, 15), dtype=torch.complex64, device="cuda"))
+        with pytest.raises(TypeError):
+            plan.reconstruct(torch.zeros(sc.data_shape, dtype=torch.complex64))
