@@ -76,27 +76,32 @@ __global__ void __launch_bounds__(nt_for(NX))
     const float *ap = v.apose + (size_t)f * v.P + (size_t)iy * v.npx;
     const float bp = v.bpair[f * v.npair + pr];
     const int jx = v.jx[pr];
+    // issue every load of this pair before consuming any (memory-level
+    // parallelism: E independent 8-byte loads per thread in flight)
+    float2 val[E];
+    float bet[E];
 #pragma unroll
     for (int e = 0; e < E; ++e) {
       const int item = tid + e * NT;
-      if (ITEMS % NT != 0 && item >= ITEMS) continue;
       const int kk = item & (KC - 1);
       const int vx = item >> 4;
       int ix = vx - jx;
       if (ix < 0) ix += NX;
-      const int k = kbase + kk;
-      if (ix < v.npx && k < v.nk) {
-        const float2 val = __ldcs(srow + (size_t)ix * v.nk + k);
-        if (v.no_comp) {
-          acc[e] = cadd(acc[e], val);
-        } else {
-          const float beta = __ldg(ap + ix) + bp;
-          float turns = beta * kt[e];
-          turns -= rintf(turns);
-          float sn, cs;
-          __sincosf(turns * 6.28318530717958647692f, &sn, &cs);
-          acc[e] = cadd(acc[e], cmul(val, make_float2(cs, sn)));
-        }
+      const bool ok = (ITEMS % NT == 0 || item < ITEMS) && ix < v.npx && kbase + kk < v.nk;
+      val[e] = ok ? __ldcs(srow + (size_t)ix * v.nk + (kbase + kk)) : make_float2(0.f, 0.f);
+      bet[e] = ok ? __ldg(ap + ix) : 0.f;
+    }
+    if (v.no_comp) {
+#pragma unroll
+      for (int e = 0; e < E; ++e) acc[e] = cadd(acc[e], val[e]);
+    } else {
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        float turns = (bet[e] + bp) * kt[e];
+        turns -= rintf(turns);
+        float sn, cs;
+        __sincosf(turns * 6.28318530717958647692f, &sn, &cs);
+        acc[e] = cadd(acc[e], cmul(val[e], make_float2(cs, sn)));
       }
     }
   }
@@ -157,11 +162,19 @@ __global__ void __launch_bounds__(nt_for(N))
 }
 
 // ---------------------------------------------------------------- K3 ------
-// Stolt pull index (readings R4, R5, R9).  fp64 with a fixed operation order
-// and no contraction, identical to oracle.stolt_index_table:
-//   ks = kz*kz + kr2;  kk = 0.5*sqrt(ks);  u = (kk - k0)/dk
-__device__ __forceinline__ bool stolt_pull(double kzj, double kr2, double k0, double dk, int nk,
-                                           int *i0, double *tau) {
+// Stolt pull index (readings R4, R5, R9).  The decisions (in band? which
+// interval?) must equal oracle.stolt_index_table bit for bit, which evaluates
+// in fp64 without contraction
+//   ks = kz*kz + kr2;  kk = 0.5*sqrt(ks);  u = (kk - k0)/dk.
+// stolt_pull_exact does exactly that (IEEE sqrt/div intrinsics).  The fast
+// path computes u with one fp32 rsqrt + one fp64 Newton step (relative error
+// <= 1.5 e^2 ~ 1e-13 for the ~2^-22 rsqrt seed) and a multiplication by 1/dk;
+// whenever that estimate lies within `delta` (100x its error bound, >= 1e-7,
+// set by the plan) of a decision boundary -- a band edge or an integer -- the
+// exact sequence decides, so the decisions are identical to the exact path
+// everywhere and tau differs by far less than its fp32 rounding.
+__device__ __forceinline__ bool stolt_pull_exact(double kzj, double kr2, double k0, double dk, int nk,
+                                                 int *i0, double *tau) {
   if (!(kzj > 0.0)) return false;
   const double ks = __dadd_rn(__dmul_rn(kzj, kzj), kr2);
   const double kk = __dmul_rn(0.5, __dsqrt_rn(ks));
@@ -173,6 +186,25 @@ __device__ __forceinline__ bool stolt_pull(double kzj, double kr2, double k0, do
   if (i > nk - 2) i = nk - 2;
   *i0 = i;
   *tau = __dsub_rn(uc, (double)i);
+  return true;
+}
+
+// sqrt(x) for x > 0 to ~1e-15 relative: fp32 rsqrt seed + one Newton step in fp64
+__device__ __forceinline__ double fast_dsqrt(double x) {
+  const double y = (double)rsqrtf((float)x);
+  const double s0 = x * y;
+  return fma(0.5 * y, fma(-s0, s0, x), s0);
+}
+
+__device__ __forceinline__ bool stolt_pull(double kzj, double kr2, double k0, double inv_dk, double dk, int nk,
+                                           double delta, int *i0, double *tau) {
+  if (!(kzj > 0.0)) return false;
+  const double u = (0.5 * fast_dsqrt(fma(kzj, kzj, kr2)) - k0) * inv_dk;
+  const double fl = floor(u);
+  const bool near = u < delta || u > (double)(nk - 1) - delta || (u - fl) < delta || (u - fl) > 1.0 - delta;
+  if (near) return stolt_pull_exact(kzj, kr2, k0, dk, nk, i0, tau);
+  *i0 = (int)fl;
+  *tau = u - fl;
   return true;
 }
 
@@ -205,25 +237,27 @@ __global__ void __launch_bounds__(K3_NT) k3_filter_stolt(const SarDeviceView v) 
   const float2 *src = v.w0 + ((size_t)f * ncol + col0) * (size_t)nk;
   const int ncc = min(K3_CC, ncol - col0);
   // 1. load + filter H = k_z exp(+j k_z R_ref) / P(f) on the source grid
-  for (int idx = tid; idx < K3_CC * nk; idx += K3_NT) {
-    const int c = idx / nk, i = idx - c * nk;
-    float2 val = make_float2(0.f, 0.f);
-    if (c < ncc) {
-      const double ki = v.k[i];
-      const double q = __dsub_rn(__dmul_rn(__dmul_rn(4.0, ki), ki), kr2s[c]);
-      if (q > 0.0) {
-        const double kz = __dsqrt_rn(q);
-        double turns = kz * rref * (1.0 / TWO_PI);
-        turns -= rint(turns);
-        float sn, cs;
-        __sincosf((float)turns * 6.28318530717958647692f, &sn, &cs);
-        const float kzf = (float)kz;
-        float2 h = make_float2(kzf * cs, kzf * sn);
-        if (v.pinv) h = cmul(h, v.pinv[i]);
-        val = cmul(__ldcs(src + idx), h);
+  for (int c = 0; c < K3_CC; ++c) {
+    const double kr2 = kr2s[c];
+    for (int i = tid; i < nk; i += K3_NT) {
+      float2 val = make_float2(0.f, 0.f);
+      if (c < ncc) {
+        const double ki = v.k[i];
+        const double q = 4.0 * ki * ki - kr2;
+        if (q > 0.0) {
+          const double kz = fast_dsqrt(q);
+          double turns = kz * rref * (1.0 / TWO_PI);
+          turns -= rint(turns);
+          float sn, cs;
+          __sincosf((float)turns * 6.28318530717958647692f, &sn, &cs);
+          const float kzf = (float)kz;
+          float2 h = make_float2(kzf * cs, kzf * sn);
+          if (v.pinv) h = cmul(h, v.pinv[i]);
+          val = cmul(__ldcs(src + (size_t)c * nk + i), h);
+        }
       }
+      fin[i * K3_LD + c] = val;
     }
-    fin[i * K3_LD + c] = val;
   }
   __syncthreads();
   // 2. Stolt pull onto the uniform k_z grid
@@ -232,7 +266,7 @@ __global__ void __launch_bounds__(K3_NT) k3_filter_stolt(const SarDeviceView v) 
     int i0;
     double tau;
     float2 o = make_float2(0.f, 0.f);
-    if (stolt_pull(v.kz[j], kr2s[c], v.k0, v.dk, nk, &i0, &tau)) {
+    if (stolt_pull(v.kz[j], kr2s[c], v.k0, v.inv_dk, v.dk, nk, v.stolt_delta, &i0, &tau)) {
       const float t = (float)tau;
       const float2 lo = fin[i0 * K3_LD + c], hi = fin[(i0 + 1) * K3_LD + c];
       o = make_float2(fmaf(t, hi.x - lo.x, lo.x), fmaf(t, hi.y - lo.y, lo.y));
@@ -258,7 +292,8 @@ __global__ void k_stolt_index(const SarDeviceView v, const int32_t *__restrict__
   const int a = cols[2 * c], b = cols[2 * c + 1];
   int i0;
   double tau;
-  if (a >= 0 && a < v.nx && b >= 0 && b < v.ny && stolt_pull(v.kz[j], kr2_of(v, a, b), v.k0, v.dk, v.nk, &i0, &tau)) {
+  if (a >= 0 && a < v.nx && b >= 0 && b < v.ny &&
+      stolt_pull(v.kz[j], kr2_of(v, a, b), v.k0, v.inv_dk, v.dk, v.nk, v.stolt_delta, &i0, &tau)) {
     i0_out[idx] = i0;
     tau_out[idx] = (float)tau;
   } else {

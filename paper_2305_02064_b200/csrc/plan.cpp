@@ -372,6 +372,13 @@ int sar_plan_create(sar_plan **out, const sar_geom_desc *g, const sar_image_desc
   v.tw_z = (const float2 *)(base + o_tw) + T.tw_z_off;
   v.k0 = T.k0;
   v.dk = T.dk;
+  v.inv_dk = 1.0 / T.dk;
+  {
+    // |u_fast - u| <= (2e-13 * kk + 4 ulp(u)) / dk with kk <= k_max (fast_dsqrt bound)
+    const double kmax = T.kd.back();
+    const double err = (2e-13 * kmax) / T.dk + 4.0 * 2.220446049250313e-16 * (double)nk;
+    v.stolt_delta = std::max(1e-7, 100.0 * err);
+  }
   v.img_scale = (float)(1.0 / ((double)p->nx * p->ny * p->nz));
   v.w0 = p->d_w0;
   v.w1 = p->d_w1;

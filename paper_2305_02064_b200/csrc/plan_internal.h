@@ -30,7 +30,8 @@ struct SarDeviceView {
   const float2 *tw_x;   // [nx] exp(-2 pi i m/nx)
   const float2 *tw_y;   // [ny]
   const float2 *tw_z;   // [nz]
-  double k0, dk;
+  double k0, dk, inv_dk;
+  double stolt_delta;   // decision guard band of the fast Stolt path (kernels.cu)
   float img_scale;      // 1/(nx ny nz)
   float2 *w0;           // [F][ny][nx][nk]  planar lattice -> spectrum
   float2 *w1;           // [F][ny][nx][nz]  Stolt output -> partial inverse

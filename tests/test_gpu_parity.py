@@ -40,18 +40,18 @@ def _data(sc, gpu_gen=None):
     if gpu_gen is None:
         gpu_gen = sc.n_samples * max(len(q) for q in sc.scat_pos) > 5e8
     if gpu_gen:
-        import scenes.gpu
-        d = scenes.gpu.synthesize_gpu(sc)
+        from scenes import gpu as sgpu
+        d = sgpu.synthesize_gpu(sc)
         return d, d.cpu().numpy()
     s = scenes.synthesize_cpu(sc)
     return torch.from_numpy(s).cuda(), s
 
 
 def test_gpu_generator_matches_cpu():
-    import scenes.gpu
+    from scenes import gpu as sgpu
     for name in ("tiny", "small"):
         sc = scenes.make_scene(name)
-        a = scenes.gpu.synthesize_gpu(sc).cpu().numpy()
+        a = sgpu.synthesize_gpu(sc).cpu().numpy()
         b = scenes.synthesize_cpu(sc)
         e2, _ = errs(a, b)
         assert e2 < 2e-6, (name, e2)
