@@ -80,13 +80,25 @@ __device__ __forceinline__ void dft(float2 *v) {
   else dft2<DIR>(v);
 }
 
+// Block barrier: BARID 0 = __syncthreads(); otherwise a named barrier over the
+// NT threads that run the transform (warp-specialised kernels keep their
+// producer warp out of it).
+template <int BARID, int NT>
+__device__ __forceinline__ void tile_sync() {
+  if constexpr (BARID == 0) {
+    __syncthreads();
+  } else {
+    asm volatile("bar.sync %0, %1;" ::"n"(BARID), "n"(NT) : "memory");
+  }
+}
+
 template <int REM>
 struct radix_for {
   static constexpr int value = (REM % 8 == 0 && REM != 16) ? 8 : (REM % 4 == 0 ? 4 : 2);
 };
 
 // One Stockham pass.  NT threads, tid in [0, NT).
-template <int N, int C, int LD, int NT, int DIR, int R, int P>
+template <int N, int C, int LD, int NT, int DIR, int R, int P, int BARID>
 __device__ __forceinline__ void stockham_pass(float2 *x, const float2 *__restrict__ tw, int tid) {
   constexpr int NR = N / R;
   constexpr int ITEMS = C * NR;              // butterflies in the tile
@@ -101,7 +113,7 @@ __device__ __forceinline__ void stockham_pass(float2 *x, const float2 *__restric
       for (int r = 0; r < R; ++r) v[it][r] = x[(i + r * NR) * LD + c];
     }
   }
-  __syncthreads();
+  tile_sync<BARID, NT>();
 #pragma unroll
   for (int it = 0; it < IT; ++it) {
     const int item = tid + it * NT;
@@ -123,24 +135,24 @@ __device__ __forceinline__ void stockham_pass(float2 *x, const float2 *__restric
       for (int r = 0; r < R; ++r) x[(j + r * P) * LD + c] = v[it][r];
     }
   }
-  __syncthreads();
+  tile_sync<BARID, NT>();
 }
 
-template <int N, int C, int LD, int NT, int DIR, int P>
+template <int N, int C, int LD, int NT, int DIR, int P, int BARID>
 __device__ __forceinline__ void fft_passes(float2 *x, const float2 *__restrict__ tw, int tid) {
   if constexpr (P < N) {
     constexpr int R = radix_for<N / P>::value;
-    stockham_pass<N, C, LD, NT, DIR, R, P>(x, tw, tid);
-    fft_passes<N, C, LD, NT, DIR, P * R>(x, tw, tid);
+    stockham_pass<N, C, LD, NT, DIR, R, P, BARID>(x, tw, tid);
+    fft_passes<N, C, LD, NT, DIR, P * R, BARID>(x, tw, tid);
   }
 }
 
 // In-place FFT of the C columns of tile x (length N, row stride LD).  Must be
-// called by all NT threads of the block; ends with a __syncthreads().
-template <int N, int C, int LD, int NT, int DIR>
+// called by all NT threads (tid in [0, NT)); ends with a barrier.
+template <int N, int C, int LD, int NT, int DIR, int BARID = 0>
 __device__ __forceinline__ void tile_fft(float2 *x, const float2 *__restrict__ tw, int tid) {
   static_assert((N & (N - 1)) == 0 && N >= 2, "power-of-two length");
-  fft_passes<N, C, LD, NT, DIR, 1>(x, tw, tid);
+  fft_passes<N, C, LD, NT, DIR, 1, BARID>(x, tw, tid);
 }
 
 }  // namespace sarfft

@@ -22,9 +22,11 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <stdlib.h>
 #include <string>
 
 #include "fft_tile.cuh"
+#include "tma.cuh"
 #include "plan_internal.h"
 
 using sarfft::cadd;
@@ -37,6 +39,9 @@ constexpr double TWO_PI = 6.283185307179586476925286766559;
 constexpr double BAND_EPS = 1e-9;  // reading R9
 
 constexpr int nt_for(int n) { return n <= 32 ? 32 : (n < 512 ? n : 512); }
+// resident CTAs requested per SM: 1024 threads' worth (caps registers at 64 per
+// thread) except for the 1024-point tiles, whose 32 elements per thread need more
+constexpr int minb_for(int n) { return n >= 1024 ? 1 : 1024 / nt_for(n); }
 
 // ---------------------------------------------------------------- K1 ------
 // One CTA = (k chunk, virtual row vy, frame f).  Thread item e covers
@@ -46,7 +51,7 @@ constexpr int nt_for(int n) { return n <= 32 ? 32 : (n < 512 ? n : 512); }
 // k_i beta / (2 pi) = kturn_i * (apose_p + bpair_tr), reduced to [-1/2, 1/2]
 // before the SFU sincos (|k beta| reaches tens of radians).
 template <int NX, bool DO_FFT>
-__global__ void __launch_bounds__(nt_for(NX))
+__global__ void __launch_bounds__(nt_for(NX), minb_for(NX))
     k1_correct_xfft(const SarDeviceView v, const float2 *__restrict__ s) {
   constexpr int NT = nt_for(NX);
   constexpr int ITEMS = NX * KC;
@@ -57,14 +62,11 @@ __global__ void __launch_bounds__(nt_for(NX))
   const int vy = blockIdx.y;
   const int f = blockIdx.z;
 
+  static_assert(NT % KC == 0, "k lane of a thread is fixed: kk = tid % 16");
   float2 acc[E];
-  float kt[E];
 #pragma unroll
-  for (int e = 0; e < E; ++e) {
-    acc[e] = make_float2(0.f, 0.f);
-    const int k = kbase + ((tid + e * NT) & (KC - 1));
-    kt[e] = k < v.nk ? __ldg(v.kturn + k) : 0.f;
-  }
+  for (int e = 0; e < E; ++e) acc[e] = make_float2(0.f, 0.f);
+  const float kt = kbase + (tid & (KC - 1)) < v.nk ? __ldg(v.kturn + kbase + (tid & (KC - 1))) : 0.f;
 
   for (int pr = 0; pr < v.npair; ++pr) {
     int iy = vy - v.jy[pr];
@@ -76,32 +78,36 @@ __global__ void __launch_bounds__(nt_for(NX))
     const float *ap = v.apose + (size_t)f * v.P + (size_t)iy * v.npx;
     const float bp = v.bpair[f * v.npair + pr];
     const int jx = v.jx[pr];
-    // issue every load of this pair before consuming any (memory-level
-    // parallelism: E independent 8-byte loads per thread in flight)
-    float2 val[E];
-    float bet[E];
+    // issue a batch of EB independent loads before consuming any (memory-level
+    // parallelism without holding all E samples in registers)
+    constexpr int EB = E < 8 ? E : 8;
 #pragma unroll
-    for (int e = 0; e < E; ++e) {
-      const int item = tid + e * NT;
-      const int kk = item & (KC - 1);
-      const int vx = item >> 4;
-      int ix = vx - jx;
-      if (ix < 0) ix += NX;
-      const bool ok = (ITEMS % NT == 0 || item < ITEMS) && ix < v.npx && kbase + kk < v.nk;
-      val[e] = ok ? __ldcs(srow + (size_t)ix * v.nk + (kbase + kk)) : make_float2(0.f, 0.f);
-      bet[e] = ok ? __ldg(ap + ix) : 0.f;
-    }
-    if (v.no_comp) {
+    for (int e0 = 0; e0 < E; e0 += EB) {
+      float2 val[EB];
+      float bet[EB];
 #pragma unroll
-      for (int e = 0; e < E; ++e) acc[e] = cadd(acc[e], val[e]);
-    } else {
+      for (int u = 0; u < EB; ++u) {
+        const int item = tid + (e0 + u) * NT;
+        const int kk = item & (KC - 1);
+        const int vx = item >> 4;
+        int ix = vx - jx;
+        if (ix < 0) ix += NX;
+        const bool ok = (ITEMS % NT == 0 || item < ITEMS) && ix < v.npx && kbase + kk < v.nk;
+        val[u] = ok ? __ldcs(srow + (size_t)ix * v.nk + (kbase + kk)) : make_float2(0.f, 0.f);
+        bet[u] = ok ? __ldg(ap + ix) : 0.f;
+      }
+      if (v.no_comp) {
 #pragma unroll
-      for (int e = 0; e < E; ++e) {
-        float turns = (bet[e] + bp) * kt[e];
-        turns -= rintf(turns);
-        float sn, cs;
-        __sincosf(turns * 6.28318530717958647692f, &sn, &cs);
-        acc[e] = cadd(acc[e], cmul(val[e], make_float2(cs, sn)));
+        for (int u = 0; u < EB; ++u) acc[e0 + u] = cadd(acc[e0 + u], val[u]);
+      } else {
+#pragma unroll
+        for (int u = 0; u < EB; ++u) {
+          float turns = (bet[u] + bp) * kt;
+          turns -= rintf(turns);
+          float sn, cs;
+          __sincosf(turns * 6.28318530717958647692f, &sn, &cs);
+          acc[e0 + u] = cadd(acc[e0 + u], cmul(val[u], make_float2(cs, sn)));
+        }
       }
     }
   }
@@ -125,11 +131,217 @@ __global__ void __launch_bounds__(nt_for(NX))
   }
 }
 
+// Persistent, TMA-pipelined K1 (used when n_k is even, npx % 4 == 0 and the
+// step phasor below is accurate).  One CTA (1024 threads) per SM walks a flat
+// sequence of "jobs" = (work item (frame, vy, k chunk of K1C), valid pair, box
+// of up to br pose rows).  Thread 0 keeps K1_STAGES jobs in flight: one 2-D
+// TMA box of raw samples [br poses][K1C k] (32 KB) plus the matching [br]
+// slice of the -2 d_z table, completing on the stage's mbarrier.  The chunk
+// width K1C = 8192/NX keeps the [NX][K1C] x-FFT tile at 64 KB.
+// Each thread owns one pose row of the box and 4 consecutive k: the rotation
+// exp(j k_i beta) of the first comes from the SFU (phase reduced in turns),
+// the next three from multiplying by the step exp(j dk beta), evaluated as its
+// 5th-order Taylor polynomial (|dk beta| <= 0.25 is checked by the plan, so
+// the truncation error is < 4e-7).  Complex arithmetic uses the sm_100 paired
+// fp32 instructions (__ffma2_rn / __fmul2_rn).
+// REGACC (all j^x offsets 0, e.g. a linear Tx/Rx column along y): each thread
+// always owns the same (vx, k) elements, so sums stay in registers; otherwise
+// they accumulate in the shared tile (one owner per element per job).
+constexpr int K1_STAGES = 4;
+constexpr int K1_BOX_BYTES = 32768;
+constexpr int K1_NT = 512;   // consumer threads (+1 producer warp)
+constexpr int K1_KT = 4;  // consecutive k per thread
+
+constexpr int k1c_for(int nx) { return nx >= 512 ? 16 : (nx == 256 ? 32 : 64); }
+
+struct K1Job {
+  int item, pr, b;
+};
+
+__device__ __forceinline__ bool k1_pair_valid(const SarDeviceView &v, int vy, int pr) {
+  int iy = vy - v.jy[pr];
+  if (iy < 0) iy += v.ny;
+  return iy < v.npy;
+}
+
+// advance j to the next job of this CTA (item stride = gridDim.x); false at the end
+__device__ __forceinline__ bool k1_next(const SarDeviceView &v, K1Job &j, int nitems, int nchunk, int nbox) {
+  if (++j.b < nbox) return true;
+  j.b = 0;
+  for (;;) {
+    const int vy = (j.item / nchunk) % v.ny;
+    while (++j.pr < v.npair)
+      if (k1_pair_valid(v, vy, j.pr)) return true;
+    j.item += gridDim.x;
+    j.pr = -1;
+    if (j.item >= nitems) return false;
+  }
+}
+
+// acc += a * b (complex), two paired-fp32 FMAs
+__device__ __forceinline__ float2 cmac2(float2 acc, float2 a, float2 b) {
+  acc = __ffma2_rn(make_float2(a.x, a.x), b, acc);
+  return __ffma2_rn(make_float2(-a.y, a.y), make_float2(b.y, b.x), acc);
+}
+__device__ __forceinline__ float2 cmul2(float2 a, float2 b) {
+  return __ffma2_rn(make_float2(a.x, a.x), b, __fmul2_rn(make_float2(-a.y, a.y), make_float2(b.y, b.x)));
+}
+
+template <int NX, bool REGACC>
+__global__ void __launch_bounds__(K1_NT + 32, 1)
+    k1_correct_xfft_tma(const SarDeviceView v, const __grid_constant__ CUtensorMap tm_s,
+                        const __grid_constant__ CUtensorMap tm_ap, int br, int nbox, int nitems) {
+  constexpr int C = k1c_for(NX);
+  constexpr int BRMAX = K1_BOX_BYTES / (C * 8);
+  constexpr int TPR = C / K1_KT;                 // consumer threads per box row
+  constexpr int RPP = K1_NT / TPR;               // box rows per consumer pass
+  constexpr int UPB = BRMAX / RPP;               // box rows per consumer thread
+  constexpr int MAXB = NX / BRMAX > 0 ? NX / BRMAX : 1;  // boxes per pose row (<= 2)
+  constexpr int NWARP = K1_NT / 32;
+  extern __shared__ __align__(128) unsigned char smraw[];
+  float2 *tile = reinterpret_cast<float2 *>(smraw);                       // [NX][C]
+  unsigned char *stages = smraw + (size_t)NX * C * sizeof(float2);
+  constexpr size_t STAGE = K1_BOX_BYTES + BRMAX * sizeof(float);
+  __shared__ __align__(8) uint64_t full[K1_STAGES], empty[K1_STAGES];
+  const int tid = threadIdx.x;
+  const int nchunk = (v.nk + C - 1) / C;
+  if (tid == 0) {
+    for (int i = 0; i < K1_STAGES; ++i) {
+      sartma::mbar_init(&full[i], 1);
+      sartma::mbar_init(&empty[i], NWARP);
+    }
+    sartma::fence_barrier_init();
+  }
+  if (!REGACC)
+    for (int i = tid; i < NX * C; i += K1_NT + 32) tile[i] = make_float2(0.f, 0.f);
+  __syncthreads();
+
+  if (tid >= K1_NT) {
+    // ---------------- producer warp: one elected lane issues every TMA ----------------
+    if (tid == K1_NT) {
+      const uint32_t tx_bytes = (uint32_t)(br * C * sizeof(float2) + br * sizeof(float));
+      K1Job j{(int)blockIdx.x, -1, nbox - 1};
+      if (j.item < nitems) {
+        unsigned n = 0;
+        for (bool more = k1_next(v, j, nitems, nchunk, nbox); more; more = k1_next(v, j, nitems, nchunk, nbox), ++n) {
+          const int st = n % K1_STAGES;
+          if (n >= K1_STAGES) sartma::mbar_wait(&empty[st], ((n / K1_STAGES) - 1) & 1);
+          const int kc = j.item % nchunk, rest = j.item / nchunk;
+          const int vy = rest % v.ny, f = rest / v.ny;
+          int iy = vy - v.jy[j.pr];
+          if (iy < 0) iy += v.ny;
+          const int t = j.pr / v.nr, r = j.pr - t * v.nr;
+          const long long row = ((long long)(f * v.nt + t) * v.nr + r) * v.P + (long long)iy * v.npx + j.b * br;
+          unsigned char *sb = stages + st * STAGE;
+          sartma::mbar_arrive_expect_tx(&full[st], tx_bytes);
+          sartma::tma_load_2d(sb, &tm_s, kc * C, (int)row, &full[st]);
+          sartma::tma_load_2d(sb + K1_BOX_BYTES, &tm_ap, j.b * br, f * v.npy + iy, &full[st]);
+        }
+      }
+    }
+    return;
+  }
+
+  // ---------------- consumers: 512 threads ----------------
+  const int kq = (tid % TPR) * K1_KT;   // first of this thread's 4 k within the chunk
+  const int r0 = tid / TPR;            // first of this thread's box rows
+  const int lane = tid & 31, warp = tid >> 5;
+  const float dkt = (float)(v.dk);
+  unsigned jobctr = 0;
+  for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
+    const int kc = item % nchunk, rest = item / nchunk;
+    const int vy = rest % v.ny, f = rest / v.ny;
+    const int k0 = kc * C + kq;
+    const float kt = k0 < v.nk ? __ldg(v.kturn + k0) : 0.f;
+    float2 acc[REGACC ? MAXB * UPB * K1_KT : 1];
+#pragma unroll
+    for (int u = 0; u < (REGACC ? MAXB * UPB * K1_KT : 1); ++u) acc[u] = make_float2(0.f, 0.f);
+    for (int pr = 0; pr < v.npair; ++pr) {
+      if (!k1_pair_valid(v, vy, pr)) continue;
+      const float bp = v.bpair[f * v.npair + pr];
+      const int jx = v.jx[pr];
+#pragma unroll
+      for (int b = 0; b < MAXB; ++b) {
+        if (b >= nbox) break;
+        const int st = jobctr % K1_STAGES;
+        sartma::mbar_wait(&full[st], (jobctr / K1_STAGES) & 1);
+        ++jobctr;
+        const float2 *sv = reinterpret_cast<const float2 *>(stages + st * STAGE);
+        const float *sap = reinterpret_cast<const float *>(stages + st * STAGE + K1_BOX_BYTES);
+#pragma unroll
+        for (int w = 0; w < UPB; ++w) {
+          const int il = r0 + w * RPP;
+          const int ix = b * br + il;
+          if (il < br && ix < v.npx) {
+            const float4 v01 = *reinterpret_cast<const float4 *>(sv + il * C + kq);
+            const float4 v23 = *reinterpret_cast<const float4 *>(sv + il * C + kq + 2);
+            float2 val[4] = {make_float2(v01.x, v01.y), make_float2(v01.z, v01.w), make_float2(v23.x, v23.y),
+                             make_float2(v23.z, v23.w)};
+            if (!v.no_comp) {
+              const float beta = sap[il] + bp;
+              float turns = beta * kt;
+              turns -= rintf(turns);
+              float2 rot;
+              __sincosf(turns * 6.28318530717958647692f, &rot.y, &rot.x);
+              const float x = dkt * beta, x2 = x * x;
+              const float2 step = make_float2(fmaf(x2, fmaf(x2, 1.f / 24.f, -0.5f), 1.f),
+                                              x * fmaf(x2, fmaf(x2, 1.f / 120.f, -1.f / 6.f), 1.f));
+#pragma unroll
+              for (int u = 0; u < K1_KT; ++u) {
+                val[u] = cmul2(val[u], rot);
+                if (u + 1 < K1_KT) rot = cmul2(rot, step);
+              }
+            }
+            if constexpr (REGACC) {
+#pragma unroll
+              for (int u = 0; u < K1_KT; ++u)
+                acc[(b * UPB + w) * K1_KT + u] = __fadd2_rn(acc[(b * UPB + w) * K1_KT + u], val[u]);
+            } else {
+              int vx = ix + jx;
+              if (vx >= NX) vx -= NX;
+              float2 *t = tile + vx * C + kq;
+#pragma unroll
+              for (int u = 0; u < K1_KT; ++u) t[u] = __fadd2_rn(t[u], val[u]);
+            }
+          }
+        }
+        __syncwarp();
+        if (lane == 0) sartma::mbar_arrive(&empty[st]);
+        if (!REGACC) sarfft::tile_sync<1, K1_NT>();  // tile updates of this job complete
+      }
+    }
+    if constexpr (REGACC) {
+      // vx = ix for every pair: scatter the register sums into the tile
+#pragma unroll
+      for (int b = 0; b < MAXB; ++b)
+#pragma unroll
+        for (int w = 0; w < UPB; ++w) {
+          const int il = r0 + w * RPP;
+          const int ix = b * br + il;
+          if (b < nbox && il < br && ix < NX)
+#pragma unroll
+            for (int u = 0; u < K1_KT; ++u) tile[ix * C + kq + u] = acc[(b * UPB + w) * K1_KT + u];
+        }
+      // rows not covered by any box (npx < NX) are zero
+      for (int i = nbox * br * C + tid; i < NX * C; i += K1_NT) tile[i] = make_float2(0.f, 0.f);
+    }
+    sarfft::tile_sync<1, K1_NT>();
+    sarfft::tile_fft<NX, C, C, K1_NT, -1, 1>(tile, v.tw_x, tid);
+    float2 *out = v.w0 + ((size_t)(f * v.ny + vy) * NX) * (size_t)v.nk;
+    for (int i = tid; i < NX * C; i += K1_NT) {
+      const int vx = i / C, kk = kc * C + (i % C);
+      if (kk < v.nk) out[(size_t)vx * v.nk + kk] = tile[i];
+      if (!REGACC) tile[i] = make_float2(0.f, 0.f);
+    }
+    sarfft::tile_sync<1, K1_NT>();
+  }
+}
+
 // ------------------------------------------------------------ K2 / K4a ----
 // FFT along the middle (y) axis of a [F][N][nx][inner] complex volume for one
 // (chunk of 16 along `inner`, column a, frame f).
 template <int N, int DIR>
-__global__ void __launch_bounds__(nt_for(N))
+__global__ void __launch_bounds__(nt_for(N), minb_for(N))
     k_fft_mid(float2 *__restrict__ data, const float2 *__restrict__ tw, int nx, int inner) {
   constexpr int NT = nt_for(N);
   constexpr int ITEMS = N * KC;
@@ -159,6 +371,64 @@ __global__ void __launch_bounds__(nt_for(N))
     const int c = cbase + cc;
     if (c < inner) base[b * row + c] = tile[item];
   }
+}
+
+// Persistent, TMA-pipelined variant of k_fft_mid (used when `inner` is even,
+// i.e. the rows are 16-byte aligned).  One CTA per SM loops over work items
+// (chunk, column a, frame); the [N][16] tile of item i+1 is in flight
+// (cp.async.bulk.tensor, mbarrier completion) while item i is transformed,
+// and finished tiles go back with TMA stores, so the SM's load queue never
+// drains between tiles.  Box = {16 inner elements, 1 column, <=256 rows}.
+template <int N, int DIR>
+__global__ void __launch_bounds__(nt_for(N), 1)
+    k_fft_mid_tma(const __grid_constant__ CUtensorMap tm, const float2 *__restrict__ tw, int nx, int nchunk,
+                  int nitems) {
+  constexpr int NT = nt_for(N);
+  constexpr int ROWS = N < 256 ? N : 256;
+  constexpr int NBOX = N / ROWS;
+  constexpr uint32_t TILE_BYTES = N * KC * sizeof(float2);
+  extern __shared__ __align__(128) float2 smt[];  // [2][N][16]
+  __shared__ __align__(8) uint64_t full[2];
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    sartma::mbar_init(&full[0], 1);
+    sartma::mbar_init(&full[1], 1);
+    sartma::fence_barrier_init();
+  }
+  __syncthreads();
+  auto issue = [&](int item, int st) {
+    const int chunk = item % nchunk, rest = item / nchunk;
+    const int a = rest % nx, f = rest / nx;
+    sartma::mbar_arrive_expect_tx(&full[st], TILE_BYTES);
+#pragma unroll
+    for (int bx = 0; bx < NBOX; ++bx)
+      sartma::tma_load_3d(smt + (size_t)st * N * KC + bx * ROWS * KC, &tm, chunk * KC, a, f * N + bx * ROWS,
+                          &full[st]);
+  };
+  int item = blockIdx.x;
+  if (tid == 0 && item < nitems) issue(item, 0);
+  for (int it = 0; item < nitems; ++it, item += gridDim.x) {
+    const int st = it & 1;
+    const int next = item + gridDim.x;
+    if (tid == 0 && next < nitems) {
+      sartma::bulk_wait_read0();  // the store of stage st^1 has left shared memory
+      issue(next, st ^ 1);
+    }
+    sartma::mbar_wait(&full[st], (it >> 1) & 1);
+    float2 *tile = smt + (size_t)st * N * KC;
+    sarfft::tile_fft<N, KC, KC, NT, DIR>(tile, tw, tid);
+    sartma::fence_proxy_async();
+    __syncthreads();
+    if (tid == 0) {
+      const int chunk = item % nchunk, rest = item / nchunk;
+      const int a = rest % nx, f = rest / nx;
+#pragma unroll
+      for (int bx = 0; bx < NBOX; ++bx)
+        sartma::tma_store_3d(&tm, chunk * KC, a, f * N + bx * ROWS, tile + bx * ROWS * KC);
+      sartma::bulk_commit();
+    }
+  }
+  if (tid == 0) sartma::bulk_wait0();
 }
 
 // ---------------------------------------------------------------- K3 ------
@@ -213,74 +483,124 @@ __device__ __forceinline__ double kr2_of(const SarDeviceView &v, int a, int b) {
   return __dadd_rn(__dmul_rn(kx, kx), __dmul_rn(ky, ky));
 }
 
-constexpr int K3_CC = 8;              // columns per CTA
-constexpr int K3_LD = K3_CC + 1;      // padded row stride of the [n][CC] tiles
+constexpr int K3_CL = 2;              // mirror classes per CTA
+constexpr int K3_CC = 4 * K3_CL;      // column slots per CTA (<= 4 columns per class)
+constexpr int K3_LD = K3_CC + 1;      // padded row stride of the [NZ][CC] output tile
 constexpr int K3_NT = 256;
 
+// One CTA = 2 "mirror classes" of spectral columns.  k_r^2 = kx^2 + ky^2 is
+// the same for (a,b), (-a,b), (a,-b), (-a,-b), so the filter H(k_r, k_i) and
+// the Stolt pull weights (i0, tau)(k_r, j) -- the fp64 part of the step -- are
+// computed once per class and applied to its (up to 4) columns.  Each
+// column's n_k source samples are contiguous in W0 and arrive by TMA bulk
+// copies (cp.async.bulk + mbarrier) into fin[slot][i].
 template <int NZ, bool DO_IFFT>
 __global__ void __launch_bounds__(K3_NT) k3_filter_stolt(const SarDeviceView v) {
-  extern __shared__ float2 sm[];
-  float2 *fin = sm;                          // [nk][LD]  filtered source spectrum
-  float2 *fout = sm + (size_t)v.nk * K3_LD;  // [NZ][LD]  Stolt output
-  double *kr2s = reinterpret_cast<double *>(fout + (size_t)NZ * K3_LD);  // [CC]
+  extern __shared__ __align__(16) float2 sm[];
+  __shared__ double kr2s[K3_CL];
+  __shared__ int colof[K3_CC];   // column index (b*nx + a) of each slot, -1 = empty
+  __shared__ __align__(8) uint64_t bar;
+  const int nk = v.nk;
+  float2 *fin = sm;                                  // [CC][nk]  source spectrum -> filtered
+  float2 *fout = sm + (size_t)K3_CC * nk;            // [NZ][LD]  Stolt output
   const int tid = threadIdx.x;
   const int ncol = v.nx * v.ny;
-  const int col0 = blockIdx.x * K3_CC;
+  const int hx = v.nx / 2 + 1, hy = v.ny / 2 + 1;
+  const int nclass = hx * hy;
+  const int q0 = blockIdx.x * K3_CL;
   const int f = blockIdx.y;
-  const int nk = v.nk;
+  const float2 *wf = v.w0 + (size_t)f * ncol * (size_t)nk;
+  const bool bulk = (nk & 1) == 0;   // 16-byte aligned columns
   if (tid < K3_CC) {
-    const int col = min(col0 + tid, ncol - 1);
-    kr2s[tid] = kr2_of(v, col % v.nx, col / v.nx);
+    const int cl = tid >> 2, m = tid & 3;
+    const int q = q0 + cl;
+    int col = -1;
+    if (q < nclass) {
+      const int a = q % hx, b = q / hx;
+      const int ma = (v.nx - a) & (v.nx - 1), mb = (v.ny - b) & (v.ny - 1);
+      const bool da = ma != a, db = mb != b;
+      if (m == 0) col = b * v.nx + a;
+      if (m == 1 && da) col = b * v.nx + ma;
+      if (m == 2 && db) col = mb * v.nx + a;
+      if (m == 3 && da && db) col = mb * v.nx + ma;
+      if (m == 0) kr2s[cl] = kr2_of(v, a, b);
+    } else if (m == 0) {
+      kr2s[cl] = 0.0;
+    }
+    colof[tid] = col;
+  }
+  if (tid == 0 && bulk) {
+    sartma::mbar_init(&bar, 1);
+    sartma::fence_barrier_init();
   }
   __syncthreads();
+  // 1. load the member columns
+  if (bulk) {
+    if (tid == 0) {
+      uint32_t bytes = 0;
+      for (int sl = 0; sl < K3_CC; ++sl) bytes += colof[sl] >= 0 ? (uint32_t)nk * 8u : 0u;
+      sartma::mbar_arrive_expect_tx(&bar, bytes);
+      for (int sl = 0; sl < K3_CC; ++sl)
+        if (colof[sl] >= 0) sartma::bulk_g2s(fin + sl * nk, wf + (size_t)colof[sl] * nk, (uint32_t)nk * 8u, &bar);
+    }
+    sartma::mbar_wait(&bar, 0);
+  } else {
+    for (int sl = 0; sl < K3_CC; ++sl)
+      if (colof[sl] >= 0)
+        for (int i = tid; i < nk; i += K3_NT) fin[sl * nk + i] = __ldcs(wf + (size_t)colof[sl] * nk + i);
+    __syncthreads();
+  }
+  // 2. filter H = k_z exp(+j k_z R_ref) / P(f) on the source grid (in place),
+  //    once per class, applied to its columns
   const double rref = v.rref[f];
-  const float2 *src = v.w0 + ((size_t)f * ncol + col0) * (size_t)nk;
-  const int ncc = min(K3_CC, ncol - col0);
-  // 1. load + filter H = k_z exp(+j k_z R_ref) / P(f) on the source grid
-  for (int c = 0; c < K3_CC; ++c) {
-    const double kr2 = kr2s[c];
-    for (int i = tid; i < nk; i += K3_NT) {
-      float2 val = make_float2(0.f, 0.f);
-      if (c < ncc) {
-        const double ki = v.k[i];
-        const double q = 4.0 * ki * ki - kr2;
-        if (q > 0.0) {
-          const double kz = fast_dsqrt(q);
-          double turns = kz * rref * (1.0 / TWO_PI);
-          turns -= rint(turns);
-          float sn, cs;
-          __sincosf((float)turns * 6.28318530717958647692f, &sn, &cs);
-          const float kzf = (float)kz;
-          float2 h = make_float2(kzf * cs, kzf * sn);
-          if (v.pinv) h = cmul(h, v.pinv[i]);
-          val = cmul(__ldcs(src + (size_t)c * nk + i), h);
-        }
+  for (int idx = tid; idx < K3_CL * nk; idx += K3_NT) {
+    const int cl = idx / nk, i = idx - cl * nk;
+    const double ki = v.k[i];
+    const double q = 4.0 * ki * ki - kr2s[cl];
+    float2 h = make_float2(0.f, 0.f);
+    if (q > 0.0) {
+      const double kz = fast_dsqrt(q);
+      double turns = kz * rref * (1.0 / TWO_PI);
+      turns -= rint(turns);
+      float sn, cs;
+      __sincosf((float)turns * 6.28318530717958647692f, &sn, &cs);
+      const float kzf = (float)kz;
+      h = make_float2(kzf * cs, kzf * sn);
+      if (v.pinv) h = cmul(h, v.pinv[i]);
+    }
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+      const int sl = cl * 4 + m;
+      if (colof[sl] >= 0) fin[sl * nk + i] = cmul(fin[sl * nk + i], h);
+    }
+  }
+  __syncthreads();
+  // 3. Stolt pull onto the uniform k_z grid, weights once per class
+  for (int idx = tid; idx < K3_CL * NZ; idx += K3_NT) {
+    const int j = idx % NZ, cl = idx / NZ;
+    int i0 = 0;
+    double tau = 0.0;
+    const bool ok = stolt_pull(v.kz[j], kr2s[cl], v.k0, v.inv_dk, v.dk, nk, v.stolt_delta, &i0, &tau);
+    const float t = (float)tau;
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+      const int sl = cl * 4 + m;
+      float2 o = make_float2(0.f, 0.f);
+      if (ok && colof[sl] >= 0) {
+        const float2 lo = fin[sl * nk + i0], hi = fin[sl * nk + i0 + 1];
+        o = make_float2(fmaf(t, hi.x - lo.x, lo.x), fmaf(t, hi.y - lo.y, lo.y));
       }
-      fin[i * K3_LD + c] = val;
+      fout[j * K3_LD + sl] = o;
     }
   }
   __syncthreads();
-  // 2. Stolt pull onto the uniform k_z grid
-  for (int idx = tid; idx < K3_CC * NZ; idx += K3_NT) {
-    const int c = idx % K3_CC, j = idx / K3_CC;
-    int i0;
-    double tau;
-    float2 o = make_float2(0.f, 0.f);
-    if (stolt_pull(v.kz[j], kr2s[c], v.k0, v.inv_dk, v.dk, nk, v.stolt_delta, &i0, &tau)) {
-      const float t = (float)tau;
-      const float2 lo = fin[i0 * K3_LD + c], hi = fin[(i0 + 1) * K3_LD + c];
-      o = make_float2(fmaf(t, hi.x - lo.x, lo.x), fmaf(t, hi.y - lo.y, lo.y));
-    }
-    fout[j * K3_LD + c] = o;
-  }
-  __syncthreads();
-  // 3. inverse FFT along z
+  // 4. inverse FFT along z
   if constexpr (DO_IFFT) sarfft::tile_fft<NZ, K3_CC, K3_LD, K3_NT, +1>(fout, v.tw_z, tid);
-  // 4. store column-contiguous [col][z]
-  float2 *dst = v.w1 + ((size_t)f * ncol + col0) * (size_t)NZ;
-  for (int idx = tid; idx < ncc * NZ; idx += K3_NT) {
-    const int c = idx / NZ, z = idx - c * NZ;
-    dst[idx] = fout[z * K3_LD + c];
+  // 5. store each column contiguously [col][z]
+  float2 *dst = v.w1 + (size_t)f * ncol * (size_t)NZ;
+  for (int idx = tid; idx < K3_CC * NZ; idx += K3_NT) {
+    const int sl = idx / NZ, z = idx - sl * NZ;
+    if (colof[sl] >= 0) dst[(size_t)colof[sl] * NZ + z] = fout[z * K3_LD + sl];
   }
 }
 
@@ -306,7 +626,7 @@ __global__ void k_stolt_index(const SarDeviceView v, const int32_t *__restrict__
 // One CTA = (z chunk, image row y (pre-roll), frame).  Tile [NX][17]: the odd
 // stride makes both the FFT passes and the transposed read conflict-free.
 template <int NX, bool CPLX>
-__global__ void __launch_bounds__(nt_for(NX))
+__global__ void __launch_bounds__(nt_for(NX), minb_for(NX))
     k4_xifft_mag(const SarDeviceView v, void *__restrict__ img) {
   constexpr int NT = nt_for(NX);
   constexpr int LD = KC + 1;
@@ -368,7 +688,29 @@ cudaError_t launch(K kernel, dim3 grid, int nt, size_t smem, cudaStream_t s, con
   return cudaGetLastError();
 }
 
-cudaError_t launch_k1(const SarDeviceView &v, const float2 *data, bool fft, cudaStream_t s) {
+cudaError_t launch_k1(const SarDeviceView &v, const float2 *data, bool fft, cudaStream_t s,
+                      const CUtensorMap *tm_s, const CUtensorMap *tm_ap, int br, bool regacc, int num_sms) {
+  if (fft && tm_s && tm_ap && v.nx >= 64 && v.nx <= 512 && v.k1_step_ok) {
+    const int C = k1c_for(v.nx);
+    const int nchunk = (v.nk + C - 1) / C;
+    const int nitems = nchunk * v.ny * v.F;
+    const int nbox = (v.npx + br - 1) / br;
+    const int brmax = K1_BOX_BYTES / (C * 8);
+    const size_t smem = (size_t)v.nx * C * sizeof(float2) + K1_STAGES * ((size_t)K1_BOX_BYTES + brmax * sizeof(float));
+    const int grid = nitems < num_sms ? nitems : num_sms;
+    switch (v.nx) {
+#define X(N)                                                                                          \
+  case N: {                                                                                           \
+    auto kern = regacc ? k1_correct_xfft_tma<N, true> : k1_correct_xfft_tma<N, false>;               \
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+    if (e != cudaSuccess) return e;                                                                   \
+    kern<<<grid, K1_NT + 32, smem, s>>>(v, *tm_s, *tm_ap, br, nbox, nitems);                               \
+    return cudaGetLastError();                                                                        \
+  }
+      X(64) X(128) X(256) X(512)
+#undef X
+    }
+  }
   dim3 grid((v.nk + KC - 1) / KC, v.ny, v.F);
   const size_t smem = (size_t)v.nx * KC * sizeof(float2);
   switch (v.nx) {
@@ -383,7 +725,29 @@ cudaError_t launch_k1(const SarDeviceView &v, const float2 *data, bool fft, cuda
 }
 
 template <int DIR>
-cudaError_t launch_mid(float2 *data, const float2 *tw, int F, int ny, int nx, int inner, cudaStream_t s) {
+cudaError_t launch_mid(float2 *data, const float2 *tw, int F, int ny, int nx, int inner, cudaStream_t s,
+                       const CUtensorMap *tm, int num_sms) {
+  if (tm && ny <= 512) {
+    const int nchunk = (inner + KC - 1) / KC;
+    const int nitems = nchunk * nx * F;
+    const size_t smem = 2 * (size_t)ny * KC * sizeof(float2);
+    const int grid = nitems < num_sms ? nitems : num_sms;
+    switch (ny) {
+#define X(N)                                                                                       \
+  case N: {                                                                                        \
+    auto kern = k_fft_mid_tma<N, DIR>;                                                             \
+    if (smem > 48 * 1024) {                                                                        \
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+      if (e != cudaSuccess) return e;                                                              \
+    }                                                                                              \
+    kern<<<grid, nt_for(N), smem, s>>>(*tm, tw, nx, nchunk, nitems);                               \
+    return cudaGetLastError();                                                                     \
+  }
+      SAR_SIZES(X)
+#undef X
+    }
+    return cudaErrorInvalidValue;
+  }
   dim3 grid((inner + KC - 1) / KC, nx, F);
   const size_t smem = (size_t)ny * KC * sizeof(float2);
   switch (ny) {
@@ -414,9 +778,9 @@ cudaError_t launch_v(K kernel, dim3 grid, int nt, size_t smem, cudaStream_t s, c
 }
 
 cudaError_t launch_k3(const SarDeviceView &v, bool ifft, cudaStream_t s) {
-  const int ncol = v.nx * v.ny;
-  dim3 grid((ncol + K3_CC - 1) / K3_CC, v.F);
-  const size_t smem = (size_t)(v.nk + v.nz) * K3_LD * sizeof(float2) + K3_CC * sizeof(double);
+  const int nclass = (v.nx / 2 + 1) * (v.ny / 2 + 1);
+  dim3 grid((nclass + K3_CL - 1) / K3_CL, v.F);
+  const size_t smem = ((size_t)v.nk * K3_CC + (size_t)v.nz * K3_LD) * sizeof(float2);
   switch (v.nz) {
 #define X(N)                                                                           \
   case N:                                                                              \
@@ -471,16 +835,24 @@ int sar_launch_pipeline(sar_plan *p, const void *d_data, void *d_image, cudaStre
     }                                                                         \
   } while (0)
   if (ev) SAR_CHECK(cudaEventRecord(ev[0], s));
-  SAR_CHECK(launch_k1(v, data, stop_stage != 1, s));
+  const CUtensorMap *tm_s = nullptr;
+  if (p->tma_ap) {
+    if (p->tm_s_ptr != d_data) p->tma_s = sar_encode_input_map(p, d_data);
+    if (p->tma_s) tm_s = &p->tm_s;
+  }
+  SAR_CHECK(launch_k1(v, data, stop_stage != 1, s, tm_s, p->tma_ap ? &p->tm_ap : nullptr, p->k1_br, p->k1_regacc,
+                      p->num_sms));
   if (ev) SAR_CHECK(cudaEventRecord(ev[1], s));
   if (stop_stage == 1) return SAR_OK;
-  SAR_CHECK(launch_mid<-1>(v.w0, v.tw_y, v.F, v.ny, v.nx, v.nk, s));
+  SAR_CHECK(launch_mid<-1>(v.w0, v.tw_y, v.F, v.ny, v.nx, v.nk, s, p->tma_mid0 ? &p->tm_w0_mid : nullptr,
+                           p->num_sms));
   if (ev) SAR_CHECK(cudaEventRecord(ev[2], s));
   if (stop_stage == 2) return SAR_OK;
   SAR_CHECK(launch_k3(v, stop_stage != 3, s));
   if (ev) SAR_CHECK(cudaEventRecord(ev[3], s));
   if (stop_stage == 3) return SAR_OK;
-  SAR_CHECK(launch_mid<+1>(v.w1, v.tw_y, v.F, v.ny, v.nx, v.nz, s));
+  SAR_CHECK(launch_mid<+1>(v.w1, v.tw_y, v.F, v.ny, v.nx, v.nz, s, p->tma_mid1 ? &p->tm_w1_mid : nullptr,
+                           p->num_sms));
   if (ev) SAR_CHECK(cudaEventRecord(ev[4], s));
   SAR_CHECK(launch_k4b(v, d_image, complex_out != 0, s));
   if (ev) SAR_CHECK(cudaEventRecord(ev[5], s));
@@ -499,5 +871,86 @@ int sar_launch_stolt_index(sar_plan *p, const int32_t *d_cols, int n, int32_t *d
     sar_set_error(std::string("CUDA: ") + cudaGetErrorString(e));
     return SAR_ERR_CUDA;
   }
+  return SAR_OK;
+}
+
+// ------------------------------------------------------- tensor maps ------
+#include <cudaTypedefs.h>
+
+namespace {
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void *ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+  }
+  return fn;
+}
+
+// 3-D map over a complex64 volume [d2][d1][d0] (d0 fastest), 8-byte elements.
+bool encode3d(CUtensorMap *m, void *base, uint64_t d0, uint64_t d1, uint64_t d2, uint32_t b0, uint32_t b1,
+              uint32_t b2) {
+  auto enc = get_encode();
+  if (!enc) return false;
+  if ((d0 * 8) % 16 != 0 || (reinterpret_cast<uintptr_t>(base) & 15) != 0) return false;
+  cuuint64_t dims[3] = {d0, d1, d2};
+  cuuint64_t strides[2] = {d0 * 8, d0 * d1 * 8};
+  cuuint32_t box[3] = {b0, b1, b2};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+}  // namespace
+
+// 2-D map over a row-major [d1][d0] array of `esize`-byte elements
+static bool encode2d(CUtensorMap *m, const void *base, CUtensorMapDataType dt, uint64_t esize, uint64_t d0,
+                     uint64_t d1, uint32_t b0, uint32_t b1) {
+  auto enc = get_encode();
+  if (!enc) return false;
+  if ((d0 * esize) % 16 != 0 || (reinterpret_cast<uintptr_t>(base) & 15) != 0) return false;
+  cuuint64_t dims[2] = {d0, d1};
+  cuuint64_t strides[1] = {d0 * esize};
+  cuuint32_t box[2] = {b0, b1};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = enc(m, dt, 2, const_cast<void *>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+// raw samples viewed as [F*n_tx*n_rx*P rows][n_k] complex64, box [br rows][16]
+bool sar_encode_input_map(sar_plan *p, const void *d_data) {
+  const SarDeviceView &v = p->v;
+  p->tm_s_ptr = d_data;
+  const uint64_t rows = (uint64_t)v.F * v.nt * v.nr * v.P;
+  return encode2d(&p->tm_s, d_data, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, v.nk, rows, k1c_for(v.nx), p->k1_br);
+}
+
+int sar_build_tensor_maps(sar_plan *p) {
+  const SarDeviceView &v = p->v;
+  p->tma_mid0 = p->tma_mid1 = p->tma_rows1 = false;
+  if (v.F == 0 || getenv("SAR_NO_TMA")) return SAR_OK;
+  const uint32_t rows = v.ny < 256 ? v.ny : 256;
+  p->tma_mid0 = encode3d(&p->tm_w0_mid, v.w0, v.nk, v.nx, (uint64_t)v.F * v.ny, KC, 1, rows);
+  p->tma_mid1 = encode3d(&p->tm_w1_mid, v.w1, v.nz, v.nx, (uint64_t)v.F * v.ny, KC, 1, rows);
+  const uint32_t xr = v.nx < 256 ? v.nx : 256;
+  p->tma_rows1 = encode3d(&p->tm_w1_rows, v.w1, v.nz, v.nx, (uint64_t)v.F * v.ny, KC, xr, 1);
+  // K1: -2 d_z table [F*npy][npx] float32 with box [1][br]; input map per call
+  const int brmax = K1_BOX_BYTES / (k1c_for(v.nx) * 8);
+  p->k1_br = v.npx < brmax ? v.npx : brmax;
+  p->k1_regacc = true;
+  for (int i = 0; i < v.npair; ++i) p->k1_regacc = p->k1_regacc && v.jx[i] == 0;
+  p->tma_ap = (v.npx % 4 == 0) && (v.nk % 2 == 0) && p->k1_br % 8 == 0 &&
+              encode2d(&p->tm_ap, v.apose, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, v.npx, (uint64_t)v.F * v.npy,
+                       p->k1_br, 1);
+  p->tm_s_ptr = nullptr;
+  p->tma_s = false;
   return SAR_OK;
 }

@@ -380,9 +380,18 @@ int sar_plan_create(sar_plan **out, const sar_geom_desc *g, const sar_image_desc
     v.stolt_delta = std::max(1e-7, 100.0 * err);
   }
   v.img_scale = (float)(1.0 / ((double)p->nx * p->ny * p->nz));
+  {
+    // K1 step phasor exp(j dk beta): 5th-order Taylor needs |dk beta| small
+    float amax = 0.f, bmax = 0.f;
+    for (float a : T.apose) amax = std::max(amax, fabsf(a));
+    for (float b : T.bpair) bmax = std::max(bmax, fabsf(b));
+    v.k1_step_ok = (T.dk * ((double)amax + (double)bmax) <= 0.25) ? 1 : 0;
+  }
   v.w0 = p->d_w0;
   v.w1 = p->d_w1;
 
+  p->num_sms = prop.multiProcessorCount;
+  sar_build_tensor_maps(p);
   if (flags & SAR_PROFILE_STAGES) {
     for (int i = 0; i < SAR_PROFILE_RING; ++i)
       for (int j = 0; j <= SAR_N_STAGES; ++j) cudaEventCreate(&p->ev[i][j]);

@@ -1,6 +1,7 @@
 // plan_internal.h -- the plan object shared by the host C ABI (plan.cpp) and
 // the kernel launchers (kernels.cu).  Not part of the public ABI.
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -32,6 +33,7 @@ struct SarDeviceView {
   const float2 *tw_z;   // [nz]
   double k0, dk, inv_dk;
   double stolt_delta;   // decision guard band of the fast Stolt path (kernels.cu)
+  int k1_step_ok;       // max |dk * beta| <= 0.25: K1 may use the Taylor step phasor
   float img_scale;      // 1/(nx ny nz)
   float2 *w0;           // [F][ny][nx][nk]  planar lattice -> spectrum
   float2 *w1;           // [F][ny][nx][nz]  Stolt output -> partial inverse
@@ -59,6 +61,13 @@ struct sar_plan {
   int n_prof = 0;
   bool prof_events = false;
   cudaStream_t last_stream = nullptr;
+  // TMA tensor maps over the workspace (built once per plan; valid flags)
+  CUtensorMap tm_w0_mid, tm_w1_mid, tm_w1_rows, tm_ap, tm_s;
+  bool tma_mid0 = false, tma_mid1 = false, tma_rows1 = false, tma_ap = false, tma_s = false;
+  const void *tm_s_ptr = nullptr;  // data pointer tm_s was encoded for
+  int k1_br = 0;                   // pose rows per K1 TMA box
+  bool k1_regacc = false;          // every j^x offset is 0: K1 sums in registers
+  int num_sms = 148;
 };
 
 // kernels.cu
@@ -67,3 +76,5 @@ int sar_launch_pipeline(sar_plan *p, const void *d_data, void *d_image, cudaStre
 int sar_launch_stolt_index(sar_plan *p, const int32_t *d_cols, int n, int32_t *d_i0, float *d_tau,
                            cudaStream_t s);
 void sar_set_error(const std::string &msg);
+int sar_build_tensor_maps(sar_plan *p);
+bool sar_encode_input_map(sar_plan *p, const void *d_data);

@@ -134,9 +134,9 @@ def test_stolt_index_bit_exact(name, n_sample):
     assert (i0 >= 0).any() and (i0 < 0).any()
 
 
-def _custom(npx, npy, nx, ny, nk, nz, dz, z_ref, n_frames=1, monostatic=False, n_tx=2, nsc=4, seed=0):
+def _custom(npx, npy, nx, ny, nk, nz, dz, z_ref, n_frames=1, monostatic=False, n_tx=2, nsc=4, seed=0, jz=2e-3):
     sc = scenes.raster_scene(npx, npy, nx, ny, nk, nz, dz, z_ref, monostatic=monostatic, n_tx=n_tx,
-                             jitter_xy=0.5e-3, jitter_z=2e-3, n_frames=n_frames, seed=seed)
+                             jitter_xy=0.5e-3, jitter_z=jz, n_frames=n_frames, seed=seed)
     rng = np.random.default_rng(seed + 1)
     pos, amp = [], []
     cx = sc.x0 + npx * sc.dx / 2
@@ -163,13 +163,17 @@ EDGE = [
     dict(npx=2, npy=1, nx=2, ny=4, nk=3, nz=4, dz=5e-3, z_ref=0.25),
     # several frames with their own geometry; 3 Tx
     dict(npx=24, npy=20, nx=32, ny=32, nk=32, nz=32, dz=5e-3, z_ref=0.2, n_frames=3, n_tx=3),
+    # large plane displacements (P:339 sweeps max|d_z| up to 20 cm): |dk beta|
+    # beyond the K1 step-phasor bound -> exact per-sample rotation path
+    dict(npx=64, npy=40, nx=64, ny=64, nk=16, nz=32, dz=5e-3, z_ref=0.45, jz=0.05),
     # maximum FFT size along x and z (1024), small elsewhere
     dict(npx=600, npy=4, nx=1024, ny=16, nk=16, nz=1024, dz=1e-3, z_ref=0.3),
     dict(npx=4, npy=700, nx=8, ny=1024, nk=24, nz=8, dz=5e-3, z_ref=0.3),
 ]
 
 
-@pytest.mark.parametrize("kw", EDGE, ids=lambda kw: "x".join(str(kw[k]) for k in ("npx", "npy", "nx", "ny", "nk", "nz")))
+@pytest.mark.parametrize("kw", EDGE, ids=lambda kw: "x".join(str(kw[k]) for k in ("npx", "npy", "nx", "ny", "nk", "nz"))
+                         + ("_jz" if "jz" in kw else ""))
 def test_edge_cases(kw):
     _check_e2e(_custom(**kw), gpu_gen=False)
 
@@ -254,3 +258,27 @@ def test_bad_tensor_arguments():
             plan.reconstruct(torch.zeros((1, 2, 4, 256, 15), dtype=torch.complex64, device="cuda"))
         with pytest.raises(TypeError):
             plan.reconstruct(torch.zeros(sc.data_shape, dtype=torch.complex64))
+
+
+@pytest.mark.parametrize("name", ["small", "realtime"])
+def test_non_tma_fallback_path(name, monkeypatch):
+    """The plain (non-TMA) kernels used for odd n_k / unaligned rasters are
+    forced with SAR_NO_TMA and must meet the same bar."""
+    monkeypatch.setenv("SAR_NO_TMA", "1")
+    _check_e2e(scenes.make_scene(name))
+
+
+def test_tma_and_plain_paths_agree():
+    sc = scenes.make_scene("small")
+    d, _ = _data(sc)
+    with sar.Plan.from_scene(sc) as plan:
+        a = plan.reconstruct(d).cpu().numpy()
+    import os
+    os.environ["SAR_NO_TMA"] = "1"
+    try:
+        with sar.Plan.from_scene(sc) as plan:
+            b = plan.reconstruct(d).cpu().numpy()
+    finally:
+        del os.environ["SAR_NO_TMA"]
+    e2, _ = errs(a, b.astype(np.float64))
+    assert e2 < 1e-5
