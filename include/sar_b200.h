@@ -59,6 +59,7 @@ enum sar_flags {
 /* Limits of this build. */
 #define SAR_MAX_FFT 1024  /* nx, ny, nz <= 1024 (powers of two >= 2) */
 #define SAR_MAX_PAIRS 64  /* n_tx * n_rx <= 64 */
+#define SAR_MAX_NK 2048   /* n_k <= 2048 (a Stolt column must fit in shared memory) */
 
 /* Acquisition geometry (host memory; copied by sar_plan_create, so the caller
  * may free every array as soon as the call returns). */
@@ -74,7 +75,7 @@ typedef struct {
                               coordinate gives the plane displacement d_z (Eq. (4)); x,y are
                               not used in RASTER placement (reading R7) */
   const double *z0;        /* [F] reference plane Z_0 per frame (m), or NULL = mean of scan z */
-  int32_t n_k;             /* >= 2 frequency samples */
+  int32_t n_k;             /* 2 <= n_k <= SAR_MAX_NK frequency samples */
   const double *k;         /* [n_k] wavenumbers 2*pi*f/c (rad/m), uniform (1e-9 rel.), ascending */
   const double *pulse;     /* [n_k][2] complex P(f) (re,im) or NULL for P == 1 (Eq. (14)) */
   int32_t device;          /* CUDA device ordinal */

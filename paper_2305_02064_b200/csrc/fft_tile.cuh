@@ -20,11 +20,13 @@
 
 namespace sarfft {
 
+// Complex arithmetic on the sm_100 paired-fp32 pipe (FADD2 / FMUL2 / FFMA2):
+// one instruction per complex add, two per complex multiply.
 __device__ __forceinline__ float2 cmul(float2 a, float2 b) {
-  return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
+  return __ffma2_rn(make_float2(a.x, a.x), b, __fmul2_rn(make_float2(-a.y, a.y), make_float2(b.y, b.x)));
 }
-__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
-__device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return __fadd2_rn(a, b); }
+__device__ __forceinline__ float2 csub(float2 a, float2 b) { return __fadd2_rn(a, make_float2(-b.x, -b.y)); }
 // multiply by -i (DIR = -1) or +i (DIR = +1)
 template <int DIR>
 __device__ __forceinline__ float2 mul_mi(float2 a) {
@@ -59,11 +61,12 @@ __device__ __forceinline__ void dft8(float2 *v) {
     c[r] = csub(v[r], v[r + 4]);
   }
   // c_r *= W8^{r} with W8 = exp(DIR * 2 pi i / 8)
-  c[1] = DIR < 0 ? make_float2(h * (c[1].x + c[1].y), h * (c[1].y - c[1].x))
-                 : make_float2(h * (c[1].x - c[1].y), h * (c[1].y + c[1].x));
+  const float2 hh = make_float2(h, h);
+  c[1] = DIR < 0 ? __fmul2_rn(hh, __fadd2_rn(c[1], make_float2(c[1].y, -c[1].x)))
+                 : __fmul2_rn(hh, __fadd2_rn(c[1], make_float2(-c[1].y, c[1].x)));
   c[2] = mul_mi<DIR>(c[2]);
-  c[3] = DIR < 0 ? make_float2(h * (c[3].y - c[3].x), -h * (c[3].x + c[3].y))
-                 : make_float2(-h * (c[3].x + c[3].y), h * (c[3].x - c[3].y));
+  c[3] = DIR < 0 ? __fmul2_rn(hh, __fadd2_rn(make_float2(c[3].y, -c[3].x), make_float2(-c[3].x, -c[3].y)))
+                 : __fmul2_rn(hh, __fadd2_rn(make_float2(-c[3].y, c[3].x), make_float2(-c[3].x, -c[3].y)));
   dft4<DIR>(b);
   dft4<DIR>(c);
 #pragma unroll

@@ -24,6 +24,7 @@
 
 #include <stdlib.h>
 #include <string>
+#include <type_traits>
 
 #include "fft_tile.cuh"
 #include "tma.cuh"
@@ -42,6 +43,10 @@ constexpr int nt_for(int n) { return n <= 32 ? 32 : (n < 512 ? n : 512); }
 // resident CTAs requested per SM: 1024 threads' worth (caps registers at 64 per
 // thread) except for the 1024-point tiles, whose 32 elements per thread need more
 constexpr int minb_for(int n) { return n >= 1024 ? 1 : 1024 / nt_for(n); }
+// persistent tile kernels: 2N threads (8 elements each of a 16-column tile),
+// capped at 1024, and as many CTAs per SM as make 1024 threads
+constexpr int ntp_for(int n) { return 2 * n < 64 ? 64 : (2 * n > 1024 ? 1024 : 2 * n); }
+constexpr int ctas_for(int n) { return 1024 / ntp_for(n); }
 
 // ---------------------------------------------------------------- K1 ------
 // One CTA = (k chunk, virtual row vy, frame f).  Thread item e covers
@@ -380,16 +385,18 @@ __global__ void __launch_bounds__(nt_for(N), minb_for(N))
 // and finished tiles go back with TMA stores, so the SM's load queue never
 // drains between tiles.  Box = {16 inner elements, 1 column, <=256 rows}.
 template <int N, int DIR>
-__global__ void __launch_bounds__(nt_for(N), 1)
-    k_fft_mid_tma(const __grid_constant__ CUtensorMap tm, const float2 *__restrict__ tw, int nx, int nchunk,
+__global__ void __launch_bounds__(ntp_for(N), ctas_for(N))
+    k_fft_mid_tma(const __grid_constant__ CUtensorMap tm, const float2 *__restrict__ twg, int nx, int nchunk,
                   int nitems) {
-  constexpr int NT = nt_for(N);
+  constexpr int NT = ntp_for(N);
   constexpr int ROWS = N < 256 ? N : 256;
   constexpr int NBOX = N / ROWS;
   constexpr uint32_t TILE_BYTES = N * KC * sizeof(float2);
   extern __shared__ __align__(128) float2 smt[];  // [2][N][16]
   __shared__ __align__(8) uint64_t full[2];
+  __shared__ float2 tw[N];
   const int tid = threadIdx.x;
+  for (int i = tid; i < N; i += NT) tw[i] = twg[i];
   if (tid == 0) {
     sartma::mbar_init(&full[0], 1);
     sartma::mbar_init(&full[1], 1);
@@ -470,8 +477,12 @@ __device__ __forceinline__ bool stolt_pull(double kzj, double kr2, double k0, do
                                            double delta, int *i0, double *tau) {
   if (!(kzj > 0.0)) return false;
   const double u = (0.5 * fast_dsqrt(fma(kzj, kzj, kr2)) - k0) * inv_dk;
+  const double top = (double)(nk - 1);
+  // clearly out of band (|u - u_exact| << delta and the edges sit within
+  // BAND_EPS << delta of 0 and n_k-1)
+  if (u < -delta || u > top + delta) return false;
   const double fl = floor(u);
-  const bool near = u < delta || u > (double)(nk - 1) - delta || (u - fl) < delta || (u - fl) > 1.0 - delta;
+  const bool near = u < delta || u > top - delta || (u - fl) < delta || (u - fl) > 1.0 - delta;
   if (near) return stolt_pull_exact(kzj, kr2, k0, dk, nk, i0, tau);
   *i0 = (int)fl;
   *tau = u - fl;
@@ -483,124 +494,285 @@ __device__ __forceinline__ double kr2_of(const SarDeviceView &v, int a, int b) {
   return __dadd_rn(__dmul_rn(kx, kx), __dmul_rn(ky, ky));
 }
 
-constexpr int K3_CL = 2;              // mirror classes per CTA
-constexpr int K3_CC = 4 * K3_CL;      // column slots per CTA (<= 4 columns per class)
-constexpr int K3_LD = K3_CC + 1;      // padded row stride of the [NZ][CC] output tile
+// One CTA = CL "mirror classes" of spectral columns (CL = 2 for n_z >= 128,
+// more for short columns so that the CTA's 256 threads stay busy).
+// k_r^2 = kx^2 + ky^2 is the same for (a,b), (-a,b), (a,-b), (-a,-b), so the
+// filter H(k_r, k_i) and the Stolt pull weights (i0, tau)(k_r, j) -- the fp64
+// part of the step -- are computed once per class and applied to its (up to
+// 4) columns.  Each column's n_k source samples are contiguous in W0 and
+// arrive by TMA bulk copies (cp.async.bulk + mbarrier) into fin[slot][i].
 constexpr int K3_NT = 256;
+constexpr int k3_cl_for(int nz) { return nz >= 128 ? 2 : (nz >= 64 ? 4 : 8); }
 
-// One CTA = 2 "mirror classes" of spectral columns.  k_r^2 = kx^2 + ky^2 is
-// the same for (a,b), (-a,b), (a,-b), (-a,-b), so the filter H(k_r, k_i) and
-// the Stolt pull weights (i0, tau)(k_r, j) -- the fp64 part of the step -- are
-// computed once per class and applied to its (up to 4) columns.  Each
-// column's n_k source samples are contiguous in W0 and arrive by TMA bulk
-// copies (cp.async.bulk + mbarrier) into fin[slot][i].
-template <int NZ, bool DO_IFFT>
+template <int NZ, int CL, bool DO_IFFT>
 __global__ void __launch_bounds__(K3_NT) k3_filter_stolt(const SarDeviceView v) {
+  constexpr int CC = 4 * CL;        // column slots
+  constexpr int LD = CC + 1;        // padded row stride of the [NZ][CC] output tile
   extern __shared__ __align__(16) float2 sm[];
-  __shared__ double kr2s[K3_CL];
-  __shared__ int colof[K3_CC];   // column index (b*nx + a) of each slot, -1 = empty
+  __shared__ double kr2s[CL];
+  __shared__ int nmem[CL], mslot[CL][4];
+  __shared__ int colof[CC];        // column index of each used slot
+  __shared__ int nused;
   __shared__ __align__(8) uint64_t bar;
   const int nk = v.nk;
   float2 *fin = sm;                                  // [CC][nk]  source spectrum -> filtered
-  float2 *fout = sm + (size_t)K3_CC * nk;            // [NZ][LD]  Stolt output
+  float2 *fout = sm + (size_t)CC * nk;               // [NZ][LD]  Stolt output
   const int tid = threadIdx.x;
   const int ncol = v.nx * v.ny;
   const int hx = v.nx / 2 + 1, hy = v.ny / 2 + 1;
   const int nclass = hx * hy;
-  const int q0 = blockIdx.x * K3_CL;
+  const int q0 = blockIdx.x * CL;
   const int f = blockIdx.y;
   const float2 *wf = v.w0 + (size_t)f * ncol * (size_t)nk;
   const bool bulk = (nk & 1) == 0;   // 16-byte aligned columns
-  if (tid < K3_CC) {
-    const int cl = tid >> 2, m = tid & 3;
-    const int q = q0 + cl;
-    int col = -1;
-    if (q < nclass) {
+  if (tid == 0) {
+    int n = 0;
+    for (int cl = 0; cl < CL; ++cl) {
+      const int q = q0 + cl;
+      nmem[cl] = 0;
+      kr2s[cl] = 0.0;
+      if (q >= nclass) continue;
       const int a = q % hx, b = q / hx;
       const int ma = (v.nx - a) & (v.nx - 1), mb = (v.ny - b) & (v.ny - 1);
-      const bool da = ma != a, db = mb != b;
-      if (m == 0) col = b * v.nx + a;
-      if (m == 1 && da) col = b * v.nx + ma;
-      if (m == 2 && db) col = mb * v.nx + a;
-      if (m == 3 && da && db) col = mb * v.nx + ma;
-      if (m == 0) kr2s[cl] = kr2_of(v, a, b);
-    } else if (m == 0) {
-      kr2s[cl] = 0.0;
+      kr2s[cl] = kr2_of(v, a, b);
+      const int c4[4] = {b * v.nx + a, b * v.nx + ma, mb * v.nx + a, mb * v.nx + ma};
+      const bool ok4[4] = {true, ma != a, mb != b, ma != a && mb != b};
+      for (int m = 0; m < 4; ++m)
+        if (ok4[m]) {
+          mslot[cl][nmem[cl]++] = n;
+          colof[n++] = c4[m];
+        }
     }
-    colof[tid] = col;
-  }
-  if (tid == 0 && bulk) {
-    sartma::mbar_init(&bar, 1);
-    sartma::fence_barrier_init();
+    nused = n;
+    if (bulk) {
+      sartma::mbar_init(&bar, 1);
+      sartma::fence_barrier_init();
+      sartma::mbar_arrive_expect_tx(&bar, (uint32_t)n * (uint32_t)nk * 8u);
+      for (int sl = 0; sl < n; ++sl) sartma::bulk_g2s(fin + sl * nk, wf + (size_t)colof[sl] * nk, (uint32_t)nk * 8u, &bar);
+    }
   }
   __syncthreads();
+  const int nu = nused;
   // 1. load the member columns
   if (bulk) {
-    if (tid == 0) {
-      uint32_t bytes = 0;
-      for (int sl = 0; sl < K3_CC; ++sl) bytes += colof[sl] >= 0 ? (uint32_t)nk * 8u : 0u;
-      sartma::mbar_arrive_expect_tx(&bar, bytes);
-      for (int sl = 0; sl < K3_CC; ++sl)
-        if (colof[sl] >= 0) sartma::bulk_g2s(fin + sl * nk, wf + (size_t)colof[sl] * nk, (uint32_t)nk * 8u, &bar);
-    }
     sartma::mbar_wait(&bar, 0);
   } else {
-    for (int sl = 0; sl < K3_CC; ++sl)
-      if (colof[sl] >= 0)
-        for (int i = tid; i < nk; i += K3_NT) fin[sl * nk + i] = __ldcs(wf + (size_t)colof[sl] * nk + i);
+    for (int sl = 0; sl < nu; ++sl) {
+      const float2 *src = wf + (size_t)colof[sl] * nk;
+      for (int i = tid; i < nk; i += K3_NT) fin[sl * nk + i] = __ldcs(src + i);
+    }
     __syncthreads();
   }
   // 2. filter H = k_z exp(+j k_z R_ref) / P(f) on the source grid (in place),
   //    once per class, applied to its columns
-  const double rref = v.rref[f];
-  for (int idx = tid; idx < K3_CL * nk; idx += K3_NT) {
-    const int cl = idx / nk, i = idx - cl * nk;
-    const double ki = v.k[i];
-    const double q = 4.0 * ki * ki - kr2s[cl];
-    float2 h = make_float2(0.f, 0.f);
-    if (q > 0.0) {
-      const double kz = fast_dsqrt(q);
-      double turns = kz * rref * (1.0 / TWO_PI);
-      turns -= rint(turns);
-      float sn, cs;
-      __sincosf((float)turns * 6.28318530717958647692f, &sn, &cs);
-      const float kzf = (float)kz;
-      h = make_float2(kzf * cs, kzf * sn);
-      if (v.pinv) h = cmul(h, v.pinv[i]);
-    }
+  const double rr = v.rref[f] * (1.0 / TWO_PI);
 #pragma unroll
-    for (int m = 0; m < 4; ++m) {
-      const int sl = cl * 4 + m;
-      if (colof[sl] >= 0) fin[sl * nk + i] = cmul(fin[sl * nk + i], h);
+  for (int cl = 0; cl < CL; ++cl) {
+    const double kr2 = kr2s[cl];
+    const int nm = nmem[cl];
+    if (nm == 0) continue;
+    for (int i = tid; i < nk; i += K3_NT) {
+      const double ki = v.k[i];
+      const double q = 4.0 * ki * ki - kr2;
+      float2 h = make_float2(0.f, 0.f);
+      if (q > 0.0) {
+        const double kz = fast_dsqrt(q);
+        double turns = kz * rr;
+        turns -= rint(turns);
+        float sn, cs;
+        __sincosf((float)turns * 6.28318530717958647692f, &sn, &cs);
+        const float kzf = (float)kz;
+        h = make_float2(kzf * cs, kzf * sn);
+        if (v.pinv) h = cmul(h, v.pinv[i]);
+      }
+      for (int m = 0; m < nm; ++m) {
+        float2 *x = fin + mslot[cl][m] * nk + i;
+        *x = cmul(*x, h);
+      }
     }
   }
   __syncthreads();
   // 3. Stolt pull onto the uniform k_z grid, weights once per class
-  for (int idx = tid; idx < K3_CL * NZ; idx += K3_NT) {
+  for (int idx = tid; idx < CL * NZ; idx += K3_NT) {
     const int j = idx % NZ, cl = idx / NZ;
+    const int nm = nmem[cl];
     int i0 = 0;
     double tau = 0.0;
-    const bool ok = stolt_pull(v.kz[j], kr2s[cl], v.k0, v.inv_dk, v.dk, nk, v.stolt_delta, &i0, &tau);
+    const bool ok = nm > 0 && stolt_pull(v.kz[j], kr2s[cl], v.k0, v.inv_dk, v.dk, nk, v.stolt_delta, &i0, &tau);
     const float t = (float)tau;
-#pragma unroll
-    for (int m = 0; m < 4; ++m) {
-      const int sl = cl * 4 + m;
+    for (int m = 0; m < nm; ++m) {
+      const int sl = mslot[cl][m];
       float2 o = make_float2(0.f, 0.f);
-      if (ok && colof[sl] >= 0) {
+      if (ok) {
         const float2 lo = fin[sl * nk + i0], hi = fin[sl * nk + i0 + 1];
         o = make_float2(fmaf(t, hi.x - lo.x, lo.x), fmaf(t, hi.y - lo.y, lo.y));
       }
-      fout[j * K3_LD + sl] = o;
+      fout[j * LD + sl] = o;
     }
   }
   __syncthreads();
-  // 4. inverse FFT along z
-  if constexpr (DO_IFFT) sarfft::tile_fft<NZ, K3_CC, K3_LD, K3_NT, +1>(fout, v.tw_z, tid);
+  // 4. inverse FFT along z (unused slots hold stale values; never stored)
+  if constexpr (DO_IFFT) sarfft::tile_fft<NZ, CC, LD, K3_NT, +1>(fout, v.tw_z, tid);
   // 5. store each column contiguously [col][z]
   float2 *dst = v.w1 + (size_t)f * ncol * (size_t)NZ;
-  for (int idx = tid; idx < K3_CC * NZ; idx += K3_NT) {
-    const int sl = idx / NZ, z = idx - sl * NZ;
-    if (colof[sl] >= 0) dst[(size_t)colof[sl] * NZ + z] = fout[z * K3_LD + sl];
+  for (int sl = 0; sl < nu; ++sl) {
+    float2 *d = dst + (size_t)colof[sl] * NZ;
+    for (int z = tid; z < NZ; z += K3_NT) d[z] = fout[z * LD + sl];
+  }
+}
+
+// Warp-specialised persistent K3 (n_k even: 16-byte aligned columns).  A
+// producer warp decodes work items (CL mirror classes) into a 2-deep ring of
+// shared-memory stages and fills them with TMA bulk copies (full/empty
+// mbarriers); 8 consumer warps filter, resample and z-transform one item
+// while the next one lands.  The stage is released right after the Stolt
+// pull, so the z-IFFT and the stores overlap the following copies too.
+template <int CL>
+struct K3Hdr {
+  int f, nused;
+  int nmem[CL], mslot[CL][4];
+  int colof[4 * CL];
+  double kr2[CL];
+};
+
+constexpr int K3W_NT = 512;   // consumer threads
+constexpr int K3W_STAGES = 2;
+
+template <int NZ, int CL, bool DO_IFFT>
+__global__ void __launch_bounds__(K3W_NT + 32, 2) k3_filter_stolt_ws(const SarDeviceView v, int nitems_f) {
+  constexpr int CC = 4 * CL;
+  constexpr int LD = CC + 1;
+  constexpr int NWARP = K3W_NT / 32;
+  extern __shared__ __align__(16) unsigned char smb[];
+  const int nk = v.nk;
+  const size_t hdr_bytes = (sizeof(K3Hdr<CL>) + 15) & ~(size_t)15;
+  const size_t stage_bytes = hdr_bytes + (size_t)CC * nk * sizeof(float2);
+  float2 *fout = reinterpret_cast<float2 *>(smb + K3W_STAGES * stage_bytes);  // [NZ][LD]
+  float2 *htab = fout + (size_t)NZ * LD;                                        // [CL][nk] filter
+  const float inv_nk = 1.0f / (float)nk;
+  __shared__ __align__(8) uint64_t full[K3W_STAGES], empty[K3W_STAGES];
+  __shared__ float2 tw[NZ];
+  const int tid = threadIdx.x;
+  const int ncol = v.nx * v.ny;
+  const int hx = v.nx / 2 + 1, hy = v.ny / 2 + 1;
+  const int nclass = hx * hy;
+  const int nitems = nitems_f * v.F;
+  for (int i = tid; i < NZ; i += K3W_NT + 32) tw[i] = v.tw_z[i];
+  if (tid == 0) {
+    for (int i = 0; i < K3W_STAGES; ++i) {
+      sartma::mbar_init(&full[i], 1);
+      sartma::mbar_init(&empty[i], NWARP);
+    }
+    sartma::fence_barrier_init();
+  }
+  __syncthreads();
+  if (tid >= K3W_NT) {
+    if (tid == K3W_NT) {  // producer
+      unsigned n = 0;
+      for (int item = blockIdx.x; item < nitems; item += gridDim.x, ++n) {
+        const int st = n % K3W_STAGES;
+        if (n >= K3W_STAGES) sartma::mbar_wait(&empty[st], ((n / K3W_STAGES) - 1) & 1);
+        unsigned char *sb = smb + st * stage_bytes;
+        K3Hdr<CL> &h = *reinterpret_cast<K3Hdr<CL> *>(sb);
+        float2 *fin = reinterpret_cast<float2 *>(sb + hdr_bytes);
+        const int f = item / nitems_f;
+        const int q0 = (item - f * nitems_f) * CL;
+        int cnt = 0;
+        for (int cl = 0; cl < CL; ++cl) {
+          const int q = q0 + cl;
+          h.nmem[cl] = 0;
+          h.kr2[cl] = 0.0;
+          if (q >= nclass) continue;
+          const int a = q % hx, b = q / hx;
+          const int ma = (v.nx - a) & (v.nx - 1), mb = (v.ny - b) & (v.ny - 1);
+          h.kr2[cl] = kr2_of(v, a, b);
+          const int c4[4] = {b * v.nx + a, b * v.nx + ma, mb * v.nx + a, mb * v.nx + ma};
+          const bool ok4[4] = {true, ma != a, mb != b, ma != a && mb != b};
+          for (int m = 0; m < 4; ++m)
+            if (ok4[m]) {
+              h.mslot[cl][h.nmem[cl]++] = cnt;
+              h.colof[cnt++] = c4[m];
+            }
+        }
+        h.nused = cnt;
+        h.f = f;
+        const float2 *wf = v.w0 + (size_t)f * ncol * (size_t)nk;
+        sartma::mbar_arrive_expect_tx(&full[st], (uint32_t)cnt * (uint32_t)nk * 8u);
+        for (int sl = 0; sl < cnt; ++sl)
+          sartma::bulk_g2s(fin + sl * nk, wf + (size_t)h.colof[sl] * nk, (uint32_t)nk * 8u, &full[st]);
+      }
+    }
+    return;
+  }
+  // consumers
+  const int lane = tid & 31;
+  unsigned n = 0;
+  for (int item = blockIdx.x; item < nitems; item += gridDim.x, ++n) {
+    const int st = n % K3W_STAGES;
+    sartma::mbar_wait(&full[st], (n / K3W_STAGES) & 1);
+    unsigned char *sb = smb + st * stage_bytes;
+    const K3Hdr<CL> &h = *reinterpret_cast<const K3Hdr<CL> *>(sb);
+    float2 *fin = reinterpret_cast<float2 *>(sb + hdr_bytes);
+    const int f = h.f, nu = h.nused;
+    // filter H(k_r, k_i) = k_z exp(+j k_z R_ref) / P(f) of every class, into a
+    // table (the fp64 work is per class, not per column)
+    const double rr = v.rref[f] * (1.0 / TWO_PI);
+    for (int idx = tid; idx < CL * nk; idx += K3W_NT) {
+      const int cl = (int)(((float)idx + 0.5f) * inv_nk);   // exact: idx < 2^14
+      const int i = idx - cl * nk;
+      const double ki = v.k[i];
+      const double q = 4.0 * ki * ki - h.kr2[cl];
+      float2 hh = make_float2(0.f, 0.f);
+      if (q > 0.0) {
+        const double kz = fast_dsqrt(q);
+        double turns = kz * rr;
+        turns -= rint(turns);
+        float sn, cs;
+        __sincosf((float)turns * 6.28318530717958647692f, &sn, &cs);
+        const float kzf = (float)kz;
+        hh = make_float2(kzf * cs, kzf * sn);
+        if (v.pinv) hh = cmul(hh, v.pinv[i]);
+      }
+      htab[idx] = hh;
+    }
+    sarfft::tile_sync<1, K3W_NT>();
+    // Stolt pull with the filter folded into complex weights:
+    //   O_j = (1-tau) H_{i0} S_{i0} + tau H_{i0+1} S_{i0+1}
+    // weights once per (class, j), two complex FMAs per column
+    for (int idx = tid; idx < CL * NZ; idx += K3W_NT) {
+      const int j = idx % NZ, cl = idx / NZ;
+      const int nm = h.nmem[cl];
+      int i0 = 0;
+      double tau = 0.0;
+      const bool ok = nm > 0 && stolt_pull(v.kz[j], h.kr2[cl], v.k0, v.inv_dk, v.dk, nk, v.stolt_delta, &i0, &tau);
+      const float t = (float)tau;
+      const float2 hl = ok ? htab[cl * nk + i0] : make_float2(0.f, 0.f);
+      const float2 hu = ok ? htab[cl * nk + i0 + 1] : make_float2(0.f, 0.f);
+      const float2 wl = make_float2((1.f - t) * hl.x, (1.f - t) * hl.y);
+      const float2 wu = make_float2(t * hu.x, t * hu.y);
+      for (int m = 0; m < nm; ++m) {
+        const int sl = h.mslot[cl][m];
+        float2 o = make_float2(0.f, 0.f);
+        if (ok) o = cmac2(cmul2(wl, fin[sl * nk + i0]), wu, fin[sl * nk + i0 + 1]);
+        fout[j * LD + sl] = o;
+      }
+    }
+    int colof[CC];
+#pragma unroll
+    for (int sl = 0; sl < CC; ++sl) colof[sl] = sl < nu ? h.colof[sl] : 0;
+    sarfft::tile_sync<1, K3W_NT>();
+    // the stage (header + fin) is free: let the producer refill it
+    __syncwarp();
+    if (lane == 0) sartma::mbar_arrive(&empty[st]);
+    if constexpr (DO_IFFT) sarfft::tile_fft<NZ, CC, LD, K3W_NT, +1, 1>(fout, tw, tid);
+    float2 *dst = v.w1 + (size_t)f * ncol * (size_t)NZ;
+#pragma unroll
+    for (int sl = 0; sl < CC; ++sl) {
+      if (sl >= nu) break;
+      float2 *d = dst + (size_t)colof[sl] * NZ;
+      for (int z = tid; z < NZ; z += K3W_NT) d[z] = fout[z * LD + sl];
+    }
+    sarfft::tile_sync<1, K3W_NT>();
   }
 }
 
@@ -674,6 +846,88 @@ __global__ void __launch_bounds__(nt_for(NX), minb_for(NX))
   }
 }
 
+// Persistent, TMA-pipelined K4b (n_z even, 32 <= nx <= 512).  Item = (frame,
+// image row y, 16-wide z chunk): the [nx][16] tile of item i+1 is in flight
+// (cp.async.bulk.tensor + mbarrier) while item i is inverse-transformed along
+// x; the magnitudes (or scaled complex values) are transposed through a padded
+// [16][nx+1] buffer with the x roll applied, so every image row segment is
+// written with coalesced stores.
+template <int NX, bool CPLX>
+__global__ void __launch_bounds__(ntp_for(NX), ctas_for(NX))
+    k4_xifft_mag_tma(const SarDeviceView v, const __grid_constant__ CUtensorMap tm, void *__restrict__ img,
+                     int nzc, int nitems) {
+  constexpr int NT = ntp_for(NX);
+  constexpr int ROWS = NX < 256 ? NX : 256;
+  constexpr int NBOX = NX / ROWS;
+  constexpr uint32_t TILE_BYTES = NX * KC * sizeof(float2);
+  using OT = typename std::conditional<CPLX, float2, float>::type;
+  extern __shared__ __align__(128) float2 smk[];    // [2][NX][16] tiles, then [16][NX+1] output rows
+  OT *ob = reinterpret_cast<OT *>(smk + 2 * (size_t)NX * KC);
+  __shared__ __align__(8) uint64_t full[2];
+  __shared__ float2 tw[NX];
+  const int tid = threadIdx.x;
+  const int nz = v.nz;
+  for (int i = tid; i < NX; i += NT) tw[i] = v.tw_x[i];
+  if (tid == 0) {
+    sartma::mbar_init(&full[0], 1);
+    sartma::mbar_init(&full[1], 1);
+    sartma::fence_barrier_init();
+  }
+  __syncthreads();
+  auto issue = [&](int item, int st) {
+    const int zc = item % nzc, fy = item / nzc;  // fy = f*ny + y
+    sartma::mbar_arrive_expect_tx(&full[st], TILE_BYTES);
+#pragma unroll
+    for (int bx = 0; bx < NBOX; ++bx)
+      sartma::tma_load_3d(smk + (size_t)st * NX * KC + bx * ROWS * KC, &tm, zc * KC, bx * ROWS, fy, &full[st]);
+  };
+  const int rx = ((v.roll_x % NX) + NX) % NX;
+  const int ry = ((v.roll_y % v.ny) + v.ny) % v.ny;
+  const float sc = v.img_scale;
+  int item = blockIdx.x;
+  if (tid == 0 && item < nitems) issue(item, 0);
+  for (int it = 0; item < nitems; ++it, item += gridDim.x) {
+    const int st = it & 1;
+    const int next = item + gridDim.x;
+    if (tid == 0 && next < nitems) issue(next, st ^ 1);
+    sartma::mbar_wait(&full[st], (it >> 1) & 1);
+    float2 *tile = smk + (size_t)st * NX * KC;
+    sarfft::tile_fft<NX, KC, KC, NT, +1>(tile, tw, tid);
+    // transpose into output rows: ob[zz][ix] with ix = (a - r_x) mod nx
+#pragma unroll
+    for (int i = tid; i < NX * KC; i += NT) {
+      const int a = i / KC, zz = i % KC;
+      const float2 o = tile[i];
+      const int ix = (a - rx) & (NX - 1);
+      if constexpr (CPLX) {
+        ob[zz * (NX + 1) + ix] = make_float2(o.x * sc, o.y * sc);
+      } else {
+        const float p = fmaf(o.x, o.x, o.y * o.y);
+        ob[zz * (NX + 1) + ix] = p > 0.f ? p * rsqrtf(p) * sc : 0.f;   // |o| (rsqrt: 2 ulp)
+      }
+    }
+    sartma::fence_proxy_async();
+    __syncthreads();  // tile st is free (next-next load may overwrite it), ob complete
+    const int zc = item % nzc, fy = item / nzc;
+    const int f = fy / v.ny, y = fy - f * v.ny;
+    int iy = y - ry;
+    if (iy < 0) iy += v.ny;
+    OT *outp = reinterpret_cast<OT *>(img) + ((size_t)f * nz * v.ny + iy) * NX;
+    const size_t zstride = (size_t)v.ny * NX;
+#pragma unroll
+    for (int i = tid; i < NX * KC; i += NT) {
+      const int zz = i / NX, ix = i % NX;
+      const int z = zc * KC + zz;
+      if (z < nz) {
+        int m = z + nz / 2;
+        if (m >= nz) m -= nz;
+        outp[m * zstride + ix] = ob[zz * (NX + 1) + ix];
+      }
+    }
+    __syncthreads();  // ob free
+  }
+}
+
 // ------------------------------------------------------------ dispatch ----
 #define SAR_SIZES(X) X(2) X(4) X(8) X(16) X(32) X(64) X(128) X(256) X(512) X(1024)
 
@@ -731,7 +985,6 @@ cudaError_t launch_mid(float2 *data, const float2 *tw, int F, int ny, int nx, in
     const int nchunk = (inner + KC - 1) / KC;
     const int nitems = nchunk * nx * F;
     const size_t smem = 2 * (size_t)ny * KC * sizeof(float2);
-    const int grid = nitems < num_sms ? nitems : num_sms;
     switch (ny) {
 #define X(N)                                                                                       \
   case N: {                                                                                        \
@@ -740,7 +993,8 @@ cudaError_t launch_mid(float2 *data, const float2 *tw, int F, int ny, int nx, in
       cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
       if (e != cudaSuccess) return e;                                                              \
     }                                                                                              \
-    kern<<<grid, nt_for(N), smem, s>>>(*tm, tw, nx, nchunk, nitems);                               \
+    const int maxg = num_sms * ctas_for(N);                                                        \
+    kern<<<nitems < maxg ? nitems : maxg, ntp_for(N), smem, s>>>(*tm, tw, nx, nchunk, nitems);     \
     return cudaGetLastError();                                                                     \
   }
       SAR_SIZES(X)
@@ -777,15 +1031,51 @@ cudaError_t launch_v(K kernel, dim3 grid, int nt, size_t smem, cudaStream_t s, c
   return cudaGetLastError();
 }
 
-cudaError_t launch_k3(const SarDeviceView &v, bool ifft, cudaStream_t s) {
+cudaError_t launch_k3(const SarDeviceView &v, bool ifft, cudaStream_t s, int num_sms) {
+  if ((v.nk & 1) == 0 && !getenv("SAR_K3_PLAIN")) {
+    const int nclass = (v.nx / 2 + 1) * (v.ny / 2 + 1);
+    switch (v.nz) {
+#define X(N)                                                                                                   \
+  case N: {                                                                                                    \
+    constexpr int CL = k3_cl_for(N);                                                                           \
+    const size_t hdr = (sizeof(K3Hdr<CL>) + 15) & ~(size_t)15;                                                 \
+    const size_t smem = K3W_STAGES * (hdr + (size_t)4 * CL * v.nk * sizeof(float2)) +                         \
+                        ((size_t)N * (4 * CL + 1) + (size_t)CL * v.nk) * sizeof(float2);                      \
+    if (smem <= 110 * 1024) {                                                                                  \
+      const int nitems_f = (nclass + CL - 1) / CL;                                                             \
+      const int nitems = nitems_f * v.F;                                                                       \
+      const int grid = nitems < 2 * num_sms ? nitems : 2 * num_sms;                                            \
+      auto kern = ifft ? k3_filter_stolt_ws<N, CL, true> : k3_filter_stolt_ws<N, CL, false>;                 \
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);      \
+      if (e != cudaSuccess) return e;                                                                          \
+      kern<<<grid, K3W_NT + 32, smem, s>>>(v, nitems_f);                                                       \
+      return cudaGetLastError();                                                                               \
+    }                                                                                                          \
+    break;                                                                                                     \
+  }
+      SAR_SIZES(X)
+#undef X
+    }
+  }
   const int nclass = (v.nx / 2 + 1) * (v.ny / 2 + 1);
-  dim3 grid((nclass + K3_CL - 1) / K3_CL, v.F);
-  const size_t smem = ((size_t)v.nk * K3_CC + (size_t)v.nz * K3_LD) * sizeof(float2);
   switch (v.nz) {
-#define X(N)                                                                           \
-  case N:                                                                              \
-    return ifft ? launch_v(k3_filter_stolt<N, true>, grid, K3_NT, smem, s, v)          \
-                : launch_v(k3_filter_stolt<N, false>, grid, K3_NT, smem, s, v);
+#define X(N)                                                                                                   \
+  case N: {                                                                                                    \
+    constexpr int CLW = k3_cl_for(N);                                                                          \
+    const size_t smw = ((size_t)v.nk * 4 * CLW + (size_t)N * (4 * CLW + 1)) * sizeof(float2);               \
+    const bool wide = CLW > 2 && smw <= 220 * 1024;                                                          \
+    const int CL = wide ? CLW : 2;                                                                             \
+    const size_t smem = ((size_t)v.nk * 4 * CL + (size_t)N * (4 * CL + 1)) * sizeof(float2);                 \
+    dim3 grid((nclass + CL - 1) / CL, v.F);                                                                    \
+    auto kern = wide ? (ifft ? k3_filter_stolt<N, CLW, true> : k3_filter_stolt<N, CLW, false>)               \
+                     : (ifft ? k3_filter_stolt<N, 2, true> : k3_filter_stolt<N, 2, false>);                  \
+    if (smem > 48 * 1024) {                                                                                    \
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);      \
+      if (e != cudaSuccess) return e;                                                                          \
+    }                                                                                                          \
+    kern<<<grid, K3_NT, smem, s>>>(v);                                                                         \
+    return cudaGetLastError();                                                                                 \
+  }
     SAR_SIZES(X)
 #undef X
   }
@@ -803,7 +1093,27 @@ cudaError_t launch_img(K kernel, dim3 grid, int nt, size_t smem, cudaStream_t s,
   return cudaGetLastError();
 }
 
-cudaError_t launch_k4b(const SarDeviceView &v, void *img, bool cplx, cudaStream_t s) {
+cudaError_t launch_k4b(const SarDeviceView &v, void *img, bool cplx, cudaStream_t s, const CUtensorMap *tm,
+                       int num_sms) {
+  if (tm && v.nx >= 32 && v.nx <= 512) {
+    const int nzc = (v.nz + KC - 1) / KC;
+    const int nitems = nzc * v.ny * v.F;
+    const size_t smem = 2 * (size_t)v.nx * KC * sizeof(float2) + (size_t)KC * (v.nx + 1) * (cplx ? 8 : 4);
+    switch (v.nx) {
+#define X(N)                                                                                           \
+  case N: {                                                                                            \
+    auto kern = cplx ? k4_xifft_mag_tma<N, true> : k4_xifft_mag_tma<N, false>;                        \
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+    if (e != cudaSuccess) return e;                                                                    \
+    const int cps = ctas_for(N) * smem <= 200 * 1024 ? ctas_for(N) : 1;                               \
+    const int maxg = num_sms * cps;                                                                    \
+    kern<<<nitems < maxg ? nitems : maxg, ntp_for(N), smem, s>>>(v, *tm, img, nzc, nitems);            \
+    return cudaGetLastError();                                                                         \
+  }
+      X(32) X(64) X(128) X(256) X(512)
+#undef X
+    }
+  }
   dim3 grid((v.nz + KC - 1) / KC, v.ny, v.F);
   const size_t smem = (size_t)v.nx * (KC + 1) * sizeof(float2);
   switch (v.nx) {
@@ -848,13 +1158,13 @@ int sar_launch_pipeline(sar_plan *p, const void *d_data, void *d_image, cudaStre
                            p->num_sms));
   if (ev) SAR_CHECK(cudaEventRecord(ev[2], s));
   if (stop_stage == 2) return SAR_OK;
-  SAR_CHECK(launch_k3(v, stop_stage != 3, s));
+  SAR_CHECK(launch_k3(v, stop_stage != 3, s, p->num_sms));
   if (ev) SAR_CHECK(cudaEventRecord(ev[3], s));
   if (stop_stage == 3) return SAR_OK;
   SAR_CHECK(launch_mid<+1>(v.w1, v.tw_y, v.F, v.ny, v.nx, v.nz, s, p->tma_mid1 ? &p->tm_w1_mid : nullptr,
                            p->num_sms));
   if (ev) SAR_CHECK(cudaEventRecord(ev[4], s));
-  SAR_CHECK(launch_k4b(v, d_image, complex_out != 0, s));
+  SAR_CHECK(launch_k4b(v, d_image, complex_out != 0, s, p->tma_rows1 ? &p->tm_w1_rows : nullptr, p->num_sms));
   if (ev) SAR_CHECK(cudaEventRecord(ev[5], s));
   return SAR_OK;
 }

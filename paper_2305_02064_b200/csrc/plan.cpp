@@ -112,6 +112,7 @@ int host_decompose(const sar_geom_desc *g, const sar_image_desc *im, uint32_t fl
   if (g->n_frames > 0 && !g->scan_xyz) return fail(SAR_ERR_INVALID_ARG, "scan_xyz is NULL");
   if (g->npx < 1 || g->npy < 1) return fail(SAR_ERR_INVALID_ARG, "npx, npy must be >= 1");
   if (g->n_k < 2) return fail(SAR_ERR_INVALID_ARG, "n_k must be >= 2");
+  if (g->n_k > SAR_MAX_NK) return fail(SAR_ERR_UNSUPPORTED, "n_k > SAR_MAX_NK");
   if (!pow2_in_range(im->nx) || !pow2_in_range(im->ny) || !pow2_in_range(im->nz))
     return fail(SAR_ERR_INVALID_ARG, "nx, ny, nz must be powers of two in [2, SAR_MAX_FFT]");
   if (g->npx > im->nx || g->npy > im->ny) return fail(SAR_ERR_INVALID_ARG, "raster larger than the FFT grid");

@@ -265,6 +265,7 @@ def test_non_tma_fallback_path(name, monkeypatch):
     """The plain (non-TMA) kernels used for odd n_k / unaligned rasters are
     forced with SAR_NO_TMA and must meet the same bar."""
     monkeypatch.setenv("SAR_NO_TMA", "1")
+    monkeypatch.setenv("SAR_K3_PLAIN", "1")
     _check_e2e(scenes.make_scene(name))
 
 
