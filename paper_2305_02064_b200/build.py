@@ -19,7 +19,7 @@ LIB = os.path.join(HERE, "libsar_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 SOURCES = ["plan.cpp", "kernels.cu"]
-HEADERS = [os.path.join(CSRC, h) for h in ("plan_internal.h", "fft_tile.cuh")] + \
+HEADERS = [os.path.join(CSRC, h) for h in ("plan_internal.h", "fft_tile.cuh", "fft_reg.cuh", "tma.cuh")] + \
     [os.path.join(ROOT, "include", "sar_b200.h")]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-ffp-contract=off,-O2",
          "-Xptxas", "-v", "--expt-relaxed-constexpr", "-I", os.path.join(ROOT, "include")]

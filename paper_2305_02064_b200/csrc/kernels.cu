@@ -27,6 +27,7 @@
 #include <type_traits>
 
 #include "fft_tile.cuh"
+#include "fft_reg.cuh"
 #include "tma.cuh"
 #include "plan_internal.h"
 
@@ -207,6 +208,7 @@ __global__ void __launch_bounds__(K1_NT + 32, 1)
   float2 *tile = reinterpret_cast<float2 *>(smraw);                       // [NX][C]
   unsigned char *stages = smraw + (size_t)NX * C * sizeof(float2);
   constexpr size_t STAGE = K1_BOX_BYTES + BRMAX * sizeof(float);
+  float2 *tws = reinterpret_cast<float2 *>(stages + K1_STAGES * STAGE);   // [NX] twiddles
   __shared__ __align__(8) uint64_t full[K1_STAGES], empty[K1_STAGES];
   const int tid = threadIdx.x;
   const int nchunk = (v.nk + C - 1) / C;
@@ -219,6 +221,7 @@ __global__ void __launch_bounds__(K1_NT + 32, 1)
   }
   if (!REGACC)
     for (int i = tid; i < NX * C; i += K1_NT + 32) tile[i] = make_float2(0.f, 0.f);
+  for (int i = tid; i < NX; i += K1_NT + 32) tws[i] = v.tw_x[i];
   __syncthreads();
 
   if (tid >= K1_NT) {
@@ -331,14 +334,20 @@ __global__ void __launch_bounds__(K1_NT + 32, 1)
       for (int i = nbox * br * C + tid; i < NX * C; i += K1_NT) tile[i] = make_float2(0.f, 0.f);
     }
     sarfft::tile_sync<1, K1_NT>();
-    sarfft::tile_fft<NX, C, C, K1_NT, -1, 1>(tile, v.tw_x, tid);
-    float2 *out = v.w0 + ((size_t)(f * v.ny + vy) * NX) * (size_t)v.nk;
-    for (int i = tid; i < NX * C; i += K1_NT) {
-      const int vx = i / C, kk = kc * C + (i % C);
-      if (kk < v.nk) out[(size_t)vx * v.nk + kk] = tile[i];
-      if (!REGACC) tile[i] = make_float2(0.f, 0.f);
-    }
+    // x-FFT (two-pass register FFT; the accumulation tile doubles as its work
+    // tile) with the transformed rows stored straight to W0
+    float2 *out = v.w0 + ((size_t)(f * v.ny + vy) * NX) * (size_t)v.nk + kc * C;
+    const int cmax = v.nk - kc * C;
+    sarfft2::fft<NX, C, C, K1_NT, -1, 1, false, (NX == 512 ? 16 : 0)>(
+        tile, tws, tid, [&](int c, int m) { return tile[m * C + c]; }, [] {},
+        [&](int c, int m, float2 x) {
+          if (c < cmax) __stcs(out + (size_t)m * v.nk + c, x);
+        });
     sarfft::tile_sync<1, K1_NT>();
+    if (!REGACC) {
+      for (int i = tid; i < NX * C; i += K1_NT) tile[i] = make_float2(0.f, 0.f);
+      sarfft::tile_sync<1, K1_NT>();
+    }
   }
 }
 
@@ -436,6 +445,176 @@ __global__ void __launch_bounds__(ntp_for(N), ctas_for(N))
     }
   }
   if (tid == 0) sartma::bulk_wait0();
+}
+
+// Warp-specialised persistent mid-axis FFT (K2 / K4a, ny <= 512, `inner`
+// even).  A producer warp streams [N][16] tiles (3-D TMA boxes {16 inner, 1
+// column, <=256 rows}) into an S-stage mbarrier ring; NTC consumer threads run
+// the two-pass register FFT (fft_reg.cuh), hand the stage back right after
+// the pass-1 loads, and store the transformed rows straight to global memory
+// (each warp store = two full 128-byte lines).
+template <int N>
+constexpr int mid2_stages() { return N >= 256 ? 2 : 4; }
+template <int N>
+constexpr size_t mid2_smem() {
+  return ((size_t)mid2_stages<N>() * N * KC + (size_t)N * KC + N) * sizeof(float2);
+}
+template <int N>
+constexpr int mid2_ctas() {
+  return (int)((200 * 1024) / mid2_smem<N>()) < 1 ? 1 : (int)((200 * 1024) / mid2_smem<N>());
+}
+
+template <int N, int DIR>
+__global__ void __launch_bounds__(sarfft2::nt_fft<N, KC>() + 32)
+    k_fft_mid2(const __grid_constant__ CUtensorMap tm, float2 *__restrict__ data, const float2 *__restrict__ twg,
+               int nx, int inner, int nchunk, int nitems) {
+  constexpr int NTC = sarfft2::nt_fft<N, KC>();
+  constexpr int S = mid2_stages<N>();
+  constexpr int ROWS = N < 256 ? N : 256;
+  constexpr int NBOX = N / ROWS;
+  constexpr uint32_t TILE_BYTES = N * KC * sizeof(float2);
+  extern __shared__ __align__(128) float2 smm[];
+  float2 *ring = smm;                         // [S][N][16]
+  float2 *work = smm + (size_t)S * N * KC;    // [N][16]
+  float2 *tw = work + (size_t)N * KC;         // [N]
+  __shared__ __align__(8) uint64_t full[S], empty[S];
+  const int tid = threadIdx.x;
+  for (int i = tid; i < N; i += NTC + 32) tw[i] = twg[i];
+  if (tid == 0) {
+    for (int i = 0; i < S; ++i) {
+      sartma::mbar_init(&full[i], 1);
+      sartma::mbar_init(&empty[i], 1);
+    }
+    sartma::fence_barrier_init();
+  }
+  __syncthreads();
+  if (tid >= NTC) {
+    if (tid == NTC) {
+      unsigned n = 0;
+      for (int item = blockIdx.x; item < nitems; item += gridDim.x, ++n) {
+        const int st = n % S;
+        if (n >= S) sartma::mbar_wait(&empty[st], ((n / S) - 1) & 1);
+        const int chunk = item % nchunk, rest = item / nchunk;
+        const int a = rest % nx, f = rest / nx;
+        sartma::mbar_arrive_expect_tx(&full[st], TILE_BYTES);
+#pragma unroll
+        for (int bx = 0; bx < NBOX; ++bx)
+          sartma::tma_load_3d(ring + (size_t)st * N * KC + bx * ROWS * KC, &tm, chunk * KC, a, f * N + bx * ROWS,
+                              &full[st]);
+      }
+    }
+    return;
+  }
+  const size_t row = (size_t)nx * inner;
+  unsigned n = 0;
+  for (int item = blockIdx.x; item < nitems; item += gridDim.x, ++n) {
+    const int st = n % S;
+    sartma::mbar_wait(&full[st], (n / S) & 1);
+    const int chunk = item % nchunk, rest = item / nchunk;
+    const int a = rest % nx, f = rest / nx;
+    const float2 *stage = ring + (size_t)st * N * KC;
+    float2 *base = data + ((size_t)f * N * nx + a) * (size_t)inner + chunk * KC;
+    const int cmax = inner - chunk * KC;
+    sarfft2::fft<N, KC, KC, NTC, DIR, 1, false>(
+        work, tw, tid, [&](int c, int m) { return stage[m * KC + c]; },
+        [&] {
+          if (tid == 0) sartma::mbar_arrive(&empty[st]);
+        },
+        [&](int c, int m, float2 v) {
+          if (c < cmax) __stcs(base + (size_t)m * row + c, v);
+        });
+  }
+}
+
+// Warp-specialised persistent K4b (nx <= 512, n_z even): [nx][16 z] tiles of
+// W1 row y stream through an S-stage TMA ring; the consumers run the inverse
+// x-FFT (pass 2 mapped so that one warp owns 32 consecutive x of one z) and
+// write |o|/(nx ny nz) (or the scaled complex value) straight into the rolled
+// image rows (reading R8, R11): coalesced 128-byte segments, no transpose
+// buffer.
+template <int NX, bool CPLX>
+constexpr size_t k4b2_smem() {
+  return ((size_t)2 * NX * KC + (size_t)NX * (KC + 1) + NX) * sizeof(float2);
+}
+template <int NX>
+constexpr int k4b2_ctas() {
+  return (int)((200 * 1024) / k4b2_smem<NX, false>()) < 1 ? 1 : (int)((200 * 1024) / k4b2_smem<NX, false>());
+}
+
+template <int NX, bool CPLX>
+__global__ void __launch_bounds__(sarfft2::nt_fft<NX, KC>() + 32)
+    k4_xifft_mag2(const SarDeviceView v, const __grid_constant__ CUtensorMap tm, void *__restrict__ img, int nzc,
+                  int nitems) {
+  constexpr int NTC = sarfft2::nt_fft<NX, KC>();
+  constexpr int S = 2;
+  constexpr int ROWS = NX < 256 ? NX : 256;
+  constexpr int NBOX = NX / ROWS;
+  constexpr uint32_t TILE_BYTES = NX * KC * sizeof(float2);
+  using OT = typename std::conditional<CPLX, float2, float>::type;
+  extern __shared__ __align__(128) float2 smk[];
+  float2 *ring = smk;                          // [S][NX][16]
+  float2 *work = smk + (size_t)S * NX * KC;    // [NX][17]
+  float2 *tw = work + (size_t)NX * (KC + 1);   // [NX]
+  __shared__ __align__(8) uint64_t full[S], empty[S];
+  const int tid = threadIdx.x;
+  for (int i = tid; i < NX; i += NTC + 32) tw[i] = v.tw_x[i];
+  if (tid == 0) {
+    for (int i = 0; i < S; ++i) {
+      sartma::mbar_init(&full[i], 1);
+      sartma::mbar_init(&empty[i], 1);
+    }
+    sartma::fence_barrier_init();
+  }
+  __syncthreads();
+  if (tid >= NTC) {
+    if (tid == NTC) {
+      unsigned n = 0;
+      for (int item = blockIdx.x; item < nitems; item += gridDim.x, ++n) {
+        const int st = n % S;
+        if (n >= S) sartma::mbar_wait(&empty[st], ((n / S) - 1) & 1);
+        const int zc = item % nzc, fy = item / nzc;  // fy = f*ny + y
+        sartma::mbar_arrive_expect_tx(&full[st], TILE_BYTES);
+#pragma unroll
+        for (int bx = 0; bx < NBOX; ++bx)
+          sartma::tma_load_3d(ring + (size_t)st * NX * KC + bx * ROWS * KC, &tm, zc * KC, bx * ROWS, fy, &full[st]);
+      }
+    }
+    return;
+  }
+  const int nz = v.nz;
+  const int rx = ((v.roll_x % NX) + NX) % NX;
+  const int ry = ((v.roll_y % v.ny) + v.ny) % v.ny;
+  const float sc = v.img_scale;
+  const size_t zstride = (size_t)v.ny * NX;
+  unsigned n = 0;
+  for (int item = blockIdx.x; item < nitems; item += gridDim.x, ++n) {
+    const int st = n % S;
+    sartma::mbar_wait(&full[st], (n / S) & 1);
+    const int zc = item % nzc, fy = item / nzc;
+    const int f = fy / v.ny, y = fy - f * v.ny;
+    int iy = y - ry;
+    if (iy < 0) iy += v.ny;
+    OT *outp = reinterpret_cast<OT *>(img) + ((size_t)f * nz * v.ny + iy) * NX;
+    const float2 *stage = ring + (size_t)st * NX * KC;
+    sarfft2::fft<NX, KC, KC + 1, NTC, +1, 1, true>(
+        work, tw, tid, [&](int c, int m) { return stage[m * KC + c]; },
+        [&] {
+          if (tid == 0) sartma::mbar_arrive(&empty[st]);
+        },
+        [&](int c, int a, float2 o) {
+          const int z = zc * KC + c;
+          if (z < nz) {
+            int m = z + nz / 2;
+            if (m >= nz) m -= nz;
+            const int ix = (a - rx) & (NX - 1);
+            if constexpr (CPLX) {
+              __stcs(reinterpret_cast<float2 *>(outp) + (size_t)m * zstride + ix, make_float2(o.x * sc, o.y * sc));
+            } else {
+              __stcs(reinterpret_cast<float *>(outp) + (size_t)m * zstride + ix, sqrtf(fmaf(o.x, o.x, o.y * o.y)) * sc);
+            }
+          }
+        });
+  }
 }
 
 // ---------------------------------------------------------------- K3 ------
@@ -950,7 +1129,8 @@ cudaError_t launch_k1(const SarDeviceView &v, const float2 *data, bool fft, cuda
     const int nitems = nchunk * v.ny * v.F;
     const int nbox = (v.npx + br - 1) / br;
     const int brmax = K1_BOX_BYTES / (C * 8);
-    const size_t smem = (size_t)v.nx * C * sizeof(float2) + K1_STAGES * ((size_t)K1_BOX_BYTES + brmax * sizeof(float));
+    const size_t smem = (size_t)v.nx * C * sizeof(float2) + K1_STAGES * ((size_t)K1_BOX_BYTES + brmax * sizeof(float)) +
+                        (size_t)v.nx * sizeof(float2);
     const int grid = nitems < num_sms ? nitems : num_sms;
     switch (v.nx) {
 #define X(N)                                                                                          \
@@ -981,6 +1161,28 @@ cudaError_t launch_k1(const SarDeviceView &v, const float2 *data, bool fft, cuda
 template <int DIR>
 cudaError_t launch_mid(float2 *data, const float2 *tw, int F, int ny, int nx, int inner, cudaStream_t s,
                        const CUtensorMap *tm, int num_sms) {
+  if (tm && ny <= 512 && !getenv("SAR_MID_OLD")) {
+    const int nchunk = (inner + KC - 1) / KC;
+    const int nitems = nchunk * nx * F;
+    switch (ny) {
+#define X(N)                                                                                       \
+  case N: {                                                                                        \
+    auto kern = k_fft_mid2<N, DIR>;                                                                \
+    constexpr size_t smem = mid2_smem<N>();                                                        \
+    if (smem > 48 * 1024) {                                                                        \
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+      if (e != cudaSuccess) return e;                                                              \
+    }                                                                                              \
+    const int maxg = num_sms * mid2_ctas<N>();                                                     \
+    kern<<<nitems < maxg ? nitems : maxg, sarfft2::nt_fft<N, KC>() + 32, smem, s>>>(*tm, data, tw, nx, inner, \
+                                                                                  nchunk, nitems); \
+    return cudaGetLastError();                                                                     \
+  }
+      X(2) X(4) X(8) X(16) X(32) X(64) X(128) X(256) X(512)
+#undef X
+    }
+    return cudaErrorInvalidValue;
+  }
   if (tm && ny <= 512) {
     const int nchunk = (inner + KC - 1) / KC;
     const int nitems = nchunk * nx * F;
@@ -1095,6 +1297,26 @@ cudaError_t launch_img(K kernel, dim3 grid, int nt, size_t smem, cudaStream_t s,
 
 cudaError_t launch_k4b(const SarDeviceView &v, void *img, bool cplx, cudaStream_t s, const CUtensorMap *tm,
                        int num_sms) {
+  if (tm && v.nx <= 512 && !getenv("SAR_K4B_OLD")) {
+    const int nzc = (v.nz + KC - 1) / KC;
+    const int nitems = nzc * v.ny * v.F;
+    switch (v.nx) {
+#define X(N)                                                                                           \
+  case N: {                                                                                            \
+    auto kern = cplx ? k4_xifft_mag2<N, true> : k4_xifft_mag2<N, false>;                               \
+    constexpr size_t smem = k4b2_smem<N, false>();                                                     \
+    if (smem > 48 * 1024) {                                                                            \
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+      if (e != cudaSuccess) return e;                                                                  \
+    }                                                                                                  \
+    const int maxg = num_sms * k4b2_ctas<N>();                                                         \
+    kern<<<nitems < maxg ? nitems : maxg, sarfft2::nt_fft<N, KC>() + 32, smem, s>>>(v, *tm, img, nzc, nitems); \
+    return cudaGetLastError();                                                                         \
+  }
+      X(2) X(4) X(8) X(16) X(32) X(64) X(128) X(256) X(512)
+#undef X
+    }
+  }
   if (tm && v.nx >= 32 && v.nx <= 512) {
     const int nzc = (v.nz + KC - 1) / KC;
     const int nitems = nzc * v.ny * v.F;

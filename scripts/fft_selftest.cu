@@ -1,0 +1,145 @@
+// fft_selftest.cu -- accuracy and throughput check of the two tile FFT engines
+// (fft_tile.cuh: 3-pass radix-8 Stockham; fft_reg.cuh: 2-pass register DFTs)
+// against an fp64 direct DFT, all on the GPU.  Build + run:
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 --expt-relaxed-constexpr \
+//        -I paper_2305_02064_b200/csrc scripts/fft_selftest.cu -o scripts/fft_selftest && scripts/fft_selftest
+#include <cstdio>
+#include <cmath>
+#include <vector>
+
+#include "fft_reg.cuh"
+#include "fft_tile.cuh"
+
+constexpr int C = 16;
+
+__global__ void dft_ref(const float2 *x, double2 *X, int N, int dir) {
+  const int c = blockIdx.y, n = blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= N) return;
+  double re = 0, im = 0;
+  for (int m = 0; m < N; ++m) {
+    const long long t = ((long long)m * n) % N;
+    double s, co;
+    sincospi(2.0 * dir * (double)t / N, &s, &co);
+    const float2 v = x[m * C + c];
+    re += v.x * co - v.y * s;
+    im += v.x * s + v.y * co;
+  }
+  X[n * C + c] = make_double2(re, im);
+}
+
+template <int N, int DIR, int NT>
+__global__ void __launch_bounds__(NT) run_new(const float2 *x, float2 *y, const float2 *twg, int reps) {
+  extern __shared__ float2 sm[];
+  float2 *work = sm;
+  float2 *tw = sm + N * C;
+  for (int i = threadIdx.x; i < N; i += NT) tw[i] = twg[i];
+  __syncthreads();
+  const float2 *src = x + (size_t)blockIdx.x * N * C * 0;
+  for (int rep = 0; rep < reps; ++rep) {
+    sarfft2::fft<N, C, C, NT, DIR, 0, false>(
+        work, tw, threadIdx.x, [&](int c, int n) { return src[n * C + c]; }, [] {},
+        [&](int c, int n, float2 v) {
+          if (rep == reps - 1 && blockIdx.x == 0) y[n * C + c] = v;
+          else if (v.x == 12345.f) y[0] = v;  // keep the work alive
+        });
+  }
+}
+
+template <int N, int DIR, int NT>
+__global__ void __launch_bounds__(NT) run_old(const float2 *x, float2 *y, const float2 *twg, int reps) {
+  extern __shared__ float2 sm[];
+  float2 *tile = sm;
+  float2 *tw = sm + N * C;
+  for (int i = threadIdx.x; i < N; i += NT) tw[i] = twg[i];
+  for (int rep = 0; rep < reps; ++rep) {
+    for (int i = threadIdx.x; i < N * C; i += NT) tile[i] = x[i];
+    __syncthreads();
+    sarfft::tile_fft<N, C, C, NT, DIR>(tile, tw, threadIdx.x);
+    for (int i = threadIdx.x; i < N * C; i += NT) {
+      const float2 v = tile[i];
+      if (rep == reps - 1 && blockIdx.x == 0) y[i] = v;
+      else if (v.x == 12345.f) y[0] = v;
+    }
+    __syncthreads();
+  }
+}
+
+template <int N, int DIR>
+void check(float2 *dx, float2 *dy, double2 *dX, float2 *dtw, bool bench) {
+  constexpr int NT = 256;
+  constexpr int NTO = N * C / 8 < 32 ? 32 : (N * C / 8 > 1024 ? 1024 : N * C / 8);
+  std::vector<float2> tw(N);
+  for (int m = 0; m < N; ++m) tw[m] = make_float2((float)cos(-2 * M_PI * m / N), (float)sin(-2 * M_PI * m / N));
+  cudaMemcpy(dtw, tw.data(), N * 8, cudaMemcpyHostToDevice);
+  dft_ref<<<dim3((N + 127) / 128, C), 128>>>(dx, dX, N, DIR);
+  const size_t smn = (size_t)(N * C + N) * 8;
+  const size_t smo = (size_t)(N * C + N) * 8;
+  cudaFuncSetAttribute(run_new<N, DIR, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smn);
+  cudaFuncSetAttribute(run_old<N, DIR, NTO>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smo);
+  std::vector<double2> X(N * C);
+  std::vector<float2> Y(N * C);
+  cudaMemcpy(X.data(), dX, N * C * 16, cudaMemcpyDeviceToHost);
+  for (int which = 0; which < 2; ++which) {
+    cudaMemset(dy, 0, N * C * 8);
+    if (which == 0) run_new<N, DIR, NT><<<1, NT, smn>>>(dx, dy, dtw, 1);
+    else run_old<N, DIR, NTO><<<1, NTO, smo>>>(dx, dy, dtw, 1);
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) { printf("CUDA error %s\n", cudaGetErrorString(e)); exit(1); }
+    cudaMemcpy(Y.data(), dy, N * C * 8, cudaMemcpyDeviceToHost);
+    double num = 0, den = 0;
+    for (int i = 0; i < N * C; ++i) {
+      const double dr = Y[i].x - X[i].x, di = Y[i].y - X[i].y;
+      num += dr * dr + di * di;
+      den += X[i].x * X[i].x + X[i].y * X[i].y;
+    }
+    float ms = 0;
+    double gel = 0;
+    if (bench) {
+      const int reps = 200, blocks = 148 * 4;
+      cudaEvent_t a, b;
+      cudaEventCreate(&a);
+      cudaEventCreate(&b);
+      cudaEventRecord(a);
+      if (which == 0) run_new<N, DIR, NT><<<blocks, NT, smn>>>(dx, dy, dtw, reps);
+      else run_old<N, DIR, NTO><<<blocks, NTO, smo>>>(dx, dy, dtw, reps);
+      cudaEventRecord(b);
+      cudaEventSynchronize(b);
+      cudaEventElapsedTime(&ms, a, b);
+      gel = (double)blocks * reps * N * C / (ms * 1e-3) / 1e9;
+    }
+    printf("N=%5d DIR=%+d %s rel-L2 %.3e  %s%.1f Gelem/s\n", N, DIR, which == 0 ? "reg2 " : "tile3", sqrt(num / den),
+           bench ? "" : "(no bench) ", gel);
+    if (!(sqrt(num / den) < 5e-6)) { printf("FAIL\n"); exit(1); }
+  }
+}
+
+int main() {
+  float2 *dx, *dy, *dtw;
+  double2 *dX;
+  cudaMalloc(&dx, 1024 * C * 8);
+  cudaMalloc(&dy, 1024 * C * 8);
+  cudaMalloc(&dX, 1024 * C * 16);
+  cudaMalloc(&dtw, 1024 * 8);
+  std::vector<float2> h(1024 * C);
+  unsigned s = 12345;
+  for (auto &v : h) {
+    s = s * 1664525u + 1013904223u;
+    v.x = (float)((s >> 8) & 0xffff) / 65536.f - 0.5f;
+    s = s * 1664525u + 1013904223u;
+    v.y = (float)((s >> 8) & 0xffff) / 65536.f - 0.5f;
+  }
+  cudaMemcpy(dx, h.data(), h.size() * 8, cudaMemcpyHostToDevice);
+  check<2, -1>(dx, dy, dX, dtw, false);
+  check<4, -1>(dx, dy, dX, dtw, false);
+  check<8, 1>(dx, dy, dX, dtw, false);
+  check<16, -1>(dx, dy, dX, dtw, false);
+  check<32, 1>(dx, dy, dX, dtw, false);
+  check<64, -1>(dx, dy, dX, dtw, true);
+  check<128, 1>(dx, dy, dX, dtw, true);
+  check<256, -1>(dx, dy, dX, dtw, true);
+  check<512, -1>(dx, dy, dX, dtw, true);
+  check<512, 1>(dx, dy, dX, dtw, true);
+  check<1024, 1>(dx, dy, dX, dtw, true);
+  printf("ALL OK\n");
+  return 0;
+}
