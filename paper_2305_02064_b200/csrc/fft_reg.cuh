@@ -160,10 +160,14 @@ struct Split {
 
 // Named barrier over the NT threads running the transform (BARID 0 =
 // __syncthreads; warp-specialised kernels keep their producer warp out).
+// BARID < 0: the barrier id is the runtime value rbar (groups of threads that
+// run the same code on different barriers share one copy of it).
 template <int BARID, int NT>
-__device__ __forceinline__ void sync() {
+__device__ __forceinline__ void sync(int rbar = 0) {
   if constexpr (BARID == 0) {
     __syncthreads();
+  } else if constexpr (BARID < 0) {
+    asm volatile("bar.sync %0, %1;" ::"r"(rbar), "n"(NT) : "memory");
   } else {
     asm volatile("bar.sync %0, %1;" ::"n"(BARID), "n"(NT) : "memory");
   }
@@ -186,7 +190,7 @@ __device__ __forceinline__ void sync() {
 template <int N, int C, int LDW, int NT, int DIR, int BARID, bool I_FAST2, int R1SEL = 0, typename Load,
           typename Loaded, typename Store>
 __device__ __forceinline__ void fft(float2 *__restrict__ work, const float2 *__restrict__ tw, int tid, Load &&load,
-                                    Loaded &&loaded, Store &&store) {
+                                    Loaded &&loaded, Store &&store, int rbar = 0) {
   static_assert((N & (N - 1)) == 0 && N >= 2 && N <= 1024, "power-of-two length in [2, 1024]");
   constexpr int R1 = R1SEL ? R1SEL : Split<N>::R1, R2 = N / R1;
   static_assert(R1 <= 32 && R2 <= 32, "two passes of radix <= 32");
@@ -202,7 +206,7 @@ __device__ __forceinline__ void fft(float2 *__restrict__ work, const float2 *__r
         for (int r = 0; r < R1; ++r) v[it][r] = load(c, r);
       }
     }
-    sync<BARID, NT>();
+    sync<BARID, NT>(rbar);
     loaded();
 #pragma unroll
     for (int it = 0; it < IT; ++it) {
@@ -229,7 +233,7 @@ __device__ __forceinline__ void fft(float2 *__restrict__ work, const float2 *__r
         for (int r = 0; r < R1; ++r) v[it][r] = load(c, i + r * R2);
       }
     }
-    sync<BARID, NT>();
+    sync<BARID, NT>(rbar);
     loaded();
 #pragma unroll
     for (int it = 0; it < IT1; ++it) {
@@ -243,7 +247,7 @@ __device__ __forceinline__ void fft(float2 *__restrict__ work, const float2 *__r
         });
       }
     }
-    sync<BARID, NT>();
+    sync<BARID, NT>(rbar);
     // pass 2: butterflies one at a time (reads and writes disjoint per thread)
     constexpr int NB2 = C * R1;
     constexpr int IT2 = (NB2 + NT - 1) / NT;

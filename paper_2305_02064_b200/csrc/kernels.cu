@@ -673,37 +673,92 @@ __device__ __forceinline__ double kr2_of(const SarDeviceView &v, int a, int b) {
   return __dadd_rn(__dmul_rn(kx, kx), __dmul_rn(ky, ky));
 }
 
-// One CTA = CL "mirror classes" of spectral columns (CL = 2 for n_z >= 128,
-// more for short columns so that the CTA's 256 threads stay busy).
-// k_r^2 = kx^2 + ky^2 is the same for (a,b), (-a,b), (a,-b), (-a,-b), so the
-// filter H(k_r, k_i) and the Stolt pull weights (i0, tau)(k_r, j) -- the fp64
-// part of the step -- are computed once per class and applied to its (up to
-// 4) columns.  Each column's n_k source samples are contiguous in W0 and
-// arrive by TMA bulk copies (cp.async.bulk + mbarrier) into fin[slot][i].
-constexpr int K3_NT = 256;
-constexpr int k3_cl_for(int nz) { return nz >= 128 ? 2 : (nz >= 64 ? 4 : 8); }
+// Filter value H(k_r, k_i) = k_z e^{+j k_z R_ref} / P(f_i) (0 when evanescent),
+// readings R2-R4; rr = R_ref / (2 pi), phase reduced in turns.
+__device__ __forceinline__ float2 filter_h(const SarDeviceView &v, double ki, double kr2, double rr, int i) {
+  const double q = 4.0 * ki * ki - kr2;
+  float2 hh = make_float2(0.f, 0.f);
+  if (q > 0.0) {
+    const double kz = fast_dsqrt(q);
+    double turns = kz * rr;
+    turns -= rint(turns);
+    float sn, cs;
+    __sincosf((float)turns * 6.28318530717958647692f, &sn, &cs);
+    const float kzf = (float)kz;
+    hh = make_float2(kzf * cs, kzf * sn);
+    if (v.pinv) hh = cmul(hh, v.pinv[i]);
+  }
+  return hh;
+}
 
-template <int NZ, int CL, bool DO_IFFT>
-__global__ void __launch_bounds__(K3_NT) k3_filter_stolt(const SarDeviceView v) {
-  constexpr int CC = 4 * CL;        // column slots
-  constexpr int LD = CC + 1;        // padded row stride of the [NZ][CC] output tile
-  extern __shared__ __align__(16) float2 sm[];
+// U independent evaluations per thread of the filter table [CL][nk] (ILP for
+// the fp64 chains); idx = t0 + u*stride
+template <int U, typename KR2, typename KS>
+__device__ __forceinline__ void filter_table(const SarDeviceView &v, float2 *htab, int total, int nk, int t0,
+                                             int stride, double rr, KR2 &&kr2_of_cl, KS &&ks) {
+  for (int base = t0; base < total; base += U * stride) {
+    float2 hv[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int idx = base + u * stride;
+      hv[u] = make_float2(0.f, 0.f);
+      if (idx < total) {
+        const int cl = idx / nk, i = idx - cl * nk;
+        hv[u] = filter_h(v, ks(i), kr2_of_cl(cl), rr, i);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int idx = base + u * stride;
+      if (idx < total) htab[idx] = hv[u];
+    }
+  }
+}
+
+// K3, one small CTA per CL mirror classes (CL = 1 at n_z = 512: the <= 4
+// columns (+-a, +-b) that share k_r^2).  128 threads and ~40 KB of shared
+// memory, so ~5 CTAs are resident per SM and the hardware overlaps their
+// load / fp64 / FFT phases.  Steps: (1) stream the member columns in (n_k
+// contiguous samples each); (2) filter H = k_z e^{+j k_z R_ref}/P on the
+// source grid, once per class (readings R2-R4); (3) Stolt pull with the
+// filter folded into the two complex interpolation weights, decisions bit-exact
+// (R5, R9), once per (class, j), applied to every member; (4) inverse z-FFT
+// (two-pass register FFT, the Stolt tile doubles as its work tile) whose
+// pass 2 stores each column contiguously [col][z].
+constexpr int K3C_NT = 128;
+template <int NZ>
+constexpr int k3c_r1() { return NZ == 512 ? 16 : sarfft2::Split<NZ>::R1; }
+template <int NZ>
+constexpr int k3c_cl() {
+  constexpr int cc = K3C_NT / (NZ / k3c_r1<NZ>());
+  return cc / 4 > 8 ? 8 : (cc / 4 < 1 ? 1 : cc / 4);
+}
+template <int NZ>
+size_t k3c_smem(int nk) {
+  constexpr int CL = k3c_cl<NZ>();
+  return ((size_t)4 * CL * nk + (size_t)CL * nk + (size_t)NZ * (4 * CL + 1)) * sizeof(float2);
+}
+
+template <int NZ, bool DO_IFFT>
+__global__ void __launch_bounds__(K3C_NT, 4) k3_class(const SarDeviceView v) {
+  constexpr int CL = k3c_cl<NZ>();
+  constexpr int CC = 4 * CL;
+  constexpr int LD = CC + 1;
+  extern __shared__ __align__(16) float2 sm3[];
   __shared__ double kr2s[CL];
   __shared__ int nmem[CL], mslot[CL][4];
-  __shared__ int colof[CC];        // column index of each used slot
+  __shared__ int colof[CC];
   __shared__ int nused;
-  __shared__ __align__(8) uint64_t bar;
   const int nk = v.nk;
-  float2 *fin = sm;                                  // [CC][nk]  source spectrum -> filtered
-  float2 *fout = sm + (size_t)CC * nk;               // [NZ][LD]  Stolt output
+  float2 *fin = sm3;                                 // [CC][nk]  source spectrum
+  float2 *htab = fin + (size_t)CC * nk;              // [CL][nk]  filter
+  float2 *fout = htab + (size_t)CL * nk;             // [NZ][LD]  Stolt output / FFT work
   const int tid = threadIdx.x;
   const int ncol = v.nx * v.ny;
   const int hx = v.nx / 2 + 1, hy = v.ny / 2 + 1;
   const int nclass = hx * hy;
   const int q0 = blockIdx.x * CL;
   const int f = blockIdx.y;
-  const float2 *wf = v.w0 + (size_t)f * ncol * (size_t)nk;
-  const bool bulk = (nk & 1) == 0;   // 16-byte aligned columns
   if (tid == 0) {
     int n = 0;
     for (int cl = 0; cl < CL; ++cl) {
@@ -722,136 +777,259 @@ __global__ void __launch_bounds__(K3_NT) k3_filter_stolt(const SarDeviceView v) 
           colof[n++] = c4[m];
         }
     }
+    for (int sl = n; sl < CC; ++sl) colof[sl] = -1;
     nused = n;
-    if (bulk) {
-      sartma::mbar_init(&bar, 1);
-      sartma::fence_barrier_init();
-      sartma::mbar_arrive_expect_tx(&bar, (uint32_t)n * (uint32_t)nk * 8u);
-      for (int sl = 0; sl < n; ++sl) sartma::bulk_g2s(fin + sl * nk, wf + (size_t)colof[sl] * nk, (uint32_t)nk * 8u, &bar);
-    }
   }
   __syncthreads();
   const int nu = nused;
-  // 1. load the member columns
-  if (bulk) {
-    sartma::mbar_wait(&bar, 0);
+  // 1. member columns (streaming loads, 16 B per thread when n_k is even)
+  const float2 *wf = v.w0 + (size_t)f * ncol * (size_t)nk;
+  if ((nk & 1) == 0) {
+    const int h2 = nk / 2;
+    for (int e = tid; e < nu * h2; e += K3C_NT) {
+      const int sl = e / h2, i = e - sl * h2;
+      const float4 x = __ldcs(reinterpret_cast<const float4 *>(wf + (size_t)colof[sl] * nk) + i);
+      reinterpret_cast<float4 *>(fin + sl * nk)[i] = x;
+    }
   } else {
-    for (int sl = 0; sl < nu; ++sl) {
-      const float2 *src = wf + (size_t)colof[sl] * nk;
-      for (int i = tid; i < nk; i += K3_NT) fin[sl * nk + i] = __ldcs(src + i);
+    for (int e = tid; e < nu * nk; e += K3C_NT) {
+      const int sl = e / nk, i = e - sl * nk;
+      fin[e] = __ldcs(wf + (size_t)colof[sl] * nk + i);
     }
-    __syncthreads();
   }
-  // 2. filter H = k_z exp(+j k_z R_ref) / P(f) on the source grid (in place),
-  //    once per class, applied to its columns
+  // 2. filter table H(k_r, k_i) per class (4 independent fp64 chains per thread)
   const double rr = v.rref[f] * (1.0 / TWO_PI);
-#pragma unroll
-  for (int cl = 0; cl < CL; ++cl) {
-    const double kr2 = kr2s[cl];
-    const int nm = nmem[cl];
-    if (nm == 0) continue;
-    for (int i = tid; i < nk; i += K3_NT) {
-      const double ki = v.k[i];
-      const double q = 4.0 * ki * ki - kr2;
-      float2 h = make_float2(0.f, 0.f);
-      if (q > 0.0) {
-        const double kz = fast_dsqrt(q);
-        double turns = kz * rr;
-        turns -= rint(turns);
-        float sn, cs;
-        __sincosf((float)turns * 6.28318530717958647692f, &sn, &cs);
-        const float kzf = (float)kz;
-        h = make_float2(kzf * cs, kzf * sn);
-        if (v.pinv) h = cmul(h, v.pinv[i]);
-      }
-      for (int m = 0; m < nm; ++m) {
-        float2 *x = fin + mslot[cl][m] * nk + i;
-        *x = cmul(*x, h);
-      }
-    }
-  }
+  filter_table<4>(v, htab, CL * nk, nk, tid, K3C_NT, rr, [&](int cl) { return kr2s[cl]; },
+                  [&](int i) { return __ldg(v.k + i); });
   __syncthreads();
-  // 3. Stolt pull onto the uniform k_z grid, weights once per class
-  for (int idx = tid; idx < CL * NZ; idx += K3_NT) {
-    const int j = idx % NZ, cl = idx / NZ;
+  // 3. Stolt pull, filter folded into the weights: O_j = (1-tau) H_i0 S_i0 + tau H_i0+1 S_i0+1
+  for (int idx = tid; idx < CL * NZ; idx += K3C_NT) {
+    const int cl = idx / NZ, j = idx - cl * NZ;
     const int nm = nmem[cl];
     int i0 = 0;
     double tau = 0.0;
-    const bool ok = nm > 0 && stolt_pull(v.kz[j], kr2s[cl], v.k0, v.inv_dk, v.dk, nk, v.stolt_delta, &i0, &tau);
+    const bool ok = nm > 0 && stolt_pull(__ldg(v.kz + j), kr2s[cl], v.k0, v.inv_dk, v.dk, nk, v.stolt_delta, &i0, &tau);
     const float t = (float)tau;
+    const float2 hl = ok ? htab[cl * nk + i0] : make_float2(0.f, 0.f);
+    const float2 hu = ok ? htab[cl * nk + i0 + 1] : make_float2(0.f, 0.f);
+    const float2 wl = make_float2((1.f - t) * hl.x, (1.f - t) * hl.y);
+    const float2 wu = make_float2(t * hu.x, t * hu.y);
     for (int m = 0; m < nm; ++m) {
       const int sl = mslot[cl][m];
       float2 o = make_float2(0.f, 0.f);
-      if (ok) {
-        const float2 lo = fin[sl * nk + i0], hi = fin[sl * nk + i0 + 1];
-        o = make_float2(fmaf(t, hi.x - lo.x, lo.x), fmaf(t, hi.y - lo.y, lo.y));
-      }
+      if (ok) o = cmac2(cmul2(wl, fin[sl * nk + i0]), wu, fin[sl * nk + i0 + 1]);
       fout[j * LD + sl] = o;
     }
   }
   __syncthreads();
-  // 4. inverse FFT along z (unused slots hold stale values; never stored)
-  if constexpr (DO_IFFT) sarfft::tile_fft<NZ, CC, LD, K3_NT, +1>(fout, v.tw_z, tid);
-  // 5. store each column contiguously [col][z]
+  // 4. inverse z-FFT, columns stored contiguously [col][z]
   float2 *dst = v.w1 + (size_t)f * ncol * (size_t)NZ;
-  for (int sl = 0; sl < nu; ++sl) {
-    float2 *d = dst + (size_t)colof[sl] * NZ;
-    for (int z = tid; z < NZ; z += K3_NT) d[z] = fout[z * LD + sl];
+  if constexpr (DO_IFFT) {
+    sarfft2::fft<NZ, CC, LD, K3C_NT, +1, 0, true, (NZ == 512 ? 16 : 0)>(
+        fout, v.tw_z, tid, [&](int c, int m) { return fout[m * LD + c]; }, [] {},
+        [&](int c, int m, float2 x) {
+          const int col = colof[c];
+          if (col >= 0) __stcs(dst + (size_t)col * NZ + m, x);
+        });
+  } else {
+    for (int i = tid; i < CC * NZ; i += K3C_NT) {
+      const int sl = i / NZ, z = i - sl * NZ;
+      if (sl < nu) dst[(size_t)colof[sl] * NZ + z] = fout[z * LD + sl];
+    }
   }
 }
 
-// Warp-specialised persistent K3 (n_k even: 16-byte aligned columns).  A
-// producer warp decodes work items (CL mirror classes) into a 2-deep ring of
-// shared-memory stages and fills them with TMA bulk copies (full/empty
-// mbarriers); 8 consumer warps filter, resample and z-transform one item
-// while the next one lands.  The stage is released right after the Stolt
-// pull, so the z-IFFT and the stores overlap the following copies too.
+// K3 for the large grids: persistent, warp-specialised, ping-pong.  A
+// producer warp decodes work items (CL mirror classes = up to 4*CL spectral
+// columns that share k_r^2) into an S-stage ring and fills it with TMA bulk
+// copies (one n_k-sample column each, mbarrier completion).  Two consumer
+// groups of 256 threads take alternate items, so one group's fp64 filter /
+// Stolt phases and barrier waits overlap the other group's FFT.  Per item:
+// (1) filter table H(k_r, k_i) = k_z e^{+j k_z R_ref}/P once per class;
+// (2) Stolt pull with the filter folded into the two interpolation weights,
+// once per (class, j), applied to every member column (decisions bit-exact,
+// readings R5, R9); the stage is then handed back; (3) inverse z-FFT (two-pass
+// register FFT) whose pass 2 stores each column contiguously [col][z].
+// The k, k_z and twiddle tables live in shared memory.
 template <int CL>
 struct K3Hdr {
   int f, nused;
   int nmem[CL], mslot[CL][4];
-  int colof[4 * CL];
+  int jlo[CL], jhi[CL];   // in-band k_z bins of the class (superset, see stolt_range)
+  int colof[4 * CL], clof[4 * CL];
   double kr2[CL];
 };
 
-constexpr int K3W_NT = 512;   // consumer threads
-constexpr int K3W_STAGES = 2;
+// Superset [jlo, jhi] of the k_z bins j whose Stolt pull can be in band for
+// k_r^2 = kr2 (readings R5, R9): u(j) is monotone in j, u = 0 at
+// k_z = sqrt(4 k_0^2 - k_r^2) and u = n_k - 1 at sqrt(4 k_max^2 - k_r^2); the
+// range is widened by 2 bins on each side (the estimate is good to ~1e-12
+// bins), and to the whole axis when a band edge lies within 1e-3 bins of
+// k_z = 0 (where du/dj -> 0 and the margin would not cover the 1e-9 band
+// tolerance).  Bins outside the range are zero; inside, the bit-exact pull
+// decides.
+__device__ __forceinline__ void stolt_range(const SarDeviceView &v, double kr2, int *jlo, int *jhi) {
+  const int nz = v.nz;
+  const double kmax = v.k0 + (double)(v.nk - 1) * v.dk;
+  const double qhi = 4.0 * kmax * kmax - kr2;
+  if (!(qhi > 0.0)) {
+    *jlo = 0;
+    *jhi = -1;
+    return;
+  }
+  const double qlo = 4.0 * v.k0 * v.k0 - kr2;
+  const double kzhi = sqrt(qhi), kzlo = qlo > 0.0 ? sqrt(qlo) : 0.0;
+  const double guard = 1e-3 * v.kz_step;
+  if (kzlo < guard || kzhi < guard) {
+    *jlo = 0;
+    *jhi = nz - 1;
+    return;
+  }
+  const double jl = (double)(nz - 1) - (v.kz_top - kzlo) / v.kz_step;
+  const double jh = (double)(nz - 1) - (v.kz_top - kzhi) / v.kz_step;
+  int lo = (int)fmax(floor(jl) - 2.0, 0.0);
+  int hi = (int)fmin(ceil(jh) + 2.0, (double)(nz - 1));
+  *jlo = lo;
+  *jhi = hi < lo ? lo - 1 : hi;
+}
+constexpr int K3P_G = 256;   // threads per consumer group
+constexpr int K3P_S = 3;     // ring stages
+template <int NZ, int CL>
+size_t k3pp_smem(int nk) {
+  const size_t hdr = (sizeof(K3Hdr<CL>) + 15) & ~(size_t)15;
+  return K3P_S * (hdr + (size_t)4 * CL * nk * sizeof(float2)) +
+         2 * ((size_t)NZ * (4 * CL + 1)) * sizeof(float2) +
+         ((size_t)NZ + nk) * sizeof(double) + (size_t)NZ * sizeof(float2);
+}
 
-template <int NZ, int CL, bool DO_IFFT>
-__global__ void __launch_bounds__(K3W_NT + 32, 2) k3_filter_stolt_ws(const SarDeviceView v, int nitems_f) {
+template <int NZ, int CL, bool DO_IFFT, int BAR>
+__device__ __forceinline__ void k3pp_consume(const SarDeviceView &v, int nitems_f, int g, int gt,
+                                             unsigned char *ring, size_t stage_bytes, size_t hdr_bytes,
+                                             float2 *fout, const double *ks, const double *kzs, const float2 *tw,
+                                             uint64_t *full, uint64_t *empty, int *colofs, int *slo, int *shi) {
   constexpr int CC = 4 * CL;
   constexpr int LD = CC + 1;
-  constexpr int NWARP = K3W_NT / 32;
-  extern __shared__ __align__(16) unsigned char smb[];
+  const int nk = v.nk;
+  const int ncol = v.nx * v.ny;
+  const int nitems = nitems_f * v.F;
+  unsigned n = g;
+  for (int item = blockIdx.x + g * gridDim.x; item < nitems; item += 2 * gridDim.x, n += 2) {
+    const int st = n % K3P_S;
+    sartma::mbar_wait(&full[st], (n / K3P_S) & 1);
+    unsigned char *sb = ring + st * stage_bytes;
+    const K3Hdr<CL> &h = *reinterpret_cast<const K3Hdr<CL> *>(sb);
+    const float2 *fin = reinterpret_cast<const float2 *>(sb + hdr_bytes);
+    const int f = h.f, nu = h.nused;
+    const double rr = v.rref[f] * (1.0 / TWO_PI);
+    // Stolt pull over the in-band (class, j) pairs only, the filter evaluated
+    // at the two taps each pull uses and folded into the weights:
+    //   O_j = (1-tau) H(k_i0) S_i0 + tau H(k_i0+1) S_i0+1
+    int tot = 0;
+#pragma unroll
+    for (int cl = 0; cl < CL; ++cl) tot += h.jhi[cl] - h.jlo[cl] + 1;
+    for (int idx = (v.dbg & 2) ? tot : gt; idx < tot; idx += K3P_G) {
+      int cl = 0, j = idx;
+#pragma unroll
+      for (int q = 0; q < CL - 1; ++q) {
+        const int len = h.jhi[cl] - h.jlo[cl] + 1;
+        if (j >= len) {
+          j -= len;
+          ++cl;
+        }
+      }
+      j += h.jlo[cl];
+      const double kr2 = h.kr2[cl];
+      int i0 = 0;
+      double tau = 0.0;
+      const bool ok = stolt_pull(kzs[j], kr2, v.k0, v.inv_dk, v.dk, nk, v.stolt_delta, &i0, &tau);
+      float2 wl = make_float2(0.f, 0.f), wu = wl;
+      if (ok) {
+        const float t = (float)tau;
+        const float2 hl = filter_h(v, ks[i0], kr2, rr, i0);
+        const float2 hu = filter_h(v, ks[i0 + 1], kr2, rr, i0 + 1);
+        wl = make_float2((1.f - t) * hl.x, (1.f - t) * hl.y);
+        wu = make_float2(t * hu.x, t * hu.y);
+      }
+      const int nm = h.nmem[cl];
+      for (int m = 0; m < nm; ++m) {
+        const int sl = h.mslot[cl][m];
+        float2 o = make_float2(0.f, 0.f);
+        if (ok) o = cmac2(cmul2(wl, fin[sl * nk + i0]), wu, fin[sl * nk + i0 + 1]);
+        fout[j * LD + sl] = o;
+      }
+    }
+    if (gt < CC) {
+      const bool used = gt < nu;
+      colofs[gt] = used ? h.colof[gt] : -1;
+      slo[gt] = used ? h.jlo[h.clof[gt]] : NZ;
+      shi[gt] = used ? h.jhi[h.clof[gt]] : -1;
+    }
+    sarfft2::sync<BAR, K3P_G>();
+    if (gt == 0) sartma::mbar_arrive(&empty[st]);  // stage (header + columns) consumed
+    // inverse z-FFT (out-of-band rows read as zero), columns stored contiguously
+    float2 *dst = v.w1 + (size_t)f * ncol * (size_t)NZ;
+    auto load = [&](int c, int m) {
+      return (m >= slo[c] && m <= shi[c]) ? fout[m * LD + c] : make_float2(0.f, 0.f);
+    };
+    if (DO_IFFT && !(v.dbg & 4)) {
+      sarfft2::fft<NZ, CC, LD, K3P_G, +1, BAR, true, (NZ == 512 && CC == 8 ? 16 : 0)>(
+          fout, tw, gt, load, [] {},
+          [&](int c, int m, float2 x) {
+            const int col = colofs[c];
+            if (col >= 0) __stcs(dst + (size_t)col * NZ + m, x);
+          });
+    } else {
+      for (int i = gt; i < CC * NZ; i += K3P_G) {
+        const int sl = i / NZ, z = i - sl * NZ;
+        if (sl < nu) dst[(size_t)colofs[sl] * NZ + z] = load(sl, z);
+      }
+    }
+    sarfft2::sync<BAR, K3P_G>();  // fout / slot tables are rewritten by this group's next item
+  }
+}
+
+template <int NZ, int CL, bool DO_IFFT>
+__global__ void __launch_bounds__(2 * K3P_G + 32, 1) k3_pp(const SarDeviceView v, int nitems_f) {
+  constexpr int CC = 4 * CL;
+  constexpr int LD = CC + 1;
+  constexpr int NTH = 2 * K3P_G + 32;
+  extern __shared__ __align__(16) unsigned char smp[];
   const int nk = v.nk;
   const size_t hdr_bytes = (sizeof(K3Hdr<CL>) + 15) & ~(size_t)15;
   const size_t stage_bytes = hdr_bytes + (size_t)CC * nk * sizeof(float2);
-  float2 *fout = reinterpret_cast<float2 *>(smb + K3W_STAGES * stage_bytes);  // [NZ][LD]
-  float2 *htab = fout + (size_t)NZ * LD;                                        // [CL][nk] filter
-  const float inv_nk = 1.0f / (float)nk;
-  __shared__ __align__(8) uint64_t full[K3W_STAGES], empty[K3W_STAGES];
-  __shared__ float2 tw[NZ];
+  unsigned char *ring = smp;
+  float2 *grp = reinterpret_cast<float2 *>(smp + K3P_S * stage_bytes);
+  const size_t grp_elems = (size_t)NZ * LD;                      // fout per group
+  double *ks = reinterpret_cast<double *>(grp + 2 * grp_elems);  // [nk]
+  double *kzs = ks + nk;                                          // [NZ]
+  float2 *tw = reinterpret_cast<float2 *>(kzs + NZ);              // [NZ]
+  __shared__ __align__(8) uint64_t full[K3P_S], empty[K3P_S];
+  __shared__ int colofs[2][CC], slo[2][CC], shi[2][CC];
   const int tid = threadIdx.x;
-  const int ncol = v.nx * v.ny;
-  const int hx = v.nx / 2 + 1, hy = v.ny / 2 + 1;
-  const int nclass = hx * hy;
-  const int nitems = nitems_f * v.F;
-  for (int i = tid; i < NZ; i += K3W_NT + 32) tw[i] = v.tw_z[i];
+  for (int i = tid; i < nk; i += NTH) ks[i] = v.k[i];
+  for (int i = tid; i < NZ; i += NTH) {
+    kzs[i] = v.kz[i];
+    tw[i] = v.tw_z[i];
+  }
   if (tid == 0) {
-    for (int i = 0; i < K3W_STAGES; ++i) {
+    for (int i = 0; i < K3P_S; ++i) {
       sartma::mbar_init(&full[i], 1);
-      sartma::mbar_init(&empty[i], NWARP);
+      sartma::mbar_init(&empty[i], 1);
     }
     sartma::fence_barrier_init();
   }
   __syncthreads();
-  if (tid >= K3W_NT) {
-    if (tid == K3W_NT) {  // producer
+  const int ncol = v.nx * v.ny;
+  const int nitems = nitems_f * v.F;
+  if (tid >= 2 * K3P_G) {
+    if (tid == 2 * K3P_G) {  // producer
+      const int hx = v.nx / 2 + 1, hy = v.ny / 2 + 1;
+      const int nclass = hx * hy;
       unsigned n = 0;
       for (int item = blockIdx.x; item < nitems; item += gridDim.x, ++n) {
-        const int st = n % K3W_STAGES;
-        if (n >= K3W_STAGES) sartma::mbar_wait(&empty[st], ((n / K3W_STAGES) - 1) & 1);
-        unsigned char *sb = smb + st * stage_bytes;
+        const int st = n % K3P_S;
+        if (n >= K3P_S) sartma::mbar_wait(&empty[st], ((n / K3P_S) - 1) & 1);
+        unsigned char *sb = ring + st * stage_bytes;
         K3Hdr<CL> &h = *reinterpret_cast<K3Hdr<CL> *>(sb);
         float2 *fin = reinterpret_cast<float2 *>(sb + hdr_bytes);
         const int f = item / nitems_f;
@@ -861,15 +1039,19 @@ __global__ void __launch_bounds__(K3W_NT + 32, 2) k3_filter_stolt_ws(const SarDe
           const int q = q0 + cl;
           h.nmem[cl] = 0;
           h.kr2[cl] = 0.0;
+          h.jlo[cl] = 0;
+          h.jhi[cl] = -1;
           if (q >= nclass) continue;
           const int a = q % hx, b = q / hx;
           const int ma = (v.nx - a) & (v.nx - 1), mb = (v.ny - b) & (v.ny - 1);
           h.kr2[cl] = kr2_of(v, a, b);
+          stolt_range(v, h.kr2[cl], &h.jlo[cl], &h.jhi[cl]);
           const int c4[4] = {b * v.nx + a, b * v.nx + ma, mb * v.nx + a, mb * v.nx + ma};
           const bool ok4[4] = {true, ma != a, mb != b, ma != a && mb != b};
           for (int m = 0; m < 4; ++m)
             if (ok4[m]) {
               h.mslot[cl][h.nmem[cl]++] = cnt;
+              h.clof[cnt] = cl;
               h.colof[cnt++] = c4[m];
             }
         }
@@ -883,76 +1065,14 @@ __global__ void __launch_bounds__(K3W_NT + 32, 2) k3_filter_stolt_ws(const SarDe
     }
     return;
   }
-  // consumers
-  const int lane = tid & 31;
-  unsigned n = 0;
-  for (int item = blockIdx.x; item < nitems; item += gridDim.x, ++n) {
-    const int st = n % K3W_STAGES;
-    sartma::mbar_wait(&full[st], (n / K3W_STAGES) & 1);
-    unsigned char *sb = smb + st * stage_bytes;
-    const K3Hdr<CL> &h = *reinterpret_cast<const K3Hdr<CL> *>(sb);
-    float2 *fin = reinterpret_cast<float2 *>(sb + hdr_bytes);
-    const int f = h.f, nu = h.nused;
-    // filter H(k_r, k_i) = k_z exp(+j k_z R_ref) / P(f) of every class, into a
-    // table (the fp64 work is per class, not per column)
-    const double rr = v.rref[f] * (1.0 / TWO_PI);
-    for (int idx = tid; idx < CL * nk; idx += K3W_NT) {
-      const int cl = (int)(((float)idx + 0.5f) * inv_nk);   // exact: idx < 2^14
-      const int i = idx - cl * nk;
-      const double ki = v.k[i];
-      const double q = 4.0 * ki * ki - h.kr2[cl];
-      float2 hh = make_float2(0.f, 0.f);
-      if (q > 0.0) {
-        const double kz = fast_dsqrt(q);
-        double turns = kz * rr;
-        turns -= rint(turns);
-        float sn, cs;
-        __sincosf((float)turns * 6.28318530717958647692f, &sn, &cs);
-        const float kzf = (float)kz;
-        hh = make_float2(kzf * cs, kzf * sn);
-        if (v.pinv) hh = cmul(hh, v.pinv[i]);
-      }
-      htab[idx] = hh;
-    }
-    sarfft::tile_sync<1, K3W_NT>();
-    // Stolt pull with the filter folded into complex weights:
-    //   O_j = (1-tau) H_{i0} S_{i0} + tau H_{i0+1} S_{i0+1}
-    // weights once per (class, j), two complex FMAs per column
-    for (int idx = tid; idx < CL * NZ; idx += K3W_NT) {
-      const int j = idx % NZ, cl = idx / NZ;
-      const int nm = h.nmem[cl];
-      int i0 = 0;
-      double tau = 0.0;
-      const bool ok = nm > 0 && stolt_pull(v.kz[j], h.kr2[cl], v.k0, v.inv_dk, v.dk, nk, v.stolt_delta, &i0, &tau);
-      const float t = (float)tau;
-      const float2 hl = ok ? htab[cl * nk + i0] : make_float2(0.f, 0.f);
-      const float2 hu = ok ? htab[cl * nk + i0 + 1] : make_float2(0.f, 0.f);
-      const float2 wl = make_float2((1.f - t) * hl.x, (1.f - t) * hl.y);
-      const float2 wu = make_float2(t * hu.x, t * hu.y);
-      for (int m = 0; m < nm; ++m) {
-        const int sl = h.mslot[cl][m];
-        float2 o = make_float2(0.f, 0.f);
-        if (ok) o = cmac2(cmul2(wl, fin[sl * nk + i0]), wu, fin[sl * nk + i0 + 1]);
-        fout[j * LD + sl] = o;
-      }
-    }
-    int colof[CC];
-#pragma unroll
-    for (int sl = 0; sl < CC; ++sl) colof[sl] = sl < nu ? h.colof[sl] : 0;
-    sarfft::tile_sync<1, K3W_NT>();
-    // the stage (header + fin) is free: let the producer refill it
-    __syncwarp();
-    if (lane == 0) sartma::mbar_arrive(&empty[st]);
-    if constexpr (DO_IFFT) sarfft::tile_fft<NZ, CC, LD, K3W_NT, +1, 1>(fout, tw, tid);
-    float2 *dst = v.w1 + (size_t)f * ncol * (size_t)NZ;
-#pragma unroll
-    for (int sl = 0; sl < CC; ++sl) {
-      if (sl >= nu) break;
-      float2 *d = dst + (size_t)colof[sl] * NZ;
-      for (int z = tid; z < NZ; z += K3W_NT) d[z] = fout[z * LD + sl];
-    }
-    sarfft::tile_sync<1, K3W_NT>();
-  }
+  const int g = tid / K3P_G, gt = tid - g * K3P_G;
+  float2 *fout = grp + g * grp_elems;
+  if (g == 0)
+    k3pp_consume<NZ, CL, DO_IFFT, 1>(v, nitems_f, 0, gt, ring, stage_bytes, hdr_bytes, fout, ks, kzs, tw, full, empty,
+                                     colofs[0], slo[0], shi[0]);
+  else
+    k3pp_consume<NZ, CL, DO_IFFT, 2>(v, nitems_f, 1, gt, ring, stage_bytes, hdr_bytes, fout, ks, kzs, tw, full, empty,
+                                     colofs[1], slo[1], shi[1]);
 }
 
 __global__ void k_stolt_index(const SarDeviceView v, const int32_t *__restrict__ cols, int n,
@@ -1234,28 +1354,24 @@ cudaError_t launch_v(K kernel, dim3 grid, int nt, size_t smem, cudaStream_t s, c
 }
 
 cudaError_t launch_k3(const SarDeviceView &v, bool ifft, cudaStream_t s, int num_sms) {
-  if ((v.nk & 1) == 0 && !getenv("SAR_K3_PLAIN")) {
+  if ((v.nk & 1) == 0 && v.nz >= 256 && !getenv("SAR_K3_PLAIN")) {
     const int nclass = (v.nx / 2 + 1) * (v.ny / 2 + 1);
     switch (v.nz) {
 #define X(N)                                                                                                   \
   case N: {                                                                                                    \
-    constexpr int CL = k3_cl_for(N);                                                                           \
-    const size_t hdr = (sizeof(K3Hdr<CL>) + 15) & ~(size_t)15;                                                 \
-    const size_t smem = K3W_STAGES * (hdr + (size_t)4 * CL * v.nk * sizeof(float2)) +                         \
-                        ((size_t)N * (4 * CL + 1) + (size_t)CL * v.nk) * sizeof(float2);                      \
-    if (smem <= 110 * 1024) {                                                                                  \
-      const int nitems_f = (nclass + CL - 1) / CL;                                                             \
-      const int nitems = nitems_f * v.F;                                                                       \
-      const int grid = nitems < 2 * num_sms ? nitems : 2 * num_sms;                                            \
-      auto kern = ifft ? k3_filter_stolt_ws<N, CL, true> : k3_filter_stolt_ws<N, CL, false>;                 \
-      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);      \
-      if (e != cudaSuccess) return e;                                                                          \
-      kern<<<grid, K3W_NT + 32, smem, s>>>(v, nitems_f);                                                       \
-      return cudaGetLastError();                                                                               \
-    }                                                                                                          \
-    break;                                                                                                     \
+    constexpr int CL = 2;                                                                                      \
+    const size_t smem = k3pp_smem<N, CL>(v.nk);                                                                \
+    if (smem > 225 * 1024) break;                                                                              \
+    const int nitems_f = (nclass + CL - 1) / CL;                                                               \
+    const int nitems = nitems_f * v.F;                                                                         \
+    const int grid = nitems < num_sms ? nitems : num_sms;                                                      \
+    auto kern = ifft ? k3_pp<N, CL, true> : k3_pp<N, CL, false>;                                               \
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);        \
+    if (e != cudaSuccess) return e;                                                                            \
+    kern<<<grid, 2 * K3P_G + 32, smem, s>>>(v, nitems_f);                                                      \
+    return cudaGetLastError();                                                                                 \
   }
-      SAR_SIZES(X)
+      X(256) X(512) X(1024)
 #undef X
     }
   }
@@ -1263,19 +1379,16 @@ cudaError_t launch_k3(const SarDeviceView &v, bool ifft, cudaStream_t s, int num
   switch (v.nz) {
 #define X(N)                                                                                                   \
   case N: {                                                                                                    \
-    constexpr int CLW = k3_cl_for(N);                                                                          \
-    const size_t smw = ((size_t)v.nk * 4 * CLW + (size_t)N * (4 * CLW + 1)) * sizeof(float2);               \
-    const bool wide = CLW > 2 && smw <= 220 * 1024;                                                          \
-    const int CL = wide ? CLW : 2;                                                                             \
-    const size_t smem = ((size_t)v.nk * 4 * CL + (size_t)N * (4 * CL + 1)) * sizeof(float2);                 \
+    constexpr int CL = k3c_cl<N>();                                                                            \
+    const size_t smem = k3c_smem<N>(v.nk);                                                                     \
+    if (smem > 220 * 1024) return cudaErrorInvalidValue;                                                       \
     dim3 grid((nclass + CL - 1) / CL, v.F);                                                                    \
-    auto kern = wide ? (ifft ? k3_filter_stolt<N, CLW, true> : k3_filter_stolt<N, CLW, false>)               \
-                     : (ifft ? k3_filter_stolt<N, 2, true> : k3_filter_stolt<N, 2, false>);                  \
+    auto kern = ifft ? k3_class<N, true> : k3_class<N, false>;                                                 \
     if (smem > 48 * 1024) {                                                                                    \
       cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);      \
       if (e != cudaSuccess) return e;                                                                          \
     }                                                                                                          \
-    kern<<<grid, K3_NT, smem, s>>>(v);                                                                         \
+    kern<<<grid, K3C_NT, smem, s>>>(v);                                                                        \
     return cudaGetLastError();                                                                                 \
   }
     SAR_SIZES(X)

@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -98,12 +99,13 @@ struct HostTables {
   std::vector<double> kx, ky, kz, kd, rref;
   size_t tw_y_off = 0, tw_z_off = 0;
   int roll_x = 0, roll_y = 0;
-  double k0 = 0, dk = 0;
+  double k0 = 0, dk = 0, dkz = 0;
 };
 
 // Validation + Eqs. (3),(4),(7),(12) decomposition, no device involved.
 int host_decompose(const sar_geom_desc *g, const sar_image_desc *im, uint32_t flags, sar_plan *p,
                    HostTables &T) {
+  double &dkz = T.dkz;
   if (!g || !im) return fail(SAR_ERR_INVALID_ARG, "geometry or image descriptor is NULL");
   if (g->n_frames < 0) return fail(SAR_ERR_INVALID_ARG, "n_frames < 0");
   if (g->n_tx < 1 || g->n_rx < 1) return fail(SAR_ERR_INVALID_ARG, "n_tx and n_rx must be >= 1");
@@ -202,7 +204,7 @@ int host_decompose(const sar_geom_desc *g, const sar_image_desc *im, uint32_t fl
     const int bs = b < p->ny / 2 ? b : b - p->ny;
     T.ky[b] = 2.0 * M_PI * (double)bs / ((double)p->ny * g->dy);
   }
-  const double dkz = 2.0 * M_PI / ((double)p->nz * im->dz);
+  dkz = 2.0 * M_PI / ((double)p->nz * im->dz);
   for (int j = 0; j < p->nz; ++j) T.kz[j] = 2.0 * g->k[nk - 1] - (double)(p->nz - 1 - j) * dkz;
   T.kturn.resize(nk);
   for (int i = 0; i < nk; ++i) T.kturn[i] = (float)(g->k[i] / (2.0 * M_PI));
@@ -374,6 +376,8 @@ int sar_plan_create(sar_plan **out, const sar_geom_desc *g, const sar_image_desc
   v.k0 = T.k0;
   v.dk = T.dk;
   v.inv_dk = 1.0 / T.dk;
+  v.kz_top = T.kz.back();
+  v.kz_step = T.dkz;
   {
     // |u_fast - u| <= (2e-13 * kk + 4 ulp(u)) / dk with kk <= k_max (fast_dsqrt bound)
     const double kmax = T.kd.back();
@@ -389,6 +393,7 @@ int sar_plan_create(sar_plan **out, const sar_geom_desc *g, const sar_image_desc
     v.k1_step_ok = (T.dk * ((double)amax + (double)bmax) <= 0.25) ? 1 : 0;
   }
   v.w0 = p->d_w0;
+  v.dbg = getenv("SAR_DBG") ? atoi(getenv("SAR_DBG")) : 0;
   v.w1 = p->d_w1;
 
   p->num_sms = prop.multiProcessorCount;

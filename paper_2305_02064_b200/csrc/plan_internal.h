@@ -32,8 +32,10 @@ struct SarDeviceView {
   const float2 *tw_y;   // [ny]
   const float2 *tw_z;   // [nz]
   double k0, dk, inv_dk;
+  double kz_top, kz_step;  // k_z[nz-1] = 2 k_max and the k_z bin width (reading R5)
   double stolt_delta;   // decision guard band of the fast Stolt path (kernels.cu)
   int k1_step_ok;       // max |dk * beta| <= 0.25: K1 may use the Taylor step phasor
+  int dbg;              // ablation switches (env SAR_DBG; 0 in production)
   float img_scale;      // 1/(nx ny nz)
   float2 *w0;           // [F][ny][nx][nk]  planar lattice -> spectrum
   float2 *w1;           // [F][ny][nx][nz]  Stolt output -> partial inverse
