@@ -56,6 +56,8 @@ void free_plan(sar_plan *p) {
   cudaFree(p->d_w1);
   cudaFree(p->d_in);
   cudaFree(p->d_img);
+  cudaFree(p->d_items);
+  cudaFree(p->d_cnt);
   delete p;
 }
 
@@ -398,6 +400,11 @@ int sar_plan_create(sar_plan **out, const sar_geom_desc *g, const sar_image_desc
 
   p->num_sms = prop.multiProcessorCount;
   sar_build_tensor_maps(p);
+  st = sar_setup_passb(p);
+  if (st != SAR_OK) {
+    free_plan(p);
+    return fail(st, "pass-B work list allocation failed");
+  }
   if (flags & SAR_PROFILE_STAGES) {
     for (int i = 0; i < SAR_PROFILE_RING; ++i)
       for (int j = 0; j <= SAR_N_STAGES; ++j) cudaEventCreate(&p->ev[i][j]);
@@ -466,7 +473,7 @@ int sar_plan_workspace_bytes(const sar_plan *p, size_t *bytes) {
 
 int sar_plan_launches_per_call(const sar_plan *p, int32_t *n) {
   if (!p || !n) return fail(SAR_ERR_INVALID_ARG, "NULL argument");
-  *n = p->F > 0 ? SAR_N_STAGES : 0;
+  *n = p->F > 0 ? (p->fused ? 3 : SAR_N_STAGES) : 0;
   return SAR_OK;
 }
 

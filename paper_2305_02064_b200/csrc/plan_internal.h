@@ -70,6 +70,12 @@ struct sar_plan {
   int k1_br = 0;                   // pose rows per K1 TMA box
   bool k1_regacc = false;          // every j^x offset is 0: K1 sums in registers
   int num_sms = 148;
+  // fused pass B (K2 + K3 + K4a): work list and dependency counters
+  bool fused = false, passb_discard = false, tma_pb = false;
+  CUtensorMap tm_w0_pb, tm_w1_pb;  // [ny][8] boxes over W0 / W1
+  int4 *d_items = nullptr;
+  int n_items = 0;
+  int *d_cnt = nullptr;
 };
 
 // kernels.cu
@@ -79,4 +85,5 @@ int sar_launch_stolt_index(sar_plan *p, const int32_t *d_cols, int n, int32_t *d
                            cudaStream_t s);
 void sar_set_error(const std::string &msg);
 int sar_build_tensor_maps(sar_plan *p);
+int sar_setup_passb(sar_plan *p);
 bool sar_encode_input_map(sar_plan *p, const void *d_data);

@@ -41,9 +41,21 @@ with open(f"profiles/{name}_ncu.csv", "w", newline="") as fh:
     w.writeheader()
     for d in out:
         w.writerow(d)
-# path kernels appear in launch order K1, K2, K3, K4a, K4b
-for i, d in enumerate(out[:5]):
-    traffic[str(i)] = int(d["dram__bytes_read.sum"] + d["dram__bytes_write.sum"])
+# kernel -> stage slot (K1 0, K2 1, K3 / fused pass B 2, K4a 3, K4b 4)
+def slot(name):
+    if "k1_" in name:
+        return 0
+    if "k_passb" in name or "k3_" in name:
+        return 2
+    if "k4_" in name:
+        return 4
+    if "k_fft_mid" in name:
+        return 1 if "-1" in name.split(">")[0] else 3
+    return None
+for d in out:
+    sl = slot(d["Kernel Name"])
+    if sl is not None and str(sl) not in traffic:
+        traffic[str(sl)] = int(d["dram__bytes_read.sum"] + d["dram__bytes_write.sum"])
 json.dump(traffic, open(f"profiles/{config}_traffic.json", "w"))
 for d in out:
     print(d["Kernel Name"][:50], "ms=%.4f" % d["gpu__time_duration.sum"], "R=%.3fGB W=%.3fGB" % (

@@ -283,3 +283,21 @@ def test_tma_and_plain_paths_agree():
         del os.environ["SAR_NO_TMA"]
     e2, _ = errs(a, b.astype(np.float64))
     assert e2 < 1e-5
+
+
+@pytest.mark.parametrize("name", ["small", "freehand", "realtime"])
+def test_fused_pass_b_parity(name, monkeypatch):
+    """The opt-in fused K2+K3+K4a kernel (SAR_FUSE=1, dependency counters and
+    L2 discards) meets the same bar, per stage and end to end."""
+    monkeypatch.setenv("SAR_FUSE", "1")
+    sc = scenes.make_scene(name)
+    with sar.Plan.from_scene(sc) as plan:
+        assert plan.launches_per_call() == 3
+    _check_e2e(sc)
+    if name == "small":
+        d, s = _data(sc)
+        _, _, st = oracle.reconstruct(s, sc, complex_out=True, return_stages=True)
+        with sar.Plan.from_scene(sc) as plan:
+            for stage, key in ((2, "spectrum"), (3, "stolt")):
+                e2, _ = errs(plan.debug_stage(stage, d).cpu().numpy(), st[key])
+                assert e2 <= STAGE_BAR, (key, e2)
