@@ -737,97 +737,108 @@ constexpr int k3c_cl() {
 template <int NZ>
 size_t k3c_smem(int nk) {
   constexpr int CL = k3c_cl<NZ>();
-  return ((size_t)4 * CL * nk + (size_t)CL * nk + (size_t)NZ * (4 * CL + 1)) * sizeof(float2);
+  return ((size_t)4 * CL * nk + (size_t)NZ * (4 * CL + 1)) * sizeof(float2);
 }
 
 template <int NZ, bool DO_IFFT>
 __global__ void __launch_bounds__(K3C_NT, 4) k3_class(const SarDeviceView v) {
   constexpr int CL = k3c_cl<NZ>();
-  constexpr int CC = 4 * CL;
+  constexpr int CC = 4 * CL;   // slot 4*cl + m = member m of class cl
   constexpr int LD = CC + 1;
   extern __shared__ __align__(16) float2 sm3[];
   __shared__ double kr2s[CL];
-  __shared__ int nmem[CL], mslot[CL][4];
-  __shared__ int colof[CC];
-  __shared__ int nused;
+  __shared__ int jlos[CL], jhis[CL], colof[CC];
   const int nk = v.nk;
   float2 *fin = sm3;                                 // [CC][nk]  source spectrum
-  float2 *htab = fin + (size_t)CC * nk;              // [CL][nk]  filter
-  float2 *fout = htab + (size_t)CL * nk;             // [NZ][LD]  Stolt output / FFT work
+  float2 *fout = fin + (size_t)CC * nk;              // [NZ][LD]  Stolt output / FFT work
   const int tid = threadIdx.x;
   const int ncol = v.nx * v.ny;
-  const int hx = v.nx / 2 + 1, hy = v.ny / 2 + 1;
-  const int nclass = hx * hy;
+  const int nclass = (v.nx / 2 + 1) * (v.ny / 2 + 1);
   const int q0 = blockIdx.x * CL;
   const int f = blockIdx.y;
-  if (tid == 0) {
-    int n = 0;
-    for (int cl = 0; cl < CL; ++cl) {
-      const int q = q0 + cl;
-      nmem[cl] = 0;
-      kr2s[cl] = 0.0;
-      if (q >= nclass) continue;
-      const int a = q % hx, b = q / hx;
-      const int ma = (v.nx - a) & (v.nx - 1), mb = (v.ny - b) & (v.ny - 1);
-      kr2s[cl] = kr2_of(v, a, b);
-      const int c4[4] = {b * v.nx + a, b * v.nx + ma, mb * v.nx + a, mb * v.nx + ma};
-      const bool ok4[4] = {true, ma != a, mb != b, ma != a && mb != b};
-      for (int m = 0; m < 4; ++m)
-        if (ok4[m]) {
-          mslot[cl][nmem[cl]++] = n;
-          colof[n++] = c4[m];
-        }
+  if (tid < CL) {
+    const int q = q0 + tid;
+    if (q < nclass) {
+      const SarClass &c = v.cls[q];
+      kr2s[tid] = c.kr2;
+      jlos[tid] = c.jlo;
+      jhis[tid] = c.jhi;
+#pragma unroll
+      for (int m = 0; m < 4; ++m) colof[4 * tid + m] = m < c.nmem ? c.col[m] : -1;
+    } else {
+      kr2s[tid] = 0.0;
+      jlos[tid] = 0;
+      jhis[tid] = -1;
+#pragma unroll
+      for (int m = 0; m < 4; ++m) colof[4 * tid + m] = -1;
     }
-    for (int sl = n; sl < CC; ++sl) colof[sl] = -1;
-    nused = n;
   }
   __syncthreads();
-  const int nu = nused;
   // 1. member columns (streaming loads, 16 B per thread when n_k is even)
   const float2 *wf = v.w0 + (size_t)f * ncol * (size_t)nk;
   if ((nk & 1) == 0) {
     const int h2 = nk / 2;
-    for (int e = tid; e < nu * h2; e += K3C_NT) {
+    for (int e = tid; e < CC * h2; e += K3C_NT) {
       const int sl = e / h2, i = e - sl * h2;
-      const float4 x = __ldcs(reinterpret_cast<const float4 *>(wf + (size_t)colof[sl] * nk) + i);
-      reinterpret_cast<float4 *>(fin + sl * nk)[i] = x;
+      if (colof[sl] >= 0)
+        reinterpret_cast<float4 *>(fin + sl * nk)[i] =
+            __ldcs(reinterpret_cast<const float4 *>(wf + (size_t)colof[sl] * nk) + i);
     }
   } else {
-    for (int e = tid; e < nu * nk; e += K3C_NT) {
+    for (int e = tid; e < CC * nk; e += K3C_NT) {
       const int sl = e / nk, i = e - sl * nk;
-      fin[e] = __ldcs(wf + (size_t)colof[sl] * nk + i);
+      if (colof[sl] >= 0) fin[e] = __ldcs(wf + (size_t)colof[sl] * nk + i);
     }
   }
-  // 2. filter table H(k_r, k_i) per class (4 independent fp64 chains per thread)
-  const double rr = v.rref[f] * (1.0 / TWO_PI);
-  filter_table<4>(v, htab, CL * nk, nk, tid, K3C_NT, rr, [&](int cl) { return kr2s[cl]; },
-                  [&](int i) { return __ldg(v.k + i); });
   __syncthreads();
-  // 3. Stolt pull, filter folded into the weights: O_j = (1-tau) H_i0 S_i0 + tau H_i0+1 S_i0+1
-  for (int idx = tid; idx < CL * NZ; idx += K3C_NT) {
-    const int cl = idx / NZ, j = idx - cl * NZ;
-    const int nm = nmem[cl];
+  // 2. Stolt pull over the in-band (class, j) pairs, filter at the two taps
+  //    folded into the weights (readings R2-R5, R9)
+  const double rr = v.rref[f] * (1.0 / TWO_PI);
+  int tot = 0;
+#pragma unroll
+  for (int cl = 0; cl < CL; ++cl) tot += jhis[cl] - jlos[cl] + 1;
+  for (int idx = tid; idx < tot; idx += K3C_NT) {
+    int cl = 0, j = idx;
+#pragma unroll
+    for (int q = 0; q < CL - 1; ++q) {
+      const int len = jhis[cl] - jlos[cl] + 1;
+      if (j >= len) {
+        j -= len;
+        ++cl;
+      }
+    }
+    j += jlos[cl];
+    const double kr2 = kr2s[cl];
     int i0 = 0;
     double tau = 0.0;
-    const bool ok = nm > 0 && stolt_pull(__ldg(v.kz + j), kr2s[cl], v.k0, v.inv_dk, v.dk, nk, v.stolt_delta, &i0, &tau);
-    const float t = (float)tau;
-    const float2 hl = ok ? htab[cl * nk + i0] : make_float2(0.f, 0.f);
-    const float2 hu = ok ? htab[cl * nk + i0 + 1] : make_float2(0.f, 0.f);
-    const float2 wl = make_float2((1.f - t) * hl.x, (1.f - t) * hl.y);
-    const float2 wu = make_float2(t * hu.x, t * hu.y);
-    for (int m = 0; m < nm; ++m) {
-      const int sl = mslot[cl][m];
+    const bool ok = stolt_pull(__ldg(v.kz + j), kr2, v.k0, v.inv_dk, v.dk, nk, v.stolt_delta, &i0, &tau);
+    float2 wl = make_float2(0.f, 0.f), wu = wl;
+    if (ok) {
+      const float tt = (float)tau;
+      const float2 hl = filter_h(v, __ldg(v.k + i0), kr2, rr, i0);
+      const float2 hu = filter_h(v, __ldg(v.k + i0 + 1), kr2, rr, i0 + 1);
+      wl = make_float2((1.f - tt) * hl.x, (1.f - tt) * hl.y);
+      wu = make_float2(tt * hu.x, tt * hu.y);
+    }
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+      const int sl = 4 * cl + m;
+      if (colof[sl] < 0) break;
       float2 o = make_float2(0.f, 0.f);
       if (ok) o = cmac2(cmul2(wl, fin[sl * nk + i0]), wu, fin[sl * nk + i0 + 1]);
       fout[j * LD + sl] = o;
     }
   }
   __syncthreads();
-  // 4. inverse z-FFT, columns stored contiguously [col][z]
+  // 3. inverse z-FFT (out-of-band bins read as zero), columns stored [col][z]
   float2 *dst = v.w1 + (size_t)f * ncol * (size_t)NZ;
+  auto load = [&](int c, int m) {
+    const int cl = c >> 2;
+    return (m >= jlos[cl] && m <= jhis[cl]) ? fout[m * LD + c] : make_float2(0.f, 0.f);
+  };
   if constexpr (DO_IFFT) {
     sarfft2::fft<NZ, CC, LD, K3C_NT, +1, 0, true, (NZ == 512 ? 16 : 0)>(
-        fout, v.tw_z, tid, [&](int c, int m) { return fout[m * LD + c]; }, [] {},
+        fout, v.tw_z, tid, load, [] {},
         [&](int c, int m, float2 x) {
           const int col = colof[c];
           if (col >= 0) __stcs(dst + (size_t)col * NZ + m, x);
@@ -835,7 +846,7 @@ __global__ void __launch_bounds__(K3C_NT, 4) k3_class(const SarDeviceView v) {
   } else {
     for (int i = tid; i < CC * NZ; i += K3C_NT) {
       const int sl = i / NZ, z = i - sl * NZ;
-      if (sl < nu) dst[(size_t)colof[sl] * NZ + z] = fout[z * LD + sl];
+      if (colof[sl] >= 0) dst[(size_t)colof[sl] * NZ + z] = load(sl, z);
     }
   }
 }
@@ -1043,18 +1054,15 @@ __global__ void __launch_bounds__(2 * K3P_G + 32, 1) k3_pp(const SarDeviceView v
           h.jlo[cl] = 0;
           h.jhi[cl] = -1;
           if (q >= nclass) continue;
-          const int a = q % hx, b = q / hx;
-          const int ma = (v.nx - a) & (v.nx - 1), mb = (v.ny - b) & (v.ny - 1);
-          h.kr2[cl] = kr2_of(v, a, b);
-          stolt_range(v, h.kr2[cl], &h.jlo[cl], &h.jhi[cl]);
-          const int c4[4] = {b * v.nx + a, b * v.nx + ma, mb * v.nx + a, mb * v.nx + ma};
-          const bool ok4[4] = {true, ma != a, mb != b, ma != a && mb != b};
-          for (int m = 0; m < 4; ++m)
-            if (ok4[m]) {
-              h.mslot[cl][h.nmem[cl]++] = cnt;
-              h.clof[cnt] = cl;
-              h.colof[cnt++] = c4[m];
-            }
+          const SarClass &c = v.cls[q];
+          h.kr2[cl] = c.kr2;
+          h.jlo[cl] = c.jlo;
+          h.jhi[cl] = c.jhi;
+          for (int m = 0; m < c.nmem; ++m) {
+            h.mslot[cl][h.nmem[cl]++] = cnt;
+            h.clof[cnt] = cl;
+            h.colof[cnt++] = c.col[m];
+          }
         }
         h.nused = cnt;
         h.f = f;
@@ -1461,20 +1469,16 @@ __global__ void __launch_bounds__(PB_NT + 32, 2)
             h.jlo[cl] = 0;
             h.jhi[cl] = -1;
             if (b >= v.ny / 2 + 1) continue;
-            const int a = pp;
-            const int ma = (nx - a) & (nx - 1), mb = (v.ny - b) & (v.ny - 1);
-            h.kr2[cl] = kr2_of(v, a, b);
-            stolt_range(v, h.kr2[cl], &h.jlo[cl], &h.jhi[cl]);
-            const int c4[4] = {b * nx + a, b * nx + ma, mb * nx + a, mb * nx + ma};
-            const bool ok4[4] = {true, ma != a, mb != b, ma != a && mb != b};
-            for (int m = 0; m < 4; ++m)
-              if (ok4[m]) {
-                h.mslot[cl][h.nmem[cl]++] = nc;
-                h.clof[nc] = cl;
-                h.colof[nc++] = c4[m];
-              }
+            const SarClass &c = v.cls[b * hx + pp];
+            h.kr2[cl] = c.kr2;
+            h.jlo[cl] = c.jlo;
+            h.jhi[cl] = c.jhi;
+            for (int m = 0; m < c.nmem; ++m) {
+              h.mslot[cl][h.nmem[cl]++] = nc;
+              h.clof[nc] = cl;
+              h.colof[nc++] = c.col[m];
+            }
           }
-          (void)hx;
           h.nused = nc;
           h.f = f;
           const float2 *wf = v.w0 + (size_t)f * nx * v.ny * (size_t)nk;

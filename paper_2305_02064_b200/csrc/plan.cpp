@@ -98,6 +98,7 @@ namespace {
 // Host tables produced by the fp64 decomposition (uploaded by sar_plan_create).
 struct HostTables {
   std::vector<float> apose, bpair, kturn, pinv, tw;
+  std::vector<SarClass> cls;
   std::vector<double> kx, ky, kz, kd, rref;
   size_t tw_y_off = 0, tw_z_off = 0;
   int roll_x = 0, roll_y = 0;
@@ -227,6 +228,48 @@ int host_decompose(const sar_geom_desc *g, const sar_image_desc *im, uint32_t fl
   T.tw_z_off = T.tw.size() / 2;
   twiddles(T.tw, p->nz);
 
+  // Stolt mirror classes: k_r^2, member columns and a superset of the in-band
+  // k_z bins.  u(j) = (sqrt(k_z,j^2 + k_r^2)/2 - k_0)/dk is monotone in j; the
+  // band edges u = 0 and u = n_k - 1 sit at k_z = sqrt(4 k_0^2 - k_r^2) and
+  // sqrt(4 k_max^2 - k_r^2); the range is widened by 2 bins each side and to
+  // the whole axis when an edge lies within 1e-3 bins of k_z = 0 (du/dj -> 0
+  // there).  Bins outside are zero; the device's bit-exact pull decides inside.
+  {
+    const int hx = p->nx / 2 + 1, hy = p->ny / 2 + 1, nz = p->nz;
+    const double kmax = T.k0 + (double)(nk - 1) * T.dk, kz_top = T.kz[nz - 1];
+    T.cls.resize((size_t)hx * hy);
+    for (int b = 0; b < hy; ++b)
+      for (int a = 0; a < hx; ++a) {
+        SarClass &c = T.cls[(size_t)b * hx + a];
+        memset(&c, 0, sizeof(c));
+        const double kxa = T.kx[a] * T.kx[a], kyb = T.ky[b] * T.ky[b];
+        c.kr2 = kxa + kyb;
+        const int ma = (p->nx - a) & (p->nx - 1), mb = (p->ny - b) & (p->ny - 1);
+        const int c4[4] = {b * p->nx + a, b * p->nx + ma, mb * p->nx + a, mb * p->nx + ma};
+        const bool ok4[4] = {true, ma != a, mb != b, ma != a && mb != b};
+        for (int m = 0; m < 4; ++m)
+          if (ok4[m]) c.col[c.nmem++] = c4[m];
+        const double qhi = 4.0 * kmax * kmax - c.kr2, qlo = 4.0 * T.k0 * T.k0 - c.kr2;
+        if (!(qhi > 0.0)) {
+          c.jlo = 0;
+          c.jhi = -1;
+          continue;
+        }
+        const double kzhi = sqrt(qhi), kzlo = qlo > 0.0 ? sqrt(qlo) : 0.0;
+        if (kzlo < 1e-3 * dkz || kzhi < 1e-3 * dkz) {
+          c.jlo = 0;
+          c.jhi = nz - 1;
+          continue;
+        }
+        const double jl = (double)(nz - 1) - (kz_top - kzlo) / dkz;
+        const double jh = (double)(nz - 1) - (kz_top - kzhi) / dkz;
+        const int lo = (int)std::max(floor(jl) - 2.0, 0.0);
+        const int hi = (int)std::min(ceil(jh) + 2.0, (double)(nz - 1));
+        c.jlo = lo;
+        c.jhi = hi < lo ? lo - 1 : hi;
+      }
+  }
+
   // O7 rolls and axes (reading R8)
   T.roll_x = p->nvx / 2 - p->nx / 2;
   T.roll_y = p->nvy / 2 - p->ny / 2;
@@ -322,6 +365,7 @@ int sar_plan_create(sar_plan **out, const sar_geom_desc *g, const sar_image_desc
   const size_t o_rr = off; off += al(T.rref.size() * 8 + 8);
   const size_t o_pi = off; off += al(T.pinv.size() * 4);
   const size_t o_tw = off; off += al(T.tw.size() * 4);
+  const size_t o_cl = off; off += al(T.cls.size() * sizeof(SarClass));
   ce = cudaMalloc(&p->d_tables, off);
   if (ce != cudaSuccess) {
     cudaGetLastError();
@@ -341,7 +385,8 @@ int sar_plan_create(sar_plan **out, const sar_geom_desc *g, const sar_image_desc
       (ce = up(o_kz, T.kz.data(), T.kz.size() * 8)) != cudaSuccess ||
       (ce = up(o_rr, T.rref.data(), T.rref.size() * 8)) != cudaSuccess ||
       (ce = up(o_pi, T.pinv.data(), T.pinv.size() * 4)) != cudaSuccess ||
-      (ce = up(o_tw, T.tw.data(), T.tw.size() * 4)) != cudaSuccess) {
+      (ce = up(o_tw, T.tw.data(), T.tw.size() * 4)) != cudaSuccess ||
+      (ce = up(o_cl, T.cls.data(), T.cls.size() * sizeof(SarClass))) != cudaSuccess) {
     free_plan(p);
     return cuda_fail(ce, "table upload");
   }
@@ -371,6 +416,7 @@ int sar_plan_create(sar_plan **out, const sar_geom_desc *g, const sar_image_desc
   v.ky = (const double *)(base + o_ky);
   v.kz = (const double *)(base + o_kz);
   v.rref = (const double *)(base + o_rr);
+  v.cls = (const SarClass *)(base + o_cl);
   v.pinv = T.pinv.empty() ? nullptr : (const float2 *)(base + o_pi);
   v.tw_x = (const float2 *)(base + o_tw);
   v.tw_y = (const float2 *)(base + o_tw) + T.tw_y_off;

@@ -13,6 +13,15 @@
 #define SAR_PROFILE_RING 1024
 #define SAR_N_STAGES 5
 
+// One Stolt mirror class (a, b), 0 <= a <= nx/2, 0 <= b <= ny/2: the up to 4
+// spectral columns (+-a, +-b) that share k_r^2 (built on the host, plan.cpp).
+struct SarClass {
+  double kr2;      // k_x[a]^2 + k_y[b]^2 (IEEE, no contraction; reading R9)
+  int jlo, jhi;    // superset of the in-band k_z bins (empty if jhi < jlo)
+  int nmem, pad;   // member columns
+  int col[4];      // column index b'*nx + a' of each member
+};
+
 // Everything a kernel needs, passed by value (fits the 32 KB parameter space).
 struct SarDeviceView {
   int F, nt, nr, npair, npx, npy, P, nk, nx, ny, nz;
@@ -27,6 +36,7 @@ struct SarDeviceView {
   const double *ky;     // [ny]
   const double *kz;     // [nz]        uniform Stolt grid (reading R5)
   const double *rref;   // [F]         R_ref = z_ref - Z_0
+  const SarClass *cls;  // [(ny/2+1)*(nx/2+1)] mirror classes, q = b*(nx/2+1) + a
   const float2 *pinv;   // [nk] 1/P(f) or nullptr (P == 1)
   const float2 *tw_x;   // [nx] exp(-2 pi i m/nx)
   const float2 *tw_y;   // [ny]
