@@ -905,12 +905,13 @@ __device__ __forceinline__ void stolt_range(const SarDeviceView &v, double kr2, 
   *jhi = hi < lo ? lo - 1 : hi;
 }
 constexpr int K3P_G = 256;   // threads per consumer group
+constexpr int K3P_NG = 2;    // consumer groups (alternate items)
 constexpr int K3P_S = 3;     // ring stages
 template <int NZ, int CL>
 size_t k3pp_smem(int nk) {
   const size_t hdr = (sizeof(K3Hdr<CL>) + 15) & ~(size_t)15;
   return K3P_S * (hdr + (size_t)4 * CL * nk * sizeof(float2)) +
-         2 * ((size_t)NZ * (4 * CL + 1)) * sizeof(float2) +
+         K3P_NG * ((size_t)NZ * (4 * CL + 1)) * sizeof(float2) +
          ((size_t)NZ + nk) * sizeof(double) + (size_t)NZ * sizeof(float2);
 }
 
@@ -925,7 +926,7 @@ __device__ __forceinline__ void k3pp_consume(const SarDeviceView &v, int nitems_
   const int ncol = v.nx * v.ny;
   const int nitems = nitems_f * v.F;
   unsigned n = g;
-  for (int item = blockIdx.x + g * gridDim.x; item < nitems; item += 2 * gridDim.x, n += 2) {
+  for (int item = blockIdx.x + g * gridDim.x; item < nitems; item += K3P_NG * gridDim.x, n += K3P_NG) {
     const int st = n % K3P_S;
     sartma::mbar_wait(&full[st], (n / K3P_S) & 1);
     unsigned char *sb = ring + st * stage_bytes;
@@ -1001,10 +1002,10 @@ __device__ __forceinline__ void k3pp_consume(const SarDeviceView &v, int nitems_
 }
 
 template <int NZ, int CL, bool DO_IFFT>
-__global__ void __launch_bounds__(2 * K3P_G + 32, 1) k3_pp(const SarDeviceView v, int nitems_f) {
+__global__ void __launch_bounds__(K3P_NG * K3P_G + 32, 1) k3_pp(const SarDeviceView v, int nitems_f) {
   constexpr int CC = 4 * CL;
   constexpr int LD = CC + 1;
-  constexpr int NTH = 2 * K3P_G + 32;
+  constexpr int NTH = K3P_NG * K3P_G + 32;
   extern __shared__ __align__(16) unsigned char smp[];
   const int nk = v.nk;
   const size_t hdr_bytes = (sizeof(K3Hdr<CL>) + 15) & ~(size_t)15;
@@ -1012,11 +1013,11 @@ __global__ void __launch_bounds__(2 * K3P_G + 32, 1) k3_pp(const SarDeviceView v
   unsigned char *ring = smp;
   float2 *grp = reinterpret_cast<float2 *>(smp + K3P_S * stage_bytes);
   const size_t grp_elems = (size_t)NZ * LD;                      // fout per group
-  double *ks = reinterpret_cast<double *>(grp + 2 * grp_elems);  // [nk]
+  double *ks = reinterpret_cast<double *>(grp + K3P_NG * grp_elems);  // [nk]
   double *kzs = ks + nk;                                          // [NZ]
   float2 *tw = reinterpret_cast<float2 *>(kzs + NZ);              // [NZ]
   __shared__ __align__(8) uint64_t full[K3P_S], empty[K3P_S];
-  __shared__ int colofs[2][CC], slo[2][CC], shi[2][CC];
+  __shared__ int colofs[K3P_NG][CC], slo[K3P_NG][CC], shi[K3P_NG][CC];
   const int tid = threadIdx.x;
   for (int i = tid; i < nk; i += NTH) ks[i] = v.k[i];
   for (int i = tid; i < NZ; i += NTH) {
@@ -1033,8 +1034,8 @@ __global__ void __launch_bounds__(2 * K3P_G + 32, 1) k3_pp(const SarDeviceView v
   __syncthreads();
   const int ncol = v.nx * v.ny;
   const int nitems = nitems_f * v.F;
-  if (tid >= 2 * K3P_G) {
-    if (tid == 2 * K3P_G) {  // producer
+  if (tid >= K3P_NG * K3P_G) {
+    if (tid == K3P_NG * K3P_G) {  // producer
       const int hx = v.nx / 2 + 1, hy = v.ny / 2 + 1;
       const int nclass = hx * hy;
       unsigned n = 0;
@@ -1669,7 +1670,7 @@ cudaError_t launch_k3(const SarDeviceView &v, bool ifft, cudaStream_t s, int num
     auto kern = ifft ? k3_pp<N, CL, true> : k3_pp<N, CL, false>;                                               \
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);        \
     if (e != cudaSuccess) return e;                                                                            \
-    kern<<<grid, 2 * K3P_G + 32, smem, s>>>(v, nitems_f);                                                      \
+    kern<<<grid, K3P_NG * K3P_G + 32, smem, s>>>(v, nitems_f);                                                 \
     return cudaGetLastError();                                                                                 \
   }
       X(256) X(512) X(1024)
