@@ -371,3 +371,14 @@ def raster_scene(npx, npy, nx, ny, n_k, nz, dz_img, z_ref, *, n_tx=2, monostatic
                  scan[:, :, 2].mean(axis=1), wavenumbers(n_k), nx, ny, nz, dz_img, z_ref,
                  [np.zeros((0, 3))] * n_frames, [np.zeros(0, complex)] * n_frames,
                  _noise_key(1000 + seed), 0.0)
+
+
+def frame_subset(sc: Scene, lo: int, hi: int) -> Scene:
+    """Frames [lo, hi) of a multi-frame scene as a scene of its own, with the
+    noise counter shifted so that its echo equals frames lo..hi-1 of the full
+    scene's echo (sample n of the subset uses counter key + 2*(n + offset))."""
+    lo, hi = max(0, lo), min(sc.n_frames, hi)
+    per_frame = sc.n_tx * sc.n_rx * sc.n_pos * sc.n_k
+    key = (int(sc.noise_key) + 2 * lo * per_frame) & 0xFFFFFFFFFFFFFFFF
+    return dataclasses.replace(sc, n_frames=hi - lo, scan=sc.scan[lo:hi], z0=sc.z0[lo:hi],
+                               scat_pos=sc.scat_pos[lo:hi], scat_amp=sc.scat_amp[lo:hi], noise_key=key)
