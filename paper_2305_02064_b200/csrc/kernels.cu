@@ -1392,7 +1392,7 @@ __device__ __noinline__ void pb_stolt(const SarDeviceView *vp, unsigned char *sb
 template <int NY, int NZ, bool DO_IFFT>
 __global__ void __launch_bounds__(PB_NT + 32, 2)
     k_passb(const __grid_constant__ SarDeviceView v, const __grid_constant__ CUtensorMap tm0, const __grid_constant__ CUtensorMap tm1,
-            const int4 *__restrict__ items, int nitems, int *__restrict__ cnt, int stop, int discard) {
+            const int4 *__restrict__ items, int nitems, int *__restrict__ cnt, int stop, int discard, int plain) {
   constexpr int CL = PB_CL, CC = 4 * CL, LD = CC + 1;
   constexpr int ROWS = NY < 256 ? NY : 256;
   constexpr int NBOX = NY / ROWS;
@@ -1444,6 +1444,8 @@ __global__ void __launch_bounds__(PB_NT + 32, 2)
           for (int bx = 0; bx < NBOX; ++bx)
             sartma::tma_load_3d(sb + bx * ROWS * PB_KC * sizeof(float2), &tm0, it.w * PB_KC, it.z,
                                 f * NY + bx * ROWS, &full[st]);
+        } else if (it.x == 2 && plain) {
+          sartma::mbar_arrive(&full[st]);  // consumers wait for S(G) and load the tile themselves
         } else if (it.x == 2) {
           const int pp = it.z < nx - it.z ? it.z : nx - it.z;
           const int *c = cnt + FP + f * P + pp;
@@ -1458,8 +1460,10 @@ __global__ void __launch_bounds__(PB_NT + 32, 2)
           const int pp = it.z;
           const int nkx = (pp == 0 || 2 * pp == nx) ? 1 : 2;
           const int *c = cnt + f * P + pp;
-          while (ld_acquire(c) < nkx * nchunk_k) __nanosleep(64);
-          fence_proxy_async_global();
+          if (!plain) {
+            while (ld_acquire(c) < nkx * nchunk_k) __nanosleep(64);
+            fence_proxy_async_global();
+          }
           K3Hdr<CL> &h = *reinterpret_cast<K3Hdr<CL> *>(sb);
           float2 *fin = reinterpret_cast<float2 *>(sb + hdr_bytes);
           int nc = 0;
@@ -1483,9 +1487,13 @@ __global__ void __launch_bounds__(PB_NT + 32, 2)
           h.nused = nc;
           h.f = f;
           const float2 *wf = v.w0 + (size_t)f * nx * v.ny * (size_t)nk;
-          sartma::mbar_arrive_expect_tx(&full[st], (uint32_t)nc * (uint32_t)nk * 8u);
-          for (int sl = 0; sl < nc; ++sl)
-            sartma::bulk_g2s(fin + sl * nk, wf + (size_t)h.colof[sl] * nk, (uint32_t)nk * 8u, &full[st]);
+          if (plain) {
+            sartma::mbar_arrive(&full[st]);  // consumers wait for Y(G) and load the columns
+          } else {
+            sartma::mbar_arrive_expect_tx(&full[st], (uint32_t)nc * (uint32_t)nk * 8u);
+            for (int sl = 0; sl < nc; ++sl)
+              sartma::bulk_g2s(fin + sl * nk, wf + (size_t)h.colof[sl] * nk, (uint32_t)nk * 8u, &full[st]);
+          }
         }
         ++n;
       }
@@ -1501,6 +1509,38 @@ __global__ void __launch_bounds__(PB_NT + 32, 2)
     sartma::mbar_wait(&full[st], (n / PB_S) & 1);
     unsigned char *sb = ring + st * stage_bytes;
     const int f = it.y;
+    if (plain && it.x != 0) {
+      // wait for the producing items, then load through L2 with ordinary
+      // (coherent) loads: no TMA read of lines this kernel just wrote
+      if (tid == 0) {
+        const int pp = it.x == 2 ? (it.z < nx - it.z ? it.z : nx - it.z) : it.z;
+        const int nkx = (pp == 0 || 2 * pp == nx) ? 1 : 2;
+        const int *c = it.x == 2 ? cnt + FP + f * P + pp : cnt + f * P + pp;
+        const int target = it.x == 2 ? nS : nkx * nchunk_k;
+        while (ld_acquire(c) < target) __nanosleep(64);
+      }
+      sarfft2::sync<1, PB_NT>();
+      if (it.x == 2) {
+        const float4 *src = reinterpret_cast<const float4 *>(v.w1 + ((size_t)f * NY * nx + it.z) * (size_t)v.nz +
+                                                             it.w * PB_KC);
+        float4 *dstt = reinterpret_cast<float4 *>(sb);
+        const size_t row4 = (size_t)nx * v.nz / 2;
+        for (int e = tid; e < NY * PB_KC / 2; e += PB_NT) {
+          const int r = e / (PB_KC / 2), q = e - r * (PB_KC / 2);
+          dstt[e] = __ldcg(src + r * row4 + q);
+        }
+      } else {
+        const K3Hdr<CL> &h = *reinterpret_cast<const K3Hdr<CL> *>(sb);
+        float4 *fin4 = reinterpret_cast<float4 *>(sb + hdr_bytes);
+        const float2 *wf = v.w0 + (size_t)f * nx * v.ny * (size_t)nk;
+        const int h2 = nk / 2;
+        for (int e = tid; e < h.nused * h2; e += PB_NT) {
+          const int sl = e / h2, i = e - sl * h2;
+          fin4[e] = __ldcg(reinterpret_cast<const float4 *>(wf + (size_t)h.colof[sl] * nk) + i);
+        }
+      }
+      sarfft2::sync<1, PB_NT>();
+    }
     if (it.x != 1) {
       const int inner = it.x == 0 ? nk : v.nz;
       float2 *base = (it.x == 0 ? v.w0 : v.w1) + ((size_t)f * NY * nx + it.z) * (size_t)inner + it.w * PB_KC;
@@ -1778,6 +1818,7 @@ bool passb_supported(const SarDeviceView &v) {
 
 cudaError_t launch_passb(const SarDeviceView &v, const CUtensorMap *tm0, const CUtensorMap *tm1, const int4 *items,
                          int nitems, int *cnt, int stop, bool discard, cudaStream_t s, int num_sms) {
+  const int plain = getenv("SAR_PB_PLAIN") ? 1 : 0;
   cudaError_t e = cudaMemsetAsync(cnt, 0, (size_t)2 * v.F * (v.nx / 2 + 1) * sizeof(int), s);
   if (e != cudaSuccess) return e;
 #define X(A, B)                                                                                         \
@@ -1792,7 +1833,7 @@ cudaError_t launch_passb(const SarDeviceView &v, const CUtensorMap *tm0, const C
     if (occ < 1) return cudaErrorInvalidConfiguration;                                                  \
     const int maxg = num_sms * occ;                                                                     \
     const int grid = nitems < maxg ? nitems : maxg;                                                     \
-    kern<<<grid, PB_NT + 32, smem, s>>>(v, *tm0, *tm1, items, nitems, cnt, stop, discard ? 1 : 0);      \
+    kern<<<grid, PB_NT + 32, smem, s>>>(v, *tm0, *tm1, items, nitems, cnt, stop, discard ? 1 : 0, plain); \
     return cudaGetLastError();                                                                          \
   }
   SAR_PASSB_PAIRS(X)
