@@ -21,6 +21,8 @@ O4     filter k_z/P(f) * exp(-j k_z Z_0) with k_z^2 = 4k^2-kx^2-ky^2   Eq. (13) 
 O5     Stolt interpolation onto a uniform k_z grid                    Eq. (14)
 O6     IFT_3D                                                         Eq. (14)
 O7     magnitude, axes                                               (reading)
+O5'-7' 2-D single-plane image: back-propagate to z_s, sum over k,    Table I 2-D rows
+       IFT_2D, magnitude (oracle/plane2d.py)                          P:394, P:602-609
 =====  ==========================================================  ===========
 
 The readings taken where the paper is silent or inconsistent (sign of the 2d_z
@@ -38,3 +40,4 @@ scatterers landing on their voxel, and back-projection brute force.
 from .rma import (Geometry, decompose, compensate, fft2, rma_filter, stolt,  # noqa: F401
                   ifft3, magnitude_image, reconstruct, stolt_index_table, BAND_EPS)
 from .bpa import bpa  # noqa: F401
+from .plane2d import plane_sum, ifft2_planes, magnitude_planes, reconstruct_planes  # noqa: F401
