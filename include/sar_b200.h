@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define SAR_B200_VERSION 1
+#define SAR_B200_VERSION 2
 
 typedef struct sar_plan sar_plan;       /* opaque */
 typedef struct CUstream_st *sar_stream; /* == cudaStream_t; NULL = legacy default stream */
@@ -53,7 +53,11 @@ enum sar_flags {
   SAR_NO_COMPENSATION = 1u << 0, /* beta == 0: plain RMA on the raw samples (the paper's
                                     failure baseline) */
   SAR_OUTPUT_COMPLEX = 1u << 1,  /* image is complex64 o (scaled, rolled) instead of |o| */
-  SAR_PROFILE_STAGES = 1u << 2   /* record CUDA events around every kernel (sar_plan_profile_read) */
+  SAR_PROFILE_STAGES = 1u << 2,  /* record CUDA events around every kernel (sar_plan_profile_read) */
+  SAR_IMAGE_2D = 1u << 3         /* 2-D single-plane images (reading R18, "2-D Proposed" of Table I,
+                                    P:394): step 3 becomes the back-propagation of every
+                                    filtered column to each plane of sar_image_desc.z_planes summed
+                                    over k (no Stolt), the image is [F][nz planes][ny][nx] */
 };
 
 /* Limits of this build. */
@@ -84,9 +88,12 @@ typedef struct {
 /* Image grid. */
 typedef struct {
   int32_t nx, ny;  /* spatial FFT size = image x/y size; powers of two in [2, SAR_MAX_FFT] */
-  int32_t nz;      /* Stolt bins = image z size; power of two in [2, SAR_MAX_FFT] */
-  double dz;       /* image z pitch (m); k_z grid spacing 2*pi/(nz*dz) (reading R5) */
+  int32_t nz;      /* Stolt bins = image z size; power of two in [2, SAR_MAX_FFT].
+                      With SAR_IMAGE_2D: the number of planes, 1..SAR_MAX_FFT (any count) */
+  double dz;       /* image z pitch (m); k_z grid spacing 2*pi/(nz*dz) (reading R5); unused in 2-D */
   double z_ref;    /* reference depth (m): centre of the z window and R_ref = z_ref - Z_0 > 0 */
+  const double *z_planes; /* SAR_IMAGE_2D only: [nz] plane depths z_s (world, m; host memory, copied);
+                             ignored (may be NULL) otherwise */
 } sar_image_desc;
 
 /* Host-side result of the geometry decomposition (no device needed). */
@@ -119,7 +126,8 @@ int sar_plan_describe(const sar_geom_desc *g, const sar_image_desc *im, uint32_t
 int sar_plan_create(sar_plan **out, const sar_geom_desc *g, const sar_image_desc *im,
                     uint32_t flags);
 
-/* Reconstruct.  d_data: device, complex64 [F][n_tx][n_rx][npy*npx][n_k],
+/* Reconstruct (3-D volume, or the planes of a SAR_IMAGE_2D plan).
+ * d_data: device, complex64 [F][n_tx][n_rx][npy*npx][n_k],
  * 8-byte aligned, read only, caller-owned.  d_image: device, float32
  * [F][nz][ny][nx] (complex64 with SAR_OUTPUT_COMPLEX), caller-owned, fully
  * overwritten.  Voxel (m,iy,ix) is at world (x_first+ix*dx, y_first+iy*dy,
@@ -140,7 +148,8 @@ int sar_reconstruct_host(sar_plan *p, const void *h_data, void *h_image, sar_str
 int sar_plan_destroy(sar_plan *p);
 
 /* out[6] = {x_first, y_first, z_first, dx, dy, dz} of the output voxel grid
- * (each axis periodic with period n*pitch; reading R8). */
+ * (each axis periodic with period n*pitch; reading R8).  2-D plans: z_first =
+ * z_planes[0] and dz = z_planes[1] - z_planes[0] (0 for one plane). */
 int sar_plan_get_axes(const sar_plan *p, double out[6]);
 
 /* Bytes of device workspace owned by the plan (excluding staging buffers). */
@@ -162,7 +171,8 @@ int sar_plan_launches_per_call(const sar_plan *p, int32_t *n);
 /* Run the path up to `stage` and copy that stage's result to d_out (device):
  *   1: planar lattice after correction, complex64 [F][ny][nx][n_k]
  *   2: spatial spectrum after the 2-D FFT, complex64 [F][ny][nx][n_k]
- *   3: Stolt output before the z-IFFT, complex64 [F][ny][nx][nz]
+ *   3: Stolt output before the z-IFFT, complex64 [F][ny][nx][nz] (2-D plans:
+ *      the plane spectra [F][ny][nx][n planes])
  *   4: rolled complex image, complex64 [F][nz][ny][nx] (scaled 1/(nx ny nz))
  * Errors: INVALID_ARG (stage outside 1..4, null pointers), CUDA. */
 int sar_debug_stage(sar_plan *p, int32_t stage, const void *d_data, void *d_out,

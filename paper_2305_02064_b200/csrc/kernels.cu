@@ -605,7 +605,7 @@ __global__ void __launch_bounds__(sarfft2::nt_fft<NX, KC>() + 32)
         [&](int c, int a, float2 o) {
           const int z = zc * KC + c;
           if (z < nz) {
-            int m = z + nz / 2;
+            int m = z + v.zroll;
             if (m >= nz) m -= nz;
             const int ix = (a - rx) & (NX - 1);
             if constexpr (CPLX) {
@@ -1085,6 +1085,89 @@ __global__ void __launch_bounds__(K3P_NG * K3P_G + 32, 1) k3_pp(const SarDeviceV
                                      colofs[1], slo[1], shi[1]);
 }
 
+// ------------------------------------------------------- K3, 2-D mode ----
+// SAR_IMAGE_2D (reading R18): per Stolt mirror class (the <= 4 columns that
+// share k_r^2), k_z,i = sqrt(4 k_i^2 - k_r^2) once, then for every plane s the
+// back-propagation weights w_i = k_z,i exp(+j k_z,i (z_s - Z_0)) / P_i (phase
+// in turns, fp64) and, per member column, the sum over k of S_i w_i (one warp
+// per column: lanes stride over k, shuffle reduction).  Output W1[f][b][a][s]
+// (planes fastest), which the y- and x-inverse kernels then transform like the
+// z-chunks of the 3-D path.
+constexpr int K3P2_NT = 128;
+constexpr int K3P2_CL = 4;
+
+__global__ void __launch_bounds__(K3P2_NT) k3_plane(const SarDeviceView v) {
+  constexpr int CL = K3P2_CL, CC = 4 * CL, NW = K3P2_NT / 32;
+  extern __shared__ __align__(16) unsigned char sm2[];
+  const int nk = v.nk, ns = v.nz;
+  float2 *fin = reinterpret_cast<float2 *>(sm2);         // [CC][nk]
+  float2 *w = fin + (size_t)CC * nk;                      // [CL][nk] weights of one plane
+  double *kzt = reinterpret_cast<double *>(w + (size_t)CL * nk);  // [CL][nk] k_z (0 = evanescent)
+  __shared__ int colof[CC];
+  __shared__ double kr2s[CL];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int ncol = v.nx * v.ny;
+  const int nclass = (v.nx / 2 + 1) * (v.ny / 2 + 1);
+  const int q0 = blockIdx.x * CL;
+  const int f = blockIdx.y;
+  if (tid < CL) {
+    const int q = q0 + tid;
+    const bool ok = q < nclass;
+    kr2s[tid] = ok ? v.cls[q].kr2 : 0.0;
+#pragma unroll
+    for (int m = 0; m < 4; ++m) colof[4 * tid + m] = (ok && m < v.cls[q].nmem) ? v.cls[q].col[m] : -1;
+  }
+  __syncthreads();
+  const float2 *wf = v.w0 + (size_t)f * ncol * (size_t)nk;
+  for (int e = tid; e < CC * nk; e += K3P2_NT) {
+    const int sl = e / nk, i = e - sl * nk;
+    if (colof[sl] >= 0) fin[e] = __ldcs(wf + (size_t)colof[sl] * nk + i);
+  }
+  for (int e = tid; e < CL * nk; e += K3P2_NT) {
+    const int cl = e / nk, i = e - cl * nk;
+    const double ki = __ldg(v.k + i);
+    const double q = 4.0 * ki * ki - kr2s[cl];
+    kzt[e] = q > 0.0 ? fast_dsqrt(q) : 0.0;
+  }
+  __syncthreads();
+  const double zoff = v.rref[f];   // z_s - Z_0 = (z_s - z_ref) + R_ref
+  float2 *dst = v.w1 + (size_t)f * ncol * (size_t)ns;
+  for (int s = 0; s < ns; ++s) {
+    const double tz = (__ldg(v.kz + s) + zoff) * (1.0 / TWO_PI);
+    for (int e = tid; e < CL * nk; e += K3P2_NT) {
+      const double kz = kzt[e];
+      float2 hh = make_float2(0.f, 0.f);
+      if (kz > 0.0) {
+        double turns = kz * tz;
+        turns -= rint(turns);
+        float sn, cs;
+        __sincosf((float)turns * 6.28318530717958647692f, &sn, &cs);
+        const float kzf = (float)kz;
+        hh = make_float2(kzf * cs, kzf * sn);
+        const int i = e % nk;
+        if (v.pinv) hh = cmul(hh, v.pinv[i]);
+      }
+      w[e] = hh;
+    }
+    __syncthreads();
+    for (int sl = warp; sl < CC; sl += NW) {
+      const int col = colof[sl];
+      if (col < 0) continue;
+      const float2 *x = fin + sl * nk;
+      const float2 *ww = w + (sl >> 2) * nk;
+      float2 acc = make_float2(0.f, 0.f);
+      for (int i = lane; i < nk; i += 32) acc = cmac2(acc, x[i], ww[i]);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
+        acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
+      }
+      if (lane == 0) dst[(size_t)col * ns + s] = acc;
+    }
+    __syncthreads();
+  }
+}
+
 __global__ void k_stolt_index(const SarDeviceView v, const int32_t *__restrict__ cols, int n,
                               int32_t *__restrict__ i0_out, float *__restrict__ tau_out) {
   const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -1142,7 +1225,7 @@ __global__ void __launch_bounds__(nt_for(NX), minb_for(NX))
     const int zz = item / NX, ix = item - zz * NX;
     const int z = zbase + zz;
     if (z >= nz) continue;
-    int m = z + nz / 2;
+    int m = z + v.zroll;
     if (m >= nz) m -= nz;
     const int xs = (ix + rx) & (NX - 1);
     const float2 o = tile[xs * LD + zz];
@@ -1228,7 +1311,7 @@ __global__ void __launch_bounds__(ntp_for(NX), ctas_for(NX))
       const int zz = i / NX, ix = i % NX;
       const int z = zc * KC + zz;
       if (z < nz) {
-        int m = z + nz / 2;
+        int m = z + v.zroll;
         if (m >= nz) m -= nz;
         outp[m * zstride + ix] = ob[zz * (NX + 1) + ix];
       }
@@ -1575,7 +1658,7 @@ __global__ void __launch_bounds__(PB_NT + 32, 2)
 template <typename K>
 cudaError_t launch(K kernel, dim3 grid, int nt, size_t smem, cudaStream_t s, const SarDeviceView &v,
                    const float2 *arg) {
-  if (smem > 48 * 1024) {
+  if (smem > 40 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }
@@ -1631,7 +1714,7 @@ cudaError_t launch_mid(float2 *data, const float2 *tw, int F, int ny, int nx, in
   case N: {                                                                                        \
     auto kern = k_fft_mid2<N, DIR>;                                                                \
     constexpr size_t smem = mid2_smem<N>();                                                        \
-    if (smem > 48 * 1024) {                                                                        \
+    if (smem > 40 * 1024) {                                                                        \
       cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
       if (e != cudaSuccess) return e;                                                              \
     }                                                                                              \
@@ -1653,7 +1736,7 @@ cudaError_t launch_mid(float2 *data, const float2 *tw, int F, int ny, int nx, in
 #define X(N)                                                                                       \
   case N: {                                                                                        \
     auto kern = k_fft_mid_tma<N, DIR>;                                                             \
-    if (smem > 48 * 1024) {                                                                        \
+    if (smem > 40 * 1024) {                                                                        \
       cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
       if (e != cudaSuccess) return e;                                                              \
     }                                                                                              \
@@ -1672,7 +1755,7 @@ cudaError_t launch_mid(float2 *data, const float2 *tw, int F, int ny, int nx, in
 #define X(N)                                                                                       \
   case N: {                                                                                        \
     auto kern = k_fft_mid<N, DIR>;                                                                 \
-    if (smem > 48 * 1024) {                                                                        \
+    if (smem > 40 * 1024) {                                                                        \
       cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
       if (e != cudaSuccess) return e;                                                              \
     }                                                                                              \
@@ -1687,7 +1770,7 @@ cudaError_t launch_mid(float2 *data, const float2 *tw, int F, int ny, int nx, in
 
 template <typename K>
 cudaError_t launch_v(K kernel, dim3 grid, int nt, size_t smem, cudaStream_t s, const SarDeviceView &v) {
-  if (smem > 48 * 1024) {
+  if (smem > 40 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }
@@ -1726,7 +1809,7 @@ cudaError_t launch_k3(const SarDeviceView &v, bool ifft, cudaStream_t s, int num
     if (smem > 220 * 1024) return cudaErrorInvalidValue;                                                       \
     dim3 grid((nclass + CL - 1) / CL, v.F);                                                                    \
     auto kern = ifft ? k3_class<N, true> : k3_class<N, false>;                                                 \
-    if (smem > 48 * 1024) {                                                                                    \
+    if (smem > 40 * 1024) {                                                                                    \
       cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);      \
       if (e != cudaSuccess) return e;                                                                          \
     }                                                                                                          \
@@ -1742,7 +1825,7 @@ cudaError_t launch_k3(const SarDeviceView &v, bool ifft, cudaStream_t s, int num
 template <typename K>
 cudaError_t launch_img(K kernel, dim3 grid, int nt, size_t smem, cudaStream_t s, const SarDeviceView &v,
                        void *img) {
-  if (smem > 48 * 1024) {
+  if (smem > 40 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }
@@ -1760,7 +1843,7 @@ cudaError_t launch_k4b(const SarDeviceView &v, void *img, bool cplx, cudaStream_
   case N: {                                                                                            \
     auto kern = cplx ? k4_xifft_mag2<N, true> : k4_xifft_mag2<N, false>;                               \
     constexpr size_t smem = k4b2_smem<N, false>();                                                     \
-    if (smem > 48 * 1024) {                                                                            \
+    if (smem > 40 * 1024) {                                                                            \
       cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
       if (e != cudaSuccess) return e;                                                                  \
     }                                                                                                  \
@@ -1882,7 +1965,16 @@ int sar_launch_pipeline(sar_plan *p, const void *d_data, void *d_image, cudaStre
                              p->num_sms));
     if (ev) SAR_CHECK(cudaEventRecord(ev[2], s));
     if (stop_stage == 2) return SAR_OK;
-    SAR_CHECK(launch_k3(v, stop_stage != 3, s, p->num_sms));
+    if (v.mode2d) {
+      const int nclass = (v.nx / 2 + 1) * (v.ny / 2 + 1);
+      const size_t smem = ((size_t)4 * K3P2_CL * v.nk + (size_t)K3P2_CL * v.nk) * sizeof(float2) +
+                          (size_t)K3P2_CL * v.nk * sizeof(double);
+      SAR_CHECK(cudaFuncSetAttribute(k3_plane, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      k3_plane<<<dim3((nclass + K3P2_CL - 1) / K3P2_CL, v.F), K3P2_NT, smem, s>>>(v);
+      SAR_CHECK(cudaGetLastError());
+    } else {
+      SAR_CHECK(launch_k3(v, stop_stage != 3, s, p->num_sms));
+    }
     if (ev) SAR_CHECK(cudaEventRecord(ev[3], s));
     if (stop_stage == 3) return SAR_OK;
     SAR_CHECK(launch_mid<+1>(v.w1, v.tw_y, v.F, v.ny, v.nx, v.nz, s, p->tma_mid1 ? &p->tm_w1_mid : nullptr,
@@ -2001,7 +2093,7 @@ int sar_setup_passb(sar_plan *p) {
   // opt-in (SAR_FUSE=1): measured slower than the unfused kernels on B200 --
   // the dirty W0/W1 slabs do not survive in L2 between producer and consumer
   // items (DRAM writes 3.3 GB instead of 1.07 GB at Large), see DESIGN.md
-  if (v.F == 0 || !getenv("SAR_FUSE") || !p->tma_pb || !passb_supported(v)) return SAR_OK;
+  if (v.F == 0 || v.mode2d || !getenv("SAR_FUSE") || !p->tma_pb || !passb_supported(v)) return SAR_OK;
   const int P = v.nx / 2 + 1;
   const int nchunk_k = (v.nk + PB_KC - 1) / PB_KC, nchunk_z = (v.nz + PB_KC - 1) / PB_KC;
   const int GT = v.F * P;

@@ -118,10 +118,18 @@ int host_decompose(const sar_geom_desc *g, const sar_image_desc *im, uint32_t fl
   if (g->npx < 1 || g->npy < 1) return fail(SAR_ERR_INVALID_ARG, "npx, npy must be >= 1");
   if (g->n_k < 2) return fail(SAR_ERR_INVALID_ARG, "n_k must be >= 2");
   if (g->n_k > SAR_MAX_NK) return fail(SAR_ERR_UNSUPPORTED, "n_k > SAR_MAX_NK");
-  if (!pow2_in_range(im->nx) || !pow2_in_range(im->ny) || !pow2_in_range(im->nz))
-    return fail(SAR_ERR_INVALID_ARG, "nx, ny, nz must be powers of two in [2, SAR_MAX_FFT]");
+  const bool mode2d = (flags & SAR_IMAGE_2D) != 0;
+  if (!pow2_in_range(im->nx) || !pow2_in_range(im->ny))
+    return fail(SAR_ERR_INVALID_ARG, "nx, ny must be powers of two in [2, SAR_MAX_FFT]");
+  if (mode2d) {
+    if (im->nz < 1 || im->nz > SAR_MAX_FFT) return fail(SAR_ERR_INVALID_ARG, "2-D plans need 1..SAR_MAX_FFT planes");
+    if (!im->z_planes) return fail(SAR_ERR_INVALID_ARG, "SAR_IMAGE_2D needs z_planes");
+  } else if (!pow2_in_range(im->nz)) {
+    return fail(SAR_ERR_INVALID_ARG, "nz must be a power of two in [2, SAR_MAX_FFT]");
+  }
   if (g->npx > im->nx || g->npy > im->ny) return fail(SAR_ERR_INVALID_ARG, "raster larger than the FFT grid");
-  if (!(g->dx > 0) || !(g->dy > 0) || !(im->dz > 0)) return fail(SAR_ERR_INVALID_ARG, "pitches must be > 0");
+  if (!(g->dx > 0) || !(g->dy > 0) || (!mode2d && !(im->dz > 0)))
+    return fail(SAR_ERR_INVALID_ARG, "pitches must be > 0");
   if ((long long)g->n_frames * g->npx * g->npy > (1LL << 31)) return fail(SAR_ERR_UNSUPPORTED, "too many poses");
   if (g->n_frames > 65535) return fail(SAR_ERR_UNSUPPORTED, "n_frames > 65535");
 
@@ -207,8 +215,14 @@ int host_decompose(const sar_geom_desc *g, const sar_image_desc *im, uint32_t fl
     const int bs = b < p->ny / 2 ? b : b - p->ny;
     T.ky[b] = 2.0 * M_PI * (double)bs / ((double)p->ny * g->dy);
   }
-  dkz = 2.0 * M_PI / ((double)p->nz * im->dz);
-  for (int j = 0; j < p->nz; ++j) T.kz[j] = 2.0 * g->k[nk - 1] - (double)(p->nz - 1 - j) * dkz;
+  if (mode2d) {
+    // 2-D plans: the "k_z table" holds the plane offsets z_s - z_ref (reading R18)
+    dkz = 1.0;
+    for (int j = 0; j < p->nz; ++j) T.kz[j] = im->z_planes[j] - im->z_ref;
+  } else {
+    dkz = 2.0 * M_PI / ((double)p->nz * im->dz);
+    for (int j = 0; j < p->nz; ++j) T.kz[j] = 2.0 * g->k[nk - 1] - (double)(p->nz - 1 - j) * dkz;
+  }
   T.kturn.resize(nk);
   for (int i = 0; i < nk; ++i) T.kturn[i] = (float)(g->k[i] / (2.0 * M_PI));
   T.pinv.clear();
@@ -236,7 +250,7 @@ int host_decompose(const sar_geom_desc *g, const sar_image_desc *im, uint32_t fl
   // there).  Bins outside are zero; the device's bit-exact pull decides inside.
   {
     const int hx = p->nx / 2 + 1, hy = p->ny / 2 + 1, nz = p->nz;
-    const double kmax = T.k0 + (double)(nk - 1) * T.dk, kz_top = T.kz[nz - 1];
+    const double kmax = T.k0 + (double)(nk - 1) * T.dk, kz_top = mode2d ? 2.0 * kmax : T.kz[nz - 1];
     T.cls.resize((size_t)hx * hy);
     for (int b = 0; b < hy; ++b)
       for (int a = 0; a < hx; ++a) {
@@ -275,10 +289,10 @@ int host_decompose(const sar_geom_desc *g, const sar_image_desc *im, uint32_t fl
   T.roll_y = p->nvy / 2 - p->ny / 2;
   p->axes[0] = g->x0 + (double)(p->jx_min + T.roll_x) * g->dx;
   p->axes[1] = g->y0 + (double)(p->jy_min + T.roll_y) * g->dy;
-  p->axes[2] = im->z_ref - (double)(p->nz / 2) * im->dz;
+  p->axes[2] = mode2d ? im->z_planes[0] : im->z_ref - (double)(p->nz / 2) * im->dz;
   p->axes[3] = g->dx;
   p->axes[4] = g->dy;
-  p->axes[5] = im->dz;
+  p->axes[5] = mode2d ? (p->nz > 1 ? im->z_planes[1] - im->z_planes[0] : 0.0) : im->dz;
   p->ws_bytes = ((size_t)F * p->ny * p->nx * ((size_t)nk + p->nz)) * sizeof(float2);
   return SAR_OK;
 }
@@ -432,7 +446,9 @@ int sar_plan_create(sar_plan **out, const sar_geom_desc *g, const sar_image_desc
     const double err = (2e-13 * kmax) / T.dk + 4.0 * 2.220446049250313e-16 * (double)nk;
     v.stolt_delta = std::max(1e-7, 100.0 * err);
   }
-  v.img_scale = (float)(1.0 / ((double)p->nx * p->ny * p->nz));
+  v.mode2d = (flags & SAR_IMAGE_2D) ? 1 : 0;
+  v.zroll = v.mode2d ? 0 : p->nz / 2;
+  v.img_scale = (float)(1.0 / ((double)p->nx * p->ny * (v.mode2d ? 1 : p->nz)));
   {
     // K1 step phasor exp(j dk beta): 5th-order Taylor needs |dk beta| small
     float amax = 0.f, bmax = 0.f;

@@ -26,6 +26,8 @@ struct SarClass {
 struct SarDeviceView {
   int F, nt, nr, npair, npx, npy, P, nk, nx, ny, nz;
   int roll_x, roll_y;
+  int zroll;            // output z roll: nz/2 (3-D, reading R8), 0 (2-D planes)
+  int mode2d;           // SAR_IMAGE_2D: kz[] holds z_s - z_ref per plane (reading R18)
   int no_comp;
   int jx[SAR_MAX_PAIRS], jy[SAR_MAX_PAIRS];  // virtual-node offsets, pair = t*nr + r
   const float *apose;   // [F][P]      -2 d_z (m), fp32

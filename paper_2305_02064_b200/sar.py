@@ -19,6 +19,7 @@ SAR_OK = 0
 SAR_NO_COMPENSATION = 1
 SAR_OUTPUT_COMPLEX = 2
 SAR_PROFILE_STAGES = 4
+SAR_IMAGE_2D = 8
 STAGE_NAMES = ("K1 correct+x-FFT", "K2 y-FFT", "K3 filter+Stolt+z-IFFT", "K4a y-IFFT", "K4b x-IFFT+|.|")
 
 
@@ -40,7 +41,7 @@ class GeomDesc(C.Structure):
 
 class ImageDesc(C.Structure):
     _fields_ = [("nx", C.c_int32), ("ny", C.c_int32), ("nz", C.c_int32),
-                ("dz", C.c_double), ("z_ref", C.c_double)]
+                ("dz", C.c_double), ("z_ref", C.c_double), ("z_planes", C.POINTER(C.c_double))]
 
 
 class PlanInfo(C.Structure):
@@ -116,7 +117,8 @@ def _stream_ptr(stream):
     return C.c_void_p(stream.cuda_stream)
 
 
-def _descriptors(tx, rx, scan, npx, npy, x0, y0, dx, dy, z0, k, nx, ny, nz, dz, z_ref, pulse, device):
+def _descriptors(tx, rx, scan, npx, npy, x0, y0, dx, dy, z0, k, nx, ny, nz, dz, z_ref, pulse, device,
+                 z_planes=None):
     keep = []
 
     def arr(a):
@@ -140,6 +142,10 @@ def _descriptors(tx, rx, scan, npx, npy, x0, y0, dx, dy, z0, k, nx, ny, nz, dz, 
         g.pulse = _dptr(arr(np.stack([pc.real, pc.imag], axis=-1)))
     g.device = int(device)
     im = ImageDesc(int(nx), int(ny), int(nz), float(dz), float(z_ref))
+    if z_planes is not None:
+        zp = arr(np.atleast_1d(z_planes))
+        im.nz = zp.shape[0]
+        im.z_planes = _dptr(zp)
     return g, im, keep
 
 
@@ -175,11 +181,15 @@ class Plan:
     the library; the plan owns the device tables and workspace."""
 
     def __init__(self, tx, rx, scan, npx, npy, x0, y0, dx, dy, z0, k, nx, ny, nz, dz, z_ref,
-                 pulse=None, flags=0, device=0):
+                 pulse=None, flags=0, device=0, z_planes=None):
+        """``z_planes`` (m) selects the 2-D single-plane mode (SAR_IMAGE_2D): the
+        image is then [F, len(z_planes), ny, nx] and nz/dz are ignored."""
         lib = load_library()
         self._lib = lib
+        if z_planes is not None:
+            flags |= SAR_IMAGE_2D
         g, im, keep = _descriptors(tx, rx, scan, npx, npy, x0, y0, dx, dy, z0, k, nx, ny, nz, dz, z_ref,
-                                   pulse, device)
+                                   pulse, device, z_planes)
         h = C.c_void_p()
         _check(lib.sar_plan_create(C.byref(h), C.byref(g), C.byref(im), C.c_uint32(flags)))
         del keep
@@ -191,10 +201,11 @@ class Plan:
         self.nx, self.ny, self.nz = im.nx, im.ny, im.nz
 
     @classmethod
-    def from_scene(cls, sc, flags=0, device=0, pulse=None):
+    def from_scene(cls, sc, flags=0, device=0, pulse=None, z_planes=None):
         """Plan for any object with the attributes of ``scenes.Scene``."""
         return cls(sc.tx, sc.rx, sc.scan, sc.npx, sc.npy, sc.x0, sc.y0, sc.dx, sc.dy, sc.z0, sc.k,
-                   sc.nx, sc.ny, sc.nz, sc.dz_img, sc.z_ref, pulse=pulse, flags=flags, device=device)
+                   sc.nx, sc.ny, sc.nz, sc.dz_img, sc.z_ref, pulse=pulse, flags=flags, device=device,
+                   z_planes=z_planes)
 
     # ---- shapes -------------------------------------------------------------
     @property

@@ -301,3 +301,32 @@ def test_fused_pass_b_parity(name, monkeypatch):
             for stage, key in ((2, "spectrum"), (3, "stolt")):
                 e2, _ = errs(plan.debug_stage(stage, d).cpu().numpy(), st[key])
                 assert e2 <= STAGE_BAR, (key, e2)
+
+
+# ---- 2-D single-plane images (SAR_IMAGE_2D, reading R18) -------------------
+@pytest.mark.parametrize("name,planes", [("tiny", [0.25]), ("small", [0.2, 0.25, 0.3]),
+                                         ("freehand", [0.30]), ("realtime", [0.25, 0.3])])
+def test_plane2d_parity(name, planes):
+    sc = scenes.make_scene(name)
+    d, s = _data(sc)
+    want, _ = oracle.reconstruct_planes(s, sc, planes)
+    with sar.Plan.from_scene(sc, z_planes=planes) as plan:
+        assert plan.image_shape == (sc.n_frames, len(planes), sc.ny, sc.nx)
+        got = plan.reconstruct(d)
+        torch.cuda.synchronize()
+        got = got.cpu().numpy()
+        ax = plan.axes()
+    e2, einf = errs(got, want)
+    assert e2 <= E2_BAR and einf <= EINF_BAR, (name, e2, einf)
+    assert ax[2] == planes[0]
+
+
+def test_plane2d_many_planes_and_complex():
+    sc = scenes.make_scene("small")
+    d, s = _data(sc)
+    planes = list(np.linspace(0.19, 0.36, 8))
+    want, _ = oracle.reconstruct_planes(s, sc, planes, complex_out=True)
+    with sar.Plan.from_scene(sc, z_planes=planes, flags=sar.SAR_OUTPUT_COMPLEX) as plan:
+        got = plan.reconstruct(d).cpu().numpy()
+    e2, _ = errs(got, want)
+    assert e2 <= E2_BAR
