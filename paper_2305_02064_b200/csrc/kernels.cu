@@ -1093,78 +1093,77 @@ __global__ void __launch_bounds__(K3P_NG * K3P_G + 32, 1) k3_pp(const SarDeviceV
 // per column: lanes stride over k, shuffle reduction).  Output W1[f][b][a][s]
 // (planes fastest), which the y- and x-inverse kernels then transform like the
 // z-chunks of the 3-D path.
-constexpr int K3P2_NT = 128;
-constexpr int K3P2_CL = 4;
+constexpr int K3P2_NT = 256;   // 8 warps = 8 mirror classes per CTA
+constexpr int K3P2_PS = 4;     // planes per pass (accumulators in registers)
 
 __global__ void __launch_bounds__(K3P2_NT) k3_plane(const SarDeviceView v) {
-  constexpr int CL = K3P2_CL, CC = 4 * CL, NW = K3P2_NT / 32;
-  extern __shared__ __align__(16) unsigned char sm2[];
-  const int nk = v.nk, ns = v.nz;
-  float2 *fin = reinterpret_cast<float2 *>(sm2);         // [CC][nk]
-  float2 *w = fin + (size_t)CC * nk;                      // [CL][nk] weights of one plane
-  double *kzt = reinterpret_cast<double *>(w + (size_t)CL * nk);  // [CL][nk] k_z (0 = evanescent)
-  __shared__ int colof[CC];
-  __shared__ double kr2s[CL];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int ncol = v.nx * v.ny;
-  const int nclass = (v.nx / 2 + 1) * (v.ny / 2 + 1);
-  const int q0 = blockIdx.x * CL;
+  const int lane = threadIdx.x & 31;
+  const int q = blockIdx.x * (K3P2_NT / 32) + (threadIdx.x >> 5);
   const int f = blockIdx.y;
-  if (tid < CL) {
-    const int q = q0 + tid;
-    const bool ok = q < nclass;
-    kr2s[tid] = ok ? v.cls[q].kr2 : 0.0;
-#pragma unroll
-    for (int m = 0; m < 4; ++m) colof[4 * tid + m] = (ok && m < v.cls[q].nmem) ? v.cls[q].col[m] : -1;
-  }
-  __syncthreads();
-  const float2 *wf = v.w0 + (size_t)f * ncol * (size_t)nk;
-  for (int e = tid; e < CC * nk; e += K3P2_NT) {
-    const int sl = e / nk, i = e - sl * nk;
-    if (colof[sl] >= 0) fin[e] = __ldcs(wf + (size_t)colof[sl] * nk + i);
-  }
-  for (int e = tid; e < CL * nk; e += K3P2_NT) {
-    const int cl = e / nk, i = e - cl * nk;
-    const double ki = __ldg(v.k + i);
-    const double q = 4.0 * ki * ki - kr2s[cl];
-    kzt[e] = q > 0.0 ? fast_dsqrt(q) : 0.0;
-  }
-  __syncthreads();
+  const int nclass = (v.nx / 2 + 1) * (v.ny / 2 + 1);
+  if (q >= nclass) return;
+  const SarClass &c = v.cls[q];
+  const int nm = c.nmem, nk = v.nk, ns = v.nz;
+  const int ncol = v.nx * v.ny;
+  const double kr2 = c.kr2;
   const double zoff = v.rref[f];   // z_s - Z_0 = (z_s - z_ref) + R_ref
-  float2 *dst = v.w1 + (size_t)f * ncol * (size_t)ns;
-  for (int s = 0; s < ns; ++s) {
-    const double tz = (__ldg(v.kz + s) + zoff) * (1.0 / TWO_PI);
-    for (int e = tid; e < CL * nk; e += K3P2_NT) {
-      const double kz = kzt[e];
-      float2 hh = make_float2(0.f, 0.f);
-      if (kz > 0.0) {
-        double turns = kz * tz;
-        turns -= rint(turns);
-        float sn, cs;
-        __sincosf((float)turns * 6.28318530717958647692f, &sn, &cs);
-        const float kzf = (float)kz;
-        hh = make_float2(kzf * cs, kzf * sn);
-        const int i = e % nk;
-        if (v.pinv) hh = cmul(hh, v.pinv[i]);
-      }
-      w[e] = hh;
-    }
-    __syncthreads();
-    for (int sl = warp; sl < CC; sl += NW) {
-      const int col = colof[sl];
-      if (col < 0) continue;
-      const float2 *x = fin + sl * nk;
-      const float2 *ww = w + (sl >> 2) * nk;
-      float2 acc = make_float2(0.f, 0.f);
-      for (int i = lane; i < nk; i += 32) acc = cmac2(acc, x[i], ww[i]);
+  const float2 *wf = v.w0 + (size_t)f * ncol * (size_t)nk;
+  const float2 *col[4];
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
-        acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
+  for (int m = 0; m < 4; ++m) col[m] = wf + (size_t)(m < nm ? c.col[m] : c.col[0]) * nk;
+  float2 *dst = v.w1 + (size_t)f * ncol * (size_t)ns;
+  for (int s0 = 0; s0 < ns; s0 += K3P2_PS) {
+    double tz[K3P2_PS];
+#pragma unroll
+    for (int u = 0; u < K3P2_PS; ++u) tz[u] = s0 + u < ns ? (__ldg(v.kz + s0 + u) + zoff) * (1.0 / TWO_PI) : 0.0;
+    float2 acc[K3P2_PS][4];
+#pragma unroll
+    for (int u = 0; u < K3P2_PS; ++u)
+#pragma unroll
+      for (int m = 0; m < 4; ++m) acc[u][m] = make_float2(0.f, 0.f);
+#pragma unroll 4
+    for (int i = lane; i < nk; i += 32) {
+      float2 x[4];
+#pragma unroll
+      for (int m = 0; m < 4; ++m) x[m] = __ldcs(col[m] + i);
+      const double ki = __ldg(v.k + i);
+      const double qq = 4.0 * ki * ki - kr2;
+      if (qq > 0.0) {
+        const double kz = fast_dsqrt(qq);
+        const float kzf = (float)kz;
+        float2 pinv = make_float2(1.f, 0.f);
+        if (v.pinv) pinv = v.pinv[i];
+#pragma unroll
+        for (int u = 0; u < K3P2_PS; ++u) {
+          double turns = kz * tz[u];
+          turns -= rint(turns);
+          float sn, cs;
+          __sincosf((float)turns * 6.28318530717958647692f, &sn, &cs);
+          const float2 w = cmul(make_float2(kzf * cs, kzf * sn), pinv);
+#pragma unroll
+          for (int m = 0; m < 4; ++m) acc[u][m] = cmac2(acc[u][m], x[m], w);
+        }
       }
-      if (lane == 0) dst[(size_t)col * ns + s] = acc;
     }
-    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < K3P2_PS; ++u)
+#pragma unroll
+      for (int m = 0; m < 4; ++m)
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          acc[u][m].x += __shfl_xor_sync(0xffffffffu, acc[u][m].x, o);
+          acc[u][m].y += __shfl_xor_sync(0xffffffffu, acc[u][m].y, o);
+        }
+    if (lane < 4 * K3P2_PS) {
+      const int u = lane >> 2, m = lane & 3;
+      float2 r = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int uu = 0; uu < K3P2_PS; ++uu)
+#pragma unroll
+        for (int mm = 0; mm < 4; ++mm)
+          if (uu == u && mm == m) r = acc[uu][mm];
+      if (m < nm && s0 + u < ns) dst[(size_t)c.col[m] * ns + s0 + u] = r;
+    }
   }
 }
 
@@ -1967,10 +1966,8 @@ int sar_launch_pipeline(sar_plan *p, const void *d_data, void *d_image, cudaStre
     if (stop_stage == 2) return SAR_OK;
     if (v.mode2d) {
       const int nclass = (v.nx / 2 + 1) * (v.ny / 2 + 1);
-      const size_t smem = ((size_t)4 * K3P2_CL * v.nk + (size_t)K3P2_CL * v.nk) * sizeof(float2) +
-                          (size_t)K3P2_CL * v.nk * sizeof(double);
-      SAR_CHECK(cudaFuncSetAttribute(k3_plane, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      k3_plane<<<dim3((nclass + K3P2_CL - 1) / K3P2_CL, v.F), K3P2_NT, smem, s>>>(v);
+      const int cpb = K3P2_NT / 32;
+      k3_plane<<<dim3((nclass + cpb - 1) / cpb, v.F), K3P2_NT, 0, s>>>(v);
       SAR_CHECK(cudaGetLastError());
     } else {
       SAR_CHECK(launch_k3(v, stop_stage != 3, s, p->num_sms));
