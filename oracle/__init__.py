@@ -23,6 +23,8 @@ O6     IFT_3D                                                         Eq. (14) P
 O7     magnitude, axes                                               (reading)
 O5'-7' 2-D single-plane image: back-propagate to z_s, sum over k,    Table I 2-D rows
        IFT_2D, magnitude (oracle/plane2d.py)                          P:394, P:602-609
+O3''   NUFFT mode: type-1 transform from the true (x', y') positions
+       (direct sum and FGG, oracle/nufft.py)
 =====  ==========================================================  ===========
 
 The readings taken where the paper is silent or inconsistent (sign of the 2d_z
@@ -41,3 +43,4 @@ from .rma import (Geometry, decompose, compensate, fft2, rma_filter, stolt,  # n
                   ifft3, magnitude_image, reconstruct, stolt_index_table, BAND_EPS)
 from .bpa import bpa  # noqa: F401
 from .plane2d import plane_sum, ifft2_planes, magnitude_planes, reconstruct_planes  # noqa: F401
+from . import nufft  # noqa: F401
