@@ -127,7 +127,7 @@ def _dist():
     return rank, world, local
 
 
-def oracle_sample(sc, s_host, max_pairs=1, planes=None):
+def oracle_sample(sc, s_host, max_pairs=1, planes=None, nufft=False):
     """Time the fp64 oracle (as it stands) on a bounded sample of the workload:
     the first Tx/Rx channel(s) through the whole O1..O7 pipeline (the full-size
     3-D RMA included; O5'-O7' for 2-D planes).  ``sc`` is the 3-D scene.
@@ -137,7 +137,10 @@ def oracle_sample(sc, s_host, max_pairs=1, planes=None):
     geo = oracle.decompose(sc.tx[:1], sc.rx[:max_pairs], sc.scan, sc.npx, sc.npy, sc.x0, sc.y0, sc.dx, sc.dy,
                            sc.z0, sc.k, sc.nx, sc.ny, sc.nz, sc.dz_img, sc.z_ref)
     t0 = time.perf_counter()
-    if planes:
+    if nufft:
+        sc1 = dataclasses.replace(sc, tx=sc.tx[:1], rx=sc.rx[:max_pairs])
+        oracle.nufft.reconstruct_nufft(sub, sc1)
+    elif planes:
         oracle.reconstruct_planes(sub, geo, planes)
     else:
         oracle.reconstruct(sub, geo)
@@ -216,7 +219,8 @@ def run_ours(args):
     sc3 = sc
     if planes:
         sc = dataclasses.replace(sc, nz=len(planes))       # image [F][planes][ny][nx]
-    plan = sar.Plan.from_scene(sc, flags=sar.SAR_PROFILE_STAGES, device=local, z_planes=planes)
+    gflag = sar.SAR_GRID_NUFFT if args.grid == "nufft" else 0
+    plan = sar.Plan.from_scene(sc, flags=sar.SAR_PROFILE_STAGES | gflag, device=local, z_planes=planes)
     out = torch.empty(sc.image_shape, dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream(dev)
 
@@ -267,7 +271,7 @@ def run_ours(args):
         h_in = torch.empty(sc.data_shape, dtype=torch.complex64, pin_memory=True)
         h_in.copy_(data)
         h_out = torch.empty(sc.image_shape, dtype=torch.float32, pin_memory=True)
-        plan2 = sar.Plan.from_scene(sc, device=local, z_planes=planes)
+        plan2 = sar.Plan.from_scene(sc, flags=gflag, device=local, z_planes=planes)
         plan2.reconstruct_host(h_in, h_out, stream)  # warm-up (allocates staging)
         ke = max(1, min(args.steps, args.e2e_steps))
         if world > 1:
@@ -289,7 +293,7 @@ def run_ours(args):
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         s_host = data[:, :1, :1].cpu().numpy()
         sub = dataclasses.replace(sc3, tx=sc3.tx[:1], rx=sc3.rx[:1])
-        dt, n, cores = oracle_sample(sub, s_host, planes=planes)
+        dt, n, cores = oracle_sample(sub, s_host, planes=planes, nufft=bool(gflag))
         what = f"O1..O4 + O5'..O7' on {len(planes)} plane(s)" if planes else \
             f"O1..O7 incl. the {sc.nx}x{sc.ny}x{sc.nz} RMA"
         cpu = {"value": n / dt / 1e9, "unit": UNIT, "cores": cores, "kind": "oracle",
@@ -302,7 +306,8 @@ def run_ours(args):
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "strong" if sharded else "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded scenes, GPU-synthesised Eq. (9) echo)",
-            "config": {"workload": args.config + (f" 2-D planes {planes}" if planes else ""),
+            "config": {"workload": args.config + (f" 2-D planes {planes}" if planes else "") +
+                       (" NUFFT placement" if gflag else ""),
                        "frames": sc.n_frames, "tx": sc.n_tx, "rx": sc.n_rx,
                        "poses": sc.n_pos, "n_k": sc.n_k, "image": [sc.nx, sc.ny, sc.nz],
                        "samples_per_step": samples, "raw_GiB_per_gpu": sc.raw_bytes() / 2**30,
@@ -334,6 +339,8 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="large", choices=["tiny", "small", "freehand", "large", "realtime"])
+    ap.add_argument("--grid", default="raster", choices=["raster", "nufft"],
+                    help="in-plane placement: RASTER lattice (reading R7) or FGG-NUFFT from the true positions (R19)")
     ap.add_argument("--planes", type=str, default=None,
                     help="comma-separated z planes (m): 2-D single-plane images (SAR_IMAGE_2D, Table I '2-D' rows) "
                          "instead of the 3-D volume")

@@ -57,7 +57,13 @@ enum sar_flags {
   SAR_IMAGE_2D = 1u << 3         /* 2-D single-plane images (reading R18, "2-D Proposed" of Table I,
                                     P:394): step 3 becomes the back-propagation of every
                                     filtered column to each plane of sar_image_desc.z_planes summed
-                                    over k (no Stolt), the image is [F][nz planes][ny][nx] */
+                                    over k (no Stolt), the image is [F][nz planes][ny][nx] */,
+  SAR_GRID_NUFFT = 1u << 4       /* NUFFT placement (reading R19; FGG-NUFFT of P:239-242): steps 1-2
+                                    become a type-1 non-uniform transform of the compensated samples
+                                    from their TRUE (x', y') positions (fast Gaussian gridding,
+                                    oversampling 2, half width 6 fine cells) instead of the RASTER
+                                    lattice + FFT.  Needs nx <= 512, npx <= 512; debug stage 1 is
+                                    not available (there is no lattice) */
 };
 
 /* Limits of this build. */
@@ -77,7 +83,8 @@ typedef struct {
   double dx, dy;           /* raster = virtual-lattice pitch (m), lambda/4 in the paper */
   const double *scan_xyz;  /* [F][npy*npx][3] actual radar positions, world frame (m); the z
                               coordinate gives the plane displacement d_z (Eq. (4)); x,y are
-                              not used in RASTER placement (reading R7) */
+                              not used in RASTER placement (reading R7), they are the
+                              non-uniform positions of SAR_GRID_NUFFT (reading R19) */
   const double *z0;        /* [F] reference plane Z_0 per frame (m), or NULL = mean of scan z */
   int32_t n_k;             /* 2 <= n_k <= SAR_MAX_NK frequency samples */
   const double *k;         /* [n_k] wavenumbers 2*pi*f/c (rad/m), uniform (1e-9 rel.), ascending */

@@ -1651,6 +1651,205 @@ __global__ void __launch_bounds__(PB_NT + 32, 2)
   }
 }
 
+// --------------------------------------------------------- NUFFT mode ----
+// SAR_GRID_NUFFT (reading R19, FGG-NUFFT of P:239-242).  K1n: one CTA per
+// (16-wide k chunk, fine row jy of the 2ny x 2nx oversampled grid, frame).
+// For each (pair, pose row) that can reach the fine row (host-built list) the
+// CTA stages the pose row's samples rotated by e^{+j k beta} (Eq. (11)) and
+// weighted by the row's Gaussian y-weight, plus each pose's x-weights; then
+// every thread gathers into the fine-grid cells it owns (deterministic, no
+// atomics).  Finally the fine row is transformed along x (N = 2nx), cropped
+// to |a_s| < nx/2 and deconvolved by 1/Phi_x: Wh[f][jy][a][k].
+// K2n: y-FFT over the 2ny fine rows, crop to |b_s| < ny/2, 1/Phi_y: W0.
+constexpr int K1N_WT = 14;      // taps per axis: 2W + 2 with W = 6
+constexpr int K1N_PCH = 256;    // poses staged at a time
+template <int RX>
+constexpr int k1n_nt() { return sarfft2::nt_fft<RX, KC>() < 256 ? 256 : sarfft2::nt_fft<RX, KC>(); }
+
+template <int RX>
+__global__ void __launch_bounds__(k1n_nt<RX>(), 1) k1n_spread_xfft(const __grid_constant__ SarDeviceView v,
+                                                                   const float2 *__restrict__ s) {
+  constexpr int NT = k1n_nt<RX>();
+  extern __shared__ __align__(16) unsigned char smn[];
+  const int npx = v.npx, nk = v.nk, W = v.nu_w, PH = v.nu_phases;
+  float2 *tile = reinterpret_cast<float2 *>(smn);                    // [RX][16] fine row (accumulator)
+  const int pch = npx < K1N_PCH ? npx : K1N_PCH;
+  float2 *sval = tile + (size_t)RX * KC;                              // [pch][16] staged samples
+  float *wx = reinterpret_cast<float *>(sval + (size_t)pch * KC);     // [pch][WT]
+  int *x0s = reinterpret_cast<int *>(wx + (size_t)pch * K1N_WT);      // [pch]
+  __shared__ float2 twx[RX];
+  const int tid = threadIdx.x;
+  const int kc = blockIdx.x, jyf = blockIdx.y, f = blockIdx.z;
+  const int RY = 2 * v.ny;
+  for (int i = tid; i < RX; i += NT) {
+    float sn, cs;
+    sincospif(-2.0f * (float)i / (float)RX, &sn, &cs);   // twiddles of the fine x-FFT
+    twx[i] = make_float2(cs, sn);
+  }
+  for (int i = tid; i < RX * KC; i += NT) tile[i] = make_float2(0.f, 0.f);
+  const float inv2s2 = 0.5f / v.nu_s2;
+  const int e0 = v.nu_off[f * RY + jyf], e1 = v.nu_off[f * RY + jyf + 1];
+  const int npp = (K1N_PCH + PH - 1) / PH;   // poses per phase and chunk
+  for (int e = e0; e < e1; ++e) {
+    const int code = __ldg(v.nu_cand + e);
+    const int pr = code >> 16, iy = code & 0xffff;
+    const int t = pr / v.nr, r = pr - t * v.nr;
+    const int jx = v.jx[pr];
+    const size_t prow = (size_t)f * v.P + (size_t)iy * npx;
+    const float2 *sg = s + (((size_t)(f * v.nt + t) * v.nr + r) * v.P + (size_t)iy * npx) * nk;
+    const float bp = v.no_comp ? 0.f : v.bpair[f * v.npair + pr];
+    for (int p0 = 0; p0 < npx; p0 += K1N_PCH) {     // pose chunks of the row
+      const int pn = npx - p0 < K1N_PCH ? npx - p0 : K1N_PCH;
+      __syncthreads();   // the previous scatter is done before the stage is rewritten
+      // stage: samples rotated by e^{+j k beta} (Eq. (11)) times the pose's y-weight
+      for (int idx = tid; idx < pn * KC; idx += NT) {
+        const int il = idx / KC, q = idx - il * KC, ix = p0 + il;
+        const float vf = (float)(2 * (iy + v.jy[pr])) + __ldg(v.nu_dv + prow + ix);
+        float d = (float)jyf - vf;
+        d -= (float)RY * rintf(d / (float)RY);               // periodic fine rows (reading R6)
+        const float wy = fabsf(d) <= (float)W ? __expf(-d * d * inv2s2) : 0.f;
+        const int kq = kc * KC + q;
+        float2 val = make_float2(0.f, 0.f);
+        if (kq < nk && wy != 0.f) {
+          val = __ldcs(sg + (size_t)ix * nk + kq);
+          if (!v.no_comp) {
+            float turns = (__ldg(v.apose + prow + ix) + bp) * __ldg(v.kturn + kq);
+            turns -= rintf(turns);
+            float sn, cs;
+            __sincosf(turns * 6.28318530717958647692f, &sn, &cs);
+            val = cmul(val, make_float2(cs, sn));
+          }
+          val.x *= wy;
+          val.y *= wy;
+        }
+        sval[idx] = val;
+        if (q == 0) {
+          const float xf = (float)(2 * (ix + jx)) + __ldg(v.nu_du + prow + ix);
+          const int x0 = (int)floorf(xf) - W;
+          x0s[il] = x0;
+#pragma unroll
+          for (int tt = 0; tt < K1N_WT; ++tt) {
+            const float dx = (float)(x0 + tt) - xf;
+            wx[il * K1N_WT + tt] = fabsf(dx) <= (float)W ? __expf(-dx * dx * inv2s2) : 0.f;
+          }
+        }
+      }
+      __syncthreads();
+      // scatter in phases (ix = ph mod P) whose footprints never overlap
+      // (plan-checked): no atomics, a fixed summation order
+      for (int ph = 0; ph < PH; ++ph) {
+        const int first = (ph - p0 % PH + PH) % PH;   // first chunk-local pose of the phase
+        for (int idx = tid; idx < npp * KC; idx += NT) {
+          const int il = first + PH * (idx / KC), q = idx & (KC - 1);
+          if (il >= pn) continue;
+          const float2 val = sval[il * KC + q];
+          if (val.x == 0.f && val.y == 0.f) continue;
+          int col = x0s[il] % RX;
+          if (col < 0) col += RX;
+#pragma unroll
+          for (int tt = 0; tt < K1N_WT; ++tt) {
+            const float w = wx[il * K1N_WT + tt];
+            float2 *c = tile + (size_t)col * KC + q;
+            c->x = fmaf(w, val.x, c->x);
+            c->y = fmaf(w, val.y, c->y);
+            col = col + 1 == RX ? 0 : col + 1;
+          }
+        }
+        __syncthreads();
+      }
+    }
+  }
+  __syncthreads();
+  // the fine row -> x-FFT (N = RX), crop |a_s| < nx/2, deconvolve
+  const int nx = v.nx;
+  float2 *out = v.wh + ((size_t)(f * RY + jyf) * nx) * (size_t)nk + kc * KC;
+  const int cmax = nk - kc * KC;
+  sarfft2::fft<RX, KC, KC, NT, -1, 0, false>(
+      tile, twx, tid, [&](int c, int n) { return tile[n * KC + c]; }, [] {},
+      [&](int c, int n, float2 x) {
+        const int as = n < RX / 2 ? n : n - RX;
+        if (c < cmax && as >= -nx / 2 && as < nx / 2) {
+          const int a = as < 0 ? as + nx : as;
+          const float d = __ldg(v.nu_decx + a);
+          out[(size_t)a * nk + c] = make_float2(x.x * d, x.y * d);
+        }
+      });
+}
+
+template <int RY>
+__global__ void __launch_bounds__(sarfft2::nt_fft<RY, KC>()) k2n_yfft_crop(const __grid_constant__ SarDeviceView v) {
+  constexpr int NT = sarfft2::nt_fft<RY, KC>();
+  extern __shared__ __align__(16) float2 tly[];   // [RY][16]
+  __shared__ float2 twy[RY];
+  const int tid = threadIdx.x;
+  const int kc = blockIdx.x, a = blockIdx.y, f = blockIdx.z;
+  const int nx = v.nx, nk = v.nk, ny = v.ny;
+  for (int i = tid; i < RY; i += NT) {
+    float sn, cs;
+    sincospif(-2.0f * (float)i / (float)RY, &sn, &cs);
+    twy[i] = make_float2(cs, sn);
+  }
+  const float2 *src = v.wh + ((size_t)f * RY * nx + a) * (size_t)nk + kc * KC;
+  const size_t row = (size_t)nx * nk;
+  const int cmax = nk - kc * KC;
+  for (int i = tid; i < RY * KC; i += NT) {
+    const int n = i / KC, c = i - n * KC;
+    tly[i] = c < cmax ? __ldcs(src + (size_t)n * row + c) : make_float2(0.f, 0.f);
+  }
+  __syncthreads();
+  float2 *dst = v.w0 + ((size_t)f * ny * nx + a) * (size_t)nk + kc * KC;
+  sarfft2::fft<RY, KC, KC, NT, -1, 0, false>(
+      tly, twy, tid, [&](int c, int n) { return tly[n * KC + c]; }, [] {},
+      [&](int c, int n, float2 x) {
+        const int bs = n < RY / 2 ? n : n - RY;
+        if (c < cmax && bs >= -ny / 2 && bs < ny / 2) {
+          const int b = bs < 0 ? bs + ny : bs;
+          const float d = __ldg(v.nu_decy + b);
+          dst[(size_t)b * row + c] = make_float2(x.x * d, x.y * d);
+        }
+      });
+}
+
+cudaError_t launch_nufft(const SarDeviceView &v, const float2 *data, cudaStream_t s) {
+  const int nchunk = (v.nk + KC - 1) / KC;
+  {
+    const size_t stage = (size_t)(v.npx < K1N_PCH ? v.npx : K1N_PCH) *
+                         (KC * sizeof(float2) + K1N_WT * sizeof(float) + sizeof(int));
+    const size_t tile = (size_t)2 * v.nx * KC * sizeof(float2);
+    const size_t smem = stage + tile;
+    dim3 grid(nchunk, 2 * v.ny, v.F);
+    switch (2 * v.nx) {
+#define X(N)                                                                                        \
+  case N: {                                                                                         \
+    cudaError_t e = cudaFuncSetAttribute(k1n_spread_xfft<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+    if (e != cudaSuccess) return e;                                                                 \
+    k1n_spread_xfft<N><<<grid, k1n_nt<N>(), smem, s>>>(v, data);                                     \
+    e = cudaGetLastError();                                                                         \
+    if (e != cudaSuccess) return e;                                                                 \
+    break;                                                                                          \
+  }
+      X(64) X(128) X(256) X(512) X(1024)
+#undef X
+      default:
+        return cudaErrorInvalidValue;
+    }
+  }
+  dim3 grid(nchunk, v.nx, v.F);
+  switch (2 * v.ny) {
+#define X(N)                                                                                         \
+  case N: {                                                                                          \
+    const size_t smem = (size_t)N * KC * sizeof(float2);                                             \
+    cudaError_t e = cudaFuncSetAttribute(k2n_yfft_crop<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+    if (e != cudaSuccess) return e;                                                                  \
+    k2n_yfft_crop<N><<<grid, sarfft2::nt_fft<N, KC>(), smem, s>>>(v);                                \
+    return cudaGetLastError();                                                                       \
+  }
+    X(4) X(8) X(16) X(32) X(64) X(128) X(256) X(512) X(1024)
+#undef X
+  }
+  return cudaErrorInvalidValue;
+}
+
 // ------------------------------------------------------------ dispatch ----
 #define SAR_SIZES(X) X(2) X(4) X(8) X(16) X(32) X(64) X(128) X(256) X(512) X(1024)
 
@@ -1946,6 +2145,23 @@ int sar_launch_pipeline(sar_plan *p, const void *d_data, void *d_image, cudaStre
     if (p->tm_s_ptr != d_data) p->tma_s = sar_encode_input_map(p, d_data);
     if (p->tma_s) tm_s = &p->tm_s;
   }
+  if (v.nufft) {
+    // K1n (spread + fine x-FFT) and K2n (fine y-FFT + crop) replace K1 and K2;
+    // their times are reported in the K1 and K2 slots
+    SAR_CHECK(launch_nufft(v, data, s));
+    if (ev) SAR_CHECK(cudaEventRecord(ev[1], s));
+    if (ev) SAR_CHECK(cudaEventRecord(ev[2], s));
+    if (stop_stage == 2) return SAR_OK;
+    SAR_CHECK(launch_k3(v, stop_stage != 3, s, p->num_sms));
+    if (ev) SAR_CHECK(cudaEventRecord(ev[3], s));
+    if (stop_stage == 3) return SAR_OK;
+    SAR_CHECK(launch_mid<+1>(v.w1, v.tw_y, v.F, v.ny, v.nx, v.nz, s, p->tma_mid1 ? &p->tm_w1_mid : nullptr,
+                             p->num_sms));
+    if (ev) SAR_CHECK(cudaEventRecord(ev[4], s));
+    SAR_CHECK(launch_k4b(v, d_image, complex_out != 0, s, p->tma_rows1 ? &p->tm_w1_rows : nullptr, p->num_sms));
+    if (ev) SAR_CHECK(cudaEventRecord(ev[5], s));
+    return SAR_OK;
+  }
   SAR_CHECK(launch_k1(v, data, stop_stage != 1, s, tm_s, p->tma_ap ? &p->tm_ap : nullptr, p->k1_br, p->k1_regacc,
                       p->num_sms));
   if (ev) SAR_CHECK(cudaEventRecord(ev[1], s));
@@ -2090,7 +2306,7 @@ int sar_setup_passb(sar_plan *p) {
   // opt-in (SAR_FUSE=1): measured slower than the unfused kernels on B200 --
   // the dirty W0/W1 slabs do not survive in L2 between producer and consumer
   // items (DRAM writes 3.3 GB instead of 1.07 GB at Large), see DESIGN.md
-  if (v.F == 0 || v.mode2d || !getenv("SAR_FUSE") || !p->tma_pb || !passb_supported(v)) return SAR_OK;
+  if (v.F == 0 || v.mode2d || v.nufft || !getenv("SAR_FUSE") || !p->tma_pb || !passb_supported(v)) return SAR_OK;
   const int P = v.nx / 2 + 1;
   const int nchunk_k = (v.nk + PB_KC - 1) / PB_KC, nchunk_z = (v.nz + PB_KC - 1) / PB_KC;
   const int GT = v.F * P;

@@ -58,6 +58,7 @@ void free_plan(sar_plan *p) {
   cudaFree(p->d_img);
   cudaFree(p->d_items);
   cudaFree(p->d_cnt);
+  cudaFree(p->d_wh);
   delete p;
 }
 
@@ -99,6 +100,11 @@ namespace {
 struct HostTables {
   std::vector<float> apose, bpair, kturn, pinv, tw;
   std::vector<SarClass> cls;
+  // NUFFT mode
+  std::vector<float> nu_du, nu_dv, nu_decx, nu_decy;
+  std::vector<int> nu_off, nu_cand;
+  float nu_dumax = 0.f;
+  int nu_phases = 1;
   std::vector<double> kx, ky, kz, kd, rref;
   size_t tw_y_off = 0, tw_z_off = 0;
   int roll_x = 0, roll_y = 0;
@@ -128,6 +134,8 @@ int host_decompose(const sar_geom_desc *g, const sar_image_desc *im, uint32_t fl
     return fail(SAR_ERR_INVALID_ARG, "nz must be a power of two in [2, SAR_MAX_FFT]");
   }
   if (g->npx > im->nx || g->npy > im->ny) return fail(SAR_ERR_INVALID_ARG, "raster larger than the FFT grid");
+  if ((flags & SAR_GRID_NUFFT) && (im->nx > 512 || im->ny > 512 || g->npx > 512 || im->nx < 32))
+    return fail(SAR_ERR_UNSUPPORTED, "SAR_GRID_NUFFT needs 32 <= nx <= 512, ny <= 512, npx <= 512");
   if (!(g->dx > 0) || !(g->dy > 0) || (!mode2d && !(im->dz > 0)))
     return fail(SAR_ERR_INVALID_ARG, "pitches must be > 0");
   if ((long long)g->n_frames * g->npx * g->npy > (1LL << 31)) return fail(SAR_ERR_UNSUPPORTED, "too many poses");
@@ -284,6 +292,84 @@ int host_decompose(const sar_geom_desc *g, const sar_image_desc *im, uint32_t fl
       }
   }
 
+  // NUFFT placement tables (reading R19; must match oracle/nufft.py): fine
+  // grid 2N per axis, Gaussian of half width W = 6 fine cells, variance
+  // s2 = W / (2 pi (1 - 1/(2 sigma))), deconvolution 1/Phi(a) with
+  // Phi(a) = sqrt(2 pi s2) exp(-2 pi^2 s2 a^2 / R^2)
+  if (flags & SAR_GRID_NUFFT) {
+    const int W = 6, sig = 2;
+    const double s2 = W / (2.0 * M_PI * (1.0 - 1.0 / (2.0 * sig)));
+    const int Rx = sig * p->nx, Ry = sig * p->ny;
+    T.nu_du.resize((size_t)F * P);
+    T.nu_dv.resize((size_t)F * P);
+    double dmax = 0;
+    for (int f = 0; f < F; ++f)
+      for (int q = 0; q < P; ++q) {
+        const int iy = q / g->npx, ix = q - iy * g->npx;
+        const double *sp = g->scan_xyz + ((size_t)f * P + q) * 3;
+        const double du = sig * ((sp[0] - g->x0) / g->dx - ix), dv = sig * ((sp[1] - g->y0) / g->dy - iy);
+        T.nu_du[(size_t)f * P + q] = (float)du;
+        T.nu_dv[(size_t)f * P + q] = (float)dv;
+        dmax = std::max(dmax, fabs(du));
+      }
+    T.nu_dumax = (float)dmax;
+    // scatter phases: the smallest power of two P such that the footprints
+    // [x - W, x + W + 1] of poses ix and ix + m P (same row, any pair offset)
+    // never share a fine column, circularly mod 2 nx
+    {
+      int Pph = 1;
+      for (;; Pph *= 2) {
+        if (Pph >= g->npx) {
+          Pph = g->npx;
+          break;
+        }
+        bool ok = true;
+        for (int f = 0; f < F && ok; ++f)
+          for (int iy = 0; iy < g->npy && ok; ++iy)
+            for (int q = 0; q < Pph && ok; ++q) {
+              // positions of the phase's poses (pair offsets shift them all equally)
+              std::vector<double> xs;
+              for (int ix = q; ix < g->npx; ix += Pph) xs.push_back(2.0 * ix + T.nu_du[(size_t)f * P + iy * g->npx + ix]);
+              std::sort(xs.begin(), xs.end());
+              for (size_t i = 0; i + 1 < xs.size() && ok; ++i) ok = xs[i + 1] - xs[i] >= 2.0 * W + 2.0;
+              if (ok && xs.size() > 1) ok = xs.front() + Rx - xs.back() >= 2.0 * W + 2.0;
+            }
+        if (ok) break;
+      }
+      T.nu_phases = Pph;
+    }
+    // candidate (pair, pose row) lists per (frame, fine row)
+    std::vector<std::vector<int>> lists((size_t)F * Ry);
+    for (int f = 0; f < F; ++f)
+      for (int pr = 0; pr < p->npair; ++pr)
+        for (int iy = 0; iy < g->npy; ++iy) {
+          double vmin = 1e300, vmax = -1e300;
+          for (int ix = 0; ix < g->npx; ++ix) {
+            const double vv = sig * (double)(iy + p->jy[pr]) + T.nu_dv[(size_t)f * P + iy * g->npx + ix];
+            vmin = std::min(vmin, vv);
+            vmax = std::max(vmax, vv);
+          }
+          for (long long r = (long long)ceil(vmin - W - 1e-6); r <= (long long)floor(vmax + W + 1e-6); ++r) {
+            const int rr = (int)(((r % Ry) + Ry) % Ry);
+            lists[(size_t)f * Ry + rr].push_back((pr << 16) | iy);
+          }
+        }
+    T.nu_off.assign((size_t)F * Ry + 1, 0);
+    for (size_t i = 0; i < lists.size(); ++i) {
+      T.nu_off[i + 1] = T.nu_off[i] + (int)lists[i].size();
+      T.nu_cand.insert(T.nu_cand.end(), lists[i].begin(), lists[i].end());
+    }
+    auto dec = [&](int n, int R, std::vector<float> &o) {
+      o.resize(n);
+      for (int a = 0; a < n; ++a) {
+        const double as = a < n / 2 ? a : a - n;
+        o[a] = (float)(1.0 / (sqrt(2.0 * M_PI * s2) * exp(-2.0 * M_PI * M_PI * s2 * as * as / ((double)R * R))));
+      }
+    };
+    dec(p->nx, Rx, T.nu_decx);
+    dec(p->ny, Ry, T.nu_decy);
+  }
+
   // O7 rolls and axes (reading R8)
   T.roll_x = p->nvx / 2 - p->nx / 2;
   T.roll_y = p->nvy / 2 - p->ny / 2;
@@ -293,7 +379,8 @@ int host_decompose(const sar_geom_desc *g, const sar_image_desc *im, uint32_t fl
   p->axes[3] = g->dx;
   p->axes[4] = g->dy;
   p->axes[5] = mode2d ? (p->nz > 1 ? im->z_planes[1] - im->z_planes[0] : 0.0) : im->dz;
-  p->ws_bytes = ((size_t)F * p->ny * p->nx * ((size_t)nk + p->nz)) * sizeof(float2);
+  p->ws_bytes = ((size_t)F * p->ny * p->nx * ((size_t)nk + p->nz + ((flags & SAR_GRID_NUFFT) ? 2 * (size_t)nk : 0))) *
+                sizeof(float2);
   return SAR_OK;
 }
 
@@ -380,6 +467,12 @@ int sar_plan_create(sar_plan **out, const sar_geom_desc *g, const sar_image_desc
   const size_t o_pi = off; off += al(T.pinv.size() * 4);
   const size_t o_tw = off; off += al(T.tw.size() * 4);
   const size_t o_cl = off; off += al(T.cls.size() * sizeof(SarClass));
+  const size_t o_nu_du = off; off += al(T.nu_du.size() * 4);
+  const size_t o_nu_dv = off; off += al(T.nu_dv.size() * 4);
+  const size_t o_nu_off = off; off += al(T.nu_off.size() * 4);
+  const size_t o_nu_cand = off; off += al(T.nu_cand.size() * 4);
+  const size_t o_nu_dx = off; off += al(T.nu_decx.size() * 4);
+  const size_t o_nu_dy = off; off += al(T.nu_decy.size() * 4);
   ce = cudaMalloc(&p->d_tables, off);
   if (ce != cudaSuccess) {
     cudaGetLastError();
@@ -400,14 +493,21 @@ int sar_plan_create(sar_plan **out, const sar_geom_desc *g, const sar_image_desc
       (ce = up(o_rr, T.rref.data(), T.rref.size() * 8)) != cudaSuccess ||
       (ce = up(o_pi, T.pinv.data(), T.pinv.size() * 4)) != cudaSuccess ||
       (ce = up(o_tw, T.tw.data(), T.tw.size() * 4)) != cudaSuccess ||
-      (ce = up(o_cl, T.cls.data(), T.cls.size() * sizeof(SarClass))) != cudaSuccess) {
+      (ce = up(o_cl, T.cls.data(), T.cls.size() * sizeof(SarClass))) != cudaSuccess ||
+      (ce = up(o_nu_du, T.nu_du.data(), T.nu_du.size() * 4)) != cudaSuccess ||
+      (ce = up(o_nu_dv, T.nu_dv.data(), T.nu_dv.size() * 4)) != cudaSuccess ||
+      (ce = up(o_nu_off, T.nu_off.data(), T.nu_off.size() * 4)) != cudaSuccess ||
+      (ce = up(o_nu_cand, T.nu_cand.data(), T.nu_cand.size() * 4)) != cudaSuccess ||
+      (ce = up(o_nu_dx, T.nu_decx.data(), T.nu_decx.size() * 4)) != cudaSuccess ||
+      (ce = up(o_nu_dy, T.nu_decy.data(), T.nu_decy.size() * 4)) != cudaSuccess) {
     free_plan(p);
     return cuda_fail(ce, "table upload");
   }
   const size_t n0 = (size_t)F * p->ny * p->nx * nk, n1 = (size_t)F * p->ny * p->nx * p->nz;
   if (F > 0) {
     if (cudaMalloc(&p->d_w0, n0 * sizeof(float2)) != cudaSuccess ||
-        cudaMalloc(&p->d_w1, n1 * sizeof(float2)) != cudaSuccess) {
+        cudaMalloc(&p->d_w1, n1 * sizeof(float2)) != cudaSuccess ||
+      ((flags & SAR_GRID_NUFFT) && cudaMalloc(&p->d_wh, 2 * n0 * sizeof(float2)) != cudaSuccess)) {
       cudaGetLastError();
       free_plan(p);
       return fail(SAR_ERR_OOM, "workspace allocation failed");
@@ -430,6 +530,17 @@ int sar_plan_create(sar_plan **out, const sar_geom_desc *g, const sar_image_desc
   v.ky = (const double *)(base + o_ky);
   v.kz = (const double *)(base + o_kz);
   v.rref = (const double *)(base + o_rr);
+  v.nufft = (flags & SAR_GRID_NUFFT) ? 1 : 0;
+  v.nu_w = 6;
+  v.nu_s2 = (float)(6.0 / (2.0 * M_PI * (1.0 - 1.0 / 4.0)));
+  v.nu_dumax = T.nu_dumax;
+  v.nu_phases = T.nu_phases;
+  v.nu_du = (const float *)(base + o_nu_du);
+  v.nu_dv = (const float *)(base + o_nu_dv);
+  v.nu_off = (const int *)(base + o_nu_off);
+  v.nu_cand = (const int *)(base + o_nu_cand);
+  v.nu_decx = (const float *)(base + o_nu_dx);
+  v.nu_decy = (const float *)(base + o_nu_dy);
   v.cls = (const SarClass *)(base + o_cl);
   v.pinv = T.pinv.empty() ? nullptr : (const float2 *)(base + o_pi);
   v.tw_x = (const float2 *)(base + o_tw);
@@ -457,6 +568,7 @@ int sar_plan_create(sar_plan **out, const sar_geom_desc *g, const sar_image_desc
     v.k1_step_ok = (T.dk * ((double)amax + (double)bmax) <= 0.25) ? 1 : 0;
   }
   v.w0 = p->d_w0;
+  v.wh = p->d_wh;
   v.dbg = getenv("SAR_DBG") ? atoi(getenv("SAR_DBG")) : 0;
   v.w1 = p->d_w1;
 
@@ -567,6 +679,7 @@ int sar_plan_profile_read(sar_plan *p, float ms_out[5], int32_t *n_calls) {
 int sar_debug_stage(sar_plan *p, int32_t stage, const void *d_data, void *d_out, sar_stream stream) {
   if (!p) return fail(SAR_ERR_INVALID_ARG, "plan is NULL");
   if (stage < 1 || stage > 4) return fail(SAR_ERR_INVALID_ARG, "stage must be 1..4");
+  if (stage == 1 && (p->flags & SAR_GRID_NUFFT)) return fail(SAR_ERR_INVALID_ARG, "no planar lattice in NUFFT mode");
   if (p->F == 0) return SAR_OK;
   if (!d_data || !d_out) return fail(SAR_ERR_INVALID_ARG, "NULL pointer");
   DeviceGuard g(p->device);

@@ -30,6 +30,15 @@ struct SarDeviceView {
   int mode2d;           // SAR_IMAGE_2D: kz[] holds z_s - z_ref per plane (reading R18)
   int no_comp;
   int jx[SAR_MAX_PAIRS], jy[SAR_MAX_PAIRS];  // virtual-node offsets, pair = t*nr + r
+  // SAR_GRID_NUFFT (reading R19): fine grid 2 nx x 2 ny, Gaussian half width
+  // nu_w fine cells, variance nu_s2; per pose the fine-cell offset of the true
+  // position from its raster node (du = 2((x-x0)/dx - ix), dv likewise)
+  int nufft, nu_w, nu_phases;  // nu_phases: poses ix = q (mod P) of a row never overlap
+  float nu_s2, nu_dumax;
+  const float *nu_du, *nu_dv;      // [F*P]
+  const int *nu_off, *nu_cand;     // CSR per (frame, fine row): (pair << 16 | pose row)
+  const float *nu_decx, *nu_decy;  // [nx], [ny] 1/Phi deconvolution factors
+  float2 *wh;                      // [F][2 ny][nx][nk] x-transformed fine rows
   const float *apose;   // [F][P]      -2 d_z (m), fp32
   const float *bpair;   // [F][npair]  (d_x^2+d_y^2)/(4 R_ref) (m), fp32
   const float *kturn;   // [nk]        k_i / (2 pi) (turns per metre), fp32
@@ -88,6 +97,9 @@ struct sar_plan {
   int4 *d_items = nullptr;
   int n_items = 0;
   int *d_cnt = nullptr;
+  // NUFFT mode tables and the half-transformed fine grid
+  void *d_nu = nullptr;
+  float2 *d_wh = nullptr;
 };
 
 // kernels.cu

@@ -330,3 +330,34 @@ def test_plane2d_many_planes_and_complex():
         got = plan.reconstruct(d).cpu().numpy()
     e2, _ = errs(got, want)
     assert e2 <= E2_BAR
+
+
+# ---- NUFFT placement (SAR_GRID_NUFFT, reading R19) -------------------------
+@pytest.mark.parametrize("name", ["tiny", "small"])
+def test_nufft_parity(name):
+    from oracle import nufft
+    sc = scenes.make_scene(name)
+    d, s = _data(sc)
+    S, geo = nufft.spectrum_nufft(s, sc)
+    want, _ = nufft.reconstruct_nufft(s, sc)
+    with sar.Plan.from_scene(sc, flags=sar.SAR_GRID_NUFFT) as plan:
+        g2 = plan.debug_stage(2, d).cpu().numpy()
+        got = plan.reconstruct(d)
+        torch.cuda.synchronize()
+        got = got.cpu().numpy()
+        with pytest.raises(sar.SarError):
+            plan.debug_stage(1, d)
+    e2s, _ = errs(g2, S)
+    assert e2s <= STAGE_BAR, e2s
+    e2, einf = errs(got, want)
+    assert e2 <= E2_BAR and einf <= EINF_BAR, (name, e2, einf)
+
+
+def test_nufft_equals_raster_without_inplane_jitter():
+    sc = scenes.with_geometry(scenes.make_scene("small"), jitter_xy=0.0)
+    d = torch.from_numpy(scenes.synthesize_cpu(sc)).cuda()
+    with sar.Plan.from_scene(sc) as p0, sar.Plan.from_scene(sc, flags=sar.SAR_GRID_NUFFT) as p1:
+        a = p0.reconstruct(d).cpu().numpy()
+        b = p1.reconstruct(d).cpu().numpy()
+    e2, _ = errs(b, a.astype(np.float64))
+    assert e2 <= 2e-5
