@@ -103,8 +103,9 @@ struct HostTables {
   // NUFFT mode
   std::vector<float> nu_du, nu_dv, nu_decx, nu_decy;
   std::vector<int> nu_off, nu_cand;
+  std::vector<short> nu_perm;
+  int nu_br = 8;
   float nu_dumax = 0.f;
-  int nu_phases = 1;
   std::vector<double> kx, ky, kz, kd, rref;
   size_t tw_y_off = 0, tw_z_off = 0;
   int roll_x = 0, roll_y = 0;
@@ -313,33 +314,12 @@ int host_decompose(const sar_geom_desc *g, const sar_image_desc *im, uint32_t fl
         dmax = std::max(dmax, fabs(du));
       }
     T.nu_dumax = (float)dmax;
-    // scatter phases: the smallest power of two P such that the footprints
-    // [x - W, x + W + 1] of poses ix and ix + m P (same row, any pair offset)
-    // never share a fine column, circularly mod 2 nx
-    {
-      int Pph = 1;
-      for (;; Pph *= 2) {
-        if (Pph >= g->npx) {
-          Pph = g->npx;
-          break;
-        }
-        bool ok = true;
-        for (int f = 0; f < F && ok; ++f)
-          for (int iy = 0; iy < g->npy && ok; ++iy)
-            for (int q = 0; q < Pph && ok; ++q) {
-              // positions of the phase's poses (pair offsets shift them all equally)
-              std::vector<double> xs;
-              for (int ix = q; ix < g->npx; ix += Pph) xs.push_back(2.0 * ix + T.nu_du[(size_t)f * P + iy * g->npx + ix]);
-              std::sort(xs.begin(), xs.end());
-              for (size_t i = 0; i + 1 < xs.size() && ok; ++i) ok = xs[i + 1] - xs[i] >= 2.0 * W + 2.0;
-              if (ok && xs.size() > 1) ok = xs.front() + Rx - xs.back() >= 2.0 * W + 2.0;
-            }
-        if (ok) break;
-      }
-      T.nu_phases = Pph;
-    }
-    // candidate (pair, pose row) lists per (frame, fine row)
-    std::vector<std::vector<int>> lists((size_t)F * Ry);
+
+    // bands of BR fine rows; candidate (pair, pose row) lists per (frame, band)
+    const int BR = Rx >= 1024 ? 4 : 8;
+    T.nu_br = BR;
+    const int NB = (Ry + BR - 1) / BR;
+    std::vector<std::vector<int>> lists((size_t)F * NB);
     for (int f = 0; f < F; ++f)
       for (int pr = 0; pr < p->npair; ++pr)
         for (int iy = 0; iy < g->npy; ++iy) {
@@ -349,16 +329,31 @@ int host_decompose(const sar_geom_desc *g, const sar_image_desc *im, uint32_t fl
             vmin = std::min(vmin, vv);
             vmax = std::max(vmax, vv);
           }
+          std::vector<char> hit(NB, 0);
           for (long long r = (long long)ceil(vmin - W - 1e-6); r <= (long long)floor(vmax + W + 1e-6); ++r) {
             const int rr = (int)(((r % Ry) + Ry) % Ry);
-            lists[(size_t)f * Ry + rr].push_back((pr << 16) | iy);
+            hit[rr / BR] = 1;
           }
+          for (int bnd = 0; bnd < NB; ++bnd)
+            if (hit[bnd]) lists[(size_t)f * NB + bnd].push_back((pr << 16) | iy);
         }
-    T.nu_off.assign((size_t)F * Ry + 1, 0);
+    T.nu_off.assign((size_t)F * NB + 1, 0);
     for (size_t i = 0; i < lists.size(); ++i) {
       T.nu_off[i + 1] = T.nu_off[i] + (int)lists[i].size();
       T.nu_cand.insert(T.nu_cand.end(), lists[i].begin(), lists[i].end());
     }
+    // poses of each row sorted by fine x position (the gather sweeps them)
+    T.nu_perm.resize((size_t)F * P);
+    for (int f = 0; f < F; ++f)
+      for (int iy = 0; iy < g->npy; ++iy) {
+        std::vector<int> idx(g->npx);
+        for (int ix = 0; ix < g->npx; ++ix) idx[ix] = ix;
+        const float *du = T.nu_du.data() + (size_t)f * P + (size_t)iy * g->npx;
+        std::stable_sort(idx.begin(), idx.end(), [&](int a, int b) {
+          return floorf((float)(2 * a) + du[a]) < floorf((float)(2 * b) + du[b]);
+        });
+        for (int ix = 0; ix < g->npx; ++ix) T.nu_perm[(size_t)f * P + (size_t)iy * g->npx + ix] = (short)idx[ix];
+      }
     auto dec = [&](int n, int R, std::vector<float> &o) {
       o.resize(n);
       for (int a = 0; a < n; ++a) {
@@ -473,6 +468,7 @@ int sar_plan_create(sar_plan **out, const sar_geom_desc *g, const sar_image_desc
   const size_t o_nu_cand = off; off += al(T.nu_cand.size() * 4);
   const size_t o_nu_dx = off; off += al(T.nu_decx.size() * 4);
   const size_t o_nu_dy = off; off += al(T.nu_decy.size() * 4);
+  const size_t o_nu_pm = off; off += al(T.nu_perm.size() * 2);
   ce = cudaMalloc(&p->d_tables, off);
   if (ce != cudaSuccess) {
     cudaGetLastError();
@@ -499,7 +495,8 @@ int sar_plan_create(sar_plan **out, const sar_geom_desc *g, const sar_image_desc
       (ce = up(o_nu_off, T.nu_off.data(), T.nu_off.size() * 4)) != cudaSuccess ||
       (ce = up(o_nu_cand, T.nu_cand.data(), T.nu_cand.size() * 4)) != cudaSuccess ||
       (ce = up(o_nu_dx, T.nu_decx.data(), T.nu_decx.size() * 4)) != cudaSuccess ||
-      (ce = up(o_nu_dy, T.nu_decy.data(), T.nu_decy.size() * 4)) != cudaSuccess) {
+      (ce = up(o_nu_dy, T.nu_decy.data(), T.nu_decy.size() * 4)) != cudaSuccess ||
+      (ce = up(o_nu_pm, T.nu_perm.data(), T.nu_perm.size() * 2)) != cudaSuccess) {
     free_plan(p);
     return cuda_fail(ce, "table upload");
   }
@@ -534,13 +531,14 @@ int sar_plan_create(sar_plan **out, const sar_geom_desc *g, const sar_image_desc
   v.nu_w = 6;
   v.nu_s2 = (float)(6.0 / (2.0 * M_PI * (1.0 - 1.0 / 4.0)));
   v.nu_dumax = T.nu_dumax;
-  v.nu_phases = T.nu_phases;
+  v.nu_br = T.nu_br;
   v.nu_du = (const float *)(base + o_nu_du);
   v.nu_dv = (const float *)(base + o_nu_dv);
   v.nu_off = (const int *)(base + o_nu_off);
   v.nu_cand = (const int *)(base + o_nu_cand);
   v.nu_decx = (const float *)(base + o_nu_dx);
   v.nu_decy = (const float *)(base + o_nu_dy);
+  v.nu_perm = (const short *)(base + o_nu_pm);
   v.cls = (const SarClass *)(base + o_cl);
   v.pinv = T.pinv.empty() ? nullptr : (const float2 *)(base + o_pi);
   v.tw_x = (const float2 *)(base + o_tw);

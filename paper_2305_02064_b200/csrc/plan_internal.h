@@ -33,10 +33,12 @@ struct SarDeviceView {
   // SAR_GRID_NUFFT (reading R19): fine grid 2 nx x 2 ny, Gaussian half width
   // nu_w fine cells, variance nu_s2; per pose the fine-cell offset of the true
   // position from its raster node (du = 2((x-x0)/dx - ix), dv likewise)
-  int nufft, nu_w, nu_phases;  // nu_phases: poses ix = q (mod P) of a row never overlap
+  int nufft, nu_w;
   float nu_s2, nu_dumax;
   const float *nu_du, *nu_dv;      // [F*P]
-  const int *nu_off, *nu_cand;     // CSR per (frame, fine row): (pair << 16 | pose row)
+  const int *nu_off, *nu_cand;     // CSR per (frame, band of fine rows): (pair << 16 | pose row)
+  const short *nu_perm;            // [F][npy][npx] poses of a row sorted by fine x position
+  int nu_br;                       // fine rows per band
   const float *nu_decx, *nu_decy;  // [nx], [ny] 1/Phi deconvolution factors
   float2 *wh;                      // [F][2 ny][nx][nk] x-transformed fine rows
   const float *apose;   // [F][P]      -2 d_z (m), fp32
