@@ -50,7 +50,7 @@ def slot(name):
     if "k4_" in name:
         return 4
     if "k_fft_mid" in name:
-        return 1 if "-1" in name.split(">")[0] else 3
+        return 1 if ("(int)-1" in name or ", -1>" in name) else 3
     return None
 for d in out:
     sl = slot(d["Kernel Name"])
