@@ -110,7 +110,8 @@ def test_node_offsets_match_oracle():
             assert plan.axes() == tuple(geo.axes)
 
 
-@pytest.mark.parametrize("name,n_sample", [("tiny", None), ("small", None), ("large", 8192)])
+@pytest.mark.parametrize("name,n_sample", [("tiny", None), ("small", None), ("freehand", 8192),
+                                           ("realtime", 8192), ("large", 8192)])
 def test_stolt_index_bit_exact(name, n_sample):
     """Device Stolt decisions (the code K3 runs) == oracle table, bit for bit
     in the index, to fp32 rounding in the weight.  Large: a random sample of
@@ -183,6 +184,21 @@ def test_no_compensation_parity_and_contrast():
     a, _, _, _ = _check_e2e(sc, flags=sar.SAR_NO_COMPENSATION)
     b, _, _, _ = _check_e2e(sc)
     assert np.linalg.norm(a - b) / np.linalg.norm(b) > 0.05
+
+
+@pytest.mark.parametrize("name", ["tiny", "freehand", "large", "realtime"])
+def test_compensation_changes_every_config(name):
+    """on every config the NO_COMPENSATION image (the paper's
+    plain-RMA failure baseline) differs from the compensated one,
+    i.e. beta is really applied (GPU vs GPU; parity of both modes is pinned
+    against the oracle elsewhere)."""
+    sc = scenes.make_scene(name)
+    d, _ = _data(sc, gpu_gen=name in ("freehand", "large", "realtime"))
+    with sar.Plan.from_scene(sc) as p0, sar.Plan.from_scene(sc, flags=sar.SAR_NO_COMPENSATION) as p1:
+        a = p0.reconstruct(d)
+        b = p1.reconstruct(d)
+        rel = float(torch.linalg.vector_norm(a - b) / torch.linalg.vector_norm(a))
+    assert rel > 0.05, rel
 
 
 def test_pulse_spectrum_parity():
