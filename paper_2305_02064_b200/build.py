@@ -18,8 +18,8 @@ BUILD = os.path.join(HERE, "_build")
 LIB = os.path.join(HERE, "libsar_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-SOURCES = ["plan.cpp", "kernels.cu"]
-HEADERS = [os.path.join(CSRC, h) for h in ("plan_internal.h", "fft_tile.cuh", "fft_reg.cuh", "tma.cuh")] + \
+SOURCES = ["plan.cpp", "pipeline.cu", "k1.cu", "fft_mid.cu", "k3.cu", "k4.cu", "nufft.cu", "passb.cu"]
+HEADERS = [os.path.join(CSRC, h) for h in ("plan_internal.h", "fft_tile.cuh", "fft_reg.cuh", "tma.cuh", "common.cuh")] + \
     [os.path.join(ROOT, "include", "sar_b200.h")]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-ffp-contract=off,-O2",
          "-Xptxas", "-v", "--expt-relaxed-constexpr", "-I", os.path.join(ROOT, "include")]
@@ -32,24 +32,30 @@ def _newer(target, deps):
     return any(os.path.getmtime(d) > t for d in deps)
 
 
+def _compile(src, force, verbose):
+    s = os.path.join(CSRC, src)
+    o = os.path.join(BUILD, src + ".o")
+    if force or _newer(o, [s] + HEADERS):
+        if src.endswith(".cpp"):
+            cmd = [NVCC, *FLAGS, "-x", "c++", "-c", s, "-o", o]
+        else:
+            cmd = [NVCC, *ARCH, *FLAGS, "-x", "cu", "-c", s, "-o", o]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if verbose or r.returncode:
+            sys.stderr.write(r.stdout + r.stderr)
+        if r.returncode:
+            raise RuntimeError(f"nvcc failed on {src}")
+        with open(o + ".ptxas.txt", "w") as fh:
+            fh.write(r.stderr)
+    return o
+
+
 def build(verbose: bool = False, force: bool = False) -> str:
+    """Compile every translation unit (in parallel) and link the library."""
+    from concurrent.futures import ThreadPoolExecutor
     os.makedirs(BUILD, exist_ok=True)
-    objs = []
-    for src in SOURCES:
-        s = os.path.join(CSRC, src)
-        o = os.path.join(BUILD, src + ".o")
-        objs.append(o)
-        if force or _newer(o, [s] + HEADERS):
-            cmd = [NVCC, *ARCH, *FLAGS, "-x", "cu" if src.endswith(".cu") else "c++", "-c", s, "-o", o]
-            if src.endswith(".cpp"):
-                cmd = [NVCC, *FLAGS, "-x", "c++", "-c", s, "-o", o]
-            r = subprocess.run(cmd, capture_output=True, text=True)
-            if verbose or r.returncode:
-                sys.stderr.write(r.stdout + r.stderr)
-            if r.returncode:
-                raise RuntimeError(f"nvcc failed on {src}")
-            with open(o + ".ptxas.txt", "w") as fh:
-                fh.write(r.stderr)
+    with ThreadPoolExecutor(max_workers=min(len(SOURCES), os.cpu_count() or 1)) as ex:
+        objs = list(ex.map(lambda src: _compile(src, force, verbose), SOURCES))
     if force or _newer(LIB, objs):
         cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lcudart_static", "-lrt", "-ldl", "-lpthread"]
         r = subprocess.run(cmd, capture_output=True, text=True)

@@ -1,0 +1,264 @@
+// fft_mid.cu -- K2 / K4a: FFT along the middle (y) axis, forward on W0 and
+// inverse on W1 (FT_2D / IFT_3D of Eq. (14)).
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdlib.h>
+
+#include <string>
+#include <type_traits>
+#include <vector>
+
+#include "common.cuh"
+
+namespace sark {
+namespace {
+
+// ------------------------------------------------------------ K2 / K4a ----
+// FFT along the middle (y) axis of a [F][N][nx][inner] complex volume for one
+// (chunk of 16 along `inner`, column a, frame f).
+template <int N, int DIR>
+__global__ void __launch_bounds__(nt_for(N), minb_for(N))
+    k_fft_mid(float2 *__restrict__ data, const float2 *__restrict__ tw, int nx, int inner) {
+  constexpr int NT = nt_for(N);
+  constexpr int ITEMS = N * KC;
+  constexpr int E = (ITEMS + NT - 1) / NT;
+  extern __shared__ float2 tile[];  // [N][16]
+  const int tid = threadIdx.x;
+  const int cbase = blockIdx.x * KC;
+  const int a = blockIdx.y;
+  const int f = blockIdx.z;
+  float2 *base = data + ((size_t)f * N * nx + a) * (size_t)inner;
+  const size_t row = (size_t)nx * inner;
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int item = tid + e * NT;
+    if (ITEMS % NT != 0 && item >= ITEMS) continue;
+    const int cc = item & (KC - 1), b = item >> 4;
+    const int c = cbase + cc;
+    tile[item] = c < inner ? base[b * row + c] : make_float2(0.f, 0.f);
+  }
+  __syncthreads();
+  sarfft::tile_fft<N, KC, KC, NT, DIR>(tile, tw, tid);
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int item = tid + e * NT;
+    if (ITEMS % NT != 0 && item >= ITEMS) continue;
+    const int cc = item & (KC - 1), b = item >> 4;
+    const int c = cbase + cc;
+    if (c < inner) base[b * row + c] = tile[item];
+  }
+}
+
+// Persistent, TMA-pipelined variant of k_fft_mid (used when `inner` is even,
+// i.e. the rows are 16-byte aligned).  One CTA per SM loops over work items
+// (chunk, column a, frame); the [N][16] tile of item i+1 is in flight
+// (cp.async.bulk.tensor, mbarrier completion) while item i is transformed,
+// and finished tiles go back with TMA stores, so the SM's load queue never
+// drains between tiles.  Box = {16 inner elements, 1 column, <=256 rows}.
+template <int N, int DIR>
+__global__ void __launch_bounds__(ntp_for(N), ctas_for(N))
+    k_fft_mid_tma(const __grid_constant__ CUtensorMap tm, const float2 *__restrict__ twg, int nx, int nchunk,
+                  int nitems) {
+  constexpr int NT = ntp_for(N);
+  constexpr int ROWS = N < 256 ? N : 256;
+  constexpr int NBOX = N / ROWS;
+  constexpr uint32_t TILE_BYTES = N * KC * sizeof(float2);
+  extern __shared__ __align__(128) float2 smt[];  // [2][N][16]
+  __shared__ __align__(8) uint64_t full[2];
+  __shared__ float2 tw[N];
+  const int tid = threadIdx.x;
+  for (int i = tid; i < N; i += NT) tw[i] = twg[i];
+  if (tid == 0) {
+    sartma::mbar_init(&full[0], 1);
+    sartma::mbar_init(&full[1], 1);
+    sartma::fence_barrier_init();
+  }
+  __syncthreads();
+  auto issue = [&](int item, int st) {
+    const int chunk = item % nchunk, rest = item / nchunk;
+    const int a = rest % nx, f = rest / nx;
+    sartma::mbar_arrive_expect_tx(&full[st], TILE_BYTES);
+#pragma unroll
+    for (int bx = 0; bx < NBOX; ++bx)
+      sartma::tma_load_3d(smt + (size_t)st * N * KC + bx * ROWS * KC, &tm, chunk * KC, a, f * N + bx * ROWS,
+                          &full[st]);
+  };
+  int item = blockIdx.x;
+  if (tid == 0 && item < nitems) issue(item, 0);
+  for (int it = 0; item < nitems; ++it, item += gridDim.x) {
+    const int st = it & 1;
+    const int next = item + gridDim.x;
+    if (tid == 0 && next < nitems) {
+      sartma::bulk_wait_read0();  // the store of stage st^1 has left shared memory
+      issue(next, st ^ 1);
+    }
+    sartma::mbar_wait(&full[st], (it >> 1) & 1);
+    float2 *tile = smt + (size_t)st * N * KC;
+    sarfft::tile_fft<N, KC, KC, NT, DIR>(tile, tw, tid);
+    sartma::fence_proxy_async();
+    __syncthreads();
+    if (tid == 0) {
+      const int chunk = item % nchunk, rest = item / nchunk;
+      const int a = rest % nx, f = rest / nx;
+#pragma unroll
+      for (int bx = 0; bx < NBOX; ++bx)
+        sartma::tma_store_3d(&tm, chunk * KC, a, f * N + bx * ROWS, tile + bx * ROWS * KC);
+      sartma::bulk_commit();
+    }
+  }
+  if (tid == 0) sartma::bulk_wait0();
+}
+
+// Warp-specialised persistent mid-axis FFT (K2 / K4a, ny <= 512, `inner`
+// even).  A producer warp streams [N][16] tiles (3-D TMA boxes {16 inner, 1
+// column, <=256 rows}) into an S-stage mbarrier ring; NTC consumer threads run
+// the two-pass register FFT (fft_reg.cuh), hand the stage back right after
+// the pass-1 loads, and store the transformed rows straight to global memory
+// (each warp store = two full 128-byte lines).
+template <int N>
+constexpr int mid2_stages() { return N >= 256 ? 2 : 4; }
+template <int N>
+constexpr size_t mid2_smem() {
+  return ((size_t)mid2_stages<N>() * N * KC + (size_t)N * KC + N) * sizeof(float2);
+}
+template <int N>
+constexpr int mid2_ctas() {
+  return (int)((200 * 1024) / mid2_smem<N>()) < 1 ? 1 : (int)((200 * 1024) / mid2_smem<N>());
+}
+
+template <int N, int DIR>
+__global__ void __launch_bounds__(sarfft2::nt_fft<N, KC>() + 32)
+    k_fft_mid2(const __grid_constant__ CUtensorMap tm, float2 *__restrict__ data, const float2 *__restrict__ twg,
+               int nx, int inner, int nchunk, int nitems) {
+  constexpr int NTC = sarfft2::nt_fft<N, KC>();
+  constexpr int S = mid2_stages<N>();
+  constexpr int ROWS = N < 256 ? N : 256;
+  constexpr int NBOX = N / ROWS;
+  constexpr uint32_t TILE_BYTES = N * KC * sizeof(float2);
+  extern __shared__ __align__(128) float2 smm[];
+  float2 *ring = smm;                         // [S][N][16]
+  float2 *work = smm + (size_t)S * N * KC;    // [N][16]
+  float2 *tw = work + (size_t)N * KC;         // [N]
+  __shared__ __align__(8) uint64_t full[S], empty[S];
+  const int tid = threadIdx.x;
+  for (int i = tid; i < N; i += NTC + 32) tw[i] = twg[i];
+  if (tid == 0) {
+    for (int i = 0; i < S; ++i) {
+      sartma::mbar_init(&full[i], 1);
+      sartma::mbar_init(&empty[i], 1);
+    }
+    sartma::fence_barrier_init();
+  }
+  __syncthreads();
+  if (tid >= NTC) {
+    if (tid == NTC) {
+      unsigned n = 0;
+      for (int item = blockIdx.x; item < nitems; item += gridDim.x, ++n) {
+        const int st = n % S;
+        if (n >= S) sartma::mbar_wait(&empty[st], ((n / S) - 1) & 1);
+        const int chunk = item % nchunk, rest = item / nchunk;
+        const int a = rest % nx, f = rest / nx;
+        sartma::mbar_arrive_expect_tx(&full[st], TILE_BYTES);
+#pragma unroll
+        for (int bx = 0; bx < NBOX; ++bx)
+          sartma::tma_load_3d(ring + (size_t)st * N * KC + bx * ROWS * KC, &tm, chunk * KC, a, f * N + bx * ROWS,
+                              &full[st]);
+      }
+    }
+    return;
+  }
+  const size_t row = (size_t)nx * inner;
+  unsigned n = 0;
+  for (int item = blockIdx.x; item < nitems; item += gridDim.x, ++n) {
+    const int st = n % S;
+    sartma::mbar_wait(&full[st], (n / S) & 1);
+    const int chunk = item % nchunk, rest = item / nchunk;
+    const int a = rest % nx, f = rest / nx;
+    const float2 *stage = ring + (size_t)st * N * KC;
+    float2 *base = data + ((size_t)f * N * nx + a) * (size_t)inner + chunk * KC;
+    const int cmax = inner - chunk * KC;
+    sarfft2::fft<N, KC, KC, NTC, DIR, 1, false>(
+        work, tw, tid, [&](int c, int m) { return stage[m * KC + c]; },
+        [&] {
+          if (tid == 0) sartma::mbar_arrive(&empty[st]);
+        },
+        [&](int c, int m, float2 v) {
+          if (c < cmax) __stcs(base + (size_t)m * row + c, v);
+        });
+  }
+}
+
+
+}  // namespace
+
+template <int DIR>
+cudaError_t launch_mid(float2 *data, const float2 *tw, int F, int ny, int nx, int inner, cudaStream_t s,
+                       const CUtensorMap *tm, int num_sms) {
+  if (tm && ny <= 512 && !getenv("SAR_MID_OLD")) {
+    const int nchunk = (inner + KC - 1) / KC;
+    const int nitems = nchunk * nx * F;
+    switch (ny) {
+#define X(N)                                                                                       \
+  case N: {                                                                                        \
+    auto kern = k_fft_mid2<N, DIR>;                                                                \
+    constexpr size_t smem = mid2_smem<N>();                                                        \
+    if (smem > 40 * 1024) {                                                                        \
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+      if (e != cudaSuccess) return e;                                                              \
+    }                                                                                              \
+    const int maxg = num_sms * mid2_ctas<N>();                                                     \
+    kern<<<nitems < maxg ? nitems : maxg, sarfft2::nt_fft<N, KC>() + 32, smem, s>>>(*tm, data, tw, nx, inner, \
+                                                                                  nchunk, nitems); \
+    return cudaGetLastError();                                                                     \
+  }
+      X(2) X(4) X(8) X(16) X(32) X(64) X(128) X(256) X(512)
+#undef X
+    }
+    return cudaErrorInvalidValue;
+  }
+  if (tm && ny <= 512) {
+    const int nchunk = (inner + KC - 1) / KC;
+    const int nitems = nchunk * nx * F;
+    const size_t smem = 2 * (size_t)ny * KC * sizeof(float2);
+    switch (ny) {
+#define X(N)                                                                                       \
+  case N: {                                                                                        \
+    auto kern = k_fft_mid_tma<N, DIR>;                                                             \
+    if (smem > 40 * 1024) {                                                                        \
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+      if (e != cudaSuccess) return e;                                                              \
+    }                                                                                              \
+    const int maxg = num_sms * ctas_for(N);                                                        \
+    kern<<<nitems < maxg ? nitems : maxg, ntp_for(N), smem, s>>>(*tm, tw, nx, nchunk, nitems);     \
+    return cudaGetLastError();                                                                     \
+  }
+      SAR_SIZES(X)
+#undef X
+    }
+    return cudaErrorInvalidValue;
+  }
+  dim3 grid((inner + KC - 1) / KC, nx, F);
+  const size_t smem = (size_t)ny * KC * sizeof(float2);
+  switch (ny) {
+#define X(N)                                                                                       \
+  case N: {                                                                                        \
+    auto kern = k_fft_mid<N, DIR>;                                                                 \
+    if (smem > 40 * 1024) {                                                                        \
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+      if (e != cudaSuccess) return e;                                                              \
+    }                                                                                              \
+    kern<<<grid, nt_for(N), smem, s>>>(data, tw, nx, inner);                                       \
+    return cudaGetLastError();                                                                     \
+  }
+    SAR_SIZES(X)
+#undef X
+  }
+  return cudaErrorInvalidValue;
+}
+
+
+template cudaError_t launch_mid<-1>(float2 *, const float2 *, int, int, int, int, cudaStream_t, const CUtensorMap *, int);
+template cudaError_t launch_mid<+1>(float2 *, const float2 *, int, int, int, int, cudaStream_t, const CUtensorMap *, int);
+
+}  // namespace sark

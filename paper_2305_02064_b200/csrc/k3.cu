@@ -1,0 +1,508 @@
+// k3.cu -- K3: RMA filter + Stolt resampling + inverse z-FFT (Eqs. (13)-(14),
+// P:204-226; readings R2-R5, R9), W0 -> W1; the 2-D plane sum (reading R18);
+// the device Stolt index table for the bit-exact tests.
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdlib.h>
+
+#include <string>
+#include <type_traits>
+#include <vector>
+
+#include "common.cuh"
+
+namespace sark {
+namespace {
+
+// K3, one small CTA per CL mirror classes (CL = 1 at n_z = 512: the <= 4
+// columns (+-a, +-b) that share k_r^2).  128 threads and ~40 KB of shared
+// memory, so ~5 CTAs are resident per SM and the hardware overlaps their
+// load / fp64 / FFT phases.  Steps: (1) stream the member columns in (n_k
+// contiguous samples each); (2) filter H = k_z e^{+j k_z R_ref}/P on the
+// source grid, once per class (readings R2-R4); (3) Stolt pull with the
+// filter folded into the two complex interpolation weights, decisions bit-exact
+// (R5, R9), once per (class, j), applied to every member; (4) inverse z-FFT
+// (two-pass register FFT, the Stolt tile doubles as its work tile) whose
+// pass 2 stores each column contiguously [col][z].
+constexpr int K3C_NT = 128;
+template <int NZ>
+constexpr int k3c_r1() { return NZ == 512 ? 16 : sarfft2::Split<NZ>::R1; }
+template <int NZ>
+constexpr int k3c_cl() {
+  constexpr int cc = K3C_NT / (NZ / k3c_r1<NZ>());
+  return cc / 4 > 8 ? 8 : (cc / 4 < 1 ? 1 : cc / 4);
+}
+template <int NZ>
+size_t k3c_smem(int nk) {
+  constexpr int CL = k3c_cl<NZ>();
+  return ((size_t)4 * CL * nk + (size_t)NZ * (4 * CL + 1)) * sizeof(float2);
+}
+
+template <int NZ, bool DO_IFFT>
+__global__ void __launch_bounds__(K3C_NT, 4) k3_class(const SarDeviceView v) {
+  constexpr int CL = k3c_cl<NZ>();
+  constexpr int CC = 4 * CL;   // slot 4*cl + m = member m of class cl
+  constexpr int LD = CC + 1;
+  extern __shared__ __align__(16) float2 sm3[];
+  __shared__ double kr2s[CL];
+  __shared__ int jlos[CL], jhis[CL], colof[CC];
+  const int nk = v.nk;
+  float2 *fin = sm3;                                 // [CC][nk]  source spectrum
+  float2 *fout = fin + (size_t)CC * nk;              // [NZ][LD]  Stolt output / FFT work
+  const int tid = threadIdx.x;
+  const int ncol = v.nx * v.ny;
+  const int nclass = (v.nx / 2 + 1) * (v.ny / 2 + 1);
+  const int q0 = blockIdx.x * CL;
+  const int f = blockIdx.y;
+  if (tid < CL) {
+    const int q = q0 + tid;
+    if (q < nclass) {
+      const SarClass &c = v.cls[q];
+      kr2s[tid] = c.kr2;
+      jlos[tid] = c.jlo;
+      jhis[tid] = c.jhi;
+#pragma unroll
+      for (int m = 0; m < 4; ++m) colof[4 * tid + m] = m < c.nmem ? c.col[m] : -1;
+    } else {
+      kr2s[tid] = 0.0;
+      jlos[tid] = 0;
+      jhis[tid] = -1;
+#pragma unroll
+      for (int m = 0; m < 4; ++m) colof[4 * tid + m] = -1;
+    }
+  }
+  __syncthreads();
+  // 1. member columns (streaming loads, 16 B per thread when n_k is even)
+  const float2 *wf = v.w0 + (size_t)f * ncol * (size_t)nk;
+  if ((nk & 1) == 0) {
+    const int h2 = nk / 2;
+    for (int e = tid; e < CC * h2; e += K3C_NT) {
+      const int sl = e / h2, i = e - sl * h2;
+      if (colof[sl] >= 0)
+        reinterpret_cast<float4 *>(fin + sl * nk)[i] =
+            __ldcs(reinterpret_cast<const float4 *>(wf + (size_t)colof[sl] * nk) + i);
+    }
+  } else {
+    for (int e = tid; e < CC * nk; e += K3C_NT) {
+      const int sl = e / nk, i = e - sl * nk;
+      if (colof[sl] >= 0) fin[e] = __ldcs(wf + (size_t)colof[sl] * nk + i);
+    }
+  }
+  __syncthreads();
+  // 2. Stolt pull over the in-band (class, j) pairs, filter at the two taps
+  //    folded into the weights (readings R2-R5, R9)
+  const double rr = v.rref[f] * (1.0 / TWO_PI);
+  int tot = 0;
+#pragma unroll
+  for (int cl = 0; cl < CL; ++cl) tot += jhis[cl] - jlos[cl] + 1;
+  for (int idx = tid; idx < tot; idx += K3C_NT) {
+    int cl = 0, j = idx;
+#pragma unroll
+    for (int q = 0; q < CL - 1; ++q) {
+      const int len = jhis[cl] - jlos[cl] + 1;
+      if (j >= len) {
+        j -= len;
+        ++cl;
+      }
+    }
+    j += jlos[cl];
+    const double kr2 = kr2s[cl];
+    int i0 = 0;
+    double tau = 0.0;
+    const bool ok = stolt_pull(__ldg(v.kz + j), kr2, v.k0, v.inv_dk, v.dk, nk, v.stolt_delta, &i0, &tau);
+    float2 wl = make_float2(0.f, 0.f), wu = wl;
+    if (ok) {
+      const float tt = (float)tau;
+      const float2 hl = filter_h(v, __ldg(v.k + i0), kr2, rr, i0);
+      const float2 hu = filter_h(v, __ldg(v.k + i0 + 1), kr2, rr, i0 + 1);
+      wl = make_float2((1.f - tt) * hl.x, (1.f - tt) * hl.y);
+      wu = make_float2(tt * hu.x, tt * hu.y);
+    }
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+      const int sl = 4 * cl + m;
+      if (colof[sl] < 0) break;
+      float2 o = make_float2(0.f, 0.f);
+      if (ok) o = cmac2(cmul2(wl, fin[sl * nk + i0]), wu, fin[sl * nk + i0 + 1]);
+      fout[j * LD + sl] = o;
+    }
+  }
+  __syncthreads();
+  // 3. inverse z-FFT (out-of-band bins read as zero), columns stored [col][z]
+  float2 *dst = v.w1 + (size_t)f * ncol * (size_t)NZ;
+  auto load = [&](int c, int m) {
+    const int cl = c >> 2;
+    return (m >= jlos[cl] && m <= jhis[cl]) ? fout[m * LD + c] : make_float2(0.f, 0.f);
+  };
+  if constexpr (DO_IFFT) {
+    sarfft2::fft<NZ, CC, LD, K3C_NT, +1, 0, true, (NZ == 512 ? 16 : 0)>(
+        fout, v.tw_z, tid, load, [] {},
+        [&](int c, int m, float2 x) {
+          const int col = colof[c];
+          if (col >= 0) __stcs(dst + (size_t)col * NZ + m, x);
+        });
+  } else {
+    for (int i = tid; i < CC * NZ; i += K3C_NT) {
+      const int sl = i / NZ, z = i - sl * NZ;
+      if (colof[sl] >= 0) dst[(size_t)colof[sl] * NZ + z] = load(sl, z);
+    }
+  }
+}
+
+constexpr int K3P_G = 256;   // threads per consumer group
+constexpr int K3P_NG = 2;    // consumer groups (alternate items)
+constexpr int K3P_S = 3;     // ring stages
+template <int NZ, int CL>
+size_t k3pp_smem(int nk) {
+  const size_t hdr = (sizeof(K3Hdr<CL>) + 15) & ~(size_t)15;
+  return K3P_S * (hdr + (size_t)4 * CL * nk * sizeof(float2)) +
+         K3P_NG * ((size_t)NZ * (4 * CL + 1)) * sizeof(float2) +
+         ((size_t)NZ + nk) * sizeof(double) + (size_t)NZ * sizeof(float2);
+}
+
+template <int NZ, int CL, bool DO_IFFT, int BAR>
+__device__ __forceinline__ void k3pp_consume(const SarDeviceView &v, int nitems_f, int g, int gt,
+                                             unsigned char *ring, size_t stage_bytes, size_t hdr_bytes,
+                                             float2 *fout, const double *ks, const double *kzs, const float2 *tw,
+                                             uint64_t *full, uint64_t *empty, int *colofs, int *slo, int *shi) {
+  constexpr int CC = 4 * CL;
+  constexpr int LD = CC + 1;
+  const int nk = v.nk;
+  const int ncol = v.nx * v.ny;
+  const int nitems = nitems_f * v.F;
+  unsigned n = g;
+  for (int item = blockIdx.x + g * gridDim.x; item < nitems; item += K3P_NG * gridDim.x, n += K3P_NG) {
+    const int st = n % K3P_S;
+    sartma::mbar_wait(&full[st], (n / K3P_S) & 1);
+    unsigned char *sb = ring + st * stage_bytes;
+    const K3Hdr<CL> &h = *reinterpret_cast<const K3Hdr<CL> *>(sb);
+    const float2 *fin = reinterpret_cast<const float2 *>(sb + hdr_bytes);
+    const int f = h.f, nu = h.nused;
+    const double rr = v.rref[f] * (1.0 / TWO_PI);
+    // Stolt pull over the in-band (class, j) pairs only, the filter evaluated
+    // at the two taps each pull uses and folded into the weights:
+    //   O_j = (1-tau) H(k_i0) S_i0 + tau H(k_i0+1) S_i0+1
+    int tot = 0;
+#pragma unroll
+    for (int cl = 0; cl < CL; ++cl) tot += h.jhi[cl] - h.jlo[cl] + 1;
+    for (int idx = (v.dbg & 2) ? tot : gt; idx < tot; idx += K3P_G) {
+      int cl = 0, j = idx;
+#pragma unroll
+      for (int q = 0; q < CL - 1; ++q) {
+        const int len = h.jhi[cl] - h.jlo[cl] + 1;
+        if (j >= len) {
+          j -= len;
+          ++cl;
+        }
+      }
+      j += h.jlo[cl];
+      const double kr2 = h.kr2[cl];
+      int i0 = 0;
+      double tau = 0.0;
+      const bool ok = stolt_pull(kzs[j], kr2, v.k0, v.inv_dk, v.dk, nk, v.stolt_delta, &i0, &tau);
+      float2 wl = make_float2(0.f, 0.f), wu = wl;
+      if (ok) {
+        const float t = (float)tau;
+        const float2 hl = filter_h(v, ks[i0], kr2, rr, i0);
+        const float2 hu = filter_h(v, ks[i0 + 1], kr2, rr, i0 + 1);
+        wl = make_float2((1.f - t) * hl.x, (1.f - t) * hl.y);
+        wu = make_float2(t * hu.x, t * hu.y);
+      }
+      const int nm = h.nmem[cl];
+      for (int m = 0; m < nm; ++m) {
+        const int sl = h.mslot[cl][m];
+        float2 o = make_float2(0.f, 0.f);
+        if (ok) o = cmac2(cmul2(wl, fin[sl * nk + i0]), wu, fin[sl * nk + i0 + 1]);
+        fout[j * LD + sl] = o;
+      }
+    }
+    if (gt < CC) {
+      const bool used = gt < nu;
+      colofs[gt] = used ? h.colof[gt] : -1;
+      slo[gt] = used ? h.jlo[h.clof[gt]] : NZ;
+      shi[gt] = used ? h.jhi[h.clof[gt]] : -1;
+    }
+    sarfft2::sync<BAR, K3P_G>();
+    if (gt == 0) sartma::mbar_arrive(&empty[st]);  // stage (header + columns) consumed
+    // inverse z-FFT (out-of-band rows read as zero), columns stored contiguously
+    float2 *dst = v.w1 + (size_t)f * ncol * (size_t)NZ;
+    auto load = [&](int c, int m) {
+      return (m >= slo[c] && m <= shi[c]) ? fout[m * LD + c] : make_float2(0.f, 0.f);
+    };
+    if (DO_IFFT && !(v.dbg & 4)) {
+      sarfft2::fft<NZ, CC, LD, K3P_G, +1, BAR, true, (NZ == 512 && CC == 8 ? 16 : 0)>(
+          fout, tw, gt, load, [] {},
+          [&](int c, int m, float2 x) {
+            const int col = colofs[c];
+            if (col >= 0) __stcs(dst + (size_t)col * NZ + m, x);
+          });
+    } else {
+      for (int i = gt; i < CC * NZ; i += K3P_G) {
+        const int sl = i / NZ, z = i - sl * NZ;
+        if (sl < nu) dst[(size_t)colofs[sl] * NZ + z] = load(sl, z);
+      }
+    }
+    sarfft2::sync<BAR, K3P_G>();  // fout / slot tables are rewritten by this group's next item
+  }
+}
+
+template <int NZ, int CL, bool DO_IFFT>
+__global__ void __launch_bounds__(K3P_NG * K3P_G + 32, 1) k3_pp(const SarDeviceView v, int nitems_f) {
+  constexpr int CC = 4 * CL;
+  constexpr int LD = CC + 1;
+  constexpr int NTH = K3P_NG * K3P_G + 32;
+  extern __shared__ __align__(16) unsigned char smp[];
+  const int nk = v.nk;
+  const size_t hdr_bytes = (sizeof(K3Hdr<CL>) + 15) & ~(size_t)15;
+  const size_t stage_bytes = hdr_bytes + (size_t)CC * nk * sizeof(float2);
+  unsigned char *ring = smp;
+  float2 *grp = reinterpret_cast<float2 *>(smp + K3P_S * stage_bytes);
+  const size_t grp_elems = (size_t)NZ * LD;                      // fout per group
+  double *ks = reinterpret_cast<double *>(grp + K3P_NG * grp_elems);  // [nk]
+  double *kzs = ks + nk;                                          // [NZ]
+  float2 *tw = reinterpret_cast<float2 *>(kzs + NZ);              // [NZ]
+  __shared__ __align__(8) uint64_t full[K3P_S], empty[K3P_S];
+  __shared__ int colofs[K3P_NG][CC], slo[K3P_NG][CC], shi[K3P_NG][CC];
+  const int tid = threadIdx.x;
+  for (int i = tid; i < nk; i += NTH) ks[i] = v.k[i];
+  for (int i = tid; i < NZ; i += NTH) {
+    kzs[i] = v.kz[i];
+    tw[i] = v.tw_z[i];
+  }
+  if (tid == 0) {
+    for (int i = 0; i < K3P_S; ++i) {
+      sartma::mbar_init(&full[i], 1);
+      sartma::mbar_init(&empty[i], 1);
+    }
+    sartma::fence_barrier_init();
+  }
+  __syncthreads();
+  const int ncol = v.nx * v.ny;
+  const int nitems = nitems_f * v.F;
+  if (tid >= K3P_NG * K3P_G) {
+    if (tid == K3P_NG * K3P_G) {  // producer
+      const int hx = v.nx / 2 + 1, hy = v.ny / 2 + 1;
+      const int nclass = hx * hy;
+      unsigned n = 0;
+      for (int item = blockIdx.x; item < nitems; item += gridDim.x, ++n) {
+        const int st = n % K3P_S;
+        if (n >= K3P_S) sartma::mbar_wait(&empty[st], ((n / K3P_S) - 1) & 1);
+        unsigned char *sb = ring + st * stage_bytes;
+        K3Hdr<CL> &h = *reinterpret_cast<K3Hdr<CL> *>(sb);
+        float2 *fin = reinterpret_cast<float2 *>(sb + hdr_bytes);
+        const int f = item / nitems_f;
+        const int q0 = (item - f * nitems_f) * CL;
+        int cnt = 0;
+        for (int cl = 0; cl < CL; ++cl) {
+          const int q = q0 + cl;
+          h.nmem[cl] = 0;
+          h.kr2[cl] = 0.0;
+          h.jlo[cl] = 0;
+          h.jhi[cl] = -1;
+          if (q >= nclass) continue;
+          const SarClass &c = v.cls[q];
+          h.kr2[cl] = c.kr2;
+          h.jlo[cl] = c.jlo;
+          h.jhi[cl] = c.jhi;
+          for (int m = 0; m < c.nmem; ++m) {
+            h.mslot[cl][h.nmem[cl]++] = cnt;
+            h.clof[cnt] = cl;
+            h.colof[cnt++] = c.col[m];
+          }
+        }
+        h.nused = cnt;
+        h.f = f;
+        const float2 *wf = v.w0 + (size_t)f * ncol * (size_t)nk;
+        sartma::mbar_arrive_expect_tx(&full[st], (uint32_t)cnt * (uint32_t)nk * 8u);
+        for (int sl = 0; sl < cnt; ++sl)
+          sartma::bulk_g2s(fin + sl * nk, wf + (size_t)h.colof[sl] * nk, (uint32_t)nk * 8u, &full[st]);
+      }
+    }
+    return;
+  }
+  const int g = tid / K3P_G, gt = tid - g * K3P_G;
+  float2 *fout = grp + g * grp_elems;
+  if (g == 0)
+    k3pp_consume<NZ, CL, DO_IFFT, 1>(v, nitems_f, 0, gt, ring, stage_bytes, hdr_bytes, fout, ks, kzs, tw, full, empty,
+                                     colofs[0], slo[0], shi[0]);
+  else
+    k3pp_consume<NZ, CL, DO_IFFT, 2>(v, nitems_f, 1, gt, ring, stage_bytes, hdr_bytes, fout, ks, kzs, tw, full, empty,
+                                     colofs[1], slo[1], shi[1]);
+}
+
+// ------------------------------------------------------- K3, 2-D mode ----
+// SAR_IMAGE_2D (reading R18): per Stolt mirror class (the <= 4 columns that
+// share k_r^2), k_z,i = sqrt(4 k_i^2 - k_r^2) once, then for every plane s the
+// back-propagation weights w_i = k_z,i exp(+j k_z,i (z_s - Z_0)) / P_i (phase
+// in turns, fp64) and, per member column, the sum over k of S_i w_i (one warp
+// per column: lanes stride over k, shuffle reduction).  Output W1[f][b][a][s]
+// (planes fastest), which the y- and x-inverse kernels then transform like the
+// z-chunks of the 3-D path.
+constexpr int K3P2_NT = 256;   // 8 warps = 8 mirror classes per CTA
+constexpr int K3P2_PS = 4;     // planes per pass (accumulators in registers)
+
+__global__ void __launch_bounds__(K3P2_NT) k3_plane(const SarDeviceView v) {
+  const int lane = threadIdx.x & 31;
+  const int q = blockIdx.x * (K3P2_NT / 32) + (threadIdx.x >> 5);
+  const int f = blockIdx.y;
+  const int nclass = (v.nx / 2 + 1) * (v.ny / 2 + 1);
+  if (q >= nclass) return;
+  const SarClass &c = v.cls[q];
+  const int nm = c.nmem, nk = v.nk, ns = v.nz;
+  const int ncol = v.nx * v.ny;
+  const double kr2 = c.kr2;
+  const double zoff = v.rref[f];   // z_s - Z_0 = (z_s - z_ref) + R_ref
+  const float2 *wf = v.w0 + (size_t)f * ncol * (size_t)nk;
+  const float2 *col[4];
+#pragma unroll
+  for (int m = 0; m < 4; ++m) col[m] = wf + (size_t)(m < nm ? c.col[m] : c.col[0]) * nk;
+  float2 *dst = v.w1 + (size_t)f * ncol * (size_t)ns;
+  for (int s0 = 0; s0 < ns; s0 += K3P2_PS) {
+    double tz[K3P2_PS];
+#pragma unroll
+    for (int u = 0; u < K3P2_PS; ++u) tz[u] = s0 + u < ns ? (__ldg(v.kz + s0 + u) + zoff) * (1.0 / TWO_PI) : 0.0;
+    float2 acc[K3P2_PS][4];
+#pragma unroll
+    for (int u = 0; u < K3P2_PS; ++u)
+#pragma unroll
+      for (int m = 0; m < 4; ++m) acc[u][m] = make_float2(0.f, 0.f);
+#pragma unroll 4
+    for (int i = lane; i < nk; i += 32) {
+      float2 x[4];
+#pragma unroll
+      for (int m = 0; m < 4; ++m) x[m] = __ldcs(col[m] + i);
+      const double ki = __ldg(v.k + i);
+      const double qq = 4.0 * ki * ki - kr2;
+      if (qq > 0.0) {
+        const double kz = fast_dsqrt(qq);
+        const float kzf = (float)kz;
+        float2 pinv = make_float2(1.f, 0.f);
+        if (v.pinv) pinv = v.pinv[i];
+#pragma unroll
+        for (int u = 0; u < K3P2_PS; ++u) {
+          double turns = kz * tz[u];
+          turns -= rint(turns);
+          float sn, cs;
+          __sincosf((float)turns * 6.28318530717958647692f, &sn, &cs);
+          const float2 w = cmul(make_float2(kzf * cs, kzf * sn), pinv);
+#pragma unroll
+          for (int m = 0; m < 4; ++m) acc[u][m] = cmac2(acc[u][m], x[m], w);
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < K3P2_PS; ++u)
+#pragma unroll
+      for (int m = 0; m < 4; ++m)
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          acc[u][m].x += __shfl_xor_sync(0xffffffffu, acc[u][m].x, o);
+          acc[u][m].y += __shfl_xor_sync(0xffffffffu, acc[u][m].y, o);
+        }
+    if (lane < 4 * K3P2_PS) {
+      const int u = lane >> 2, m = lane & 3;
+      float2 r = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int uu = 0; uu < K3P2_PS; ++uu)
+#pragma unroll
+        for (int mm = 0; mm < 4; ++mm)
+          if (uu == u && mm == m) r = acc[uu][mm];
+      if (m < nm && s0 + u < ns) dst[(size_t)c.col[m] * ns + s0 + u] = r;
+    }
+  }
+}
+
+__global__ void k_stolt_index(const SarDeviceView v, const int32_t *__restrict__ cols, int n,
+                              int32_t *__restrict__ i0_out, float *__restrict__ tau_out) {
+  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (long long)n * v.nz) return;
+  const int c = (int)(idx / v.nz), j = (int)(idx - (long long)c * v.nz);
+  const int a = cols[2 * c], b = cols[2 * c + 1];
+  int i0;
+  double tau;
+  if (a >= 0 && a < v.nx && b >= 0 && b < v.ny &&
+      stolt_pull(v.kz[j], kr2_of(v, a, b), v.k0, v.inv_dk, v.dk, v.nk, v.stolt_delta, &i0, &tau)) {
+    i0_out[idx] = i0;
+    tau_out[idx] = (float)tau;
+  } else {
+    i0_out[idx] = -1;
+    tau_out[idx] = 0.f;
+  }
+}
+
+template <typename K>
+cudaError_t launch_v(K kernel, dim3 grid, int nt, size_t smem, cudaStream_t s, const SarDeviceView &v) {
+  if (smem > 40 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  kernel<<<grid, nt, smem, s>>>(v);
+  return cudaGetLastError();
+}
+
+
+}  // namespace
+
+cudaError_t launch_k3(const SarDeviceView &v, bool ifft, cudaStream_t s, int num_sms) {
+  if ((v.nk & 1) == 0 && v.nz >= 256 && !getenv("SAR_K3_PLAIN")) {
+    const int nclass = (v.nx / 2 + 1) * (v.ny / 2 + 1);
+    switch (v.nz) {
+#define X(N)                                                                                                   \
+  case N: {                                                                                                    \
+    constexpr int CL = 2;                                                                                      \
+    const size_t smem = k3pp_smem<N, CL>(v.nk);                                                                \
+    if (smem > 225 * 1024) break;                                                                              \
+    const int nitems_f = (nclass + CL - 1) / CL;                                                               \
+    const int nitems = nitems_f * v.F;                                                                         \
+    const int grid = nitems < num_sms ? nitems : num_sms;                                                      \
+    auto kern = ifft ? k3_pp<N, CL, true> : k3_pp<N, CL, false>;                                               \
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);        \
+    if (e != cudaSuccess) return e;                                                                            \
+    kern<<<grid, K3P_NG * K3P_G + 32, smem, s>>>(v, nitems_f);                                                 \
+    return cudaGetLastError();                                                                                 \
+  }
+      X(256) X(512) X(1024)
+#undef X
+    }
+  }
+  const int nclass = (v.nx / 2 + 1) * (v.ny / 2 + 1);
+  switch (v.nz) {
+#define X(N)                                                                                                   \
+  case N: {                                                                                                    \
+    constexpr int CL = k3c_cl<N>();                                                                            \
+    const size_t smem = k3c_smem<N>(v.nk);                                                                     \
+    if (smem > 220 * 1024) return cudaErrorInvalidValue;                                                       \
+    dim3 grid((nclass + CL - 1) / CL, v.F);                                                                    \
+    auto kern = ifft ? k3_class<N, true> : k3_class<N, false>;                                                 \
+    if (smem > 40 * 1024) {                                                                                    \
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);      \
+      if (e != cudaSuccess) return e;                                                                          \
+    }                                                                                                          \
+    kern<<<grid, K3C_NT, smem, s>>>(v);                                                                        \
+    return cudaGetLastError();                                                                                 \
+  }
+    SAR_SIZES(X)
+#undef X
+  }
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_k3_plane(const SarDeviceView &v, cudaStream_t s) {
+  const int nclass = (v.nx / 2 + 1) * (v.ny / 2 + 1);
+  const int cpb = K3P2_NT / 32;
+  k3_plane<<<dim3((nclass + cpb - 1) / cpb, v.F), K3P2_NT, 0, s>>>(v);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_stolt_index(const SarDeviceView &v, const int32_t *cols, int n, int32_t *i0, float *tau,
+                               cudaStream_t s) {
+  const long long total = (long long)n * v.nz;
+  if (total == 0) return cudaSuccess;
+  const int nt = 256;
+  k_stolt_index<<<(unsigned)((total + nt - 1) / nt), nt, 0, s>>>(v, cols, n, i0, tau);
+  return cudaGetLastError();
+}
+
+
+}  // namespace sark

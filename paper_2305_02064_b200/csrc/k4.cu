@@ -1,0 +1,312 @@
+// k4.cu -- K4b: inverse x-FFT + |.|/(nx ny nz) + integer rolls (IFT_3D of
+// Eq. (14); readings R8, R11), W1 -> image.
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdlib.h>
+
+#include <string>
+#include <type_traits>
+#include <vector>
+
+#include "common.cuh"
+
+namespace sark {
+namespace {
+
+// Warp-specialised persistent K4b (nx <= 512, n_z even): [nx][16 z] tiles of
+// W1 row y stream through an S-stage TMA ring; the consumers run the inverse
+// x-FFT (pass 2 mapped so that one warp owns 32 consecutive x of one z) and
+// write |o|/(nx ny nz) (or the scaled complex value) straight into the rolled
+// image rows (reading R8, R11): coalesced 128-byte segments, no transpose
+// buffer.
+template <int NX, bool CPLX>
+constexpr size_t k4b2_smem() {
+  return ((size_t)2 * NX * KC + (size_t)NX * (KC + 1) + NX) * sizeof(float2);
+}
+template <int NX>
+constexpr int k4b2_ctas() {
+  return (int)((200 * 1024) / k4b2_smem<NX, false>()) < 1 ? 1 : (int)((200 * 1024) / k4b2_smem<NX, false>());
+}
+
+template <int NX, bool CPLX>
+__global__ void __launch_bounds__(sarfft2::nt_fft<NX, KC>() + 32)
+    k4_xifft_mag2(const SarDeviceView v, const __grid_constant__ CUtensorMap tm, void *__restrict__ img, int nzc,
+                  int nitems) {
+  constexpr int NTC = sarfft2::nt_fft<NX, KC>();
+  constexpr int S = 2;
+  constexpr int ROWS = NX < 256 ? NX : 256;
+  constexpr int NBOX = NX / ROWS;
+  constexpr uint32_t TILE_BYTES = NX * KC * sizeof(float2);
+  using OT = typename std::conditional<CPLX, float2, float>::type;
+  extern __shared__ __align__(128) float2 smk[];
+  float2 *ring = smk;                          // [S][NX][16]
+  float2 *work = smk + (size_t)S * NX * KC;    // [NX][17]
+  float2 *tw = work + (size_t)NX * (KC + 1);   // [NX]
+  __shared__ __align__(8) uint64_t full[S], empty[S];
+  const int tid = threadIdx.x;
+  for (int i = tid; i < NX; i += NTC + 32) tw[i] = v.tw_x[i];
+  if (tid == 0) {
+    for (int i = 0; i < S; ++i) {
+      sartma::mbar_init(&full[i], 1);
+      sartma::mbar_init(&empty[i], 1);
+    }
+    sartma::fence_barrier_init();
+  }
+  __syncthreads();
+  if (tid >= NTC) {
+    if (tid == NTC) {
+      unsigned n = 0;
+      for (int item = blockIdx.x; item < nitems; item += gridDim.x, ++n) {
+        const int st = n % S;
+        if (n >= S) sartma::mbar_wait(&empty[st], ((n / S) - 1) & 1);
+        const int zc = item % nzc, fy = item / nzc;  // fy = f*ny + y
+        sartma::mbar_arrive_expect_tx(&full[st], TILE_BYTES);
+#pragma unroll
+        for (int bx = 0; bx < NBOX; ++bx)
+          sartma::tma_load_3d(ring + (size_t)st * NX * KC + bx * ROWS * KC, &tm, zc * KC, bx * ROWS, fy, &full[st]);
+      }
+    }
+    return;
+  }
+  const int nz = v.nz;
+  const int rx = ((v.roll_x % NX) + NX) % NX;
+  const int ry = ((v.roll_y % v.ny) + v.ny) % v.ny;
+  const float sc = v.img_scale;
+  const size_t zstride = (size_t)v.ny * NX;
+  unsigned n = 0;
+  for (int item = blockIdx.x; item < nitems; item += gridDim.x, ++n) {
+    const int st = n % S;
+    sartma::mbar_wait(&full[st], (n / S) & 1);
+    const int zc = item % nzc, fy = item / nzc;
+    const int f = fy / v.ny, y = fy - f * v.ny;
+    int iy = y - ry;
+    if (iy < 0) iy += v.ny;
+    OT *outp = reinterpret_cast<OT *>(img) + ((size_t)f * nz * v.ny + iy) * NX;
+    const float2 *stage = ring + (size_t)st * NX * KC;
+    sarfft2::fft<NX, KC, KC + 1, NTC, +1, 1, true>(
+        work, tw, tid, [&](int c, int m) { return stage[m * KC + c]; },
+        [&] {
+          if (tid == 0) sartma::mbar_arrive(&empty[st]);
+        },
+        [&](int c, int a, float2 o) {
+          const int z = zc * KC + c;
+          if (z < nz) {
+            int m = z + v.zroll;
+            if (m >= nz) m -= nz;
+            const int ix = (a - rx) & (NX - 1);
+            if constexpr (CPLX) {
+              __stcs(reinterpret_cast<float2 *>(outp) + (size_t)m * zstride + ix, make_float2(o.x * sc, o.y * sc));
+            } else {
+              __stcs(reinterpret_cast<float *>(outp) + (size_t)m * zstride + ix, sqrtf(fmaf(o.x, o.x, o.y * o.y)) * sc);
+            }
+          }
+        });
+  }
+}
+
+// --------------------------------------------------------------- K4b ------
+// One CTA = (z chunk, image row y (pre-roll), frame).  Tile [NX][17]: the odd
+// stride makes both the FFT passes and the transposed read conflict-free.
+template <int NX, bool CPLX>
+__global__ void __launch_bounds__(nt_for(NX), minb_for(NX))
+    k4_xifft_mag(const SarDeviceView v, void *__restrict__ img) {
+  constexpr int NT = nt_for(NX);
+  constexpr int LD = KC + 1;
+  constexpr int ITEMS = NX * KC;
+  constexpr int E = (ITEMS + NT - 1) / NT;
+  extern __shared__ float2 tile[];  // [NX][LD]
+  const int tid = threadIdx.x;
+  const int zbase = blockIdx.x * KC;
+  const int y = blockIdx.y;
+  const int f = blockIdx.z;
+  const int nz = v.nz;
+  const float2 *src = v.w1 + ((size_t)(f * v.ny + y) * NX) * (size_t)nz;
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int item = tid + e * NT;
+    if (ITEMS % NT != 0 && item >= ITEMS) continue;
+    const int zz = item & (KC - 1), a = item >> 4;
+    const int z = zbase + zz;
+    tile[a * LD + zz] = z < nz ? src[(size_t)a * nz + z] : make_float2(0.f, 0.f);
+  }
+  __syncthreads();
+  sarfft::tile_fft<NX, KC, LD, NT, +1>(tile, v.tw_x, tid);
+  int iy = y - v.roll_y % v.ny;
+  if (iy < 0) iy += v.ny;
+  if (iy >= v.ny) iy -= v.ny;
+  const int rx = ((v.roll_x % NX) + NX) % NX;
+  const float sc = v.img_scale;
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int item = tid + e * NT;
+    if (ITEMS % NT != 0 && item >= ITEMS) continue;
+    const int zz = item / NX, ix = item - zz * NX;
+    const int z = zbase + zz;
+    if (z >= nz) continue;
+    int m = z + v.zroll;
+    if (m >= nz) m -= nz;
+    const int xs = (ix + rx) & (NX - 1);
+    const float2 o = tile[xs * LD + zz];
+    const size_t off = ((size_t)(f * nz + m) * v.ny + iy) * NX + ix;
+    if constexpr (CPLX) {
+      reinterpret_cast<float2 *>(img)[off] = make_float2(o.x * sc, o.y * sc);
+    } else {
+      reinterpret_cast<float *>(img)[off] = sqrtf(fmaf(o.x, o.x, o.y * o.y)) * sc;
+    }
+  }
+}
+
+// Persistent, TMA-pipelined K4b (n_z even, 32 <= nx <= 512).  Item = (frame,
+// image row y, 16-wide z chunk): the [nx][16] tile of item i+1 is in flight
+// (cp.async.bulk.tensor + mbarrier) while item i is inverse-transformed along
+// x; the magnitudes (or scaled complex values) are transposed through a padded
+// [16][nx+1] buffer with the x roll applied, so every image row segment is
+// written with coalesced stores.
+template <int NX, bool CPLX>
+__global__ void __launch_bounds__(ntp_for(NX), ctas_for(NX))
+    k4_xifft_mag_tma(const SarDeviceView v, const __grid_constant__ CUtensorMap tm, void *__restrict__ img,
+                     int nzc, int nitems) {
+  constexpr int NT = ntp_for(NX);
+  constexpr int ROWS = NX < 256 ? NX : 256;
+  constexpr int NBOX = NX / ROWS;
+  constexpr uint32_t TILE_BYTES = NX * KC * sizeof(float2);
+  using OT = typename std::conditional<CPLX, float2, float>::type;
+  extern __shared__ __align__(128) float2 smk[];    // [2][NX][16] tiles, then [16][NX+1] output rows
+  OT *ob = reinterpret_cast<OT *>(smk + 2 * (size_t)NX * KC);
+  __shared__ __align__(8) uint64_t full[2];
+  __shared__ float2 tw[NX];
+  const int tid = threadIdx.x;
+  const int nz = v.nz;
+  for (int i = tid; i < NX; i += NT) tw[i] = v.tw_x[i];
+  if (tid == 0) {
+    sartma::mbar_init(&full[0], 1);
+    sartma::mbar_init(&full[1], 1);
+    sartma::fence_barrier_init();
+  }
+  __syncthreads();
+  auto issue = [&](int item, int st) {
+    const int zc = item % nzc, fy = item / nzc;  // fy = f*ny + y
+    sartma::mbar_arrive_expect_tx(&full[st], TILE_BYTES);
+#pragma unroll
+    for (int bx = 0; bx < NBOX; ++bx)
+      sartma::tma_load_3d(smk + (size_t)st * NX * KC + bx * ROWS * KC, &tm, zc * KC, bx * ROWS, fy, &full[st]);
+  };
+  const int rx = ((v.roll_x % NX) + NX) % NX;
+  const int ry = ((v.roll_y % v.ny) + v.ny) % v.ny;
+  const float sc = v.img_scale;
+  int item = blockIdx.x;
+  if (tid == 0 && item < nitems) issue(item, 0);
+  for (int it = 0; item < nitems; ++it, item += gridDim.x) {
+    const int st = it & 1;
+    const int next = item + gridDim.x;
+    if (tid == 0 && next < nitems) issue(next, st ^ 1);
+    sartma::mbar_wait(&full[st], (it >> 1) & 1);
+    float2 *tile = smk + (size_t)st * NX * KC;
+    sarfft::tile_fft<NX, KC, KC, NT, +1>(tile, tw, tid);
+    // transpose into output rows: ob[zz][ix] with ix = (a - r_x) mod nx
+#pragma unroll
+    for (int i = tid; i < NX * KC; i += NT) {
+      const int a = i / KC, zz = i % KC;
+      const float2 o = tile[i];
+      const int ix = (a - rx) & (NX - 1);
+      if constexpr (CPLX) {
+        ob[zz * (NX + 1) + ix] = make_float2(o.x * sc, o.y * sc);
+      } else {
+        const float p = fmaf(o.x, o.x, o.y * o.y);
+        ob[zz * (NX + 1) + ix] = p > 0.f ? p * rsqrtf(p) * sc : 0.f;   // |o| (rsqrt: 2 ulp)
+      }
+    }
+    sartma::fence_proxy_async();
+    __syncthreads();  // tile st is free (next-next load may overwrite it), ob complete
+    const int zc = item % nzc, fy = item / nzc;
+    const int f = fy / v.ny, y = fy - f * v.ny;
+    int iy = y - ry;
+    if (iy < 0) iy += v.ny;
+    OT *outp = reinterpret_cast<OT *>(img) + ((size_t)f * nz * v.ny + iy) * NX;
+    const size_t zstride = (size_t)v.ny * NX;
+#pragma unroll
+    for (int i = tid; i < NX * KC; i += NT) {
+      const int zz = i / NX, ix = i % NX;
+      const int z = zc * KC + zz;
+      if (z < nz) {
+        int m = z + v.zroll;
+        if (m >= nz) m -= nz;
+        outp[m * zstride + ix] = ob[zz * (NX + 1) + ix];
+      }
+    }
+    __syncthreads();  // ob free
+  }
+}
+
+template <typename K>
+cudaError_t launch_img(K kernel, dim3 grid, int nt, size_t smem, cudaStream_t s, const SarDeviceView &v,
+                       void *img) {
+  if (smem > 40 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  kernel<<<grid, nt, smem, s>>>(v, img);
+  return cudaGetLastError();
+}
+
+
+}  // namespace
+
+cudaError_t launch_k4b(const SarDeviceView &v, void *img, bool cplx, cudaStream_t s, const CUtensorMap *tm,
+                       int num_sms) {
+  if (tm && v.nx <= 512 && !getenv("SAR_K4B_OLD")) {
+    const int nzc = (v.nz + KC - 1) / KC;
+    const int nitems = nzc * v.ny * v.F;
+    switch (v.nx) {
+#define X(N)                                                                                           \
+  case N: {                                                                                            \
+    auto kern = cplx ? k4_xifft_mag2<N, true> : k4_xifft_mag2<N, false>;                               \
+    constexpr size_t smem = k4b2_smem<N, false>();                                                     \
+    if (smem > 40 * 1024) {                                                                            \
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+      if (e != cudaSuccess) return e;                                                                  \
+    }                                                                                                  \
+    const int maxg = num_sms * k4b2_ctas<N>();                                                         \
+    kern<<<nitems < maxg ? nitems : maxg, sarfft2::nt_fft<N, KC>() + 32, smem, s>>>(v, *tm, img, nzc, nitems); \
+    return cudaGetLastError();                                                                         \
+  }
+      X(2) X(4) X(8) X(16) X(32) X(64) X(128) X(256) X(512)
+#undef X
+    }
+  }
+  if (tm && v.nx >= 32 && v.nx <= 512) {
+    const int nzc = (v.nz + KC - 1) / KC;
+    const int nitems = nzc * v.ny * v.F;
+    const size_t smem = 2 * (size_t)v.nx * KC * sizeof(float2) + (size_t)KC * (v.nx + 1) * (cplx ? 8 : 4);
+    switch (v.nx) {
+#define X(N)                                                                                           \
+  case N: {                                                                                            \
+    auto kern = cplx ? k4_xifft_mag_tma<N, true> : k4_xifft_mag_tma<N, false>;                        \
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+    if (e != cudaSuccess) return e;                                                                    \
+    const int cps = ctas_for(N) * smem <= 200 * 1024 ? ctas_for(N) : 1;                               \
+    const int maxg = num_sms * cps;                                                                    \
+    kern<<<nitems < maxg ? nitems : maxg, ntp_for(N), smem, s>>>(v, *tm, img, nzc, nitems);            \
+    return cudaGetLastError();                                                                         \
+  }
+      X(32) X(64) X(128) X(256) X(512)
+#undef X
+    }
+  }
+  dim3 grid((v.nz + KC - 1) / KC, v.ny, v.F);
+  const size_t smem = (size_t)v.nx * (KC + 1) * sizeof(float2);
+  switch (v.nx) {
+#define X(N)                                                                             \
+  case N:                                                                                \
+    return cplx ? launch_img(k4_xifft_mag<N, true>, grid, nt_for(N), smem, s, v, img)    \
+                : launch_img(k4_xifft_mag<N, false>, grid, nt_for(N), smem, s, v, img);
+    SAR_SIZES(X)
+#undef X
+  }
+  return cudaErrorInvalidValue;
+}
+
+
+
+}  // namespace sark

@@ -1,0 +1,198 @@
+// pipeline.cu -- enqueues the kernels of the reconstruction path (one
+// translation unit per kernel family) and builds the TMA tensor maps.  Citation keys: P:n = PAPER.md line n; readings R1..R17 are in
+// DESIGN.md section 3.
+//
+//   K1  k1_correct_xfft   per (frame, virtual row vy, 16-wide k chunk):
+//                          gather every (tx,rx,pose) sample that lands on the
+//                          row, rotate it by exp(+j k beta) (Eqs. (11)-(12),
+//                          P:183-193), sum (reading R6), then FFT the row
+//                          along x in shared memory.          raw -> W0
+//   K2  k_fft_mid<-1>      FFT along y for (frame, kx, k chunk)   W0 -> W0
+//   K3  k3_filter_stolt    per 8 (kx,ky) columns: filter k_z e^{+j k_z R_ref}/P
+//                          on the source grid (readings R2-R4), linear
+//                          Stolt pull onto the k_z grid (R5, R9),
+//                          inverse FFT along z.               W0 -> W1
+//   K4a k_fft_mid<+1>      inverse FFT along y                   W1 -> W1
+//   K4b k4_xifft_mag       inverse FFT along x, |.|/(nx ny nz), integer rolls
+//                          (R8, R11), transposed store to [f][z][y][x].  W1 -> image
+//
+// All transforms are the shared-memory Stockham FFT of fft_tile.cuh.  The
+// path is HBM-bound: every kernel streams its input
+// once with coalesced 128-byte row segments and keeps the transform on chip.
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdlib.h>
+
+#include <string>
+#include <type_traits>
+#include <vector>
+
+#include "common.cuh"
+
+using namespace sark;
+
+// Enqueue the path.  stop_stage: 0 = full; 1 = K1 without the x-FFT; 2 = K1+K2;
+// 3 = K1+K2+K3 without the z-IFFT.  ev (optional, 6 events) brackets the kernels.
+int sar_launch_pipeline(sar_plan *p, const void *d_data, void *d_image, cudaStream_t s, int stop_stage,
+                        int complex_out, cudaEvent_t *ev) {
+  const SarDeviceView &v = p->v;
+  const float2 *data = reinterpret_cast<const float2 *>(d_data);
+  cudaError_t e = cudaSuccess;
+#define SAR_CHECK(call)                                                       \
+  do {                                                                        \
+    e = (call);                                                               \
+    if (e != cudaSuccess) {                                                   \
+      sar_set_error(std::string("CUDA: ") + cudaGetErrorString(e) + " in " #call); \
+      return SAR_ERR_CUDA;                                                    \
+    }                                                                         \
+  } while (0)
+  if (ev) SAR_CHECK(cudaEventRecord(ev[0], s));
+  const CUtensorMap *tm_s = nullptr;
+  if (p->tma_ap) {
+    if (p->tm_s_ptr != d_data) p->tma_s = sar_encode_input_map(p, d_data);
+    if (p->tma_s) tm_s = &p->tm_s;
+  }
+  if (v.nufft) {
+    // K1n (spread + fine x-FFT) and K2n (fine y-FFT + crop) replace K1 and K2;
+    // their times are reported in the K1 and K2 slots
+    SAR_CHECK(launch_nufft(v, data, s));
+    if (ev) SAR_CHECK(cudaEventRecord(ev[1], s));
+    if (ev) SAR_CHECK(cudaEventRecord(ev[2], s));
+    if (stop_stage == 2) return SAR_OK;
+    SAR_CHECK(launch_k3(v, stop_stage != 3, s, p->num_sms));
+    if (ev) SAR_CHECK(cudaEventRecord(ev[3], s));
+    if (stop_stage == 3) return SAR_OK;
+    SAR_CHECK(launch_mid<+1>(v.w1, v.tw_y, v.F, v.ny, v.nx, v.nz, s, p->tma_mid1 ? &p->tm_w1_mid : nullptr,
+                             p->num_sms));
+    if (ev) SAR_CHECK(cudaEventRecord(ev[4], s));
+    SAR_CHECK(launch_k4b(v, d_image, complex_out != 0, s, p->tma_rows1 ? &p->tm_w1_rows : nullptr, p->num_sms));
+    if (ev) SAR_CHECK(cudaEventRecord(ev[5], s));
+    return SAR_OK;
+  }
+  SAR_CHECK(launch_k1(v, data, stop_stage != 1, s, tm_s, p->tma_ap ? &p->tm_ap : nullptr, p->k1_br, p->k1_regacc,
+                      p->num_sms));
+  if (ev) SAR_CHECK(cudaEventRecord(ev[1], s));
+  if (stop_stage == 1) return SAR_OK;
+  if (p->fused) {
+    // K2 + K3 + K4a as one kernel (its time is reported in the K3 slot)
+    if (ev) SAR_CHECK(cudaEventRecord(ev[2], s));
+    SAR_CHECK(launch_passb(v, &p->tm_w0_pb, &p->tm_w1_pb, p->d_items, p->n_items, p->d_cnt,
+                           stop_stage == 2 || stop_stage == 3 ? stop_stage : 0,
+                           stop_stage == 0 && p->passb_discard, s, p->num_sms));
+    if (ev) SAR_CHECK(cudaEventRecord(ev[3], s));
+    if (stop_stage == 2 || stop_stage == 3) return SAR_OK;
+    if (ev) SAR_CHECK(cudaEventRecord(ev[4], s));
+  } else {
+    SAR_CHECK(launch_mid<-1>(v.w0, v.tw_y, v.F, v.ny, v.nx, v.nk, s, p->tma_mid0 ? &p->tm_w0_mid : nullptr,
+                             p->num_sms));
+    if (ev) SAR_CHECK(cudaEventRecord(ev[2], s));
+    if (stop_stage == 2) return SAR_OK;
+    if (v.mode2d) {
+      SAR_CHECK(launch_k3_plane(v, s));
+    } else {
+      SAR_CHECK(launch_k3(v, stop_stage != 3, s, p->num_sms));
+    }
+    if (ev) SAR_CHECK(cudaEventRecord(ev[3], s));
+    if (stop_stage == 3) return SAR_OK;
+    SAR_CHECK(launch_mid<+1>(v.w1, v.tw_y, v.F, v.ny, v.nx, v.nz, s, p->tma_mid1 ? &p->tm_w1_mid : nullptr,
+                             p->num_sms));
+    if (ev) SAR_CHECK(cudaEventRecord(ev[4], s));
+  }
+  SAR_CHECK(launch_k4b(v, d_image, complex_out != 0, s, p->tma_rows1 ? &p->tm_w1_rows : nullptr, p->num_sms));
+  if (ev) SAR_CHECK(cudaEventRecord(ev[5], s));
+  return SAR_OK;
+}
+
+int sar_launch_stolt_index(sar_plan *p, const int32_t *d_cols, int n, int32_t *d_i0, float *d_tau,
+                           cudaStream_t s) {
+  cudaError_t e = launch_stolt_index(p->v, d_cols, n, d_i0, d_tau, s);
+  if (e != cudaSuccess) {
+    sar_set_error(std::string("CUDA: ") + cudaGetErrorString(e));
+    return SAR_ERR_CUDA;
+  }
+  return SAR_OK;
+}
+
+// ------------------------------------------------------- tensor maps ------
+#include <cudaTypedefs.h>
+
+namespace {
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void *ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+  }
+  return fn;
+}
+
+// 3-D map over a complex64 volume [d2][d1][d0] (d0 fastest), 8-byte elements.
+bool encode3d(CUtensorMap *m, void *base, uint64_t d0, uint64_t d1, uint64_t d2, uint32_t b0, uint32_t b1,
+              uint32_t b2) {
+  auto enc = get_encode();
+  if (!enc) return false;
+  if ((d0 * 8) % 16 != 0 || (reinterpret_cast<uintptr_t>(base) & 15) != 0) return false;
+  cuuint64_t dims[3] = {d0, d1, d2};
+  cuuint64_t strides[2] = {d0 * 8, d0 * d1 * 8};
+  cuuint32_t box[3] = {b0, b1, b2};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+}  // namespace
+
+// 2-D map over a row-major [d1][d0] array of `esize`-byte elements
+static bool encode2d(CUtensorMap *m, const void *base, CUtensorMapDataType dt, uint64_t esize, uint64_t d0,
+                     uint64_t d1, uint32_t b0, uint32_t b1) {
+  auto enc = get_encode();
+  if (!enc) return false;
+  if ((d0 * esize) % 16 != 0 || (reinterpret_cast<uintptr_t>(base) & 15) != 0) return false;
+  cuuint64_t dims[2] = {d0, d1};
+  cuuint64_t strides[1] = {d0 * esize};
+  cuuint32_t box[2] = {b0, b1};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = enc(m, dt, 2, const_cast<void *>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+// raw samples viewed as [F*n_tx*n_rx*P rows][n_k] complex64, box [br rows][16]
+bool sar_encode_input_map(sar_plan *p, const void *d_data) {
+  const SarDeviceView &v = p->v;
+  p->tm_s_ptr = d_data;
+  const uint64_t rows = (uint64_t)v.F * v.nt * v.nr * v.P;
+  return encode2d(&p->tm_s, d_data, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, v.nk, rows, k1c_for(v.nx), p->k1_br);
+}
+
+int sar_build_tensor_maps(sar_plan *p) {
+  const SarDeviceView &v = p->v;
+  p->tma_mid0 = p->tma_mid1 = p->tma_rows1 = false;
+  if (v.F == 0 || getenv("SAR_NO_TMA")) return SAR_OK;
+  const uint32_t rows = v.ny < 256 ? v.ny : 256;
+  p->tma_mid0 = encode3d(&p->tm_w0_mid, v.w0, v.nk, v.nx, (uint64_t)v.F * v.ny, KC, 1, rows);
+  p->tma_mid1 = encode3d(&p->tm_w1_mid, v.w1, v.nz, v.nx, (uint64_t)v.F * v.ny, KC, 1, rows);
+  p->tma_pb = encode3d(&p->tm_w0_pb, v.w0, v.nk, v.nx, (uint64_t)v.F * v.ny, PB_KC, 1, rows) &&
+              encode3d(&p->tm_w1_pb, v.w1, v.nz, v.nx, (uint64_t)v.F * v.ny, PB_KC, 1, rows);
+  const uint32_t xr = v.nx < 256 ? v.nx : 256;
+  p->tma_rows1 = encode3d(&p->tm_w1_rows, v.w1, v.nz, v.nx, (uint64_t)v.F * v.ny, KC, xr, 1);
+  // K1: -2 d_z table [F*npy][npx] float32 with box [1][br]; input map per call
+  const int brmax = K1_BOX_BYTES / (k1c_for(v.nx) * 8);
+  p->k1_br = v.npx < brmax ? v.npx : brmax;
+  p->k1_regacc = true;
+  for (int i = 0; i < v.npair; ++i) p->k1_regacc = p->k1_regacc && v.jx[i] == 0;
+  p->tma_ap = (v.npx % 4 == 0) && (v.nk % 2 == 0) && p->k1_br % 8 == 0 &&
+              encode2d(&p->tm_ap, v.apose, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, v.npx, (uint64_t)v.F * v.npy,
+                       p->k1_br, 1);
+  p->tm_s_ptr = nullptr;
+  p->tma_s = false;
+  return SAR_OK;
+}
+

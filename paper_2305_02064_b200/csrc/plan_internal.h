@@ -1,5 +1,6 @@
 // plan_internal.h -- the plan object shared by the host C ABI (plan.cpp) and
-// the kernel launchers (kernels.cu).  Not part of the public ABI.
+// the kernel launchers (pipeline.cu and the per-kernel translation units).
+// Not part of the public ABI.
 #pragma once
 #include <cuda.h>
 #include <cuda_runtime.h>
@@ -56,7 +57,7 @@ struct SarDeviceView {
   const float2 *tw_z;   // [nz]
   double k0, dk, inv_dk;
   double kz_top, kz_step;  // k_z[nz-1] = 2 k_max and the k_z bin width (reading R5)
-  double stolt_delta;   // decision guard band of the fast Stolt path (kernels.cu)
+  double stolt_delta;   // decision guard band of the fast Stolt path (common.cuh)
   int k1_step_ok;       // max |dk * beta| <= 0.25: K1 may use the Taylor step phasor
   int dbg;              // ablation switches (env SAR_DBG; 0 in production)
   float img_scale;      // 1/(nx ny nz)
@@ -104,7 +105,7 @@ struct sar_plan {
   float2 *d_wh = nullptr;
 };
 
-// kernels.cu
+// pipeline.cu
 int sar_launch_pipeline(sar_plan *p, const void *d_data, void *d_image, cudaStream_t s,
                         int stop_stage /*0 = full*/, int complex_out, cudaEvent_t *ev /*6 or null*/);
 int sar_launch_stolt_index(sar_plan *p, const int32_t *d_cols, int n, int32_t *d_i0, float *d_tau,
