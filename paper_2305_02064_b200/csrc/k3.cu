@@ -76,12 +76,25 @@ __global__ void __launch_bounds__(K3C_NT, 4) k3_class(const SarDeviceView v) {
   // 1. member columns (streaming loads, 16 B per thread when n_k is even)
   const float2 *wf = v.w0 + (size_t)f * ncol * (size_t)nk;
   if ((nk & 1) == 0) {
-    const int h2 = nk / 2;
-    for (int e = tid; e < CC * h2; e += K3C_NT) {
-      const int sl = e / h2, i = e - sl * h2;
-      if (colof[sl] >= 0)
-        reinterpret_cast<float4 *>(fin + sl * nk)[i] =
-            __ldcs(reinterpret_cast<const float4 *>(wf + (size_t)colof[sl] * nk) + i);
+    // 8 independent 16-byte loads in flight per thread before any store
+    constexpr int U = 8;
+    const int h2 = nk / 2, tot = CC * h2;
+    for (int base = tid; base < tot; base += U * K3C_NT) {
+      float4 t[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int e = base + u * K3C_NT;
+        const int sl = e / h2, i = e - sl * h2;
+        t[u] = (e < tot && colof[sl] >= 0)
+                   ? __ldcs(reinterpret_cast<const float4 *>(wf + (size_t)colof[sl] * nk) + i)
+                   : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int e = base + u * K3C_NT;
+        const int sl = e / h2, i = e - sl * h2;
+        if (e < tot) reinterpret_cast<float4 *>(fin + sl * nk)[i] = t[u];
+      }
     }
   } else {
     for (int e = tid; e < CC * nk; e += K3C_NT) {
