@@ -58,6 +58,9 @@ enum sar_flags {
                                     P:394): step 3 becomes the back-propagation of every
                                     filtered column to each plane of sar_image_desc.z_planes summed
                                     over k (no Stolt), the image is [F][nz planes][ny][nx] */,
+  SAR_REPORT_PEAK = 1u << 5,     /* every call also records max |image| of each frame on the device
+                                    (sar_plan_peaks); the normalisation of the eps_inf metric and of
+                                    display (reading R11) without another pass over the image */
   SAR_GRID_NUFFT = 1u << 4       /* NUFFT placement (reading R19; FGG-NUFFT of P:239-242): steps 1-2
                                     become a type-1 non-uniform transform of the compensated samples
                                     from their TRUE (x', y') positions (fast Gaussian gridding,
@@ -169,6 +172,12 @@ int sar_plan_workspace_bytes(const sar_plan *p, size_t *bytes);
  * receives the number of calls summed (at most 1024 since the last reset). */
 int sar_plan_profile_read(sar_plan *p, float ms_out[5], int32_t *n_calls);
 int sar_plan_profile_reset(sar_plan *p);
+
+/* SAR_REPORT_PEAK plans: max |image voxel| of each frame of the last
+ * sar_reconstruct call (after the 1/(nx ny nz) scaling).  Synchronises the
+ * plan's last stream; h_peaks: host float[F].  Errors: INVALID_ARG (no flag,
+ * NULL), CUDA. */
+int sar_plan_peaks(sar_plan *p, float *h_peaks);
 
 /* Number of kernel launches one sar_reconstruct call enqueues (5; 0 if F = 0). */
 int sar_plan_launches_per_call(const sar_plan *p, int32_t *n);

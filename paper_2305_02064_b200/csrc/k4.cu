@@ -14,6 +14,14 @@
 namespace sark {
 namespace {
 
+// SAR_REPORT_PEAK: warp max of the magnitudes a thread wrote, one atomic per
+// warp (non-negative floats order like their bit patterns)
+__device__ __forceinline__ void report_peak(const SarDeviceView &v, int f, float pk) {
+  if (!v.peak) return;
+  const unsigned b = __reduce_max_sync(0xffffffffu, __float_as_uint(pk));
+  if ((threadIdx.x & 31) == 0 && b) atomicMax(v.peak + f, b);
+}
+
 // Warp-specialised persistent K4b (nx <= 512, n_z even): [nx][16 z] tiles of
 // W1 row y stream through an S-stage TMA ring; the consumers run the inverse
 // x-FFT (pass 2 mapped so that one warp owns 32 consecutive x of one z) and
@@ -84,6 +92,7 @@ __global__ void __launch_bounds__(sarfft2::nt_fft<NX, KC>() + 32)
     if (iy < 0) iy += v.ny;
     OT *outp = reinterpret_cast<OT *>(img) + ((size_t)f * nz * v.ny + iy) * NX;
     const float2 *stage = ring + (size_t)st * NX * KC;
+    float pk = 0.f;
     sarfft2::fft<NX, KC, KC + 1, NTC, +1, 1, true>(
         work, tw, tid, [&](int c, int m) { return stage[m * KC + c]; },
         [&] {
@@ -95,13 +104,16 @@ __global__ void __launch_bounds__(sarfft2::nt_fft<NX, KC>() + 32)
             int m = z + v.zroll;
             if (m >= nz) m -= nz;
             const int ix = (a - rx) & (NX - 1);
+            const float mag = sqrtf(fmaf(o.x, o.x, o.y * o.y)) * sc;
+            pk = fmaxf(pk, mag);
             if constexpr (CPLX) {
               __stcs(reinterpret_cast<float2 *>(outp) + (size_t)m * zstride + ix, make_float2(o.x * sc, o.y * sc));
             } else {
-              __stcs(reinterpret_cast<float *>(outp) + (size_t)m * zstride + ix, sqrtf(fmaf(o.x, o.x, o.y * o.y)) * sc);
+              __stcs(reinterpret_cast<float *>(outp) + (size_t)m * zstride + ix, mag);
             }
           }
         });
+    report_peak(v, f, pk);
   }
 }
 
@@ -137,6 +149,7 @@ __global__ void __launch_bounds__(nt_for(NX), minb_for(NX))
   if (iy >= v.ny) iy -= v.ny;
   const int rx = ((v.roll_x % NX) + NX) % NX;
   const float sc = v.img_scale;
+  float pk = 0.f;
 #pragma unroll
   for (int e = 0; e < E; ++e) {
     const int item = tid + e * NT;
@@ -149,12 +162,15 @@ __global__ void __launch_bounds__(nt_for(NX), minb_for(NX))
     const int xs = (ix + rx) & (NX - 1);
     const float2 o = tile[xs * LD + zz];
     const size_t off = ((size_t)(f * nz + m) * v.ny + iy) * NX + ix;
+    const float mag = sqrtf(fmaf(o.x, o.x, o.y * o.y)) * sc;
+    pk = fmaxf(pk, mag);
     if constexpr (CPLX) {
       reinterpret_cast<float2 *>(img)[off] = make_float2(o.x * sc, o.y * sc);
     } else {
-      reinterpret_cast<float *>(img)[off] = sqrtf(fmaf(o.x, o.x, o.y * o.y)) * sc;
+      reinterpret_cast<float *>(img)[off] = mag;
     }
   }
+  report_peak(v, f, pk);
 }
 
 // Persistent, TMA-pipelined K4b (n_z even, 32 <= nx <= 512).  Item = (frame,
@@ -204,17 +220,20 @@ __global__ void __launch_bounds__(ntp_for(NX), ctas_for(NX))
     sartma::mbar_wait(&full[st], (it >> 1) & 1);
     float2 *tile = smk + (size_t)st * NX * KC;
     sarfft::tile_fft<NX, KC, KC, NT, +1>(tile, tw, tid);
+    float pk = 0.f;
     // transpose into output rows: ob[zz][ix] with ix = (a - r_x) mod nx
 #pragma unroll
     for (int i = tid; i < NX * KC; i += NT) {
       const int a = i / KC, zz = i % KC;
       const float2 o = tile[i];
       const int ix = (a - rx) & (NX - 1);
+      const float p = fmaf(o.x, o.x, o.y * o.y);
+      const float mag = p > 0.f ? p * rsqrtf(p) * sc : 0.f;   // |o| (rsqrt: 2 ulp)
+      pk = fmaxf(pk, mag);
       if constexpr (CPLX) {
         ob[zz * (NX + 1) + ix] = make_float2(o.x * sc, o.y * sc);
       } else {
-        const float p = fmaf(o.x, o.x, o.y * o.y);
-        ob[zz * (NX + 1) + ix] = p > 0.f ? p * rsqrtf(p) * sc : 0.f;   // |o| (rsqrt: 2 ulp)
+        ob[zz * (NX + 1) + ix] = mag;
       }
     }
     sartma::fence_proxy_async();
@@ -234,6 +253,10 @@ __global__ void __launch_bounds__(ntp_for(NX), ctas_for(NX))
         if (m >= nz) m -= nz;
         outp[m * zstride + ix] = ob[zz * (NX + 1) + ix];
       }
+    }
+    {
+      const int fpk = (item / nzc) / v.ny;
+      report_peak(v, fpk, pk);
     }
     __syncthreads();  // ob free
   }

@@ -65,6 +65,7 @@ int sar_launch_pipeline(sar_plan *p, const void *d_data, void *d_image, cudaStre
     SAR_CHECK(launch_mid<+1>(v.w1, v.tw_y, v.F, v.ny, v.nx, v.nz, s, p->tma_mid1 ? &p->tm_w1_mid : nullptr,
                              p->num_sms));
     if (ev) SAR_CHECK(cudaEventRecord(ev[4], s));
+    if (v.peak) SAR_CHECK(cudaMemsetAsync(v.peak, 0, (size_t)v.F * sizeof(unsigned), s));
     SAR_CHECK(launch_k4b(v, d_image, complex_out != 0, s, p->tma_rows1 ? &p->tm_w1_rows : nullptr, p->num_sms));
     if (ev) SAR_CHECK(cudaEventRecord(ev[5], s));
     return SAR_OK;
@@ -98,6 +99,7 @@ int sar_launch_pipeline(sar_plan *p, const void *d_data, void *d_image, cudaStre
                              p->num_sms));
     if (ev) SAR_CHECK(cudaEventRecord(ev[4], s));
   }
+  if (v.peak) SAR_CHECK(cudaMemsetAsync(v.peak, 0, (size_t)v.F * sizeof(unsigned), s));
   SAR_CHECK(launch_k4b(v, d_image, complex_out != 0, s, p->tma_rows1 ? &p->tm_w1_rows : nullptr, p->num_sms));
   if (ev) SAR_CHECK(cudaEventRecord(ev[5], s));
   return SAR_OK;

@@ -59,6 +59,7 @@ void free_plan(sar_plan *p) {
   cudaFree(p->d_items);
   cudaFree(p->d_cnt);
   cudaFree(p->d_wh);
+  cudaFree(p->d_peak);
   delete p;
 }
 
@@ -565,6 +566,14 @@ int sar_plan_create(sar_plan **out, const sar_geom_desc *g, const sar_image_desc
     for (float b : T.bpair) bmax = std::max(bmax, fabsf(b));
     v.k1_step_ok = (T.dk * ((double)amax + (double)bmax) <= 0.25) ? 1 : 0;
   }
+  if ((flags & SAR_REPORT_PEAK) && F > 0) {
+    if (cudaMalloc(&p->d_peak, (size_t)F * sizeof(unsigned)) != cudaSuccess) {
+      cudaGetLastError();
+      free_plan(p);
+      return fail(SAR_ERR_OOM, "peak buffer allocation failed");
+    }
+  }
+  v.peak = p->d_peak;
   v.w0 = p->d_w0;
   v.wh = p->d_wh;
   v.dbg = getenv("SAR_DBG") ? atoi(getenv("SAR_DBG")) : 0;
@@ -634,6 +643,16 @@ int sar_plan_destroy(sar_plan *p) {
 int sar_plan_get_axes(const sar_plan *p, double out[6]) {
   if (!p || !out) return fail(SAR_ERR_INVALID_ARG, "NULL argument");
   memcpy(out, p->axes, sizeof(p->axes));
+  return SAR_OK;
+}
+
+int sar_plan_peaks(sar_plan *p, float *h_peaks) {
+  if (!p || !h_peaks) return fail(SAR_ERR_INVALID_ARG, "NULL argument");
+  if (!p->d_peak) return fail(SAR_ERR_INVALID_ARG, "plan was created without SAR_REPORT_PEAK");
+  DeviceGuard g(p->device);
+  cudaError_t e = cudaStreamSynchronize(p->last_stream);
+  if (e == cudaSuccess) e = cudaMemcpy(h_peaks, p->d_peak, (size_t)p->F * sizeof(float), cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return cuda_fail(e, "peaks");
   return SAR_OK;
 }
 

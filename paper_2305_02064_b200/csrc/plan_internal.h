@@ -61,6 +61,7 @@ struct SarDeviceView {
   int k1_step_ok;       // max |dk * beta| <= 0.25: K1 may use the Taylor step phasor
   int dbg;              // ablation switches (env SAR_DBG; 0 in production)
   float img_scale;      // 1/(nx ny nz)
+  unsigned *peak;       // [F] max |voxel| bits per frame (SAR_REPORT_PEAK) or nullptr
   float2 *w0;           // [F][ny][nx][nk]  planar lattice -> spectrum
   float2 *w1;           // [F][ny][nx][nz]  Stolt output -> partial inverse
 };
@@ -102,6 +103,7 @@ struct sar_plan {
   int *d_cnt = nullptr;
   // NUFFT mode tables and the half-transformed fine grid
   void *d_nu = nullptr;
+  unsigned *d_peak = nullptr;   // SAR_REPORT_PEAK
   float2 *d_wh = nullptr;
 };
 

@@ -21,6 +21,7 @@ SAR_OUTPUT_COMPLEX = 2
 SAR_PROFILE_STAGES = 4
 SAR_IMAGE_2D = 8
 SAR_GRID_NUFFT = 16
+SAR_REPORT_PEAK = 32
 STAGE_NAMES = ("K1 correct+x-FFT", "K2 y-FFT", "K3 filter+Stolt+z-IFFT", "K4a y-IFFT", "K4b x-IFFT+|.|")
 
 
@@ -77,6 +78,7 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         "sar_plan_profile_read": (C.c_int, [vp, C.POINTER(C.c_float), C.POINTER(i32)]),
         "sar_plan_profile_reset": (C.c_int, [vp]),
         "sar_plan_launches_per_call": (C.c_int, [vp, C.POINTER(i32)]),
+        "sar_plan_peaks": (C.c_int, [vp, C.POINTER(C.c_float)]),
         "sar_debug_stage": (C.c_int, [vp, i32, vp, vp, vp]),
         "sar_debug_node_offsets": (C.c_int, [vp, C.POINTER(i32), C.POINTER(i32), C.POINTER(i32), C.POINTER(i32)]),
         "sar_debug_stolt_index": (C.c_int, [vp, vp, i32, vp, vp, vp]),
@@ -96,7 +98,7 @@ def exported_symbols():
     """Names of the C entry points this binding expects (the header's API)."""
     return ["sar_plan_describe", "sar_plan_create", "sar_reconstruct", "sar_reconstruct_host", "sar_plan_destroy",
             "sar_plan_get_axes", "sar_plan_workspace_bytes", "sar_plan_profile_read",
-            "sar_plan_profile_reset", "sar_plan_launches_per_call", "sar_debug_stage",
+            "sar_plan_profile_reset", "sar_plan_launches_per_call", "sar_plan_peaks", "sar_debug_stage",
             "sar_debug_node_offsets", "sar_debug_stolt_index", "sar_status_string",
             "sar_last_error", "sar_version"]
 
@@ -276,6 +278,12 @@ class Plan:
         n = C.c_int32()
         _check(self._lib.sar_plan_launches_per_call(self._h, C.byref(n)))
         return n.value
+
+    def peaks(self):
+        """max |image| per frame of the last call (plans made with SAR_REPORT_PEAK)."""
+        out = (C.c_float * max(self.n_frames, 1))()
+        _check(self._lib.sar_plan_peaks(self._h, out))
+        return np.array(out[:self.n_frames], dtype=np.float32)
 
     def profile_reset(self):
         _check(self._lib.sar_plan_profile_reset(self._h))

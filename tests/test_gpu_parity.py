@@ -377,3 +377,20 @@ def test_nufft_equals_raster_without_inplane_jitter():
         b = p1.reconstruct(d).cpu().numpy()
     e2, _ = errs(b, a.astype(np.float64))
     assert e2 <= 2e-5
+
+
+@pytest.mark.parametrize("name,flags", [("small", 0), ("realtime", 0), ("tiny", sar.SAR_OUTPUT_COMPLEX)])
+def test_report_peak_equals_image_max(name, flags):
+    """SAR_REPORT_PEAK: the per-frame peak recorded by the K4b epilogue is the
+    maximum of the frame's magnitude image (the same fp32 values)."""
+    sc = scenes.make_scene(name)
+    d, _ = _data(sc, gpu_gen=name == "realtime")
+    with sar.Plan.from_scene(sc, flags=flags | sar.SAR_REPORT_PEAK) as plan:
+        img = plan.reconstruct(d)
+        pk = plan.peaks()
+    mag = img.abs() if img.is_complex() else img
+    want = mag.reshape(sc.n_frames, -1).amax(dim=1).cpu().numpy()
+    assert np.allclose(pk, want, rtol=2e-7, atol=0), (pk[:4], want[:4])
+    with sar.Plan.from_scene(sc) as plan:
+        with pytest.raises(sar.SarError):
+            plan.peaks()
