@@ -294,43 +294,67 @@ __global__ void __launch_bounds__(K3P_NG * K3P_G + 32, 1) k3_pp(const SarDeviceV
   const int ncol = v.nx * v.ny;
   const int nitems = nitems_f * v.F;
   if (tid >= K3P_NG * K3P_G) {
-    if (tid == K3P_NG * K3P_G) {  // producer
-      const int hx = v.nx / 2 + 1, hy = v.ny / 2 + 1;
-      const int nclass = hx * hy;
-      unsigned n = 0;
-      for (int item = blockIdx.x; item < nitems; item += gridDim.x, ++n) {
-        const int st = n % K3P_S;
-        if (n >= K3P_S) sartma::mbar_wait(&empty[st], ((n / K3P_S) - 1) & 1);
-        unsigned char *sb = ring + st * stage_bytes;
-        K3Hdr<CL> &h = *reinterpret_cast<K3Hdr<CL> *>(sb);
-        float2 *fin = reinterpret_cast<float2 *>(sb + hdr_bytes);
-        const int f = item / nitems_f;
-        const int q0 = (item - f * nitems_f) * CL;
-        int cnt = 0;
-        for (int cl = 0; cl < CL; ++cl) {
-          const int q = q0 + cl;
-          h.nmem[cl] = 0;
-          h.kr2[cl] = 0.0;
-          h.jlo[cl] = 0;
-          h.jhi[cl] = -1;
-          if (q >= nclass) continue;
-          const SarClass &c = v.cls[q];
-          h.kr2[cl] = c.kr2;
-          h.jlo[cl] = c.jlo;
-          h.jhi[cl] = c.jhi;
-          for (int m = 0; m < c.nmem; ++m) {
-            h.mslot[cl][h.nmem[cl]++] = cnt;
-            h.clof[cnt] = cl;
-            h.colof[cnt++] = c.col[m];
-          }
+    // producer warp: lanes < CL read their class entry one item ahead,
+    // write the stage header, and every member column is issued by its own
+    // lane (cp.async.bulk, one mbarrier transaction per item)
+    const int lane = tid & 31;
+    const int hx = v.nx / 2 + 1, hy = v.ny / 2 + 1;
+    const int nclass = hx * hy;
+    auto fetch = [&](int item, SarClass &c) {
+      const int f = item / nitems_f;
+      const int q = (item - f * nitems_f) * CL + lane;
+      if (item < nitems && lane < CL && q < nclass) {
+        c = v.cls[q];
+      } else {
+        c.kr2 = 0.0;
+        c.jlo = 0;
+        c.jhi = -1;
+        c.nmem = 0;
+      }
+    };
+    SarClass cur, nxt;
+    fetch(blockIdx.x, cur);
+    unsigned n = 0;
+    for (int item = blockIdx.x; item < nitems; item += gridDim.x, ++n) {
+      fetch(item + gridDim.x, nxt);   // in flight while this item is issued
+      const int st = n % K3P_S;
+      if (lane == 0 && n >= K3P_S) sartma::mbar_wait(&empty[st], ((n / K3P_S) - 1) & 1);
+      __syncwarp();
+      unsigned char *sb = ring + st * stage_bytes;
+      K3Hdr<CL> &h = *reinterpret_cast<K3Hdr<CL> *>(sb);
+      float2 *fin = reinterpret_cast<float2 *>(sb + hdr_bytes);
+      const int f = item / nitems_f;
+      // slot base of this lane's class = members of the classes before it
+      const int mine = lane < CL ? cur.nmem : 0;
+      int base = mine;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, base, o);
+        if (lane >= o) base += y;
+      }
+      const int cnt = __shfl_sync(0xffffffffu, base, CL - 1);
+      base -= mine;
+      if (lane < CL) {
+        h.kr2[lane] = cur.kr2;
+        h.jlo[lane] = cur.jlo;
+        h.jhi[lane] = cur.jhi;
+        h.nmem[lane] = cur.nmem;
+        for (int m = 0; m < cur.nmem; ++m) {
+          h.mslot[lane][m] = base + m;
+          h.clof[base + m] = lane;
+          h.colof[base + m] = cur.col[m];
         }
+      }
+      if (lane == 0) {
         h.nused = cnt;
         h.f = f;
-        const float2 *wf = v.w0 + (size_t)f * ncol * (size_t)nk;
-        sartma::mbar_arrive_expect_tx(&full[st], (uint32_t)cnt * (uint32_t)nk * 8u);
-        for (int sl = 0; sl < cnt; ++sl)
-          sartma::bulk_g2s(fin + sl * nk, wf + (size_t)h.colof[sl] * nk, (uint32_t)nk * 8u, &full[st]);
       }
+      __syncwarp();
+      if (lane == 0) sartma::mbar_arrive_expect_tx(&full[st], (uint32_t)cnt * (uint32_t)nk * 8u);
+      __syncwarp();
+      const float2 *wf = v.w0 + (size_t)f * ncol * (size_t)nk;
+      if (lane < cnt) sartma::bulk_g2s(fin + lane * nk, wf + (size_t)h.colof[lane] * nk, (uint32_t)nk * 8u, &full[st]);
+      cur = nxt;
     }
     return;
   }
