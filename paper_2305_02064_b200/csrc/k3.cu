@@ -165,7 +165,7 @@ __global__ void __launch_bounds__(K3C_NT, 4) k3_class(const SarDeviceView v) {
 
 constexpr int K3P_G = 256;   // threads per consumer group
 constexpr int K3P_NG = 2;    // consumer groups (alternate items)
-constexpr int K3P_S = 3;     // ring stages
+constexpr int K3P_S = 4;     // ring stages
 template <int NZ, int CL>
 size_t k3pp_smem(int nk) {
   const size_t hdr = (sizeof(K3Hdr<CL>) + 15) & ~(size_t)15;
