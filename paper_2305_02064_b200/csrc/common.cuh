@@ -25,10 +25,6 @@ constexpr int nt_for(int n) { return n <= 32 ? 32 : (n < 512 ? n : 512); }
 // resident CTAs requested per SM: 1024 threads' worth (caps registers at 64 per
 // thread) except for the 1024-point tiles, whose 32 elements per thread need more
 constexpr int minb_for(int n) { return n >= 1024 ? 1 : 1024 / nt_for(n); }
-// persistent tile kernels: 2N threads (8 elements each of a 16-column tile),
-// capped at 1024, and as many CTAs per SM as make 1024 threads
-constexpr int ntp_for(int n) { return 2 * n < 64 ? 64 : (2 * n > 1024 ? 1024 : 2 * n); }
-constexpr int ctas_for(int n) { return 1024 / ntp_for(n); }
 
 constexpr int K1_STAGES = 4;
 constexpr int K1_BOX_BYTES = 32768;

@@ -50,66 +50,6 @@ __global__ void __launch_bounds__(nt_for(N), minb_for(N))
   }
 }
 
-// Persistent, TMA-pipelined variant of k_fft_mid (used when `inner` is even,
-// i.e. the rows are 16-byte aligned).  One CTA per SM loops over work items
-// (chunk, column a, frame); the [N][16] tile of item i+1 is in flight
-// (cp.async.bulk.tensor, mbarrier completion) while item i is transformed,
-// and finished tiles go back with TMA stores, so the SM's load queue never
-// drains between tiles.  Box = {16 inner elements, 1 column, <=256 rows}.
-template <int N, int DIR>
-__global__ void __launch_bounds__(ntp_for(N), ctas_for(N))
-    k_fft_mid_tma(const __grid_constant__ CUtensorMap tm, const float2 *__restrict__ twg, int nx, int nchunk,
-                  int nitems) {
-  constexpr int NT = ntp_for(N);
-  constexpr int ROWS = N < 256 ? N : 256;
-  constexpr int NBOX = N / ROWS;
-  constexpr uint32_t TILE_BYTES = N * KC * sizeof(float2);
-  extern __shared__ __align__(128) float2 smt[];  // [2][N][16]
-  __shared__ __align__(8) uint64_t full[2];
-  __shared__ float2 tw[N];
-  const int tid = threadIdx.x;
-  for (int i = tid; i < N; i += NT) tw[i] = twg[i];
-  if (tid == 0) {
-    sartma::mbar_init(&full[0], 1);
-    sartma::mbar_init(&full[1], 1);
-    sartma::fence_barrier_init();
-  }
-  __syncthreads();
-  auto issue = [&](int item, int st) {
-    const int chunk = item % nchunk, rest = item / nchunk;
-    const int a = rest % nx, f = rest / nx;
-    sartma::mbar_arrive_expect_tx(&full[st], TILE_BYTES);
-#pragma unroll
-    for (int bx = 0; bx < NBOX; ++bx)
-      sartma::tma_load_3d(smt + (size_t)st * N * KC + bx * ROWS * KC, &tm, chunk * KC, a, f * N + bx * ROWS,
-                          &full[st]);
-  };
-  int item = blockIdx.x;
-  if (tid == 0 && item < nitems) issue(item, 0);
-  for (int it = 0; item < nitems; ++it, item += gridDim.x) {
-    const int st = it & 1;
-    const int next = item + gridDim.x;
-    if (tid == 0 && next < nitems) {
-      sartma::bulk_wait_read0();  // the store of stage st^1 has left shared memory
-      issue(next, st ^ 1);
-    }
-    sartma::mbar_wait(&full[st], (it >> 1) & 1);
-    float2 *tile = smt + (size_t)st * N * KC;
-    sarfft::tile_fft<N, KC, KC, NT, DIR>(tile, tw, tid);
-    sartma::fence_proxy_async();
-    __syncthreads();
-    if (tid == 0) {
-      const int chunk = item % nchunk, rest = item / nchunk;
-      const int a = rest % nx, f = rest / nx;
-#pragma unroll
-      for (int bx = 0; bx < NBOX; ++bx)
-        sartma::tma_store_3d(&tm, chunk * KC, a, f * N + bx * ROWS, tile + bx * ROWS * KC);
-      sartma::bulk_commit();
-    }
-  }
-  if (tid == 0) sartma::bulk_wait0();
-}
-
 // Warp-specialised persistent mid-axis FFT (K2 / K4a, ny <= 512, `inner`
 // even).  A producer warp streams [N][16] tiles (3-D TMA boxes {16 inner, 1
 // column, <=256 rows}) into an S-stage mbarrier ring; NTC consumer threads run
@@ -195,7 +135,7 @@ __global__ void __launch_bounds__(sarfft2::nt_fft<N, KC>() + 32)
 template <int DIR>
 cudaError_t launch_mid(float2 *data, const float2 *tw, int F, int ny, int nx, int inner, cudaStream_t s,
                        const CUtensorMap *tm, int num_sms) {
-  if (tm && ny <= 512 && !getenv("SAR_MID_OLD")) {
+  if (tm && ny <= 512) {
     const int nchunk = (inner + KC - 1) / KC;
     const int nitems = nchunk * nx * F;
     switch (ny) {
@@ -213,27 +153,6 @@ cudaError_t launch_mid(float2 *data, const float2 *tw, int F, int ny, int nx, in
     return cudaGetLastError();                                                                     \
   }
       X(2) X(4) X(8) X(16) X(32) X(64) X(128) X(256) X(512)
-#undef X
-    }
-    return cudaErrorInvalidValue;
-  }
-  if (tm && ny <= 512) {
-    const int nchunk = (inner + KC - 1) / KC;
-    const int nitems = nchunk * nx * F;
-    const size_t smem = 2 * (size_t)ny * KC * sizeof(float2);
-    switch (ny) {
-#define X(N)                                                                                       \
-  case N: {                                                                                        \
-    auto kern = k_fft_mid_tma<N, DIR>;                                                             \
-    if (smem > 40 * 1024) {                                                                        \
-      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
-      if (e != cudaSuccess) return e;                                                              \
-    }                                                                                              \
-    const int maxg = num_sms * ctas_for(N);                                                        \
-    kern<<<nitems < maxg ? nitems : maxg, ntp_for(N), smem, s>>>(*tm, tw, nx, nchunk, nitems);     \
-    return cudaGetLastError();                                                                     \
-  }
-      SAR_SIZES(X)
 #undef X
     }
     return cudaErrorInvalidValue;

@@ -173,95 +173,6 @@ __global__ void __launch_bounds__(nt_for(NX), minb_for(NX))
   report_peak(v, f, pk);
 }
 
-// Persistent, TMA-pipelined K4b (n_z even, 32 <= nx <= 512).  Item = (frame,
-// image row y, 16-wide z chunk): the [nx][16] tile of item i+1 is in flight
-// (cp.async.bulk.tensor + mbarrier) while item i is inverse-transformed along
-// x; the magnitudes (or scaled complex values) are transposed through a padded
-// [16][nx+1] buffer with the x roll applied, so every image row segment is
-// written with coalesced stores.
-template <int NX, bool CPLX>
-__global__ void __launch_bounds__(ntp_for(NX), ctas_for(NX))
-    k4_xifft_mag_tma(const SarDeviceView v, const __grid_constant__ CUtensorMap tm, void *__restrict__ img,
-                     int nzc, int nitems) {
-  constexpr int NT = ntp_for(NX);
-  constexpr int ROWS = NX < 256 ? NX : 256;
-  constexpr int NBOX = NX / ROWS;
-  constexpr uint32_t TILE_BYTES = NX * KC * sizeof(float2);
-  using OT = typename std::conditional<CPLX, float2, float>::type;
-  extern __shared__ __align__(128) float2 smk[];    // [2][NX][16] tiles, then [16][NX+1] output rows
-  OT *ob = reinterpret_cast<OT *>(smk + 2 * (size_t)NX * KC);
-  __shared__ __align__(8) uint64_t full[2];
-  __shared__ float2 tw[NX];
-  const int tid = threadIdx.x;
-  const int nz = v.nz;
-  for (int i = tid; i < NX; i += NT) tw[i] = v.tw_x[i];
-  if (tid == 0) {
-    sartma::mbar_init(&full[0], 1);
-    sartma::mbar_init(&full[1], 1);
-    sartma::fence_barrier_init();
-  }
-  __syncthreads();
-  auto issue = [&](int item, int st) {
-    const int zc = item % nzc, fy = item / nzc;  // fy = f*ny + y
-    sartma::mbar_arrive_expect_tx(&full[st], TILE_BYTES);
-#pragma unroll
-    for (int bx = 0; bx < NBOX; ++bx)
-      sartma::tma_load_3d(smk + (size_t)st * NX * KC + bx * ROWS * KC, &tm, zc * KC, bx * ROWS, fy, &full[st]);
-  };
-  const int rx = ((v.roll_x % NX) + NX) % NX;
-  const int ry = ((v.roll_y % v.ny) + v.ny) % v.ny;
-  const float sc = v.img_scale;
-  int item = blockIdx.x;
-  if (tid == 0 && item < nitems) issue(item, 0);
-  for (int it = 0; item < nitems; ++it, item += gridDim.x) {
-    const int st = it & 1;
-    const int next = item + gridDim.x;
-    if (tid == 0 && next < nitems) issue(next, st ^ 1);
-    sartma::mbar_wait(&full[st], (it >> 1) & 1);
-    float2 *tile = smk + (size_t)st * NX * KC;
-    sarfft::tile_fft<NX, KC, KC, NT, +1>(tile, tw, tid);
-    float pk = 0.f;
-    // transpose into output rows: ob[zz][ix] with ix = (a - r_x) mod nx
-#pragma unroll
-    for (int i = tid; i < NX * KC; i += NT) {
-      const int a = i / KC, zz = i % KC;
-      const float2 o = tile[i];
-      const int ix = (a - rx) & (NX - 1);
-      const float p = fmaf(o.x, o.x, o.y * o.y);
-      const float mag = p > 0.f ? p * rsqrtf(p) * sc : 0.f;   // |o| (rsqrt: 2 ulp)
-      pk = fmaxf(pk, mag);
-      if constexpr (CPLX) {
-        ob[zz * (NX + 1) + ix] = make_float2(o.x * sc, o.y * sc);
-      } else {
-        ob[zz * (NX + 1) + ix] = mag;
-      }
-    }
-    sartma::fence_proxy_async();
-    __syncthreads();  // tile st is free (next-next load may overwrite it), ob complete
-    const int zc = item % nzc, fy = item / nzc;
-    const int f = fy / v.ny, y = fy - f * v.ny;
-    int iy = y - ry;
-    if (iy < 0) iy += v.ny;
-    OT *outp = reinterpret_cast<OT *>(img) + ((size_t)f * nz * v.ny + iy) * NX;
-    const size_t zstride = (size_t)v.ny * NX;
-#pragma unroll
-    for (int i = tid; i < NX * KC; i += NT) {
-      const int zz = i / NX, ix = i % NX;
-      const int z = zc * KC + zz;
-      if (z < nz) {
-        int m = z + v.zroll;
-        if (m >= nz) m -= nz;
-        outp[m * zstride + ix] = ob[zz * (NX + 1) + ix];
-      }
-    }
-    {
-      const int fpk = (item / nzc) / v.ny;
-      report_peak(v, fpk, pk);
-    }
-    __syncthreads();  // ob free
-  }
-}
-
 template <typename K>
 cudaError_t launch_img(K kernel, dim3 grid, int nt, size_t smem, cudaStream_t s, const SarDeviceView &v,
                        void *img) {
@@ -278,7 +189,7 @@ cudaError_t launch_img(K kernel, dim3 grid, int nt, size_t smem, cudaStream_t s,
 
 cudaError_t launch_k4b(const SarDeviceView &v, void *img, bool cplx, cudaStream_t s, const CUtensorMap *tm,
                        int num_sms) {
-  if (tm && v.nx <= 512 && !getenv("SAR_K4B_OLD")) {
+  if (tm && v.nx <= 512) {
     const int nzc = (v.nz + KC - 1) / KC;
     const int nitems = nzc * v.ny * v.F;
     switch (v.nx) {
@@ -295,25 +206,6 @@ cudaError_t launch_k4b(const SarDeviceView &v, void *img, bool cplx, cudaStream_
     return cudaGetLastError();                                                                         \
   }
       X(2) X(4) X(8) X(16) X(32) X(64) X(128) X(256) X(512)
-#undef X
-    }
-  }
-  if (tm && v.nx >= 32 && v.nx <= 512) {
-    const int nzc = (v.nz + KC - 1) / KC;
-    const int nitems = nzc * v.ny * v.F;
-    const size_t smem = 2 * (size_t)v.nx * KC * sizeof(float2) + (size_t)KC * (v.nx + 1) * (cplx ? 8 : 4);
-    switch (v.nx) {
-#define X(N)                                                                                           \
-  case N: {                                                                                            \
-    auto kern = cplx ? k4_xifft_mag_tma<N, true> : k4_xifft_mag_tma<N, false>;                        \
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
-    if (e != cudaSuccess) return e;                                                                    \
-    const int cps = ctas_for(N) * smem <= 200 * 1024 ? ctas_for(N) : 1;                               \
-    const int maxg = num_sms * cps;                                                                    \
-    kern<<<nitems < maxg ? nitems : maxg, ntp_for(N), smem, s>>>(v, *tm, img, nzc, nitems);            \
-    return cudaGetLastError();                                                                         \
-  }
-      X(32) X(64) X(128) X(256) X(512)
 #undef X
     }
   }
