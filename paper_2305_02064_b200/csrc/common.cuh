@@ -31,7 +31,7 @@ constexpr int K1_BOX_BYTES = 32768;
 constexpr int K1_NT = 512;   // consumer threads (+1 producer warp)
 constexpr int K1_KT = 4;  // consecutive k per thread
 
-constexpr int k1c_for(int nx) { return nx >= 512 ? 16 : (nx == 256 ? 32 : 64); }
+constexpr int k1c_for(int nx) { return nx >= 256 ? 16 : 64; }
 
 // acc += a * b (complex), two paired-fp32 FMAs
 __device__ __forceinline__ float2 cmac2(float2 acc, float2 a, float2 b) {
