@@ -394,3 +394,34 @@ def test_report_peak_equals_image_max(name, flags):
     with sar.Plan.from_scene(sc) as plan:
         with pytest.raises(sar.SarError):
             plan.peaks()
+
+
+NUFFT_EDGE = [
+    dict(npx=20, npy=13, nx=32, ny=32, nk=20, nz=64, dz=4e-3, z_ref=0.2),           # ragged raster, odd-ish k
+    dict(npx=33, npy=7, nx=64, ny=16, nk=37, nz=16, dz=5e-3, z_ref=0.15),          # odd n_k, wide strip
+    dict(npx=24, npy=20, nx=32, ny=32, nk=32, nz=32, dz=5e-3, z_ref=0.2, n_frames=3, n_tx=3),  # frames, wrap
+]
+
+
+@pytest.mark.parametrize("kw", NUFFT_EDGE, ids=lambda kw: "x".join(str(kw[k]) for k in ("npx", "npy", "nx", "ny", "nk")))
+def test_nufft_edge_cases(kw):
+    from oracle import nufft
+    sc = _custom(**kw)
+    d, s = _data(sc, gpu_gen=False)
+    want, _ = nufft.reconstruct_nufft(s, sc)
+    with sar.Plan.from_scene(sc, flags=sar.SAR_GRID_NUFFT) as plan:
+        got = plan.reconstruct(d).cpu().numpy()
+    e2, einf = errs(got, want)
+    assert e2 <= E2_BAR and einf <= EINF_BAR, (sc.name, e2, einf)
+
+
+@pytest.mark.parametrize("kw,planes", [(NUFFT_EDGE[0], [0.2]), (NUFFT_EDGE[1], [0.14, 0.15, 0.16]),
+                                       (NUFFT_EDGE[2], [0.19, 0.21])])
+def test_plane2d_edge_cases(kw, planes):
+    sc = _custom(**kw)
+    d, s = _data(sc, gpu_gen=False)
+    want, _ = oracle.reconstruct_planes(s, sc, planes)
+    with sar.Plan.from_scene(sc, z_planes=planes) as plan:
+        got = plan.reconstruct(d).cpu().numpy()
+    e2, einf = errs(got, want)
+    assert e2 <= E2_BAR and einf <= EINF_BAR, (sc.name, e2, einf)
