@@ -153,6 +153,7 @@ __device__ __forceinline__ void filter_table(const SarDeviceView &v, float2 *hta
 // The k, k_z and twiddle tables live in shared memory.
 template <int CL>
 struct K3Hdr {
+  double rr;               // R_ref(f) / (2 pi), read by the producer
   int f, nused;
   int nmem[CL], mslot[CL][4];
   int jlo[CL], jhi[CL];   // in-band k_z bins of the class (superset, see stolt_range)
@@ -242,6 +243,7 @@ cudaError_t launch_k4b(const SarDeviceView &v, void *img, bool cplx, cudaStream_
 bool passb_supported(const SarDeviceView &v);
 cudaError_t launch_passb(const SarDeviceView &v, const CUtensorMap *tm0, const CUtensorMap *tm1, const int4 *items,
                          int nitems, int *cnt, int stop, bool discard, cudaStream_t s, int num_sms);
-cudaError_t launch_nufft(const SarDeviceView &v, const float2 *data, cudaStream_t s);
+cudaError_t launch_nufft(const SarDeviceView &v, const float2 *data, cudaStream_t s, const CUtensorMap *tm_fine,
+                         int num_sms, int part);
 
 }  // namespace sark

@@ -187,10 +187,23 @@ __device__ __forceinline__ void sync(int rbar = 0) {
 // store() wrote, or before the next call's pass-1 loads if they alias work.
 // R1SEL overrides the pass-1 radix (0 = Split<N>; e.g. 16 for N = 512 keeps
 // pass 1 at 16 registers pairs when the caller is register-limited).
-template <int N, int C, int LDW, int NT, int DIR, int BARID, bool I_FAST2, int R1SEL = 0, typename Load,
-          typename Loaded, typename Store>
-__device__ __forceinline__ void fft(float2 *__restrict__ work, const float2 *__restrict__ tw, int tid, Load &&load,
-                                    Loaded &&loaded, Store &&store, int rbar = 0) {
+//
+// fft_ctx: the same transform, but the output column is resolved once per
+// butterfly: ctx = prep(c), then store(ctx, n, X) for each of its outputs
+// (e.g. prep returns the column's global pointer, so the unrolled stores are
+// single instructions with immediate offsets).
+//
+// SPLIT2 halves every pass-2 butterfly between two threads (2 C R1 half
+// butterflies instead of C R1 full ones, for callers whose NT would otherwise
+// leave half the threads idle in pass 2).  With p = 2q + h and the virtual
+// index i' = i + h R1 in [0, 2 R1), the DIF radix-2 split of DFT_R2 gives
+//   g_r = W_N^{r i'} (y[i + r R1] + W_{2 R1}^{i'} y[i + (r + R2/2) R1]),
+//   X[i' + 2 q R1] = DFT_{R2/2}(g)_q,          r, q < R2/2,
+// so both halves run the same code (W_{2R1}^{R1} = -1 supplies the sign).
+template <int N, int C, int LDW, int NT, int DIR, int BARID, bool I_FAST2, int R1SEL = 0, bool SPLIT2 = false,
+          typename Load, typename Loaded, typename Prep, typename Store>
+__device__ __forceinline__ void fft_ctx(float2 *__restrict__ work, const float2 *__restrict__ tw, int tid,
+                                        Load &&load, Loaded &&loaded, Prep &&prep, Store &&store, int rbar = 0) {
   static_assert((N & (N - 1)) == 0 && N >= 2 && N <= 1024, "power-of-two length in [2, 1024]");
   constexpr int R1 = R1SEL ? R1SEL : Split<N>::R1, R2 = N / R1;
   static_assert(R1 <= 32 && R2 <= 32, "two passes of radix <= 32");
@@ -213,9 +226,10 @@ __device__ __forceinline__ void fft(float2 *__restrict__ work, const float2 *__r
       const int c = tid + it * NT;
       if (C % NT == 0 || c < C) {
         dft<R1, DIR>(v[it]);
+        const auto ctx = prep(c);
         static_for<0, R1>([&](auto P) {
           constexpr int p = decltype(P)::value;
-          store(c, freq_at(R1, p), v[it][p]);
+          store(ctx, freq_at(R1, p), v[it][p]);
         });
       }
     }
@@ -248,6 +262,42 @@ __device__ __forceinline__ void fft(float2 *__restrict__ work, const float2 *__r
       }
     }
     sync<BARID, NT>(rbar);
+    if constexpr (SPLIT2) {
+      static_assert(R2 >= 4, "split pass 2 needs R2 >= 4");
+      constexpr int H = R2 / 2;
+      constexpr int NB2 = C * 2 * R1;
+      constexpr int IT2 = (NB2 + NT - 1) / NT;
+#pragma unroll
+      for (int it = 0; it < IT2; ++it) {
+        const int b = tid + it * NT;
+        if (NB2 % NT == 0 || b < NB2) {
+          const int c = I_FAST2 ? b / (2 * R1) : b % C;
+          const int ip = I_FAST2 ? b % (2 * R1) : b / C;
+          const int i = ip & (R1 - 1);
+          float2 e = tw[H * ip];
+          if (DIR > 0) e.y = -e.y;
+          float2 g[H];
+#pragma unroll
+          for (int r = 0; r < H; ++r) {
+            const float2 t = add(work[(i + r * R1) * LDW + c], mul(work[(i + (r + H) * R1) * LDW + c], e));
+            if (r == 0) {
+              g[0] = t;
+            } else {
+              float2 w = tw[r * ip];
+              if (DIR > 0) w.y = -w.y;
+              g[r] = mul(t, w);
+            }
+          }
+          dft<H, DIR>(g);
+          const auto ctx = prep(c);
+          static_for<0, H>([&](auto P) {
+            constexpr int p = decltype(P)::value;
+            store(ctx, ip + 2 * freq_at(H, p) * R1, g[p]);
+          });
+        }
+      }
+      return;
+    }
     // pass 2: butterflies one at a time (reads and writes disjoint per thread)
     constexpr int NB2 = C * R1;
     constexpr int IT2 = (NB2 + NT - 1) / NT;
@@ -266,13 +316,22 @@ __device__ __forceinline__ void fft(float2 *__restrict__ work, const float2 *__r
           u[r] = mul(work[(i + r * R1) * LDW + c], w);
         }
         dft<R2, DIR>(u);
+        const auto ctx = prep(c);
         static_for<0, R2>([&](auto P) {
           constexpr int p = decltype(P)::value;
-          store(c, i + freq_at(R2, p) * R1, u[p]);
+          store(ctx, i + freq_at(R2, p) * R1, u[p]);
         });
       }
     }
   }
+}
+
+template <int N, int C, int LDW, int NT, int DIR, int BARID, bool I_FAST2, int R1SEL = 0, typename Load,
+          typename Loaded, typename Store>
+__device__ __forceinline__ void fft(float2 *__restrict__ work, const float2 *__restrict__ tw, int tid, Load &&load,
+                                    Loaded &&loaded, Store &&store, int rbar = 0) {
+  fft_ctx<N, C, LDW, NT, DIR, BARID, I_FAST2, R1SEL>(
+      work, tw, tid, load, loaded, [](int c) { return c; }, store, rbar);
 }
 
 // consumer threads that give every pass-1 butterfly of a C-column batch its own thread

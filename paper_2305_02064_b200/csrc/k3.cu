@@ -149,11 +149,14 @@ __global__ void __launch_bounds__(K3C_NT, 4) k3_class(const SarDeviceView v) {
     return (m >= jlos[cl] && m <= jhis[cl]) ? fout[m * LD + c] : make_float2(0.f, 0.f);
   };
   if constexpr (DO_IFFT) {
-    sarfft2::fft<NZ, CC, LD, K3C_NT, +1, 0, true, (NZ == 512 ? 16 : 0)>(
+    sarfft2::fft_ctx<NZ, CC, LD, K3C_NT, +1, 0, true, (NZ == 512 ? 16 : 0)>(
         fout, v.tw_z, tid, load, [] {},
-        [&](int c, int m, float2 x) {
+        [&](int c) {
           const int col = colof[c];
-          if (col >= 0) __stcs(dst + (size_t)col * NZ + m, x);
+          return col >= 0 ? dst + (size_t)col * NZ : nullptr;
+        },
+        [&](float2 *p, int m, float2 x) {
+          if (p) __stcs(p + m, x);
         });
   } else {
     for (int i = tid; i < CC * NZ; i += K3C_NT) {
@@ -163,9 +166,16 @@ __global__ void __launch_bounds__(K3C_NT, 4) k3_class(const SarDeviceView v) {
   }
 }
 
-constexpr int K3P_G = 256;   // threads per consumer group
-constexpr int K3P_NG = 2;    // consumer groups (alternate items)
-constexpr int K3P_S = 4;     // ring stages
+#ifndef K3P_GEOM
+#define K3P_GEOM 256, 2, 4, 2
+#endif
+// threads per consumer group, consumer groups (round-robin items), ring
+// stages, mirror classes per item
+constexpr int K3P_GEOM_[4] = {K3P_GEOM};
+constexpr int K3P_G = K3P_GEOM_[0];
+constexpr int K3P_NG = K3P_GEOM_[1];
+constexpr int K3P_S = K3P_GEOM_[2];
+constexpr int K3P_CL = K3P_GEOM_[3];
 template <int NZ, int CL>
 size_t k3pp_smem(int nk) {
   const size_t hdr = (sizeof(K3Hdr<CL>) + 15) & ~(size_t)15;
@@ -174,7 +184,7 @@ size_t k3pp_smem(int nk) {
          ((size_t)NZ + nk) * sizeof(double) + (size_t)NZ * sizeof(float2);
 }
 
-template <int NZ, int CL, bool DO_IFFT, int BAR>
+template <int NZ, int CL, bool DO_IFFT>
 __device__ __forceinline__ void k3pp_consume(const SarDeviceView &v, int nitems_f, int g, int gt,
                                              unsigned char *ring, size_t stage_bytes, size_t hdr_bytes,
                                              float2 *fout, const double *ks, const double *kzs, const float2 *tw,
@@ -192,7 +202,7 @@ __device__ __forceinline__ void k3pp_consume(const SarDeviceView &v, int nitems_
     const K3Hdr<CL> &h = *reinterpret_cast<const K3Hdr<CL> *>(sb);
     const float2 *fin = reinterpret_cast<const float2 *>(sb + hdr_bytes);
     const int f = h.f, nu = h.nused;
-    const double rr = v.rref[f] * (1.0 / TWO_PI);
+    const double rr = h.rr;
     // Stolt pull over the in-band (class, j) pairs only, the filter evaluated
     // at the two taps each pull uses and folded into the weights:
     //   O_j = (1-tau) H(k_i0) S_i0 + tau H(k_i0+1) S_i0+1
@@ -236,7 +246,7 @@ __device__ __forceinline__ void k3pp_consume(const SarDeviceView &v, int nitems_
       slo[gt] = used ? h.jlo[h.clof[gt]] : NZ;
       shi[gt] = used ? h.jhi[h.clof[gt]] : -1;
     }
-    sarfft2::sync<BAR, K3P_G>();
+    sarfft2::sync<-1, K3P_G>(1 + g);
     if (gt == 0) sartma::mbar_arrive(&empty[st]);  // stage (header + columns) consumed
     // inverse z-FFT (out-of-band rows read as zero), columns stored contiguously
     float2 *dst = v.w1 + (size_t)f * ncol * (size_t)NZ;
@@ -244,19 +254,30 @@ __device__ __forceinline__ void k3pp_consume(const SarDeviceView &v, int nitems_
       return (m >= slo[c] && m <= shi[c]) ? fout[m * LD + c] : make_float2(0.f, 0.f);
     };
     if (DO_IFFT && !(v.dbg & 4)) {
-      sarfft2::fft<NZ, CC, LD, K3P_G, +1, BAR, true, (NZ == 512 && CC == 8 ? 16 : 0)>(
+      // the output column's pointer is resolved once per butterfly, so every
+      // store is one STG with an immediate offset
+      // pass 2 split between thread pairs where C R1 butterflies would leave
+      // half the group idle (N = 512 as 16 x 32, N = 256)
+      constexpr int R1S = NZ == 512 ? 16 : 0;
+      constexpr int R1 = R1S ? R1S : sarfft2::Split<NZ>::R1;
+      constexpr bool SPL = NZ / R1 >= 4 && 2 * CC * R1 <= K3P_G;
+      sarfft2::fft_ctx<NZ, CC, LD, K3P_G, +1, -1, true, R1S, SPL>(
           fout, tw, gt, load, [] {},
-          [&](int c, int m, float2 x) {
+          [&](int c) {
             const int col = colofs[c];
-            if (col >= 0) __stcs(dst + (size_t)col * NZ + m, x);
-          });
+            return col >= 0 ? dst + (size_t)col * NZ : nullptr;
+          },
+          [&](float2 *p, int m, float2 x) {
+            if (p) __stcs(p + m, x);
+          },
+          1 + g);
     } else {
       for (int i = gt; i < CC * NZ; i += K3P_G) {
         const int sl = i / NZ, z = i - sl * NZ;
         if (sl < nu) dst[(size_t)colofs[sl] * NZ + z] = load(sl, z);
       }
     }
-    sarfft2::sync<BAR, K3P_G>();  // fout / slot tables are rewritten by this group's next item
+    sarfft2::sync<-1, K3P_G>(1 + g);  // fout / slot tables are rewritten by this group's next item
   }
 }
 
@@ -348,6 +369,7 @@ __global__ void __launch_bounds__(K3P_NG * K3P_G + 32, 1) k3_pp(const SarDeviceV
       if (lane == 0) {
         h.nused = cnt;
         h.f = f;
+        h.rr = v.rref[f] * (1.0 / TWO_PI);
       }
       __syncwarp();
       if (lane == 0) sartma::mbar_arrive_expect_tx(&full[st], (uint32_t)cnt * (uint32_t)nk * 8u);
@@ -359,13 +381,8 @@ __global__ void __launch_bounds__(K3P_NG * K3P_G + 32, 1) k3_pp(const SarDeviceV
     return;
   }
   const int g = tid / K3P_G, gt = tid - g * K3P_G;
-  float2 *fout = grp + g * grp_elems;
-  if (g == 0)
-    k3pp_consume<NZ, CL, DO_IFFT, 1>(v, nitems_f, 0, gt, ring, stage_bytes, hdr_bytes, fout, ks, kzs, tw, full, empty,
-                                     colofs[0], slo[0], shi[0]);
-  else
-    k3pp_consume<NZ, CL, DO_IFFT, 2>(v, nitems_f, 1, gt, ring, stage_bytes, hdr_bytes, fout, ks, kzs, tw, full, empty,
-                                     colofs[1], slo[1], shi[1]);
+  k3pp_consume<NZ, CL, DO_IFFT>(v, nitems_f, g, gt, ring, stage_bytes, hdr_bytes, grp + g * grp_elems, ks, kzs, tw,
+                                full, empty, colofs[g], slo[g], shi[g]);
 }
 
 // ------------------------------------------------------- K3, 2-D mode ----
@@ -487,7 +504,7 @@ cudaError_t launch_k3(const SarDeviceView &v, bool ifft, cudaStream_t s, int num
     switch (v.nz) {
 #define X(N)                                                                                                   \
   case N: {                                                                                                    \
-    constexpr int CL = 2;                                                                                      \
+    constexpr int CL = K3P_CL;                                                                                 \
     const size_t smem = k3pp_smem<N, CL>(v.nk);                                                                \
     if (smem > 225 * 1024) break;                                                                              \
     const int nitems_f = (nclass + CL - 1) / CL;                                                               \

@@ -93,23 +93,29 @@ __global__ void __launch_bounds__(sarfft2::nt_fft<NX, KC>() + 32)
     OT *outp = reinterpret_cast<OT *>(img) + ((size_t)f * nz * v.ny + iy) * NX;
     const float2 *stage = ring + (size_t)st * NX * KC;
     float pk = 0.f;
-    sarfft2::fft<NX, KC, KC + 1, NTC, +1, 1, true>(
+    // the image row of z-slot c is resolved once per butterfly (prep), so a
+    // store is the x roll plus one STG
+    sarfft2::fft_ctx<NX, KC, KC + 1, NTC, +1, 1, true>(
         work, tw, tid, [&](int c, int m) { return stage[m * KC + c]; },
         [&] {
           if (tid == 0) sartma::mbar_arrive(&empty[st]);
         },
-        [&](int c, int a, float2 o) {
+        [&](int c) -> OT * {
           const int z = zc * KC + c;
-          if (z < nz) {
-            int m = z + v.zroll;
-            if (m >= nz) m -= nz;
+          if (z >= nz) return nullptr;
+          int m = z + v.zroll;
+          if (m >= nz) m -= nz;
+          return outp + (size_t)m * zstride;
+        },
+        [&](OT *rowp, int a, float2 o) {
+          if (rowp) {
             const int ix = (a - rx) & (NX - 1);
             const float mag = sqrtf(fmaf(o.x, o.x, o.y * o.y)) * sc;
             pk = fmaxf(pk, mag);
             if constexpr (CPLX) {
-              __stcs(reinterpret_cast<float2 *>(outp) + (size_t)m * zstride + ix, make_float2(o.x * sc, o.y * sc));
+              __stcs(reinterpret_cast<float2 *>(rowp) + ix, make_float2(o.x * sc, o.y * sc));
             } else {
-              __stcs(reinterpret_cast<float *>(outp) + (size_t)m * zstride + ix, mag);
+              __stcs(reinterpret_cast<float *>(rowp) + ix, mag);
             }
           }
         });

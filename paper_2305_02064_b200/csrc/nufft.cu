@@ -15,161 +15,133 @@ namespace sark {
 namespace {
 
 // --------------------------------------------------------- NUFFT mode ----
-// SAR_GRID_NUFFT (reading R19, FGG-NUFFT of P:239-242).  K1n: one CTA per
-// (16-wide k chunk, fine row jy of the 2ny x 2nx oversampled grid, frame).
-// For each (pair, pose row) that can reach the fine row (host-built list) the
-// CTA stages the pose row's samples rotated by e^{+j k beta} (Eq. (11)) and
-// weighted by the row's Gaussian y-weight, plus each pose's x-weights; then
-// every thread gathers into the fine-grid cells it owns (deterministic, no
-// atomics).  Finally the fine row is transformed along x (N = 2nx), cropped
-// to |a_s| < nx/2 and deconvolved by 1/Phi_x: Wh[f][jy][a][k].
-// K2n: y-FFT over the 2ny fine rows, crop to |b_s| < ny/2, 1/Phi_y: W0.
-constexpr int K1N_WT = 14;      // taps per axis: 2W + 2 with W = 6
-constexpr int K1N_PCH = 256;    // poses staged at a time
-constexpr int K1N_KC = 4;       // k values per CTA
-constexpr int K1N_NT = 512;
-template <int RX>
-constexpr int k1n_br() { return RX >= 1024 ? 4 : 8; }   // fine rows per band (matches plan.cpp)
-
-// One CTA = (k chunk of 4, band of BR fine rows, frame).  Thread (row r, k q,
-// segment) owns the fine cells [seg*L, seg*L + L) x (r, q) in registers.  For
-// each candidate (pair, pose row): stage the row's samples in fine-x order
-// (host permutation) rotated by e^{+j k beta}, with each pose's x-weights and
-// its y-weights for the band's rows; then every thread sweeps the sorted poses
-// over its columns (positions may wrap by +-RX, reading R6).
-template <int RX>
-__global__ void __launch_bounds__(K1N_NT, 1) k1n_spread_xfft(const __grid_constant__ SarDeviceView v,
-                                                             const float2 *__restrict__ s) {
-  constexpr int BR = k1n_br<RX>();
-  constexpr int CB = BR * K1N_KC;              // (row, k) pairs = FFT columns
-  constexpr int SEGS = K1N_NT / CB;            // threads per (row, k)
-  constexpr int L = RX / SEGS;                 // fine columns per thread
-  extern __shared__ __align__(16) unsigned char smn[];
-  const int npx = v.npx, nk = v.nk, W = v.nu_w;
-  const int pch = npx < K1N_PCH ? npx : K1N_PCH;
-  float2 *sval = reinterpret_cast<float2 *>(smn);                     // [pch][KC] staged samples
-  float *wx = reinterpret_cast<float *>(sval + (size_t)pch * K1N_KC);  // [pch][WT]
-  float *wyb = wx + (size_t)pch * K1N_WT;                             // [pch][BR]
-  int *x0s = reinterpret_cast<int *>(wyb + (size_t)pch * BR);          // [pch] first tap column (no wrap)
-  float2 *tile = reinterpret_cast<float2 *>(smn);                     // [RX][CB] (after the gather)
-  __shared__ float2 twx[RX];
+// SAR_GRID_NUFFT (reading R19, FGG-NUFFT of P:239-242): K1s spreads the
+// compensated samples onto the 2ny x 2nx fine grid, the mid-axis FFT kernel
+// transforms the fine rows along x, and K2n transforms along y, crops to the
+// kept frequencies and deconvolves by 1/(Phi_x Phi_y) into W0.
+// K1s: the spread as a k-parallel gather.  One CTA = (4 x 8 block of fine
+// cells, frame, chunk of NT wavenumbers); thread = wavenumber k, so every
+// sample read is a coalesced run along k and the 32 cell accumulators live in
+// registers (deterministic, no atomics).  For each host-listed entry (virtual
+// element within W of the block, reading R19) the CTA stages its 32 Gaussian
+// weights phi(j - U) phi(i - V) (4 threads per entry, one fine row each);
+// then every thread rotates its sample by e^{+j k beta} (Eq. (11)) and
+// accumulates it into the 32 cells with paired-fp32 FMAs.  The block's cells
+// are written once, [F][2ny][2nx][nk]; the fine x-FFT follows (launch_mid).
+constexpr int SP_CELLS = SAR_SP_BX * SAR_SP_BY;
+template <int NT, int KPT>
+__global__ void __launch_bounds__(NT, (KPT == 1 ? 1024 : 512) / NT) k1s_spread(const __grid_constant__ SarDeviceView v,
+                                                          const float2 *__restrict__ s) {
+  constexpr int CH = NT / SAR_SP_BY;   // entries staged per round (one thread per weight row)
+  constexpr int U = 4 / KPT;           // entries whose samples are loaded ahead
+  constexpr int KB = NT * KPT;         // wavenumbers per CTA
+  __shared__ float4 ent[CH];
+  __shared__ __align__(16) float wt[CH][SP_CELLS];
   const int tid = threadIdx.x;
-  const int pair_idx = tid / SEGS, seg = tid - pair_idx * SEGS;
-  const int r = pair_idx / K1N_KC, q = pair_idx - r * K1N_KC;
-  const int c0 = seg * L;
-  const int kc = blockIdx.x, band = blockIdx.y, f = blockIdx.z;
-  const int RY = 2 * v.ny, NB = (RY + BR - 1) / BR;
-  for (int i = tid; i < RX; i += K1N_NT) {
-    float sn, cs;
-    sincospif(-2.0f * (float)i / (float)RX, &sn, &cs);   // twiddles of the fine x-FFT
-    twx[i] = make_float2(cs, sn);
+  const int nk = v.nk;
+  const int nkc = (nk + KB - 1) / KB;
+  const int bx = blockIdx.x, by = blockIdx.y;
+  const int f = blockIdx.z / nkc, kc = blockIdx.z - f * nkc;
+  int kk[KPT];
+  float kt[KPT];
+#pragma unroll
+  for (int j = 0; j < KPT; ++j) {
+    const int k = kc * KB + j * NT + tid;
+    kk[j] = k < nk ? k : nk - 1;
+    kt[j] = v.kturn[kk[j]];
   }
-  const float inv2s2 = 0.5f / v.nu_s2;
-  float2 acc[L];
+  const bool rot = !v.no_comp;
+  const float W = (float)v.nu_w, inv2s2 = 0.5f / v.nu_s2;
+  const int blk = (f * v.sp_nby + by) * v.sp_nbx + bx;
+  const int e0 = v.sp_off[blk], e1 = v.sp_off[blk + 1];
+  // accumulators: re / im parts of the cell pairs (2i, 2i+1), cell = cy*BX + cx
+  float2 are[KPT][SP_CELLS / 2], aim[KPT][SP_CELLS / 2];
 #pragma unroll
-  for (int m = 0; m < L; ++m) acc[m] = make_float2(0.f, 0.f);
-  const int e0 = v.nu_off[f * NB + band], e1 = v.nu_off[f * NB + band + 1];
-  for (int e = e0; e < e1; ++e) {
-    const int code = __ldg(v.nu_cand + e);
-    const int pr = code >> 16, iy = code & 0xffff;
-    const int t = pr / v.nr, rr = pr - t * v.nr;
-    const int jx2 = 2 * v.jx[pr];
-    const size_t prow = (size_t)f * v.P + (size_t)iy * npx;
-    const float2 *sg = s + (((size_t)(f * v.nt + t) * v.nr + rr) * v.P + (size_t)iy * npx) * nk;
-    const float bp = v.no_comp ? 0.f : v.bpair[f * v.npair + pr];
-    for (int p0 = 0; p0 < npx; p0 += K1N_PCH) {
-      const int pn = npx - p0 < K1N_PCH ? npx - p0 : K1N_PCH;
-      __syncthreads();   // the previous gather is done before the stage is rewritten
-      for (int idx = tid; idx < pn * K1N_KC; idx += K1N_NT) {
-        const int il = idx / K1N_KC, qq = idx - il * K1N_KC;
-        const int ix = __ldg(v.nu_perm + prow + p0 + il);
-        const int kq = kc * K1N_KC + qq;
-        float2 val = make_float2(0.f, 0.f);
-        if (kq < nk) {
-          val = __ldcs(sg + (size_t)ix * nk + kq);
-          if (!v.no_comp) {
-            float turns = (__ldg(v.apose + prow + ix) + bp) * __ldg(v.kturn + kq);
-            turns -= rintf(turns);
-            float sn, cs;
-            __sincosf(turns * 6.28318530717958647692f, &sn, &cs);
-            val = cmul(val, make_float2(cs, sn));
-          }
+  for (int j = 0; j < KPT; ++j)
+#pragma unroll
+    for (int i = 0; i < SP_CELLS / 2; ++i) are[j][i] = aim[j][i] = make_float2(0.f, 0.f);
+  for (int c0 = e0; c0 < e1; c0 += CH) {
+    const int n = e1 - c0 < CH ? e1 - c0 : CH;
+    __syncthreads();   // the previous round's weights are consumed
+    {
+      const int e = tid / SAR_SP_BY, cy = tid - e * SAR_SP_BY;
+      if (e < n) {
+        const SarSpreadEntry E = v.sp_ent[c0 + e];
+        if (cy == 0) ent[e] = make_float4(__int_as_float(E.row), E.du, E.dv, E.beta);
+        const float dy = (float)cy - E.dv;
+        const float wy = fabsf(dy) <= W ? __expf(-dy * dy * inv2s2) : 0.f;
+        float wr[SAR_SP_BX];
+#pragma unroll
+        for (int cx = 0; cx < SAR_SP_BX; ++cx) {
+          const float dx = (float)cx - E.du;
+          wr[cx] = fabsf(dx) <= W ? wy * __expf(-dx * dx * inv2s2) : 0.f;
         }
-        sval[idx] = val;
-        if (qq == 0) {
-          const float xf = (float)(2 * ix) + __ldg(v.nu_du + prow + ix);
-          const int xb = (int)floorf(xf) - W;
-          x0s[il] = xb + jx2;
+        float4 *dstw = reinterpret_cast<float4 *>(&wt[e][cy * SAR_SP_BX]);
 #pragma unroll
-          for (int tt = 0; tt < K1N_WT; ++tt) {
-            const float dx = (float)(xb + tt) - xf;
-            wx[il * K1N_WT + tt] = fabsf(dx) <= (float)W ? __expf(-dx * dx * inv2s2) : 0.f;
-          }
-          const float vf = (float)(2 * (iy + v.jy[pr])) + __ldg(v.nu_dv + prow + ix);
-#pragma unroll
-          for (int b = 0; b < BR; ++b) {
-            float d = (float)(band * BR + b) - vf;
-            d -= (float)RY * rintf(d / (float)RY);         // periodic fine rows (reading R6)
-            wyb[il * BR + b] = fabsf(d) <= (float)W ? __expf(-d * d * inv2s2) : 0.f;
-          }
-        }
+        for (int q = 0; q < SAR_SP_BX / 4; ++q) dstw[q] = make_float4(wr[4 * q], wr[4 * q + 1], wr[4 * q + 2], wr[4 * q + 3]);
       }
-      __syncthreads();
-      // gather over the x-sorted poses: cell c gets tap c - x0 of the poses
-      // with x0 <= c <= x0 + WT - 1, for the aliases c, c - RX, c + RX
-      const int xlo = x0s[0], xhi = x0s[pn - 1] + K1N_WT - 1;
+    }
+    __syncthreads();
+    for (int e = 0; e < n; e += U) {
+      float2 val[U][KPT];
 #pragma unroll
-      for (int wrap = -1; wrap < 2; ++wrap) {
-        const int cs = c0 + wrap * RX, ce = cs + L - 1;
-        if (ce < xlo || cs > xhi) continue;
-        // first pose whose footprint reaches cs (binary search, x0 ascending)
-        int lo = 0, hi = pn;
-        while (lo < hi) {
-          const int mid = (lo + hi) >> 1;
-          if (x0s[mid] + K1N_WT - 1 < cs) lo = mid + 1;
-          else hi = mid;
-        }
-        for (int pp = lo; pp < pn; ++pp) {
-          const int x0 = x0s[pp];
-          if (x0 > ce) break;
-          const float wyv = wyb[pp * BR + r];
-          if (wyv == 0.f) continue;
-          const float2 val = sval[pp * K1N_KC + q];
-          const float2 vw = make_float2(val.x * wyv, val.y * wyv);
+      for (int u = 0; u < U; ++u) {
+        const int row = e + u < n ? __float_as_int(ent[e + u].x) : 0;
 #pragma unroll
-          for (int m = 0; m < L; ++m) {
-            const int tt = cs + m - x0;
-            if (tt >= 0 && tt < K1N_WT) {
-              const float w = wx[pp * K1N_WT + tt];
-              acc[m].x = fmaf(w, vw.x, acc[m].x);
-              acc[m].y = fmaf(w, vw.y, acc[m].y);
+        for (int j = 0; j < KPT; ++j)
+          val[u][j] = e + u < n ? __ldg(s + (size_t)row * nk + kk[j]) : make_float2(0.f, 0.f);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (e + u < n) {
+          float2 xr[KPT], xi[KPT];
+#pragma unroll
+          for (int j = 0; j < KPT; ++j) {
+            float2 x = val[u][j];
+            if (rot) {
+              float turns = ent[e + u].w * kt[j];
+              turns -= (turns + 12582912.f) - 12582912.f;   // round to nearest on the FMA pipe
+              float sn, cs;
+              __sincosf(turns * 6.28318530717958647692f, &sn, &cs);
+              x = cmul(x, make_float2(cs, sn));
+            }
+            xr[j] = make_float2(x.x, x.x);
+            xi[j] = make_float2(x.y, x.y);
+          }
+          const float4 *w4 = reinterpret_cast<const float4 *>(wt[e + u]);
+#pragma unroll
+          for (int i = 0; i < SP_CELLS / 4; ++i) {
+            const float4 w = w4[i];
+#pragma unroll
+            for (int j = 0; j < KPT; ++j) {
+              are[j][2 * i] = __ffma2_rn(xr[j], make_float2(w.x, w.y), are[j][2 * i]);
+              are[j][2 * i + 1] = __ffma2_rn(xr[j], make_float2(w.z, w.w), are[j][2 * i + 1]);
+              aim[j][2 * i] = __ffma2_rn(xi[j], make_float2(w.x, w.y), aim[j][2 * i]);
+              aim[j][2 * i + 1] = __ffma2_rn(xi[j], make_float2(w.z, w.w), aim[j][2 * i + 1]);
             }
           }
         }
       }
     }
   }
-  __syncthreads();
-  // the band's fine rows -> x-FFT (N = RX) over CB columns, crop, deconvolve
+  const int RX = 2 * v.nx, RY = 2 * v.ny;
+  float2 *dst = v.wh + ((size_t)(f * RY + by * SAR_SP_BY) * RX + bx * SAR_SP_BX) * (size_t)nk;
 #pragma unroll
-  for (int m = 0; m < L; ++m) tile[(c0 + m) * CB + pair_idx] = acc[m];
-  __syncthreads();
-  const int nx = v.nx;
-  const int kmax = nk - kc * K1N_KC;
-  sarfft2::fft<RX, CB, CB, K1N_NT, -1, 0, false>(
-      tile, twx, tid, [&](int c, int n) { return tile[n * CB + c]; }, [] {},
-      [&](int c, int n, float2 x) {
-        const int as = n < RX / 2 ? n : n - RX;
-        const int rb = c / K1N_KC, qb = c - rb * K1N_KC;
-        const int jyf = band * BR + rb;
-        if (qb < kmax && jyf < RY && as >= -nx / 2 && as < nx / 2) {
-          const int a = as < 0 ? as + nx : as;
-          const float d = __ldg(v.nu_decx + a);
-          v.wh[((size_t)(f * RY + jyf) * nx + a) * (size_t)nk + kc * K1N_KC + qb] = make_float2(x.x * d, x.y * d);
-        }
-      });
+  for (int j = 0; j < KPT; ++j) {
+    const int k = kc * KB + j * NT + tid;
+    if (k >= nk) continue;
+#pragma unroll
+    for (int i = 0; i < SP_CELLS / 2; ++i) {
+      const int c = 2 * i, cy = c / SAR_SP_BX, cx = c - cy * SAR_SP_BX;
+      float2 *d = dst + ((size_t)cy * RX + cx) * nk + k;
+      __stcs(d, make_float2(are[j][i].x, aim[j][i].x));
+      __stcs(d + nk, make_float2(are[j][i].y, aim[j][i].y));
+    }
+  }
 }
 
+// K2n: fine y-FFT of the x-transformed fine grid at the kept x frequencies,
+// crop to |b_s| < ny/2, deconvolve by 1/(Phi_x Phi_y): W0.
 template <int RY>
 __global__ void __launch_bounds__(sarfft2::nt_fft<RY, KC>()) k2n_yfft_crop(const __grid_constant__ SarDeviceView v) {
   constexpr int NT = sarfft2::nt_fft<RY, KC>();
@@ -183,8 +155,13 @@ __global__ void __launch_bounds__(sarfft2::nt_fft<RY, KC>()) k2n_yfft_crop(const
     sincospif(-2.0f * (float)i / (float)RY, &sn, &cs);
     twy[i] = make_float2(cs, sn);
   }
-  const float2 *src = v.wh + ((size_t)f * RY * nx + a) * (size_t)nk + kc * KC;
-  const size_t row = (size_t)nx * nk;
+  const int RX = 2 * nx;
+  const int as = a < nx / 2 ? a : a - nx;
+  const int af = as < 0 ? as + RX : as;
+  const float dxa = __ldg(v.nu_decx + a);
+  const float2 *src = v.wh + ((size_t)f * RY * RX + af) * (size_t)nk + kc * KC;
+  const size_t row = (size_t)RX * nk;
+  const size_t orow = (size_t)nx * nk;
   const int cmax = nk - kc * KC;
   for (int i = tid; i < RY * KC; i += NT) {
     const int n = i / KC, c = i - n * KC;
@@ -198,40 +175,14 @@ __global__ void __launch_bounds__(sarfft2::nt_fft<RY, KC>()) k2n_yfft_crop(const
         const int bs = n < RY / 2 ? n : n - RY;
         if (c < cmax && bs >= -ny / 2 && bs < ny / 2) {
           const int b = bs < 0 ? bs + ny : bs;
-          const float d = __ldg(v.nu_decy + b);
-          dst[(size_t)b * row + c] = make_float2(x.x * d, x.y * d);
+          const float d = __ldg(v.nu_decy + b) * dxa;
+          dst[(size_t)b * orow + c] = make_float2(x.x * d, x.y * d);
         }
       });
 }
 
-
-}  // namespace
-
-cudaError_t launch_nufft(const SarDeviceView &v, const float2 *data, cudaStream_t s) {
+cudaError_t launch_k2n(const SarDeviceView &v, cudaStream_t s) {
   const int nchunk = (v.nk + KC - 1) / KC;
-  {
-    const int pch = v.npx < K1N_PCH ? v.npx : K1N_PCH;
-    switch (2 * v.nx) {
-#define X(N)                                                                                        \
-  case N: {                                                                                         \
-    constexpr int BR = k1n_br<N>();                                                                 \
-    const size_t stage = (size_t)pch * (K1N_KC * sizeof(float2) + (K1N_WT + BR) * sizeof(float) + sizeof(int)); \
-    const size_t tile = (size_t)N * BR * K1N_KC * sizeof(float2);                                   \
-    const size_t smem = stage > tile ? stage : tile;                                                \
-    dim3 grid((v.nk + K1N_KC - 1) / K1N_KC, (2 * v.ny + BR - 1) / BR, v.F);                          \
-    cudaError_t e = cudaFuncSetAttribute(k1n_spread_xfft<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
-    if (e != cudaSuccess) return e;                                                                 \
-    k1n_spread_xfft<N><<<grid, K1N_NT, smem, s>>>(v, data);                                          \
-    e = cudaGetLastError();                                                                         \
-    if (e != cudaSuccess) return e;                                                                 \
-    break;                                                                                          \
-  }
-      X(64) X(128) X(256) X(512) X(1024)
-#undef X
-      default:
-        return cudaErrorInvalidValue;
-    }
-  }
   dim3 grid(nchunk, v.nx, v.F);
   switch (2 * v.ny) {
 #define X(N)                                                                                         \
@@ -239,7 +190,7 @@ cudaError_t launch_nufft(const SarDeviceView &v, const float2 *data, cudaStream_
     const size_t smem = (size_t)N * KC * sizeof(float2);                                             \
     cudaError_t e = cudaFuncSetAttribute(k2n_yfft_crop<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
     if (e != cudaSuccess) return e;                                                                  \
-    k2n_yfft_crop<N><<<grid, sarfft2::nt_fft<N, KC>(), smem, s>>>(v);                                \
+    k2n_yfft_crop<N><<<grid, sarfft2::nt_fft<N, KC>(), smem, s>>>(v);                          \
     return cudaGetLastError();                                                                       \
   }
     X(4) X(8) X(16) X(32) X(64) X(128) X(256) X(512) X(1024)
@@ -248,5 +199,28 @@ cudaError_t launch_nufft(const SarDeviceView &v, const float2 *data, cudaStream_
   return cudaErrorInvalidValue;
 }
 
+cudaError_t launch_k1s(const SarDeviceView &v, const float2 *data, cudaStream_t s) {
+  // one wavenumber per thread, up to 256 per CTA
+  const int kb = v.nk <= 64 ? 64 : (v.nk <= 128 ? 128 : 256);
+  const int nkc = (v.nk + kb - 1) / kb;
+  dim3 grid(v.sp_nbx, v.sp_nby, v.F * nkc);
+  if (kb == 64) k1s_spread<64, 1><<<grid, 64, 0, s>>>(v, data);
+  else if (kb == 128) k1s_spread<128, 1><<<grid, 128, 0, s>>>(v, data);
+  else k1s_spread<256, 1><<<grid, 256, 0, s>>>(v, data);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+// SAR_GRID_NUFFT: part 1 = K1s spread; part 2 = fine x-FFT in place (the K2
+// kernel on the fine grid viewed as [F*2ny][2nx][1][nk]) -> K2n (fine y-FFT,
+// crop, 1/Phi).
+cudaError_t launch_nufft(const SarDeviceView &v, const float2 *data, cudaStream_t s, const CUtensorMap *tm_fine,
+                         int num_sms, int part) {
+  if (part == 1) return launch_k1s(v, data, s);
+  cudaError_t e = launch_mid<-1>(v.wh, v.tw_f, v.F * 2 * v.ny, 2 * v.nx, 1, v.nk, s, tm_fine, num_sms);
+  if (e != cudaSuccess) return e;
+  return launch_k2n(v, s);
+}
 
 }  // namespace sark

@@ -53,10 +53,12 @@ int sar_launch_pipeline(sar_plan *p, const void *d_data, void *d_image, cudaStre
     if (p->tma_s) tm_s = &p->tm_s;
   }
   if (v.nufft) {
-    // K1n (spread + fine x-FFT) and K2n (fine y-FFT + crop) replace K1 and K2;
-    // their times are reported in the K1 and K2 slots
-    SAR_CHECK(launch_nufft(v, data, s));
+    // the spread (K1s) and the fine x/y FFTs + crop (x-FFT, K2n) replace K1
+    // and K2; their times are reported in the K1 and K2 slots
+    const CUtensorMap *tmf = p->tma_fine ? &p->tm_fine : nullptr;
+    SAR_CHECK(launch_nufft(v, data, s, tmf, p->num_sms, 1));
     if (ev) SAR_CHECK(cudaEventRecord(ev[1], s));
+    SAR_CHECK(launch_nufft(v, data, s, tmf, p->num_sms, 2));
     if (ev) SAR_CHECK(cudaEventRecord(ev[2], s));
     if (stop_stage == 2) return SAR_OK;
     SAR_CHECK(launch_k3(v, stop_stage != 3, s, p->num_sms));
@@ -183,6 +185,11 @@ int sar_build_tensor_maps(sar_plan *p) {
   p->tma_mid1 = encode3d(&p->tm_w1_mid, v.w1, v.nz, v.nx, (uint64_t)v.F * v.ny, KC, 1, rows);
   p->tma_pb = encode3d(&p->tm_w0_pb, v.w0, v.nk, v.nx, (uint64_t)v.F * v.ny, PB_KC, 1, rows) &&
               encode3d(&p->tm_w1_pb, v.w1, v.nz, v.nx, (uint64_t)v.F * v.ny, PB_KC, 1, rows);
+  if (v.nufft) {
+    // fine grid [F*2ny][2nx][nk]: x-FFT boxes {16 k, 1, <=256 fine columns}
+    const uint32_t rx = 2 * v.nx, fr = rx < 256 ? rx : 256;
+    p->tma_fine = encode3d(&p->tm_fine, v.wh, v.nk, 1, (uint64_t)v.F * 2 * v.ny * rx, KC, 1, fr);
+  }
   const uint32_t xr = v.nx < 256 ? v.nx : 256;
   p->tma_rows1 = encode3d(&p->tm_w1_rows, v.w1, v.nz, v.nx, (uint64_t)v.F * v.ny, KC, xr, 1);
   // K1: -2 d_z table [F*npy][npx] float32 with box [1][br]; input map per call

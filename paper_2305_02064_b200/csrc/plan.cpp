@@ -102,11 +102,12 @@ struct HostTables {
   std::vector<float> apose, bpair, kturn, pinv, tw;
   std::vector<SarClass> cls;
   // NUFFT mode
-  std::vector<float> nu_du, nu_dv, nu_decx, nu_decy;
-  std::vector<int> nu_off, nu_cand;
-  std::vector<short> nu_perm;
-  int nu_br = 8;
-  float nu_dumax = 0.f;
+  std::vector<float> nu_decx, nu_decy;
+  // NUFFT spread blocks (K1s): CSR of entries per (frame, 4 x 8 fine-cell block)
+  std::vector<int> sp_off;
+  std::vector<SarSpreadEntry> sp_ent;
+  int sp_nbx = 0, sp_nby = 0;
+  size_t tw_f_off = 0;
   std::vector<double> kx, ky, kz, kd, rref;
   size_t tw_y_off = 0, tw_z_off = 0;
   int roll_x = 0, roll_y = 0;
@@ -302,59 +303,6 @@ int host_decompose(const sar_geom_desc *g, const sar_image_desc *im, uint32_t fl
     const int W = 6, sig = 2;
     const double s2 = W / (2.0 * M_PI * (1.0 - 1.0 / (2.0 * sig)));
     const int Rx = sig * p->nx, Ry = sig * p->ny;
-    T.nu_du.resize((size_t)F * P);
-    T.nu_dv.resize((size_t)F * P);
-    double dmax = 0;
-    for (int f = 0; f < F; ++f)
-      for (int q = 0; q < P; ++q) {
-        const int iy = q / g->npx, ix = q - iy * g->npx;
-        const double *sp = g->scan_xyz + ((size_t)f * P + q) * 3;
-        const double du = sig * ((sp[0] - g->x0) / g->dx - ix), dv = sig * ((sp[1] - g->y0) / g->dy - iy);
-        T.nu_du[(size_t)f * P + q] = (float)du;
-        T.nu_dv[(size_t)f * P + q] = (float)dv;
-        dmax = std::max(dmax, fabs(du));
-      }
-    T.nu_dumax = (float)dmax;
-
-    // bands of BR fine rows; candidate (pair, pose row) lists per (frame, band)
-    const int BR = Rx >= 1024 ? 4 : 8;
-    T.nu_br = BR;
-    const int NB = (Ry + BR - 1) / BR;
-    std::vector<std::vector<int>> lists((size_t)F * NB);
-    for (int f = 0; f < F; ++f)
-      for (int pr = 0; pr < p->npair; ++pr)
-        for (int iy = 0; iy < g->npy; ++iy) {
-          double vmin = 1e300, vmax = -1e300;
-          for (int ix = 0; ix < g->npx; ++ix) {
-            const double vv = sig * (double)(iy + p->jy[pr]) + T.nu_dv[(size_t)f * P + iy * g->npx + ix];
-            vmin = std::min(vmin, vv);
-            vmax = std::max(vmax, vv);
-          }
-          std::vector<char> hit(NB, 0);
-          for (long long r = (long long)ceil(vmin - W - 1e-6); r <= (long long)floor(vmax + W + 1e-6); ++r) {
-            const int rr = (int)(((r % Ry) + Ry) % Ry);
-            hit[rr / BR] = 1;
-          }
-          for (int bnd = 0; bnd < NB; ++bnd)
-            if (hit[bnd]) lists[(size_t)f * NB + bnd].push_back((pr << 16) | iy);
-        }
-    T.nu_off.assign((size_t)F * NB + 1, 0);
-    for (size_t i = 0; i < lists.size(); ++i) {
-      T.nu_off[i + 1] = T.nu_off[i] + (int)lists[i].size();
-      T.nu_cand.insert(T.nu_cand.end(), lists[i].begin(), lists[i].end());
-    }
-    // poses of each row sorted by fine x position (the gather sweeps them)
-    T.nu_perm.resize((size_t)F * P);
-    for (int f = 0; f < F; ++f)
-      for (int iy = 0; iy < g->npy; ++iy) {
-        std::vector<int> idx(g->npx);
-        for (int ix = 0; ix < g->npx; ++ix) idx[ix] = ix;
-        const float *du = T.nu_du.data() + (size_t)f * P + (size_t)iy * g->npx;
-        std::stable_sort(idx.begin(), idx.end(), [&](int a, int b) {
-          return floorf((float)(2 * a) + du[a]) < floorf((float)(2 * b) + du[b]);
-        });
-        for (int ix = 0; ix < g->npx; ++ix) T.nu_perm[(size_t)f * P + (size_t)iy * g->npx + ix] = (short)idx[ix];
-      }
     auto dec = [&](int n, int R, std::vector<float> &o) {
       o.resize(n);
       for (int a = 0; a < n; ++a) {
@@ -364,6 +312,53 @@ int host_decompose(const sar_geom_desc *g, const sar_image_desc *im, uint32_t fl
     };
     dec(p->nx, Rx, T.nu_decx);
     dec(p->ny, Ry, T.nu_decy);
+
+    // K1s spread entries: every virtual element (f, pair, pose) at the fine
+    // position (U, V) = sig ((x - x0)/dx + j^x, (y - y0)/dy + j^y) of its true
+    // in-plane position reaches the fine cells |j - U| <= W, |i - V| <= W
+    // (mod R, reading R6); it is listed once per SP_BY x SP_BX block those
+    // cells touch, with its position relative to the (unwrapped) block origin
+    // and its compensation term beta = -2 d_z + beta_MIMO (m; phase k beta).
+    T.sp_nbx = Rx / SAR_SP_BX;
+    T.sp_nby = Ry / SAR_SP_BY;
+    const int nbx = T.sp_nbx, nby = T.sp_nby;
+    const size_t nblk = (size_t)F * nby * nbx;
+    auto fdiv = [](long long a, long long b) { return a >= 0 ? a / b : -((-a + b - 1) / b); };
+    auto wmod = [](long long a, long long b) { return (int)(((a % b) + b) % b); };
+    T.sp_off.assign(nblk + 1, 0);
+    for (int pass = 0; pass < 2; ++pass) {
+      std::vector<int> fill;
+      if (pass == 1) {
+        for (size_t i = 0; i < nblk; ++i) T.sp_off[i + 1] += T.sp_off[i];
+        T.sp_ent.resize((size_t)T.sp_off[nblk]);
+        fill.assign(T.sp_off.begin(), T.sp_off.end() - 1);
+      }
+      for (int f = 0; f < F; ++f)
+        for (int pr = 0; pr < p->npair; ++pr)
+          for (int q = 0; q < P; ++q) {
+            const double *sp = g->scan_xyz + ((size_t)f * P + q) * 3;
+            const double U = sig * ((sp[0] - g->x0) / g->dx + p->jx[pr]);
+            const double V = sig * ((sp[1] - g->y0) / g->dy + p->jy[pr]);
+            const long long xlo = (long long)ceil(U - W - 1e-4), xhi = (long long)floor(U + W + 1e-4);
+            const long long ylo = (long long)ceil(V - W - 1e-4), yhi = (long long)floor(V + W + 1e-4);
+            const float b = T.apose[(size_t)f * P + q] + T.bpair[(size_t)f * p->npair + pr];
+            for (long long byr = fdiv(ylo, SAR_SP_BY); byr <= fdiv(yhi, SAR_SP_BY); ++byr)
+              for (long long bxr = fdiv(xlo, SAR_SP_BX); bxr <= fdiv(xhi, SAR_SP_BX); ++bxr) {
+                const size_t blk = ((size_t)f * nby + wmod(byr, nby)) * nbx + wmod(bxr, nbx);
+                if (pass == 0) {
+                  ++T.sp_off[blk + 1];
+                } else {
+                  SarSpreadEntry &e = T.sp_ent[(size_t)fill[blk]++];
+                  e.row = (int)(((size_t)f * p->npair + pr) * P + q);
+                  e.du = (float)(U - (double)(bxr * SAR_SP_BX));
+                  e.dv = (float)(V - (double)(byr * SAR_SP_BY));
+                  e.beta = b;
+                }
+              }
+          }
+    }
+    T.tw_f_off = T.tw.size() / 2;
+    twiddles(T.tw, Rx);
   }
 
   // O7 rolls and axes (reading R8)
@@ -463,13 +458,10 @@ int sar_plan_create(sar_plan **out, const sar_geom_desc *g, const sar_image_desc
   const size_t o_pi = off; off += al(T.pinv.size() * 4);
   const size_t o_tw = off; off += al(T.tw.size() * 4);
   const size_t o_cl = off; off += al(T.cls.size() * sizeof(SarClass));
-  const size_t o_nu_du = off; off += al(T.nu_du.size() * 4);
-  const size_t o_nu_dv = off; off += al(T.nu_dv.size() * 4);
-  const size_t o_nu_off = off; off += al(T.nu_off.size() * 4);
-  const size_t o_nu_cand = off; off += al(T.nu_cand.size() * 4);
   const size_t o_nu_dx = off; off += al(T.nu_decx.size() * 4);
   const size_t o_nu_dy = off; off += al(T.nu_decy.size() * 4);
-  const size_t o_nu_pm = off; off += al(T.nu_perm.size() * 2);
+  const size_t o_sp_off = off; off += al(T.sp_off.size() * 4);
+  const size_t o_sp_ent = off; off += al(T.sp_ent.size() * sizeof(SarSpreadEntry));
   ce = cudaMalloc(&p->d_tables, off);
   if (ce != cudaSuccess) {
     cudaGetLastError();
@@ -491,13 +483,10 @@ int sar_plan_create(sar_plan **out, const sar_geom_desc *g, const sar_image_desc
       (ce = up(o_pi, T.pinv.data(), T.pinv.size() * 4)) != cudaSuccess ||
       (ce = up(o_tw, T.tw.data(), T.tw.size() * 4)) != cudaSuccess ||
       (ce = up(o_cl, T.cls.data(), T.cls.size() * sizeof(SarClass))) != cudaSuccess ||
-      (ce = up(o_nu_du, T.nu_du.data(), T.nu_du.size() * 4)) != cudaSuccess ||
-      (ce = up(o_nu_dv, T.nu_dv.data(), T.nu_dv.size() * 4)) != cudaSuccess ||
-      (ce = up(o_nu_off, T.nu_off.data(), T.nu_off.size() * 4)) != cudaSuccess ||
-      (ce = up(o_nu_cand, T.nu_cand.data(), T.nu_cand.size() * 4)) != cudaSuccess ||
       (ce = up(o_nu_dx, T.nu_decx.data(), T.nu_decx.size() * 4)) != cudaSuccess ||
       (ce = up(o_nu_dy, T.nu_decy.data(), T.nu_decy.size() * 4)) != cudaSuccess ||
-      (ce = up(o_nu_pm, T.nu_perm.data(), T.nu_perm.size() * 2)) != cudaSuccess) {
+      (ce = up(o_sp_off, T.sp_off.data(), T.sp_off.size() * 4)) != cudaSuccess ||
+      (ce = up(o_sp_ent, T.sp_ent.data(), T.sp_ent.size() * sizeof(SarSpreadEntry))) != cudaSuccess) {
     free_plan(p);
     return cuda_fail(ce, "table upload");
   }
@@ -505,7 +494,7 @@ int sar_plan_create(sar_plan **out, const sar_geom_desc *g, const sar_image_desc
   if (F > 0) {
     if (cudaMalloc(&p->d_w0, n0 * sizeof(float2)) != cudaSuccess ||
         cudaMalloc(&p->d_w1, n1 * sizeof(float2)) != cudaSuccess ||
-      ((flags & SAR_GRID_NUFFT) && cudaMalloc(&p->d_wh, 2 * n0 * sizeof(float2)) != cudaSuccess)) {
+      ((flags & SAR_GRID_NUFFT) && cudaMalloc(&p->d_wh, 4 * n0 * sizeof(float2)) != cudaSuccess)) {
       cudaGetLastError();
       free_plan(p);
       return fail(SAR_ERR_OOM, "workspace allocation failed");
@@ -531,15 +520,13 @@ int sar_plan_create(sar_plan **out, const sar_geom_desc *g, const sar_image_desc
   v.nufft = (flags & SAR_GRID_NUFFT) ? 1 : 0;
   v.nu_w = 6;
   v.nu_s2 = (float)(6.0 / (2.0 * M_PI * (1.0 - 1.0 / 4.0)));
-  v.nu_dumax = T.nu_dumax;
-  v.nu_br = T.nu_br;
-  v.nu_du = (const float *)(base + o_nu_du);
-  v.nu_dv = (const float *)(base + o_nu_dv);
-  v.nu_off = (const int *)(base + o_nu_off);
-  v.nu_cand = (const int *)(base + o_nu_cand);
   v.nu_decx = (const float *)(base + o_nu_dx);
   v.nu_decy = (const float *)(base + o_nu_dy);
-  v.nu_perm = (const short *)(base + o_nu_pm);
+  v.sp_nbx = T.sp_nbx;
+  v.sp_nby = T.sp_nby;
+  v.sp_off = (const int *)(base + o_sp_off);
+  v.sp_ent = (const SarSpreadEntry *)(base + o_sp_ent);
+  v.tw_f = (const float2 *)(base + o_tw) + T.tw_f_off;
   v.cls = (const SarClass *)(base + o_cl);
   v.pinv = T.pinv.empty() ? nullptr : (const float2 *)(base + o_pi);
   v.tw_x = (const float2 *)(base + o_tw);

@@ -23,6 +23,16 @@ struct SarClass {
   int col[4];      // column index b'*nx + a' of each member
 };
 
+// NUFFT spread (K1s) block of fine cells and its entry: one virtual element
+// seen from one block (reading R19).
+#define SAR_SP_BX 4
+#define SAR_SP_BY 4
+struct SarSpreadEntry {
+  int row;      // sample row (f * npair + pair) * P + pose of the raw input
+  float du, dv; // fine position relative to the block origin (unwrapped)
+  float beta;   // -2 d_z + beta_MIMO (m); phase = beta * k
+};
+
 // Everything a kernel needs, passed by value (fits the 32 KB parameter space).
 struct SarDeviceView {
   int F, nt, nr, npair, npx, npy, P, nk, nx, ny, nz;
@@ -32,16 +42,15 @@ struct SarDeviceView {
   int no_comp;
   int jx[SAR_MAX_PAIRS], jy[SAR_MAX_PAIRS];  // virtual-node offsets, pair = t*nr + r
   // SAR_GRID_NUFFT (reading R19): fine grid 2 nx x 2 ny, Gaussian half width
-  // nu_w fine cells, variance nu_s2; per pose the fine-cell offset of the true
-  // position from its raster node (du = 2((x-x0)/dx - ix), dv likewise)
+  // nu_w fine cells, variance nu_s2
   int nufft, nu_w;
-  float nu_s2, nu_dumax;
-  const float *nu_du, *nu_dv;      // [F*P]
-  const int *nu_off, *nu_cand;     // CSR per (frame, band of fine rows): (pair << 16 | pose row)
-  const short *nu_perm;            // [F][npy][npx] poses of a row sorted by fine x position
-  int nu_br;                       // fine rows per band
+  float nu_s2;
   const float *nu_decx, *nu_decy;  // [nx], [ny] 1/Phi deconvolution factors
-  float2 *wh;                      // [F][2 ny][nx][nk] x-transformed fine rows
+  float2 *wh;                      // [F][2 ny][2 nx][nk] fine grid (spread, then x-transformed in place)
+  int sp_nbx, sp_nby;              // spread blocks per fine row / column
+  const int *sp_off;               // [F*sp_nby*sp_nbx + 1] CSR offsets
+  const SarSpreadEntry *sp_ent;    // entries
+  const float2 *tw_f;              // [2 nx] exp(-2 pi i m / (2 nx)) (fine x-FFT)
   const float *apose;   // [F][P]      -2 d_z (m), fp32
   const float *bpair;   // [F][npair]  (d_x^2+d_y^2)/(4 R_ref) (m), fp32
   const float *kturn;   // [nk]        k_i / (2 pi) (turns per metre), fp32
@@ -89,8 +98,8 @@ struct sar_plan {
   bool prof_events = false;
   cudaStream_t last_stream = nullptr;
   // TMA tensor maps over the workspace (built once per plan; valid flags)
-  CUtensorMap tm_w0_mid, tm_w1_mid, tm_w1_rows, tm_ap, tm_s;
-  bool tma_mid0 = false, tma_mid1 = false, tma_rows1 = false, tma_ap = false, tma_s = false;
+  CUtensorMap tm_w0_mid, tm_w1_mid, tm_w1_rows, tm_ap, tm_s, tm_fine;
+  bool tma_mid0 = false, tma_mid1 = false, tma_rows1 = false, tma_ap = false, tma_s = false, tma_fine = false;
   const void *tm_s_ptr = nullptr;  // data pointer tm_s was encoded for
   int k1_br = 0;                   // pose rows per K1 TMA box
   bool k1_regacc = false;          // every j^x offset is 0: K1 sums in registers

@@ -45,6 +45,25 @@ __global__ void __launch_bounds__(NT) run_new(const float2 *x, float2 *y, const 
   }
 }
 
+// the split pass-2 variant (fft_ctx SPLIT2), pass-1 radix R1S (0 = default)
+template <int N, int DIR, int NT, int R1S>
+__global__ void __launch_bounds__(NT) run_split(const float2 *x, float2 *y, const float2 *twg, int reps) {
+  extern __shared__ float2 sm[];
+  float2 *work = sm;
+  float2 *tw = sm + N * C;
+  for (int i = threadIdx.x; i < N; i += NT) tw[i] = twg[i];
+  __syncthreads();
+  for (int rep = 0; rep < reps; ++rep) {
+    sarfft2::fft_ctx<N, C, C, NT, DIR, 0, false, R1S, true>(
+        work, tw, threadIdx.x, [&](int c, int n) { return x[n * C + c]; }, [] {}, [](int c) { return c; },
+        [&](int c, int n, float2 v) {
+          if (rep == reps - 1 && blockIdx.x == 0) y[n * C + c] = v;
+          else if (v.x == 12345.f) y[0] = v;
+        });
+    __syncthreads();
+  }
+}
+
 template <int N, int DIR, int NT>
 __global__ void __launch_bounds__(NT) run_old(const float2 *x, float2 *y, const float2 *twg, int reps) {
   extern __shared__ float2 sm[];
@@ -79,10 +98,15 @@ void check(float2 *dx, float2 *dy, double2 *dX, float2 *dtw, bool bench) {
   std::vector<double2> X(N * C);
   std::vector<float2> Y(N * C);
   cudaMemcpy(X.data(), dX, N * C * 16, cudaMemcpyDeviceToHost);
-  for (int which = 0; which < 2; ++which) {
+  constexpr bool HAS_SPLIT = N >= 64;
+  constexpr int R1S = N == 512 ? 16 : 0;
+  if constexpr (HAS_SPLIT)
+    cudaFuncSetAttribute(run_split<N, DIR, NT, R1S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smn);
+  for (int which = 0; which < (HAS_SPLIT ? 3 : 2); ++which) {
     cudaMemset(dy, 0, N * C * 8);
     if (which == 0) run_new<N, DIR, NT><<<1, NT, smn>>>(dx, dy, dtw, 1);
-    else run_old<N, DIR, NTO><<<1, NTO, smo>>>(dx, dy, dtw, 1);
+    else if (which == 1) run_old<N, DIR, NTO><<<1, NTO, smo>>>(dx, dy, dtw, 1);
+    else if constexpr (HAS_SPLIT) run_split<N, DIR, NT, R1S><<<1, NT, smn>>>(dx, dy, dtw, 1);
     cudaError_t e = cudaDeviceSynchronize();
     if (e != cudaSuccess) { printf("CUDA error %s\n", cudaGetErrorString(e)); exit(1); }
     cudaMemcpy(Y.data(), dy, N * C * 8, cudaMemcpyDeviceToHost);
@@ -101,13 +125,14 @@ void check(float2 *dx, float2 *dy, double2 *dX, float2 *dtw, bool bench) {
       cudaEventCreate(&b);
       cudaEventRecord(a);
       if (which == 0) run_new<N, DIR, NT><<<blocks, NT, smn>>>(dx, dy, dtw, reps);
-      else run_old<N, DIR, NTO><<<blocks, NTO, smo>>>(dx, dy, dtw, reps);
+      else if (which == 1) run_old<N, DIR, NTO><<<blocks, NTO, smo>>>(dx, dy, dtw, reps);
+      else if constexpr (HAS_SPLIT) run_split<N, DIR, NT, R1S><<<blocks, NT, smn>>>(dx, dy, dtw, reps);
       cudaEventRecord(b);
       cudaEventSynchronize(b);
       cudaEventElapsedTime(&ms, a, b);
       gel = (double)blocks * reps * N * C / (ms * 1e-3) / 1e9;
     }
-    printf("N=%5d DIR=%+d %s rel-L2 %.3e  %s%.1f Gelem/s\n", N, DIR, which == 0 ? "reg2 " : "tile3", sqrt(num / den),
+    printf("N=%5d DIR=%+d %s rel-L2 %.3e  %s%.1f Gelem/s\n", N, DIR, which == 0 ? "reg2 " : (which == 1 ? "tile3" : "split"), sqrt(num / den),
            bench ? "" : "(no bench) ", gel);
     if (!(sqrt(num / den) < 5e-6)) { printf("FAIL\n"); exit(1); }
   }
