@@ -333,6 +333,89 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+def run_slab(args):
+    """One image split over the N ranks (single-image slab decomposition,
+    sar_slab_stage + two NCCL all-to-alls): strong scaling of the Large
+    image.  Every rank holds the raw samples of the image (K1 reads only the
+    pose rows of its lattice rows)."""
+    import torch
+    import scenes
+    import scenes.gpu
+    import paper_2305_02064_b200 as sar
+    from paper_2305_02064_b200 import build as sbuild, slab
+    from paper_2305_02064_b200.shard import max_over_ranks
+
+    rank, world, local = _dist()
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if rank == 0:
+        sbuild.build()
+        scenes.gpu.build()
+    if world > 1:
+        dist.barrier()
+    sc = scenes.make_scene(args.config)
+    if sc.n_frames != 1:
+        raise SystemExit("--slab splits one image: use a single-frame config")
+    data = scenes.gpu.synthesize_gpu(sc, device=local)
+    plan = sar.SlabPlan.from_scene(sc, rank=rank, world=world, device=local)
+    image = torch.empty(sc.image_shape, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    xfn = slab.exchange if world > 1 else (lambda t, group=None: t)
+
+    def step():
+        slab.reconstruct(plan, data, image, exchange_fn=xfn)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+        ev1.record(stream)
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+    ms_total = max_over_ranks(ev0.elapsed_time(ev1), dist if world > 1 else None, dev)
+    ms_step = ms_total / args.steps
+    value = sc.n_samples / (ms_step * 1e-3) / 1e9
+    peak, peak_src = _peaks()
+    # per-rank algorithmic bytes: its share of the raw samples and of the image
+    alg_rank = sc.alg_bytes() / world
+    ach = alg_rank / (ms_step * 1e-3) / 1e9
+    xbytes = 8 * (int(np.prod(plan.send1_shape)) + int(np.prod(plan.send2_shape)))
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded scenes, GPU-synthesised Eq. (9) echo)",
+            "config": {"workload": args.config + " single image split over the ranks",
+                       "frames": 1, "tx": sc.n_tx, "rx": sc.n_rx, "poses": sc.n_pos, "n_k": sc.n_k,
+                       "image": [sc.nx, sc.ny, sc.nz], "samples_per_step": sc.n_samples,
+                       "l2": "inputs larger than L2 (no flush)",
+                       "parallelism": f"slab x{world}: y-rows -> all-to-all -> k_x columns -> all-to-all -> z-slots",
+                       "exchange_bytes_per_rank": xbytes},
+            "ms_per_image": ms_step,
+            "roofline": {"bound": "hbm", "kernel": "whole slab step (per rank)", "achieved": ach, "peak": peak,
+                         "unit": "GB/s", "frac": ach / peak, "traffic": None, "alg_bytes": alg_rank,
+                         "ms": ms_step, "peak_source": peak_src},
+            "cpu_baseline": None, "e2e": None,
+            "gpu_launches": 5 * args.steps,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    plan.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -345,6 +428,8 @@ def main():
                     help="comma-separated z planes (m): 2-D single-plane images (SAR_IMAGE_2D, Table I '2-D' rows) "
                          "instead of the 3-D volume")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--slab", action="store_true",
+                    help="split ONE image over the ranks (slab decomposition, two all-to-alls; strong scaling)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -353,6 +438,8 @@ def main():
         print("warning: --warmup < 3 is below the timing rules", file=sys.stderr)
     if args.impl == "reference":
         run_reference(args)
+    elif args.slab:
+        run_slab(args)
     else:
         run_ours(args)
 

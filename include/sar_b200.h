@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define SAR_B200_VERSION 2
+#define SAR_B200_VERSION 3
 
 typedef struct sar_plan sar_plan;       /* opaque */
 typedef struct CUstream_st *sar_stream; /* == cudaStream_t; NULL = legacy default stream */
@@ -181,6 +181,59 @@ int sar_plan_peaks(sar_plan *p, float *h_peaks);
 
 /* Number of kernel launches one sar_reconstruct call enqueues (5; 0 if F = 0). */
 int sar_plan_launches_per_call(const sar_plan *p, int32_t *n);
+
+/* ---- single-image slab decomposition over G GPUs ----
+ *
+ * One image (F == 1) split over `world` = G ranks, one plan and one GPU per
+ * rank; the caller moves the data between the three stages with two
+ * all-to-all exchanges (e.g. NCCL all_to_all_single over NVLink).  With
+ * nx' = nx/G, ny' = ny/G, nz' = nz/G (G must divide nx, ny and nz):
+ *   stage 1 (rank r): K1 on the virtual rows [r ny', (r+1) ny') -- the
+ *     correction + MIMO accumulation + x-FFT of those lattice rows (Eqs.
+ *     (11)-(12); FT_2D along x) -- packed for exchange #1:
+ *     d_out = complex64 [G][ny'][nx'][n_k], block h = the columns
+ *     [h nx', (h+1) nx') destined for rank h.  d_in = the raw samples
+ *     (the full [1][n_tx][n_rx][npy*npx][n_k] array; only the pose rows that
+ *     reach this rank's lattice rows are read).
+ *   exchange #1: rank h receives block h of every rank g in order of g:
+ *     complex64 [G][ny'][nx'][n_k] == the x-slab [ny][nx'][n_k].
+ *   stage 2 (rank r): on the x-slab (columns [r nx', (r+1) nx')): y-FFT (in
+ *     place in d_in, which is overwritten), RMA filter + Stolt + z-IFFT
+ *     (Eqs. (13)-(14)) and y-IFFT, packed for exchange #2:
+ *     d_out = complex64 [G][ny][nx'][nz'], block h = the z-slots
+ *     [h nz', (h+1) nz').
+ *   exchange #2: rank h receives block h of every rank g in order of g:
+ *     complex64 [G][ny][nx'][nz'].
+ *   stage 3 (rank r): x-IFFT + magnitude of the z-slots [r nz', (r+1) nz'],
+ *     written into d_image = float32 (complex64 with SAR_OUTPUT_COMPLEX)
+ *     [nz][ny][nx], the same rolled layout as sar_reconstruct; only the nz'
+ *     planes this rank owns are written (plane m = (z + nz/2) mod nz of
+ *     z-slot z, reading R8), the others are left untouched.
+ * Every element is computed by the same kernel code as sar_reconstruct, so
+ * the assembled image equals the whole-image result bit for bit.  All three
+ * calls are asynchronous on `stream`; d_in / d_out / d_image are device
+ * pointers owned by the caller, 16-byte aligned, and must not alias.  The
+ * plan also works as a whole-image plan (sar_reconstruct). */
+typedef struct {
+  int32_t rank;   /* 0 <= rank < world */
+  int32_t world;  /* G >= 1, divides nx, ny and nz */
+} sar_slab_desc;
+
+/* Create the plan of one rank.  Errors: as sar_plan_create, plus
+ * INVALID_ARG (bad rank/world, G does not divide the sizes, F != 1) and
+ * UNSUPPORTED (SAR_IMAGE_2D, SAR_GRID_NUFFT or SAR_REPORT_PEAK). */
+int sar_plan_create_slab(sar_plan **out, const sar_geom_desc *g, const sar_image_desc *im,
+                         uint32_t flags, const sar_slab_desc *slab);
+
+/* Bytes of the stage-1 and stage-2 output buffers (= the exchange buffers):
+ * *send1 = ny'*nx*n_k*8 (G blocks), *send2 = ny*nx'*nz*8 (G blocks).
+ * Errors: INVALID_ARG (NULL, not a slab plan). */
+int sar_slab_buffer_bytes(const sar_plan *p, size_t *send1, size_t *send2);
+
+/* Run stage 1, 2 or 3 of this rank (see above).  Errors: INVALID_ARG (stage
+ * outside 1..3, NULL pointers, not a slab plan), CUDA. */
+int sar_slab_stage(sar_plan *p, int32_t stage, const void *d_in, void *d_out, void *d_image,
+                   sar_stream stream);
 
 /* ---- debug / parity entry points (same kernels as sar_reconstruct) ---- */
 

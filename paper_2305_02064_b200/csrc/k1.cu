@@ -31,7 +31,7 @@ __global__ void __launch_bounds__(nt_for(NX), minb_for(NX))
   extern __shared__ float2 tile[];  // [NX][16]
   const int tid = threadIdx.x;
   const int kbase = blockIdx.x * KC;
-  const int vy = blockIdx.y;
+  const int vy = v.vy0 + blockIdx.y;
   const int f = blockIdx.z;
 
   static_assert(NT % KC == 0, "k lane of a thread is fixed: kk = tid % 16");
@@ -92,7 +92,7 @@ __global__ void __launch_bounds__(nt_for(NX), minb_for(NX))
   __syncthreads();
   if constexpr (DO_FFT) sarfft::tile_fft<NX, KC, KC, NT, -1>(tile, v.tw_x, tid);
 
-  float2 *out = v.w0 + ((size_t)(f * v.ny + vy) * NX) * (size_t)v.nk;
+  float2 *out = v.w0 + ((size_t)(f * v.nvy + blockIdx.y) * NX) * (size_t)v.nk;
 #pragma unroll
   for (int e = 0; e < E; ++e) {
     const int item = tid + e * NT;
@@ -134,7 +134,7 @@ __device__ __forceinline__ bool k1_next(const SarDeviceView &v, K1Job &j, int ni
   if (++j.b < nbox) return true;
   j.b = 0;
   for (;;) {
-    const int vy = (j.item / nchunk) % v.ny;
+    const int vy = v.vy0 + (j.item / nchunk) % v.nvy;
     while (++j.pr < v.npair)
       if (k1_pair_valid(v, vy, j.pr)) return true;
     j.item += gridDim.x;
@@ -185,7 +185,7 @@ __global__ void __launch_bounds__(K1_NT + 32, 1)
           const int st = n % K1_STAGES;
           if (n >= K1_STAGES) sartma::mbar_wait(&empty[st], ((n / K1_STAGES) - 1) & 1);
           const int kc = j.item % nchunk, rest = j.item / nchunk;
-          const int vy = rest % v.ny, f = rest / v.ny;
+          const int vy = v.vy0 + rest % v.nvy, f = rest / v.nvy;
           int iy = vy - v.jy[j.pr];
           if (iy < 0) iy += v.ny;
           const int t = j.pr / v.nr, r = j.pr - t * v.nr;
@@ -208,7 +208,8 @@ __global__ void __launch_bounds__(K1_NT + 32, 1)
   unsigned jobctr = 0;
   for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
     const int kc = item % nchunk, rest = item / nchunk;
-    const int vy = rest % v.ny, f = rest / v.ny;
+    const int vyl = rest % v.nvy, f = rest / v.nvy;
+    const int vy = v.vy0 + vyl;
     const int k0 = kc * C + kq;
     const float kt = k0 < v.nk ? __ldg(v.kturn + k0) : 0.f;
     float2 acc[REGACC ? MAXB * UPB * K1_KT : 1];
@@ -286,7 +287,7 @@ __global__ void __launch_bounds__(K1_NT + 32, 1)
     sarfft::tile_sync<1, K1_NT>();
     // x-FFT (two-pass register FFT; the accumulation tile doubles as its work
     // tile) with the transformed rows stored straight to W0
-    float2 *out = v.w0 + ((size_t)(f * v.ny + vy) * NX) * (size_t)v.nk + kc * C;
+    float2 *out = v.w0 + ((size_t)(f * v.nvy + vyl) * NX) * (size_t)v.nk + kc * C;
     const int cmax = v.nk - kc * C;
     sarfft2::fft<NX, C, C, K1_NT, -1, 1, false, (NX == 512 ? 16 : 0)>(
         tile, tws, tid, [&](int c, int m) { return tile[m * C + c]; }, [] {},
@@ -320,7 +321,7 @@ cudaError_t launch_k1(const SarDeviceView &v, const float2 *data, bool fft, cuda
   if (fft && tm_s && tm_ap && v.nx >= 64 && v.nx <= 512 && v.k1_step_ok) {
     const int C = k1c_for(v.nx);
     const int nchunk = (v.nk + C - 1) / C;
-    const int nitems = nchunk * v.ny * v.F;
+    const int nitems = nchunk * v.nvy * v.F;
     const int nbox = (v.npx + br - 1) / br;
     const int brmax = K1_BOX_BYTES / (C * 8);
     const size_t smem = (size_t)v.nx * C * sizeof(float2) + K1_STAGES * ((size_t)K1_BOX_BYTES + brmax * sizeof(float)) +
@@ -339,7 +340,7 @@ cudaError_t launch_k1(const SarDeviceView &v, const float2 *data, bool fft, cuda
 #undef X
     }
   }
-  dim3 grid((v.nk + KC - 1) / KC, v.ny, v.F);
+  dim3 grid((v.nk + KC - 1) / KC, v.nvy, v.F);
   const size_t smem = (size_t)v.nx * KC * sizeof(float2);
   switch (v.nx) {
 #define X(N)                                                                                   \

@@ -52,7 +52,7 @@ __global__ void __launch_bounds__(K3C_NT, 4) k3_class(const SarDeviceView v) {
   float2 *fout = fin + (size_t)CC * nk;              // [NZ][LD]  Stolt output / FFT work
   const int tid = threadIdx.x;
   const int ncol = v.nx * v.ny;
-  const int nclass = (v.nx / 2 + 1) * (v.ny / 2 + 1);
+  const int nclass = v.ncls;
   const int q0 = blockIdx.x * CL;
   const int f = blockIdx.y;
   if (tid < CL) {
@@ -319,8 +319,7 @@ __global__ void __launch_bounds__(K3P_NG * K3P_G + 32, 1) k3_pp(const SarDeviceV
     // write the stage header, and every member column is issued by its own
     // lane (cp.async.bulk, one mbarrier transaction per item)
     const int lane = tid & 31;
-    const int hx = v.nx / 2 + 1, hy = v.ny / 2 + 1;
-    const int nclass = hx * hy;
+    const int nclass = v.ncls;
     auto fetch = [&](int item, SarClass &c) {
       const int f = item / nitems_f;
       const int q = (item - f * nitems_f) * CL + lane;
@@ -400,7 +399,7 @@ __global__ void __launch_bounds__(K3P2_NT) k3_plane(const SarDeviceView v) {
   const int lane = threadIdx.x & 31;
   const int q = blockIdx.x * (K3P2_NT / 32) + (threadIdx.x >> 5);
   const int f = blockIdx.y;
-  const int nclass = (v.nx / 2 + 1) * (v.ny / 2 + 1);
+  const int nclass = v.ncls;
   if (q >= nclass) return;
   const SarClass &c = v.cls[q];
   const int nm = c.nmem, nk = v.nk, ns = v.nz;
@@ -500,7 +499,7 @@ cudaError_t launch_v(K kernel, dim3 grid, int nt, size_t smem, cudaStream_t s, c
 
 cudaError_t launch_k3(const SarDeviceView &v, bool ifft, cudaStream_t s, int num_sms) {
   if ((v.nk & 1) == 0 && v.nz >= 256 && !getenv("SAR_K3_PLAIN")) {
-    const int nclass = (v.nx / 2 + 1) * (v.ny / 2 + 1);
+    const int nclass = v.ncls;
     switch (v.nz) {
 #define X(N)                                                                                                   \
   case N: {                                                                                                    \
@@ -520,7 +519,7 @@ cudaError_t launch_k3(const SarDeviceView &v, bool ifft, cudaStream_t s, int num
 #undef X
     }
   }
-  const int nclass = (v.nx / 2 + 1) * (v.ny / 2 + 1);
+  const int nclass = v.ncls;
   switch (v.nz) {
 #define X(N)                                                                                                   \
   case N: {                                                                                                    \
@@ -543,7 +542,7 @@ cudaError_t launch_k3(const SarDeviceView &v, bool ifft, cudaStream_t s, int num
 }
 
 cudaError_t launch_k3_plane(const SarDeviceView &v, cudaStream_t s) {
-  const int nclass = (v.nx / 2 + 1) * (v.ny / 2 + 1);
+  const int nclass = v.ncls;
   const int cpb = K3P2_NT / 32;
   k3_plane<<<dim3((nclass + cpb - 1) / cpb, v.F), K3P2_NT, 0, s>>>(v);
   return cudaGetLastError();

@@ -90,7 +90,7 @@ __global__ void __launch_bounds__(sarfft2::nt_fft<NX, KC>() + 32)
     const int f = fy / v.ny, y = fy - f * v.ny;
     int iy = y - ry;
     if (iy < 0) iy += v.ny;
-    OT *outp = reinterpret_cast<OT *>(img) + ((size_t)f * nz * v.ny + iy) * NX;
+    OT *outp = reinterpret_cast<OT *>(img) + ((size_t)f * v.nz_img * v.ny + iy) * NX;
     const float2 *stage = ring + (size_t)st * NX * KC;
     float pk = 0.f;
     // the image row of z-slot c is resolved once per butterfly (prep), so a
@@ -103,8 +103,8 @@ __global__ void __launch_bounds__(sarfft2::nt_fft<NX, KC>() + 32)
         [&](int c) -> OT * {
           const int z = zc * KC + c;
           if (z >= nz) return nullptr;
-          int m = z + v.zroll;
-          if (m >= nz) m -= nz;
+          int m = z + v.z_off + v.zroll;
+          if (m >= v.nz_img) m -= v.nz_img;
           return outp + (size_t)m * zstride;
         },
         [&](OT *rowp, int a, float2 o) {
@@ -163,11 +163,11 @@ __global__ void __launch_bounds__(nt_for(NX), minb_for(NX))
     const int zz = item / NX, ix = item - zz * NX;
     const int z = zbase + zz;
     if (z >= nz) continue;
-    int m = z + v.zroll;
-    if (m >= nz) m -= nz;
+    int m = z + v.z_off + v.zroll;
+    if (m >= v.nz_img) m -= v.nz_img;
     const int xs = (ix + rx) & (NX - 1);
     const float2 o = tile[xs * LD + zz];
-    const size_t off = ((size_t)(f * nz + m) * v.ny + iy) * NX + ix;
+    const size_t off = ((size_t)(f * v.nz_img + m) * v.ny + iy) * NX + ix;
     const float mag = sqrtf(fmaf(o.x, o.x, o.y * o.y)) * sc;
     pk = fmaxf(pk, mag);
     if constexpr (CPLX) {

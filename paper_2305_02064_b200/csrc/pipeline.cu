@@ -205,3 +205,121 @@ int sar_build_tensor_maps(sar_plan *p) {
   return SAR_OK;
 }
 
+
+// ------------------------------------------------ slab decomposition ----
+namespace {
+// dst + h*dhs + r*dp  <-  src + h*shs + r*sp, Wb bytes per (h, r), for h < G,
+// r < H: the pack / unpack of the slab exchanges (16-byte vectors, streaming)
+__global__ void k_block_copy(char *__restrict__ dst, const char *__restrict__ src, unsigned G, unsigned H, unsigned V,
+                             long long shs, long long sp, long long dhs, long long dp) {
+  const unsigned total = G * H * V;   // < 2^31 (checked by the launcher)
+  for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const unsigned q = i / V, v = i - q * V;
+    const unsigned h = q / H, r = q - h * H;
+    const float4 x = __ldcs(reinterpret_cast<const float4 *>(src + h * shs + r * sp) + v);
+    __stcs(reinterpret_cast<float4 *>(dst + h * dhs + r * dp) + v, x);
+  }
+}
+
+cudaError_t block_copy(void *dst, const void *src, int G, long long H, long long Wb, long long shs, long long sp,
+                       long long dhs, long long dp, int num_sms, cudaStream_t s) {
+  if (Wb % 16 || shs % 16 || sp % 16 || dhs % 16 || dp % 16 || (double)G * H * (Wb / 16) >= 2147483648.0) {
+    for (int h = 0; h < G; ++h) {
+      cudaError_t e = cudaMemcpy2DAsync(static_cast<char *>(dst) + h * dhs, dp, static_cast<const char *>(src) + h * shs,
+                                        sp, Wb, H, cudaMemcpyDeviceToDevice, s);
+      if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+  }
+  const int V = (int)(Wb / 16);
+  const long long total = (long long)G * H * V;
+  const long long want = (total + 255) / 256;
+  const int grid = (int)(want < 8LL * num_sms ? want : 8LL * num_sms);
+  k_block_copy<<<grid > 0 ? grid : 1, 256, 0, s>>>(static_cast<char *>(dst), static_cast<const char *>(src),
+                                                  (unsigned)G, (unsigned)H, (unsigned)V, shs, sp, dhs, dp);
+  return cudaGetLastError();
+}
+}  // namespace
+
+// Buffers of a slab plan (the whole-image workspace is reused): W0 holds the
+// K1 output of this rank's lattice rows [ny'][nx][nk] and, in stage 3, the
+// z-slab [ny][nx][nz']; W1 holds the x-slab's Stolt / y-IFFT volume
+// [ny][nx'][nz].
+int sar_slab_setup(sar_plan *p) {
+  const SarDeviceView &v = p->v;
+  const int G = p->slab_world, nxl = v.nx / G, nzl = v.nz / G;
+  if ((size_t)v.nk < (size_t)nzl) {
+    sar_set_error("slab plans need n_k >= nz / world (the z-slab reuses the lattice buffer)");
+    return SAR_ERR_UNSUPPORTED;
+  }
+  p->tma_w1x = p->tma_w1z = p->tma_r1 = false;
+  p->tm_r1_ptr = nullptr;
+  if (getenv("SAR_NO_TMA")) return SAR_OK;
+  const uint32_t rows = v.ny < 256 ? v.ny : 256, xr = v.nx < 256 ? v.nx : 256;
+  p->tma_w1x = encode3d(&p->tm_w1x_mid, v.w1, v.nz, nxl, v.ny, KC, 1, rows);
+  p->tma_w1z = encode3d(&p->tm_w1z_rows, v.w0, nzl, v.nx, v.ny, KC, xr, 1);
+  return SAR_OK;
+}
+
+int sar_slab_launch(sar_plan *p, int stage, const void *d_in, void *d_out, void *d_image, cudaStream_t s) {
+  const SarDeviceView &v = p->v;
+  const int G = p->slab_world, r = p->slab_rank;
+  const int nxl = v.nx / G, nyl = v.ny / G, nzl = v.nz / G;
+  const size_t c8 = sizeof(float2);
+  cudaError_t e = cudaSuccess;
+  if (stage == 1) {
+    SarDeviceView vk = v;
+    vk.vy0 = r * nyl;
+    vk.nvy = nyl;
+    const CUtensorMap *tm_s = nullptr;
+    if (p->tma_ap) {
+      if (p->tm_s_ptr != d_in) p->tma_s = sar_encode_input_map(p, d_in);
+      if (p->tma_s) tm_s = &p->tm_s;
+    }
+    SAR_CHECK(launch_k1(vk, static_cast<const float2 *>(d_in), true, s, tm_s, p->tma_ap ? &p->tm_ap : nullptr,
+                        p->k1_br, p->k1_regacc, p->num_sms));
+    // pack for exchange #1: block h = columns [h nx', (h+1) nx') of every row
+    SAR_CHECK(block_copy(d_out, v.w0, G, nyl, (long long)nxl * v.nk * c8, (long long)nxl * v.nk * c8,
+                         (long long)v.nx * v.nk * c8, (long long)nyl * nxl * v.nk * c8, (long long)nxl * v.nk * c8,
+                         p->num_sms, s));
+    return SAR_OK;
+  }
+  if (stage == 2) {
+    float2 *xs = static_cast<float2 *>(const_cast<void *>(d_in));   // the x-slab [ny][nx'][nk], overwritten
+    const CUtensorMap *tm = nullptr;
+    if (!getenv("SAR_NO_TMA")) {
+      if (p->tm_r1_ptr != d_in) {
+        const uint32_t rows = v.ny < 256 ? v.ny : 256;
+        p->tma_r1 = encode3d(&p->tm_r1_mid, xs, v.nk, nxl, v.ny, KC, 1, rows);
+        p->tm_r1_ptr = d_in;
+      }
+      if (p->tma_r1) tm = &p->tm_r1_mid;
+    }
+    SAR_CHECK(launch_mid<-1>(xs, v.tw_y, 1, v.ny, nxl, v.nk, s, tm, p->num_sms));
+    SarDeviceView vk = v;
+    vk.nx = nxl;
+    vk.cls = p->d_slab_cls;
+    vk.ncls = p->slab_ncls;
+    vk.w0 = xs;
+    SAR_CHECK(launch_k3(vk, true, s, p->num_sms));
+    SAR_CHECK(launch_mid<+1>(v.w1, v.tw_y, 1, v.ny, nxl, v.nz, s, p->tma_w1x ? &p->tm_w1x_mid : nullptr,
+                             p->num_sms));
+    // pack for exchange #2: block h = z-slots [h nz', (h+1) nz') of every column
+    SAR_CHECK(block_copy(d_out, v.w1, G, (long long)v.ny * nxl, (long long)nzl * c8, (long long)nzl * c8,
+                         (long long)v.nz * c8, (long long)v.ny * nxl * nzl * c8, (long long)nzl * c8, p->num_sms, s));
+    return SAR_OK;
+  }
+  // stage 3: unpack [G][ny][nx'][nz'] (block g = columns [g nx', (g+1) nx'))
+  // into the z-slab [ny][nx][nz'] (in W0), then x-IFFT + magnitude
+  float2 *zs = v.w0;
+  SAR_CHECK(block_copy(zs, d_in, G, v.ny, (long long)nxl * nzl * c8, (long long)v.ny * nxl * nzl * c8,
+                       (long long)nxl * nzl * c8, (long long)nxl * nzl * c8, (long long)v.nx * nzl * c8, p->num_sms, s));
+  SarDeviceView vk = v;
+  vk.nz = nzl;
+  vk.z_off = r * nzl;
+  vk.nz_img = v.nz;
+  vk.w1 = zs;
+  SAR_CHECK(launch_k4b(vk, d_image, (p->flags & SAR_OUTPUT_COMPLEX) != 0, s, p->tma_w1z ? &p->tm_w1z_rows : nullptr,
+                       p->num_sms));
+  return SAR_OK;
+}

@@ -60,6 +60,7 @@ void free_plan(sar_plan *p) {
   cudaFree(p->d_cnt);
   cudaFree(p->d_wh);
   cudaFree(p->d_peak);
+  cudaFree(p->d_slab_cls);
   delete p;
 }
 
@@ -545,6 +546,11 @@ int sar_plan_create(sar_plan **out, const sar_geom_desc *g, const sar_image_desc
   }
   v.mode2d = (flags & SAR_IMAGE_2D) ? 1 : 0;
   v.zroll = v.mode2d ? 0 : p->nz / 2;
+  v.vy0 = 0;
+  v.nvy = p->ny;
+  v.ncls = (p->nx / 2 + 1) * (p->ny / 2 + 1);
+  v.z_off = 0;
+  v.nz_img = p->nz;
   v.img_scale = (float)(1.0 / ((double)p->nx * p->ny * (v.mode2d ? 1 : p->nz)));
   {
     // K1 step phasor exp(j dk beta): 5th-order Taylor needs |dk beta| small
@@ -580,6 +586,84 @@ int sar_plan_create(sar_plan **out, const sar_geom_desc *g, const sar_image_desc
   }
   *out = p;
   return SAR_OK;
+}
+
+int sar_plan_create_slab(sar_plan **out, const sar_geom_desc *g, const sar_image_desc *im, uint32_t flags,
+                         const sar_slab_desc *slab) {
+  if (!out) return fail(SAR_ERR_INVALID_ARG, "out is NULL");
+  *out = nullptr;
+  if (!slab || !g || !im) return fail(SAR_ERR_INVALID_ARG, "slab, geometry or image descriptor is NULL");
+  const int G = slab->world, r = slab->rank;
+  if (G < 1 || r < 0 || r >= G) return fail(SAR_ERR_INVALID_ARG, "slab rank/world out of range");
+  if (flags & (SAR_IMAGE_2D | SAR_GRID_NUFFT | SAR_REPORT_PEAK))
+    return fail(SAR_ERR_UNSUPPORTED, "slab plans support the 3-D RASTER path only");
+  if (g->n_frames != 1) return fail(SAR_ERR_INVALID_ARG, "slab plans reconstruct one image (n_frames == 1)");
+  if (im->nx % G || im->ny % G || im->nz % G || im->nx / G < 1 || im->nz / G < 1)
+    return fail(SAR_ERR_INVALID_ARG, "world must divide nx, ny and nz");
+  sar_plan *p = nullptr;
+  int st = sar_plan_create(&p, g, im, flags);
+  if (st != SAR_OK) return st;
+  DeviceGuard guard(p->device);
+  p->slab_rank = r;
+  p->slab_world = G;
+  // the x-slab's Stolt classes: every mirror class restricted to the member
+  // columns a in [r nx', (r+1) nx'), local column index b nx' + (a - r nx');
+  // k_r^2 and the in-band range are the whole-image class's (bit-identical)
+  const int nxl = p->nx / G, a0 = r * nxl;
+  std::vector<SarClass> full((size_t)p->v.ncls), mine;
+  cudaError_t ce = cudaMemcpy(full.data(), p->v.cls, full.size() * sizeof(SarClass), cudaMemcpyDeviceToHost);
+  if (ce != cudaSuccess) {
+    sar_plan_destroy(p);
+    return cuda_fail(ce, "class table download");
+  }
+  for (const SarClass &c : full) {
+    SarClass m = c;
+    m.nmem = 0;
+    for (int i = 0; i < c.nmem; ++i) {
+      const int b = c.col[i] / p->nx, a = c.col[i] - b * p->nx;
+      if (a >= a0 && a < a0 + nxl) m.col[m.nmem++] = b * nxl + (a - a0);
+    }
+    if (m.nmem) mine.push_back(m);
+  }
+  p->slab_ncls = (int)mine.size();
+  if (cudaMalloc(&p->d_slab_cls, std::max<size_t>(1, mine.size()) * sizeof(SarClass)) != cudaSuccess) {
+    cudaGetLastError();
+    sar_plan_destroy(p);
+    return fail(SAR_ERR_OOM, "slab class table allocation failed");
+  }
+  ce = cudaMemcpy(p->d_slab_cls, mine.data(), mine.size() * sizeof(SarClass), cudaMemcpyHostToDevice);
+  if (ce != cudaSuccess) {
+    sar_plan_destroy(p);
+    return cuda_fail(ce, "slab class table upload");
+  }
+  st = sar_slab_setup(p);
+  if (st != SAR_OK) {
+    sar_plan_destroy(p);
+    return st;
+  }
+  *out = p;
+  return SAR_OK;
+}
+
+int sar_slab_buffer_bytes(const sar_plan *p, size_t *send1, size_t *send2) {
+  if (!p || !send1 || !send2) return fail(SAR_ERR_INVALID_ARG, "NULL argument");
+  if (p->slab_world < 1) return fail(SAR_ERR_INVALID_ARG, "not a slab plan");
+  const int G = p->slab_world;
+  *send1 = (size_t)(p->ny / G) * p->nx * p->nk * sizeof(float) * 2;
+  *send2 = (size_t)p->ny * (p->nx / G) * p->nz * sizeof(float) * 2;
+  return SAR_OK;
+}
+
+int sar_slab_stage(sar_plan *p, int32_t stage, const void *d_in, void *d_out, void *d_image, sar_stream stream) {
+  if (!p) return fail(SAR_ERR_INVALID_ARG, "plan is NULL");
+  if (p->slab_world < 1) return fail(SAR_ERR_INVALID_ARG, "not a slab plan");
+  if (stage < 1 || stage > 3) return fail(SAR_ERR_INVALID_ARG, "stage must be 1, 2 or 3");
+  if (!d_in || (stage < 3 && !d_out) || (stage == 3 && !d_image))
+    return fail(SAR_ERR_INVALID_ARG, "NULL buffer");
+  DeviceGuard g(p->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  p->last_stream = s;
+  return sar_slab_launch(p, stage, d_in, d_out, d_image, s);
 }
 
 int sar_reconstruct(sar_plan *p, const void *d_data, void *d_image, sar_stream stream) {

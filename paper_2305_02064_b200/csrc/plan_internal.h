@@ -37,6 +37,10 @@ struct SarSpreadEntry {
 struct SarDeviceView {
   int F, nt, nr, npair, npx, npy, P, nk, nx, ny, nz;
   int roll_x, roll_y;
+  // slab decomposition (sar_slab_*; whole-image plans: 0, ny, (nx/2+1)(ny/2+1), 0, nz)
+  int vy0, nvy;         // K1: virtual rows [vy0, vy0 + nvy) written as rows 0.. of w0
+  int ncls;             // K3: entries of cls
+  int z_off, nz_img;    // K4b: the nz z-slots are z_off.. of an nz_img-plane image
   int zroll;            // output z roll: nz/2 (3-D, reading R8), 0 (2-D planes)
   int mode2d;           // SAR_IMAGE_2D: kz[] holds z_s - z_ref per plane (reading R18)
   int no_comp;
@@ -110,6 +114,13 @@ struct sar_plan {
   int4 *d_items = nullptr;
   int n_items = 0;
   int *d_cnt = nullptr;
+  // slab decomposition (sar_plan_create_slab); slab_world == 0: whole image
+  int slab_rank = 0, slab_world = 0;
+  SarClass *d_slab_cls = nullptr;
+  int slab_ncls = 0;
+  CUtensorMap tm_w1x_mid, tm_w1z_rows, tm_r1_mid;
+  bool tma_w1x = false, tma_w1z = false, tma_r1 = false;
+  const void *tm_r1_ptr = nullptr;
   // NUFFT mode tables and the half-transformed fine grid
   void *d_nu = nullptr;
   unsigned *d_peak = nullptr;   // SAR_REPORT_PEAK
@@ -123,5 +134,7 @@ int sar_launch_stolt_index(sar_plan *p, const int32_t *d_cols, int n, int32_t *d
                            cudaStream_t s);
 void sar_set_error(const std::string &msg);
 int sar_build_tensor_maps(sar_plan *p);
+int sar_slab_setup(sar_plan *p);
+int sar_slab_launch(sar_plan *p, int stage, const void *d_in, void *d_out, void *d_image, cudaStream_t s);
 int sar_setup_passb(sar_plan *p);
 bool sar_encode_input_map(sar_plan *p, const void *d_data);

@@ -53,6 +53,10 @@ class PlanInfo(C.Structure):
                 ("workspace_bytes", C.c_size_t)]
 
 
+class SlabDesc(C.Structure):
+    _fields_ = [("rank", C.c_int32), ("world", C.c_int32)]
+
+
 _lib = None
 
 
@@ -82,6 +86,10 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         "sar_debug_stage": (C.c_int, [vp, i32, vp, vp, vp]),
         "sar_debug_node_offsets": (C.c_int, [vp, C.POINTER(i32), C.POINTER(i32), C.POINTER(i32), C.POINTER(i32)]),
         "sar_debug_stolt_index": (C.c_int, [vp, vp, i32, vp, vp, vp]),
+        "sar_plan_create_slab": (C.c_int, [C.POINTER(vp), C.POINTER(GeomDesc), C.POINTER(ImageDesc), u32,
+                                           C.POINTER(SlabDesc)]),
+        "sar_slab_buffer_bytes": (C.c_int, [vp, C.POINTER(C.c_size_t), C.POINTER(C.c_size_t)]),
+        "sar_slab_stage": (C.c_int, [vp, i32, vp, vp, vp, vp]),
         "sar_status_string": (C.c_char_p, [C.c_int]),
         "sar_last_error": (C.c_char_p, []),
         "sar_version": (C.c_int, []),
@@ -99,7 +107,8 @@ def exported_symbols():
     return ["sar_plan_describe", "sar_plan_create", "sar_reconstruct", "sar_reconstruct_host", "sar_plan_destroy",
             "sar_plan_get_axes", "sar_plan_workspace_bytes", "sar_plan_profile_read",
             "sar_plan_profile_reset", "sar_plan_launches_per_call", "sar_plan_peaks", "sar_debug_stage",
-            "sar_debug_node_offsets", "sar_debug_stolt_index", "sar_status_string",
+            "sar_debug_node_offsets", "sar_debug_stolt_index", "sar_plan_create_slab", "sar_slab_buffer_bytes",
+            "sar_slab_stage", "sar_status_string",
             "sar_last_error", "sar_version"]
 
 
@@ -184,9 +193,11 @@ class Plan:
     the library; the plan owns the device tables and workspace."""
 
     def __init__(self, tx, rx, scan, npx, npy, x0, y0, dx, dy, z0, k, nx, ny, nz, dz, z_ref,
-                 pulse=None, flags=0, device=0, z_planes=None):
+                 pulse=None, flags=0, device=0, z_planes=None, slab=None):
         """``z_planes`` (m) selects the 2-D single-plane mode (SAR_IMAGE_2D): the
-        image is then [F, len(z_planes), ny, nx] and nz/dz are ignored."""
+        image is then [F, len(z_planes), ny, nx] and nz/dz are ignored.  ``slab``
+        = (rank, world) creates one rank's plan of the single-image slab
+        decomposition (``sar_plan_create_slab``; see ``SlabPlan``)."""
         lib = load_library()
         self._lib = lib
         if z_planes is not None:
@@ -194,7 +205,11 @@ class Plan:
         g, im, keep = _descriptors(tx, rx, scan, npx, npy, x0, y0, dx, dy, z0, k, nx, ny, nz, dz, z_ref,
                                    pulse, device, z_planes)
         h = C.c_void_p()
-        _check(lib.sar_plan_create(C.byref(h), C.byref(g), C.byref(im), C.c_uint32(flags)))
+        if slab is None:
+            _check(lib.sar_plan_create(C.byref(h), C.byref(g), C.byref(im), C.c_uint32(flags)))
+        else:
+            sd = SlabDesc(int(slab[0]), int(slab[1]))
+            _check(lib.sar_plan_create_slab(C.byref(h), C.byref(g), C.byref(im), C.c_uint32(flags), C.byref(sd)))
         del keep
         self._h = h
         self.flags = flags
@@ -204,11 +219,11 @@ class Plan:
         self.nx, self.ny, self.nz = im.nx, im.ny, im.nz
 
     @classmethod
-    def from_scene(cls, sc, flags=0, device=0, pulse=None, z_planes=None):
+    def from_scene(cls, sc, flags=0, device=0, pulse=None, z_planes=None, **kw):
         """Plan for any object with the attributes of ``scenes.Scene``."""
         return cls(sc.tx, sc.rx, sc.scan, sc.npx, sc.npy, sc.x0, sc.y0, sc.dx, sc.dy, sc.z0, sc.k,
                    sc.nx, sc.ny, sc.nz, sc.dz_img, sc.z_ref, pulse=pulse, flags=flags, device=device,
-                   z_planes=z_planes)
+                   z_planes=z_planes, **kw)
 
     # ---- shapes -------------------------------------------------------------
     @property
@@ -342,3 +357,66 @@ class Plan:
 
     def __exit__(self, *exc):
         self.close()
+
+
+class SlabPlan(Plan):
+    """One rank of the single-image slab decomposition (``sar_plan_create_slab``,
+    SURVEY 8(e)): stage 1 (K1 on this rank's lattice rows, packed per
+    destination), exchange #1, stage 2 (y-FFT, filter + Stolt + z-IFFT, y-IFFT
+    on this rank's k_x columns, packed), exchange #2, stage 3 (x-IFFT +
+    magnitude of this rank's z-slots into the image).  The exchanges are the
+    caller's (``paper_2305_02064_b200.slab``)."""
+
+    def __init__(self, *args, rank=0, world=1, **kw):
+        super().__init__(*args, slab=(rank, world), **kw)
+        self.rank, self.world = rank, world
+        G = world
+        self.send1_shape = (G, self.ny // G, self.nx // G, self.n_k)
+        self.send2_shape = (G, self.ny, self.nx // G, self.nz // G)
+        b1, b2 = C.c_size_t(), C.c_size_t()
+        _check(self._lib.sar_slab_buffer_bytes(self._h, C.byref(b1), C.byref(b2)))
+        assert b1.value == 8 * int(np.prod(self.send1_shape)) and b2.value == 8 * int(np.prod(self.send2_shape))
+
+    @classmethod
+    def from_scene(cls, sc, rank=0, world=1, flags=0, device=0, pulse=None):
+        return cls(sc.tx, sc.rx, sc.scan, sc.npx, sc.npy, sc.x0, sc.y0, sc.dx, sc.dy, sc.z0, sc.k,
+                   sc.nx, sc.ny, sc.nz, sc.dz_img, sc.z_ref, pulse=pulse, flags=flags, device=device,
+                   rank=rank, world=world)
+
+    def _stage(self, stage, a, b, img, stream):
+        _check(self._lib.sar_slab_stage(self._h, stage, C.c_void_p(a.data_ptr()),
+                                        C.c_void_p(b.data_ptr() if b is not None else 0),
+                                        C.c_void_p(img.data_ptr() if img is not None else 0), _stream_ptr(stream)))
+
+    def stage1(self, data, out=None, stream=None):
+        import torch
+        self._check_tensor(data, self.data_shape, torch.complex64, "data")
+        if out is None:
+            out = torch.empty(self.send1_shape, dtype=torch.complex64, device=data.device)
+        self._check_tensor(out, self.send1_shape, torch.complex64, "out")
+        self._stage(1, data, out, None, stream)
+        return out
+
+    def stage2(self, recv1, out=None, stream=None):
+        """``recv1`` (exchange #1 result, [G, ny/G, nx/G, n_k]) is overwritten."""
+        import torch
+        self._check_tensor(recv1, self.send1_shape, torch.complex64, "recv1")
+        if out is None:
+            out = torch.empty(self.send2_shape, dtype=torch.complex64, device=recv1.device)
+        self._check_tensor(out, self.send2_shape, torch.complex64, "out")
+        self._stage(2, recv1, out, None, stream)
+        return out
+
+    def stage3(self, recv2, image, stream=None):
+        """Writes this rank's nz/G planes of ``image`` ([1, nz, ny, nx])."""
+        import torch
+        self._check_tensor(recv2, self.send2_shape, torch.complex64, "recv2")
+        odt = torch.complex64 if self.flags & SAR_OUTPUT_COMPLEX else torch.float32
+        self._check_tensor(image, self.image_shape, odt, "image")
+        self._stage(3, recv2, None, image, stream)
+        return image
+
+    def planes(self):
+        """Output planes this rank writes: (z + nz/2) mod nz of its z-slots (reading R8)."""
+        nzl = self.nz // self.world
+        return [(z + self.nz // 2) % self.nz for z in range(self.rank * nzl, (self.rank + 1) * nzl)]

@@ -41,7 +41,7 @@ def test_library_exports_every_declared_symbol():
     for d in declared:
         assert hasattr(lib, d)
     assert sorted(sarmod.exported_symbols()) == declared
-    assert lib.sar_version() == 2
+    assert lib.sar_version() == 3
 
 
 def test_no_oracle_in_product_path():

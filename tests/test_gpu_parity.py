@@ -425,3 +425,62 @@ def test_plane2d_edge_cases(kw, planes):
         got = plan.reconstruct(d).cpu().numpy()
     e2, einf = errs(got, want)
     assert e2 <= E2_BAR and einf <= EINF_BAR, (sc.name, e2, einf)
+
+
+# ---- single-image slab decomposition (sar_slab_*) -----
+@pytest.mark.parametrize("name,world,flags", [("small", 1, 0), ("small", 2, 0), ("small", 4, 0),
+                                              ("small", 2, sar.SAR_OUTPUT_COMPLEX),
+                                              ("small", 2, sar.SAR_NO_COMPENSATION),
+                                              ("freehand", 4, 0), ("large", 2, 0), ("large", 8, 0)])
+def test_slab_emulated_equals_whole_image(name, world, flags):
+    """All G ranks run in this process (exchanges by tensor indexing, the same
+    block permutation NCCL's all_to_all_single performs -- test_multiproc.py
+    checks that); every voxel comes from the same kernel code as the
+    whole-image path, so the assembled image must match it bit for bit."""
+    from paper_2305_02064_b200 import slab
+    sc = scenes.make_scene(name)
+    if name in ("freehand", "large"):
+        from scenes import gpu as sgpu
+        d = sgpu.synthesize_gpu(sc)
+    else:
+        d, _ = _data(sc)
+    with sar.Plan.from_scene(sc, flags=flags) as p0:
+        want = p0.reconstruct(d)
+    plans = [sar.SlabPlan.from_scene(sc, rank=r, world=world, flags=flags) for r in range(world)]
+    try:
+        got = torch.full_like(want, float("nan")) if not (flags & sar.SAR_OUTPUT_COMPLEX) else \
+            torch.full_like(want, complex(float("nan"), 0))
+        slab.emulate(plans, d, got)
+        owned = sorted(m for p in plans for m in p.planes())
+        assert owned == list(range(sc.nz))
+        torch.cuda.synchronize()
+        assert torch.equal(got, want), (name, world, (got - want).abs().max().item())
+    finally:
+        for p in plans:
+            p.close()
+
+
+def test_slab_rank_writes_only_its_planes_and_errors():
+    from paper_2305_02064_b200 import slab  # noqa: F401
+    sc = scenes.make_scene("small")
+    d, _ = _data(sc)
+    with sar.SlabPlan.from_scene(sc, rank=1, world=4) as p:
+        img = torch.full(p.image_shape, -1.0, device="cuda")
+        s1 = p.stage1(d)
+        # feed this rank its own blocks only: the planes it does not own stay -1
+        s2 = p.stage2(torch.zeros(p.send1_shape, dtype=torch.complex64, device="cuda"))
+        p.stage3(torch.zeros(p.send2_shape, dtype=torch.complex64, device="cuda"), img)
+        torch.cuda.synchronize()
+        mine = set(p.planes())
+        for m in range(sc.nz):
+            plane = img[0, m]
+            assert bool((plane == 0).all()) if m in mine else bool((plane == -1).all())
+        assert s1.shape == (4, sc.ny // 4, sc.nx // 4, sc.k.size) and s2.shape == (4, sc.ny, sc.nx // 4, sc.nz // 4)
+    with pytest.raises(sar.SarError):
+        sar.SlabPlan.from_scene(sc, rank=0, world=3)            # 3 does not divide 128
+    with pytest.raises(sar.SarError):
+        sar.SlabPlan.from_scene(sc, rank=4, world=4)
+    with pytest.raises(sar.SarError):
+        sar.SlabPlan.from_scene(sc, rank=0, world=2, flags=sar.SAR_GRID_NUFFT)
+    with pytest.raises(sar.SarError):
+        sar.SlabPlan.from_scene(scenes.make_scene("realtime"), rank=0, world=2)   # 64 frames

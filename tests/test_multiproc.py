@@ -71,3 +71,43 @@ def test_frame_subset_echo_matches_full_scene():
     for lo, hi in ((0, 1), (1, 3), (2, 3)):
         sub = scenes.frame_subset(sc, lo, hi)
         assert np.array_equal(scenes.synthesize_cpu(sub), full[lo:hi])
+
+
+# ---- slab decomposition: the exchange of sar_slab_stage's blocks ----------
+def _xchg_worker(rank, world, port, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2305_02064_b200.slab import exchange
+    # block h of rank g holds 1000 g + 10 h + the element index
+    send = torch.stack([torch.arange(6, dtype=torch.float32).reshape(2, 3) + 1000 * rank + 10 * h
+                        for h in range(world)])
+    recv = exchange(send)
+    out.put((rank, send.numpy(), recv.numpy()))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_slab_exchange_gloo(world):
+    """exchange() (all_to_all_single, what NCCL runs on the GPUs) delivers
+    block h of every rank g to rank h in order of g -- the layout
+    sar_slab_stage expects -- and permute_blocks (the single-process
+    emulation the GPU tests use) does the same permutation."""
+    from paper_2305_02064_b200.slab import permute_blocks
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_xchg_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict((r, (s, rv)) for r, s, rv in (q.get(timeout=120) for _ in range(world)))
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    base = np.arange(6, dtype=np.float32).reshape(2, 3)
+    emu = permute_blocks([torch.from_numpy(res[g][0]) for g in range(world)])
+    for h in range(world):
+        recv = res[h][1]
+        for g in range(world):
+            assert np.array_equal(recv[g], base + 1000 * g + 10 * h)
+        assert np.array_equal(emu[h].numpy(), recv)
