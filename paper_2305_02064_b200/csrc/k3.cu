@@ -167,7 +167,7 @@ __global__ void __launch_bounds__(K3C_NT, 4) k3_class(const SarDeviceView v) {
 }
 
 #ifndef K3P_GEOM
-#define K3P_GEOM 256, 2, 4, 2
+#define K3P_GEOM 256, 3, 3, 2
 #endif
 // threads per consumer group, consumer groups (round-robin items), ring
 // stages, mirror classes per item
