@@ -497,26 +497,45 @@ cudaError_t launch_v(K kernel, dim3 grid, int nt, size_t smem, cudaStream_t s, c
 
 }  // namespace
 
+namespace {
+// k3_pp with CL mirror classes per item if its shared memory fits
+template <int N, int CL>
+bool try_k3pp(const SarDeviceView &v, bool ifft, cudaStream_t s, int num_sms, cudaError_t *err) {
+  const size_t smem = k3pp_smem<N, CL>(v.nk);
+  if (smem > 225 * 1024) return false;
+  const int nitems_f = (v.ncls + CL - 1) / CL;
+  const int nitems = nitems_f * v.F;
+  const int grid = nitems < num_sms ? nitems : num_sms;
+  auto kern = ifft ? k3_pp<N, CL, true> : k3_pp<N, CL, false>;
+  *err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (*err != cudaSuccess) return true;
+  kern<<<grid, K3P_NG * K3P_G + 32, smem, s>>>(v, nitems_f);
+  *err = cudaGetLastError();
+  return true;
+}
+}  // namespace
+
 cudaError_t launch_k3(const SarDeviceView &v, bool ifft, cudaStream_t s, int num_sms) {
-  if ((v.nk & 1) == 0 && v.nz >= 256 && !getenv("SAR_K3_PLAIN")) {
-    const int nclass = v.ncls;
+  if ((v.nk & 1) == 0 && v.nz >= 128 && !getenv("SAR_K3_PLAIN")) {
+    // n_z >= 256: 2 classes (<= 8 columns) per item; n_z = 128: 4 classes
+    // (Freehand 0.065 -> 0.055 ms; at n_z = 64 k3_class stays faster:
+    // Realtime 0.37 vs 0.43 ms with 8 classes per item)
+    cudaError_t e = cudaSuccess;
     switch (v.nz) {
-#define X(N)                                                                                                   \
-  case N: {                                                                                                    \
-    constexpr int CL = K3P_CL;                                                                                 \
-    const size_t smem = k3pp_smem<N, CL>(v.nk);                                                                \
-    if (smem > 225 * 1024) break;                                                                              \
-    const int nitems_f = (nclass + CL - 1) / CL;                                                               \
-    const int nitems = nitems_f * v.F;                                                                         \
-    const int grid = nitems < num_sms ? nitems : num_sms;                                                      \
-    auto kern = ifft ? k3_pp<N, CL, true> : k3_pp<N, CL, false>;                                               \
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);        \
-    if (e != cudaSuccess) return e;                                                                            \
-    kern<<<grid, K3P_NG * K3P_G + 32, smem, s>>>(v, nitems_f);                                                 \
-    return cudaGetLastError();                                                                                 \
-  }
-      X(256) X(512) X(1024)
-#undef X
+      case 128:
+        if (try_k3pp<128, 4>(v, ifft, s, num_sms, &e)) return e;
+        break;
+      case 256:
+        if (try_k3pp<256, K3P_CL>(v, ifft, s, num_sms, &e)) return e;
+        break;
+      case 512:
+        if (try_k3pp<512, K3P_CL>(v, ifft, s, num_sms, &e)) return e;
+        break;
+      case 1024:
+        if (try_k3pp<1024, K3P_CL>(v, ifft, s, num_sms, &e)) return e;
+        break;
+      default:
+        break;
     }
   }
   const int nclass = v.ncls;
