@@ -67,11 +67,16 @@ constexpr int mid2_ctas() {
   return (int)((200 * 1024) / mid2_smem<N>()) < 1 ? 1 : (int)((200 * 1024) / mid2_smem<N>());
 }
 
+// consumer threads: 512 at N = 512 (pass 1 as 16 x 32, pass 2 split between
+// thread pairs: 512 butterflies in both passes)
+template <int N>
+constexpr int mid2_ntc() { return N == 512 ? 512 : sarfft2::nt_fft<N, KC>(); }
+
 template <int N, int DIR>
-__global__ void __launch_bounds__(sarfft2::nt_fft<N, KC>() + 32)
+__global__ void __launch_bounds__(mid2_ntc<N>() + 32)
     k_fft_mid2(const __grid_constant__ CUtensorMap tm, float2 *__restrict__ data, const float2 *__restrict__ twg,
                int nx, int inner, int nchunk, int nitems) {
-  constexpr int NTC = sarfft2::nt_fft<N, KC>();
+  constexpr int NTC = mid2_ntc<N>();
   constexpr int S = mid2_stages<N>();
   constexpr int ROWS = N < 256 ? N : 256;
   constexpr int NBOX = N / ROWS;
@@ -118,11 +123,12 @@ __global__ void __launch_bounds__(sarfft2::nt_fft<N, KC>() + 32)
     const float2 *stage = ring + (size_t)st * N * KC;
     float2 *base = data + ((size_t)f * N * nx + a) * (size_t)inner + chunk * KC;
     const int cmax = inner - chunk * KC;
-    sarfft2::fft<N, KC, KC, NTC, DIR, 1, false>(
+    sarfft2::fft_ctx<N, KC, KC, NTC, DIR, 1, false, (N == 512 ? 16 : 0), (N == 512)>(
         work, tw, tid, [&](int c, int m) { return stage[m * KC + c]; },
         [&] {
           if (tid == 0) sartma::mbar_arrive(&empty[st]);
         },
+        [](int c) { return c; },
         [&](int c, int m, float2 v) {
           if (c < cmax) __stcs(base + (size_t)m * row + c, v);
         });
@@ -148,7 +154,7 @@ cudaError_t launch_mid(float2 *data, const float2 *tw, int F, int ny, int nx, in
       if (e != cudaSuccess) return e;                                                              \
     }                                                                                              \
     const int maxg = num_sms * mid2_ctas<N>();                                                     \
-    kern<<<nitems < maxg ? nitems : maxg, sarfft2::nt_fft<N, KC>() + 32, smem, s>>>(*tm, data, tw, nx, inner, \
+    kern<<<nitems < maxg ? nitems : maxg, mid2_ntc<N>() + 32, smem, s>>>(*tm, data, tw, nx, inner,   \
                                                                                   nchunk, nitems); \
     return cudaGetLastError();                                                                     \
   }
