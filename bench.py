@@ -267,7 +267,20 @@ def run_ours(args):
 
     # end-to-end through the public API with host buffers (pinned)
     e2e = None
-    if not args.no_e2e:
+    e2e_ok = not args.no_e2e
+    if e2e_ok:
+        # every rank of the node pins its inputs + image: skip (rather than
+        # crash the node) when the host cannot hold them all
+        try:
+            import psutil
+            need = world * (sc.raw_bytes() + sc.image_bytes())
+            if psutil.virtual_memory().available < 1.3 * need:
+                e2e_ok = False
+                e2e = {"skipped": f"host RAM: {world} ranks x {(sc.raw_bytes() + sc.image_bytes()) / 2**30:.1f} GiB "
+                                  f"pinned > available"}
+        except ImportError:
+            pass
+    if e2e_ok:
         h_in = torch.empty(sc.data_shape, dtype=torch.complex64, pin_memory=True)
         h_in.copy_(data)
         h_out = torch.empty(sc.image_shape, dtype=torch.float32, pin_memory=True)
