@@ -33,15 +33,15 @@ constexpr int k3c_cl() {
   constexpr int cc = K3C_NT / (NZ / k3c_r1<NZ>());
   return cc / 4 > 8 ? 8 : (cc / 4 < 1 ? 1 : cc / 4);
 }
-template <int NZ>
+template <int NZ, int CL>
 size_t k3c_smem(int nk) {
-  constexpr int CL = k3c_cl<NZ>();
   return ((size_t)4 * CL * nk + (size_t)NZ * (4 * CL + 1)) * sizeof(float2);
 }
 
-template <int NZ, bool DO_IFFT>
+// CL classes per CTA: k3c_cl<NZ>() normally, 1 when n_k is so large that
+// CL whole columns do not fit in shared memory (up to SAR_MAX_NK)
+template <int NZ, bool DO_IFFT, int CL>
 __global__ void __launch_bounds__(K3C_NT, 4) k3_class(const SarDeviceView v) {
-  constexpr int CL = k3c_cl<NZ>();
   constexpr int CC = 4 * CL;   // slot 4*cl + m = member m of class cl
   constexpr int LD = CC + 1;
   extern __shared__ __align__(16) float2 sm3[];
@@ -542,11 +542,14 @@ cudaError_t launch_k3(const SarDeviceView &v, bool ifft, cudaStream_t s, int num
   switch (v.nz) {
 #define X(N)                                                                                                   \
   case N: {                                                                                                    \
-    constexpr int CL = k3c_cl<N>();                                                                            \
-    const size_t smem = k3c_smem<N>(v.nk);                                                                     \
+    constexpr int CLD = k3c_cl<N>();                                                                           \
+    const bool big = k3c_smem<N, CLD>(v.nk) > 220 * 1024;                                                      \
+    const int CL = big ? 1 : CLD;                                                                              \
+    const size_t smem = big ? k3c_smem<N, 1>(v.nk) : k3c_smem<N, CLD>(v.nk);                                   \
     if (smem > 220 * 1024) return cudaErrorInvalidValue;                                                       \
     dim3 grid((nclass + CL - 1) / CL, v.F);                                                                    \
-    auto kern = ifft ? k3_class<N, true> : k3_class<N, false>;                                                 \
+    auto kern = big ? (ifft ? k3_class<N, true, 1> : k3_class<N, false, 1>)                                   \
+                    : (ifft ? k3_class<N, true, CLD> : k3_class<N, false, CLD>);                               \
     if (smem > 40 * 1024) {                                                                                    \
       cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);      \
       if (e != cudaSuccess) return e;                                                                          \

@@ -170,6 +170,9 @@ EDGE = [
     # maximum FFT size along x and z (1024), small elsewhere
     dict(npx=600, npy=4, nx=1024, ny=16, nk=16, nz=1024, dz=1e-3, z_ref=0.3),
     dict(npx=4, npy=700, nx=8, ny=1024, nk=24, nz=8, dz=5e-3, z_ref=0.3),
+    # the maximum n_k (SAR_MAX_NK = 2048: a whole Stolt column in shared memory)
+    dict(npx=8, npy=8, nx=16, ny=16, nk=2048, nz=64, dz=5e-3, z_ref=0.25),
+    dict(npx=8, npy=6, nx=8, ny=8, nk=2048, nz=512, dz=2e-3, z_ref=0.25),
 ]
 
 
