@@ -403,6 +403,7 @@ NUFFT_EDGE = [
     dict(npx=20, npy=13, nx=32, ny=32, nk=20, nz=64, dz=4e-3, z_ref=0.2),           # ragged raster, odd-ish k
     dict(npx=33, npy=7, nx=64, ny=16, nk=37, nz=16, dz=5e-3, z_ref=0.15),          # odd n_k, wide strip
     dict(npx=24, npy=20, nx=32, ny=32, nk=32, nz=32, dz=5e-3, z_ref=0.2, n_frames=3, n_tx=3),  # frames, wrap
+    dict(npx=8, npy=6, nx=32, ny=16, nk=2048, nz=32, dz=5e-3, z_ref=0.2),          # SAR_MAX_NK: 8 k chunks
 ]
 
 
