@@ -173,6 +173,8 @@ EDGE = [
     # the maximum n_k (SAR_MAX_NK = 2048: a whole Stolt column in shared memory)
     dict(npx=8, npy=8, nx=16, ny=16, nk=2048, nz=64, dz=5e-3, z_ref=0.25),
     dict(npx=8, npy=6, nx=8, ny=8, nk=2048, nz=512, dz=2e-3, z_ref=0.25),
+    # SAR_MAX_PAIRS = 64 Tx/Rx pairs (16 Tx x 4 Rx: a 64-row virtual array)
+    dict(npx=16, npy=12, nx=16, ny=128, nk=16, nz=16, dz=5e-3, z_ref=0.25, n_tx=16),
 ]
 
 
