@@ -510,3 +510,23 @@ def test_slab_nonsquare_small_z_slots(world):
     finally:
         for p in plans:
             p.close()
+
+
+def test_slab_without_tma_equals_whole_image(monkeypatch):
+    """The slab stages on the non-TMA fallback kernels (SAR_NO_TMA)."""
+    from paper_2305_02064_b200 import slab
+    sc = scenes.make_scene("small")
+    d, _ = _data(sc)
+    with sar.Plan.from_scene(sc) as p0:
+        want = p0.reconstruct(d)
+    monkeypatch.setenv("SAR_NO_TMA", "1")
+    plans = [sar.SlabPlan.from_scene(sc, rank=r, world=4) for r in range(4)]
+    try:
+        got = torch.full_like(want, float("nan"))
+        slab.emulate(plans, d, got)
+        torch.cuda.synchronize()
+        e2, einf = errs(got.cpu().numpy(), want.cpu().numpy())
+        assert e2 <= 1e-6 and einf <= 1e-5, (e2, einf)
+    finally:
+        for p in plans:
+            p.close()
