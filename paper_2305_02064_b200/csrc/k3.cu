@@ -41,7 +41,7 @@ size_t k3c_smem(int nk) {
 // CL classes per CTA: k3c_cl<NZ>() normally, 1 when n_k is so large that
 // CL whole columns do not fit in shared memory (up to SAR_MAX_NK)
 template <int NZ, bool DO_IFFT, int CL>
-__global__ void __launch_bounds__(K3C_NT, 4) k3_class(const SarDeviceView v) {
+__global__ void __launch_bounds__(K3C_NT, 8) k3_class(const SarDeviceView v) {
   constexpr int CC = 4 * CL;   // slot 4*cl + m = member m of class cl
   constexpr int LD = CC + 1;
   extern __shared__ __align__(16) float2 sm3[];
