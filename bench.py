@@ -388,9 +388,26 @@ def run_slab(args):
     image = torch.empty(sc.image_shape, dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream(dev)
     xfn = slab.exchange if world > 1 else (lambda t, group=None: t)
+    if args.p2p:
+        # exchange by peer stores: the pack kernels write straight into every
+        # rank's receive buffer (CUDA IPC over NVLink / NVSwitch)
+        recv1 = torch.empty(plan.send1_shape, dtype=torch.complex64, device=dev)
+        recv2 = torch.empty(plan.send2_shape, dtype=torch.complex64, device=dev)
+        if world > 1:
+            peers1, keep1 = slab.open_peer_buffers(recv1)
+            peers2, keep2 = slab.open_peer_buffers(recv2)
+        else:
+            peers1, peers2 = [recv1.data_ptr()], [recv2.data_ptr()]
 
     def step():
-        slab.reconstruct(plan, data, image, exchange_fn=xfn)
+        if not args.p2p:
+            slab.reconstruct(plan, data, image, exchange_fn=xfn)
+        elif world > 1:
+            slab.reconstruct_peers(plan, data, image, recv1, recv2, peers1, peers2)
+        else:
+            plan.stage_peers(1, data, peers1)
+            plan.stage_peers(2, recv1, peers2)
+            plan.stage3(recv2, image)
 
     for _ in range(args.warmup):
         step()
@@ -424,7 +441,8 @@ def run_slab(args):
                        "frames": 1, "tx": sc.n_tx, "rx": sc.n_rx, "poses": sc.n_pos, "n_k": sc.n_k,
                        "image": [sc.nx, sc.ny, sc.nz], "samples_per_step": sc.n_samples,
                        "l2": "inputs larger than L2 (no flush)",
-                       "parallelism": f"slab x{world}: y-rows -> all-to-all -> k_x columns -> all-to-all -> z-slots",
+                       "parallelism": f"slab x{world}: y-rows -> " + ("peer stores" if args.p2p else "all-to-all") +
+                                      " -> k_x columns -> " + ("peer stores" if args.p2p else "all-to-all") + " -> z-slots",
                        "exchange_bytes_per_rank": xbytes},
             "ms_per_image": ms_step,
             "roofline": {"bound": "hbm", "kernel": "whole slab step (per rank)", "achieved": ach, "peak": peak,
@@ -454,6 +472,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--slab", action="store_true",
                     help="split ONE image over the ranks (slab decomposition, two all-to-alls; strong scaling)")
+    ap.add_argument("--p2p", action="store_true",
+                    help="with --slab: exchange by peer stores into IPC-mapped receive buffers instead of NCCL")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")

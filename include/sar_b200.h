@@ -214,9 +214,11 @@ int sar_plan_launches_per_call(const sar_plan *p, int32_t *n);
  * calls are asynchronous on `stream`; d_in / d_out / d_image are device
  * pointers owned by the caller, 16-byte aligned, and must not alias.  The
  * plan also works as a whole-image plan (sar_reconstruct). */
+#define SAR_MAX_SLAB 16 /* world <= 16 */
+
 typedef struct {
   int32_t rank;   /* 0 <= rank < world */
-  int32_t world;  /* G >= 1, divides nx, ny and nz */
+  int32_t world;  /* 1 <= G <= SAR_MAX_SLAB, divides nx, ny and nz */
 } sar_slab_desc;
 
 /* Create the plan of one rank.  Errors: as sar_plan_create, plus
@@ -234,6 +236,19 @@ int sar_slab_buffer_bytes(const sar_plan *p, size_t *send1, size_t *send2);
  * outside 1..3, NULL pointers, not a slab plan), CUDA. */
 int sar_slab_stage(sar_plan *p, int32_t stage, const void *d_in, void *d_out, void *d_image,
                    sar_stream stream);
+
+/* Exchange by peer stores: stage 1 or 2 of this rank with the exchange
+ * folded into its pack, so no all-to-all call is needed.  peer_recv: host
+ * array of G device pointers, valid in this process (this GPU's own buffer
+ * for h == rank, the others mapped from the peer GPUs, e.g. with CUDA IPC over
+ * NVLink / NVSwitch), each rank h's receive buffer of the stage's exchange
+ * (G blocks of sar_slab_buffer_bytes / G bytes); block h of this rank is
+ * stored straight into slot `rank` of peer_recv[h].  The caller orders the
+ * stages across ranks (e.g. stream sync + barrier) before the receivers read.
+ * Stage 3 is sar_slab_stage.  Errors: INVALID_ARG (stage not 1 or 2, NULL),
+ * CUDA. */
+int sar_slab_stage_peers(sar_plan *p, int32_t stage, const void *d_in, void *const *peer_recv,
+                         sar_stream stream);
 
 /* ---- debug / parity entry points (same kernels as sar_reconstruct) ---- */
 

@@ -208,25 +208,34 @@ int sar_build_tensor_maps(sar_plan *p) {
 
 // ------------------------------------------------ slab decomposition ----
 namespace {
-// dst + h*dhs + r*dp  <-  src + h*shs + r*sp, Wb bytes per (h, r), for h < G,
-// r < H: the pack / unpack of the slab exchanges (16-byte vectors, streaming)
-__global__ void k_block_copy(char *__restrict__ dst, const char *__restrict__ src, unsigned G, unsigned H, unsigned V,
-                             long long shs, long long sp, long long dhs, long long dp) {
+// Destination of every block: d[h] (this rank's pack buffer + h*dhs, or --
+// exchange by peer stores -- block h's slot in rank h's receive buffer,
+// mapped into this process over NVLink).
+struct BlockDst {
+  char *d[SAR_MAX_SLAB];
+};
+
+// d[h] + r*dp  <-  src + h*shs + r*sp, Wb bytes per (h, r), for h < G, r < H:
+// the packs / unpack of the slab exchanges (16-byte vectors, streaming)
+__global__ void k_block_copy(const BlockDst dst, const char *__restrict__ src, unsigned G, unsigned H, unsigned V,
+                             long long shs, long long sp, long long dp) {
   const unsigned total = G * H * V;   // < 2^31 (checked by the launcher)
   for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
     const unsigned q = i / V, v = i - q * V;
     const unsigned h = q / H, r = q - h * H;
     const float4 x = __ldcs(reinterpret_cast<const float4 *>(src + h * shs + r * sp) + v);
-    __stcs(reinterpret_cast<float4 *>(dst + h * dhs + r * dp) + v, x);
+    __stcs(reinterpret_cast<float4 *>(dst.d[h] + r * dp) + v, x);
   }
 }
 
-cudaError_t block_copy(void *dst, const void *src, int G, long long H, long long Wb, long long shs, long long sp,
-                       long long dhs, long long dp, int num_sms, cudaStream_t s) {
-  if (Wb % 16 || shs % 16 || sp % 16 || dhs % 16 || dp % 16 || (double)G * H * (Wb / 16) >= 2147483648.0) {
+cudaError_t block_copy(const BlockDst &dst, const void *src, int G, long long H, long long Wb, long long shs,
+                       long long sp, long long dp, int num_sms, cudaStream_t s) {
+  bool vec = !(Wb % 16 || shs % 16 || sp % 16 || dp % 16 || (double)G * H * (Wb / 16) >= 2147483648.0);
+  for (int h = 0; h < G; ++h) vec = vec && (reinterpret_cast<uintptr_t>(dst.d[h]) % 16 == 0);
+  if (!vec) {
     for (int h = 0; h < G; ++h) {
-      cudaError_t e = cudaMemcpy2DAsync(static_cast<char *>(dst) + h * dhs, dp, static_cast<const char *>(src) + h * shs,
-                                        sp, Wb, H, cudaMemcpyDeviceToDevice, s);
+      cudaError_t e = cudaMemcpy2DAsync(dst.d[h], dp, static_cast<const char *>(src) + h * shs, sp, Wb, H,
+                                        cudaMemcpyDefault, s);
       if (e != cudaSuccess) return e;
     }
     return cudaSuccess;
@@ -235,9 +244,22 @@ cudaError_t block_copy(void *dst, const void *src, int G, long long H, long long
   const long long total = (long long)G * H * V;
   const long long want = (total + 255) / 256;
   const int grid = (int)(want < 8LL * num_sms ? want : 8LL * num_sms);
-  k_block_copy<<<grid > 0 ? grid : 1, 256, 0, s>>>(static_cast<char *>(dst), static_cast<const char *>(src),
-                                                  (unsigned)G, (unsigned)H, (unsigned)V, shs, sp, dhs, dp);
+  k_block_copy<<<grid > 0 ? grid : 1, 256, 0, s>>>(dst, static_cast<const char *>(src), (unsigned)G, (unsigned)H,
+                                                  (unsigned)V, shs, sp, dp);
   return cudaGetLastError();
+}
+
+// blocks of a contiguous [G][...] buffer (block stride hs bytes)
+BlockDst dst_packed(void *base, int G, long long hs) {
+  BlockDst d{};
+  for (int h = 0; h < G; ++h) d.d[h] = static_cast<char *>(base) + h * hs;
+  return d;
+}
+// this rank's block slot in every peer's receive buffer
+BlockDst dst_peers(void *const *peers, int G, int rank, long long hs) {
+  BlockDst d{};
+  for (int h = 0; h < G; ++h) d.d[h] = static_cast<char *>(peers[h]) + rank * hs;
+  return d;
 }
 }  // namespace
 
@@ -261,7 +283,8 @@ int sar_slab_setup(sar_plan *p) {
   return SAR_OK;
 }
 
-int sar_slab_launch(sar_plan *p, int stage, const void *d_in, void *d_out, void *d_image, cudaStream_t s) {
+int sar_slab_launch(sar_plan *p, int stage, const void *d_in, void *d_out, void *d_image, cudaStream_t s,
+                    void *const *peers) {
   const SarDeviceView &v = p->v;
   const int G = p->slab_world, r = p->slab_rank;
   const int nxl = v.nx / G, nyl = v.ny / G, nzl = v.nz / G;
@@ -279,9 +302,10 @@ int sar_slab_launch(sar_plan *p, int stage, const void *d_in, void *d_out, void 
     SAR_CHECK(launch_k1(vk, static_cast<const float2 *>(d_in), true, s, tm_s, p->tma_ap ? &p->tm_ap : nullptr,
                         p->k1_br, p->k1_regacc, p->num_sms));
     // pack for exchange #1: block h = columns [h nx', (h+1) nx') of every row
-    SAR_CHECK(block_copy(d_out, v.w0, G, nyl, (long long)nxl * v.nk * c8, (long long)nxl * v.nk * c8,
-                         (long long)v.nx * v.nk * c8, (long long)nyl * nxl * v.nk * c8, (long long)nxl * v.nk * c8,
-                         p->num_sms, s));
+    const long long hs1 = (long long)nyl * nxl * v.nk * c8;
+    SAR_CHECK(block_copy(peers ? dst_peers(peers, G, r, hs1) : dst_packed(d_out, G, hs1), v.w0, G, nyl,
+                         (long long)nxl * v.nk * c8, (long long)nxl * v.nk * c8, (long long)v.nx * v.nk * c8,
+                         (long long)nxl * v.nk * c8, p->num_sms, s));
     return SAR_OK;
   }
   if (stage == 2) {
@@ -305,15 +329,18 @@ int sar_slab_launch(sar_plan *p, int stage, const void *d_in, void *d_out, void 
     SAR_CHECK(launch_mid<+1>(v.w1, v.tw_y, 1, v.ny, nxl, v.nz, s, p->tma_w1x ? &p->tm_w1x_mid : nullptr,
                              p->num_sms));
     // pack for exchange #2: block h = z-slots [h nz', (h+1) nz') of every column
-    SAR_CHECK(block_copy(d_out, v.w1, G, (long long)v.ny * nxl, (long long)nzl * c8, (long long)nzl * c8,
-                         (long long)v.nz * c8, (long long)v.ny * nxl * nzl * c8, (long long)nzl * c8, p->num_sms, s));
+    const long long hs2 = (long long)v.ny * nxl * nzl * c8;
+    SAR_CHECK(block_copy(peers ? dst_peers(peers, G, r, hs2) : dst_packed(d_out, G, hs2), v.w1, G,
+                         (long long)v.ny * nxl, (long long)nzl * c8, (long long)nzl * c8, (long long)v.nz * c8,
+                         (long long)nzl * c8, p->num_sms, s));
     return SAR_OK;
   }
   // stage 3: unpack [G][ny][nx'][nz'] (block g = columns [g nx', (g+1) nx'))
   // into the z-slab [ny][nx][nz'] (in W0), then x-IFFT + magnitude
   float2 *zs = v.w0;
-  SAR_CHECK(block_copy(zs, d_in, G, v.ny, (long long)nxl * nzl * c8, (long long)v.ny * nxl * nzl * c8,
-                       (long long)nxl * nzl * c8, (long long)nxl * nzl * c8, (long long)v.nx * nzl * c8, p->num_sms, s));
+  SAR_CHECK(block_copy(dst_packed(zs, G, (long long)nxl * nzl * c8), d_in, G, v.ny, (long long)nxl * nzl * c8,
+                       (long long)v.ny * nxl * nzl * c8, (long long)nxl * nzl * c8, (long long)v.nx * nzl * c8,
+                       p->num_sms, s));
   SarDeviceView vk = v;
   vk.nz = nzl;
   vk.z_off = r * nzl;

@@ -594,7 +594,7 @@ int sar_plan_create_slab(sar_plan **out, const sar_geom_desc *g, const sar_image
   *out = nullptr;
   if (!slab || !g || !im) return fail(SAR_ERR_INVALID_ARG, "slab, geometry or image descriptor is NULL");
   const int G = slab->world, r = slab->rank;
-  if (G < 1 || r < 0 || r >= G) return fail(SAR_ERR_INVALID_ARG, "slab rank/world out of range");
+  if (G < 1 || G > SAR_MAX_SLAB || r < 0 || r >= G) return fail(SAR_ERR_INVALID_ARG, "slab rank/world out of range");
   if (flags & (SAR_IMAGE_2D | SAR_GRID_NUFFT | SAR_REPORT_PEAK))
     return fail(SAR_ERR_UNSUPPORTED, "slab plans support the 3-D RASTER path only");
   if (g->n_frames != 1) return fail(SAR_ERR_INVALID_ARG, "slab plans reconstruct one image (n_frames == 1)");
@@ -664,6 +664,19 @@ int sar_slab_stage(sar_plan *p, int32_t stage, const void *d_in, void *d_out, vo
   cudaStream_t s = (cudaStream_t)stream;
   p->last_stream = s;
   return sar_slab_launch(p, stage, d_in, d_out, d_image, s);
+}
+
+int sar_slab_stage_peers(sar_plan *p, int32_t stage, const void *d_in, void *const *peer_recv, sar_stream stream) {
+  if (!p) return fail(SAR_ERR_INVALID_ARG, "plan is NULL");
+  if (p->slab_world < 1) return fail(SAR_ERR_INVALID_ARG, "not a slab plan");
+  if (stage != 1 && stage != 2) return fail(SAR_ERR_INVALID_ARG, "peer stores exist for stages 1 and 2");
+  if (!d_in || !peer_recv) return fail(SAR_ERR_INVALID_ARG, "NULL buffer");
+  for (int h = 0; h < p->slab_world; ++h)
+    if (!peer_recv[h]) return fail(SAR_ERR_INVALID_ARG, "NULL peer buffer");
+  DeviceGuard g(p->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  p->last_stream = s;
+  return sar_slab_launch(p, stage, d_in, nullptr, nullptr, s, peer_recv);
 }
 
 int sar_reconstruct(sar_plan *p, const void *d_data, void *d_image, sar_stream stream) {

@@ -135,6 +135,7 @@ int sar_launch_stolt_index(sar_plan *p, const int32_t *d_cols, int n, int32_t *d
 void sar_set_error(const std::string &msg);
 int sar_build_tensor_maps(sar_plan *p);
 int sar_slab_setup(sar_plan *p);
-int sar_slab_launch(sar_plan *p, int stage, const void *d_in, void *d_out, void *d_image, cudaStream_t s);
+int sar_slab_launch(sar_plan *p, int stage, const void *d_in, void *d_out, void *d_image, cudaStream_t s,
+                    void *const *peers = nullptr);
 int sar_setup_passb(sar_plan *p);
 bool sar_encode_input_map(sar_plan *p, const void *d_data);

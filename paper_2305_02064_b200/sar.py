@@ -90,6 +90,7 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
                                            C.POINTER(SlabDesc)]),
         "sar_slab_buffer_bytes": (C.c_int, [vp, C.POINTER(C.c_size_t), C.POINTER(C.c_size_t)]),
         "sar_slab_stage": (C.c_int, [vp, i32, vp, vp, vp, vp]),
+        "sar_slab_stage_peers": (C.c_int, [vp, i32, vp, C.POINTER(vp), vp]),
         "sar_status_string": (C.c_char_p, [C.c_int]),
         "sar_last_error": (C.c_char_p, []),
         "sar_version": (C.c_int, []),
@@ -108,7 +109,7 @@ def exported_symbols():
             "sar_plan_get_axes", "sar_plan_workspace_bytes", "sar_plan_profile_read",
             "sar_plan_profile_reset", "sar_plan_launches_per_call", "sar_plan_peaks", "sar_debug_stage",
             "sar_debug_node_offsets", "sar_debug_stolt_index", "sar_plan_create_slab", "sar_slab_buffer_bytes",
-            "sar_slab_stage", "sar_status_string",
+            "sar_slab_stage", "sar_slab_stage_peers", "sar_status_string",
             "sar_last_error", "sar_version"]
 
 
@@ -415,6 +416,22 @@ class SlabPlan(Plan):
         self._check_tensor(image, self.image_shape, odt, "image")
         self._stage(3, recv2, None, image, stream)
         return image
+
+    def stage_peers(self, stage, inp, peer_ptrs, stream=None):
+        """Stage 1 (inp = data) or 2 (inp = this rank's exchange-#1 receive
+        buffer, overwritten) with the exchange done by stores: block h goes
+        straight into slot ``rank`` of ``peer_ptrs[h]`` (device addresses of
+        every rank's receive buffer, valid in this process)."""
+        import torch
+        if stage == 1:
+            self._check_tensor(inp, self.data_shape, torch.complex64, "data")
+        else:
+            self._check_tensor(inp, self.send1_shape, torch.complex64, "recv1")
+        if len(peer_ptrs) != self.world:
+            raise ValueError("need one receive buffer per rank")
+        arr = (C.c_void_p * self.world)(*[C.c_void_p(int(x)) for x in peer_ptrs])
+        _check(self._lib.sar_slab_stage_peers(self._h, stage, C.c_void_p(inp.data_ptr()), arr,
+                                              _stream_ptr(stream)))
 
     def planes(self):
         """Output planes this rank writes: (z + nz/2) mod nz of its z-slots (reading R8)."""

@@ -49,3 +49,52 @@ def emulate(plans, data, image):
     for p, r in zip(plans, r2):
         p.stage3(r, image)
     return image
+
+
+# ---- exchange by peer stores (sar_slab_stage_peers) -------------------------
+def emulate_peers(plans, data, image):
+    """All ranks in this process with the exchanges done by the stage kernels'
+    own stores into every rank's receive buffer (all buffers on this GPU: the
+    same code writes to peer GPUs when the pointers are IPC-mapped)."""
+    import torch
+    recv1 = [torch.empty(p.send1_shape, dtype=torch.complex64, device=data.device) for p in plans]
+    recv2 = [torch.empty(p.send2_shape, dtype=torch.complex64, device=data.device) for p in plans]
+    p1 = [t.data_ptr() for t in recv1]
+    p2 = [t.data_ptr() for t in recv2]
+    for p in plans:
+        p.stage_peers(1, data, p1)
+    for p, r in zip(plans, recv1):
+        p.stage_peers(2, r, p2)
+    for p, r in zip(plans, recv2):
+        p.stage3(r, image)
+    return image
+
+
+def open_peer_buffers(local, group=None):
+    """Device addresses, valid in this process, of every rank's ``local``
+    receive buffer: CUDA IPC handles exchanged over ``group`` (the caller
+    keeps the returned tensors alive while the addresses are used)."""
+    import torch.distributed as dist
+    from torch.multiprocessing.reductions import reduce_tensor
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    func, args = reduce_tensor(local)
+    got = [None] * world
+    dist.all_gather_object(got, (func, args), group=group)
+    views = [local if g == rank else got[g][0](*got[g][1]) for g in range(world)]
+    return [v.data_ptr() for v in views], views
+
+
+def reconstruct_peers(plan, data, image, recv1, recv2, peers1, peers2, group=None):
+    """One rank's image pass with peer-store exchanges: stage 1 stores into
+    every rank's recv1, a stream sync + barrier orders it before stage 2
+    reads, likewise for recv2, then stage 3 on this rank's recv2."""
+    import torch
+    import torch.distributed as dist
+    plan.stage_peers(1, data, peers1)
+    torch.cuda.current_stream().synchronize()
+    dist.barrier(group=group)
+    plan.stage_peers(2, recv1, peers2)
+    torch.cuda.current_stream().synchronize()
+    dist.barrier(group=group)
+    return plan.stage3(recv2, image)
+

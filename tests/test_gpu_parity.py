@@ -530,3 +530,79 @@ def test_slab_without_tma_equals_whole_image(monkeypatch):
     finally:
         for p in plans:
             p.close()
+
+
+@pytest.mark.parametrize("name,world", [("small", 2), ("small", 4), ("large", 8)])
+def test_slab_peer_stores_equal_whole_image(name, world):
+    """Exchange by peer stores (sar_slab_stage_peers): every rank's pack kernel
+    writes its blocks straight into the other ranks' receive buffers -- here
+    all on this GPU, the same kernel writes over NVLink when the pointers are
+    IPC-mapped -- and the assembled image equals the whole image bit for bit."""
+    from paper_2305_02064_b200 import slab
+    sc = scenes.make_scene(name)
+    if name == "large":
+        from scenes import gpu as sgpu
+        d = sgpu.synthesize_gpu(sc)
+    else:
+        d, _ = _data(sc)
+    with sar.Plan.from_scene(sc) as p0:
+        want = p0.reconstruct(d)
+    plans = [sar.SlabPlan.from_scene(sc, rank=r, world=world) for r in range(world)]
+    try:
+        got = torch.full_like(want, float("nan"))
+        slab.emulate_peers(plans, d, got)
+        torch.cuda.synchronize()
+        assert torch.equal(got, want), (name, world)
+    finally:
+        for p in plans:
+            p.close()
+
+
+def _ipc_worker(rank, world, port, out):
+    import os as _os
+    import torch.distributed as dist
+    _os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    from paper_2305_02064_b200 import slab
+    sc = scenes.make_scene("small")
+    d = torch.from_numpy(scenes.synthesize_cpu(sc)).cuda()
+    with sar.Plan.from_scene(sc) as p0:
+        want = p0.reconstruct(d)
+    with sar.SlabPlan.from_scene(sc, rank=rank, world=world) as p:
+        recv1 = torch.empty(p.send1_shape, dtype=torch.complex64, device="cuda")
+        recv2 = torch.empty(p.send2_shape, dtype=torch.complex64, device="cuda")
+        peers1, keep1 = slab.open_peer_buffers(recv1)
+        peers2, keep2 = slab.open_peer_buffers(recv2)
+        img = torch.full_like(want, float("nan"))
+        slab.reconstruct_peers(p, d, img, recv1, recv2, peers1, peers2)
+        torch.cuda.synchronize()
+        mine = p.planes()
+        ok = bool(torch.equal(img[:, mine], want[:, mine]))
+        dist.barrier()
+        del keep1, keep2
+    out.put((rank, ok))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_slab_peer_stores_ipc_two_processes():
+    """The CUDA-IPC plumbing of the peer-store exchange (open_peer_buffers /
+    reconstruct_peers) with two processes; both use this GPU (one GPU per
+    gpurun call), their kernels never wait on each other (host barriers
+    between the stages)."""
+    import socket
+    import torch.multiprocessing as mp
+    with socket.socket() as s_:
+        s_.bind(("127.0.0.1", 0))
+        port = s_.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_ipc_worker, args=(r, 2, port, q)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    res = dict(q.get(timeout=300) for _ in range(2))
+    for pr in procs:
+        pr.join(timeout=120)
+        assert pr.exitcode == 0
+    assert res == {0: True, 1: True}
