@@ -231,9 +231,16 @@ __device__ __forceinline__ void discard_l2(const void *p) {
 // ---- launchers (one translation unit each) ----
 cudaError_t launch_k1(const SarDeviceView &v, const float2 *data, bool fft, cudaStream_t s,
                       const CUtensorMap *tm_s, const CUtensorMap *tm_ap, int br, bool regacc, int num_sms);
+// Optional slab epilogue of the mid-axis FFT (slab stage 2, K4a): chunk c of
+// column a goes to block h = c*16 / nzl (the packed send buffer or a peer's
+// receive buffer) at [row][a][z - h nzl] with nzl z-slots per block.
+struct MidSlabOut {
+  char *d[SAR_MAX_SLAB];
+  int nzl;   // 0: off (in place)
+};
 template <int DIR>
 cudaError_t launch_mid(float2 *data, const float2 *tw, int F, int ny, int nx, int inner, cudaStream_t s,
-                       const CUtensorMap *tm, int num_sms);
+                       const CUtensorMap *tm, int num_sms, const MidSlabOut *so = nullptr);
 cudaError_t launch_k3(const SarDeviceView &v, bool ifft, cudaStream_t s, int num_sms);
 cudaError_t launch_k3_plane(const SarDeviceView &v, cudaStream_t s);
 cudaError_t launch_stolt_index(const SarDeviceView &v, const int32_t *cols, int n, int32_t *i0, float *tau,

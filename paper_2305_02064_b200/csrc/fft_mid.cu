@@ -72,10 +72,10 @@ constexpr int mid2_ctas() {
 template <int N>
 constexpr int mid2_ntc() { return N == 512 ? 512 : sarfft2::nt_fft<N, KC>(); }
 
-template <int N, int DIR>
+template <int N, int DIR, bool SLAB>
 __global__ void __launch_bounds__(mid2_ntc<N>() + 32)
     k_fft_mid2(const __grid_constant__ CUtensorMap tm, float2 *__restrict__ data, const float2 *__restrict__ twg,
-               int nx, int inner, int nchunk, int nitems) {
+               int nx, int inner, int nchunk, int nitems, const MidSlabOut so) {
   constexpr int NTC = mid2_ntc<N>();
   constexpr int S = mid2_stages<N>();
   constexpr int ROWS = N < 256 ? N : 256;
@@ -113,7 +113,7 @@ __global__ void __launch_bounds__(mid2_ntc<N>() + 32)
     }
     return;
   }
-  const size_t row = (size_t)nx * inner;
+  const size_t row = SLAB ? (size_t)nx * so.nzl : (size_t)nx * inner;
   unsigned n = 0;
   for (int item = blockIdx.x; item < nitems; item += gridDim.x, ++n) {
     const int st = n % S;
@@ -121,7 +121,13 @@ __global__ void __launch_bounds__(mid2_ntc<N>() + 32)
     const int chunk = item % nchunk, rest = item / nchunk;
     const int a = rest % nx, f = rest / nx;
     const float2 *stage = ring + (size_t)st * N * KC;
-    float2 *base = data + ((size_t)f * N * nx + a) * (size_t)inner + chunk * KC;
+    float2 *base;
+    if constexpr (SLAB) {
+      const int h = chunk * KC / so.nzl;
+      base = reinterpret_cast<float2 *>(so.d[h]) + (size_t)a * so.nzl + (chunk * KC - h * so.nzl);
+    } else {
+      base = data + ((size_t)f * N * nx + a) * (size_t)inner + chunk * KC;
+    }
     const int cmax = inner - chunk * KC;
     sarfft2::fft_ctx<N, KC, KC, NTC, DIR, 1, false, (N == 512 ? 16 : 0), (N == 512)>(
         work, tw, tid, [&](int c, int m) { return stage[m * KC + c]; },
@@ -140,14 +146,18 @@ __global__ void __launch_bounds__(mid2_ntc<N>() + 32)
 
 template <int DIR>
 cudaError_t launch_mid(float2 *data, const float2 *tw, int F, int ny, int nx, int inner, cudaStream_t s,
-                       const CUtensorMap *tm, int num_sms) {
+                       const CUtensorMap *tm, int num_sms, const MidSlabOut *so) {
+  const MidSlabOut off{};
+  if (so && !(tm && ny <= 512 && F == 1 && so->nzl % KC == 0)) return cudaErrorInvalidValue;
   if (tm && ny <= 512) {
     const int nchunk = (inner + KC - 1) / KC;
     const int nitems = nchunk * nx * F;
     switch (ny) {
 #define X(N)                                                                                       \
   case N: {                                                                                        \
-    auto kern = k_fft_mid2<N, DIR>;                                                                \
+    void (*kern)(const CUtensorMap, float2 *, const float2 *, int, int, int, int, const MidSlabOut) =   \
+        k_fft_mid2<N, DIR, false>;                                                                 \
+    if (so) kern = k_fft_mid2<N, DIR, true>;                                                       \
     constexpr size_t smem = mid2_smem<N>();                                                        \
     if (smem > 40 * 1024) {                                                                        \
       cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
@@ -155,7 +165,7 @@ cudaError_t launch_mid(float2 *data, const float2 *tw, int F, int ny, int nx, in
     }                                                                                              \
     const int maxg = num_sms * mid2_ctas<N>();                                                     \
     kern<<<nitems < maxg ? nitems : maxg, mid2_ntc<N>() + 32, smem, s>>>(*tm, data, tw, nx, inner,   \
-                                                                                  nchunk, nitems); \
+                                                                                  nchunk, nitems, so ? *so : off); \
     return cudaGetLastError();                                                                     \
   }
       X(2) X(4) X(8) X(16) X(32) X(64) X(128) X(256) X(512)
@@ -183,7 +193,9 @@ cudaError_t launch_mid(float2 *data, const float2 *tw, int F, int ny, int nx, in
 }
 
 
-template cudaError_t launch_mid<-1>(float2 *, const float2 *, int, int, int, int, cudaStream_t, const CUtensorMap *, int);
-template cudaError_t launch_mid<+1>(float2 *, const float2 *, int, int, int, int, cudaStream_t, const CUtensorMap *, int);
+template cudaError_t launch_mid<-1>(float2 *, const float2 *, int, int, int, int, cudaStream_t, const CUtensorMap *, int,
+                                    const MidSlabOut *);
+template cudaError_t launch_mid<+1>(float2 *, const float2 *, int, int, int, int, cudaStream_t, const CUtensorMap *, int,
+                                    const MidSlabOut *);
 
 }  // namespace sark

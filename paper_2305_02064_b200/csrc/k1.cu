@@ -99,7 +99,14 @@ __global__ void __launch_bounds__(nt_for(NX), minb_for(NX))
     if (ITEMS % NT != 0 && item >= ITEMS) continue;
     const int kk = item & (KC - 1), vx = item >> 4;
     const int k = kbase + kk;
-    if (k < v.nk) out[(size_t)vx * v.nk + k] = tile[item];
+    if (k < v.nk) {
+      if (v.slab_lg >= 0) {   // slab stage 1: packed per destination rank (or into the peer)
+        const int h = vx >> v.slab_lg, al = vx & ((1 << v.slab_lg) - 1);
+        v.slab_dst[h][(((size_t)blockIdx.y << v.slab_lg) + al) * v.nk + k] = tile[item];
+      } else {
+        out[(size_t)vx * v.nk + k] = tile[item];
+      }
+    }
   }
 }
 
@@ -143,7 +150,7 @@ __device__ __forceinline__ bool k1_next(const SarDeviceView &v, K1Job &j, int ni
   }
 }
 
-template <int NX, bool REGACC>
+template <int NX, bool REGACC, bool SLAB>
 __global__ void __launch_bounds__(K1_NT + 32, 1)
     k1_correct_xfft_tma(const SarDeviceView v, const __grid_constant__ CUtensorMap tm_s,
                         const __grid_constant__ CUtensorMap tm_ap, int br, int nbox, int nitems) {
@@ -292,7 +299,14 @@ __global__ void __launch_bounds__(K1_NT + 32, 1)
     sarfft2::fft<NX, C, C, K1_NT, -1, 1, false, (NX == 512 ? 16 : 0)>(
         tile, tws, tid, [&](int c, int m) { return tile[m * C + c]; }, [] {},
         [&](int c, int m, float2 x) {
-          if (c < cmax) __stcs(out + (size_t)m * v.nk + c, x);
+          if (c < cmax) {
+            if constexpr (SLAB) {   // slab stage 1: packed per destination rank (or into the peer)
+              const int h = m >> v.slab_lg, al = m & ((1 << v.slab_lg) - 1);
+              __stcs(v.slab_dst[h] + (((size_t)vyl << v.slab_lg) + al) * v.nk + kc * C + c, x);
+            } else {
+              __stcs(out + (size_t)m * v.nk + c, x);
+            }
+          }
         });
     sarfft::tile_sync<1, K1_NT>();
     if (!REGACC) {
@@ -330,7 +344,8 @@ cudaError_t launch_k1(const SarDeviceView &v, const float2 *data, bool fft, cuda
     switch (v.nx) {
 #define X(N)                                                                                          \
   case N: {                                                                                           \
-    auto kern = regacc ? k1_correct_xfft_tma<N, true> : k1_correct_xfft_tma<N, false>;               \
+    auto kern = v.slab_lg >= 0 ? (regacc ? k1_correct_xfft_tma<N, true, true> : k1_correct_xfft_tma<N, false, true>) \
+                               : (regacc ? k1_correct_xfft_tma<N, true, false> : k1_correct_xfft_tma<N, false, false>); \
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
     if (e != cudaSuccess) return e;                                                                   \
     kern<<<grid, K1_NT + 32, smem, s>>>(v, *tm_s, *tm_ap, br, nbox, nitems);                               \

@@ -294,6 +294,14 @@ int sar_slab_launch(sar_plan *p, int stage, const void *d_in, void *d_out, void 
     SarDeviceView vk = v;
     vk.vy0 = r * nyl;
     vk.nvy = nyl;
+    // K1's epilogue stores every column straight into its destination block
+    // (the packed send buffer, or slot `rank` of the peer's receive buffer)
+    const long long hs1 = (long long)nyl * nxl * v.nk * c8;
+    const BlockDst bd = peers ? dst_peers(peers, G, r, hs1) : dst_packed(d_out, G, hs1);
+    int lg = 0;
+    while ((1 << lg) < nxl) ++lg;
+    vk.slab_lg = lg;
+    for (int h = 0; h < G; ++h) vk.slab_dst[h] = reinterpret_cast<float2 *>(bd.d[h]);
     const CUtensorMap *tm_s = nullptr;
     if (p->tma_ap) {
       if (p->tm_s_ptr != d_in) p->tma_s = sar_encode_input_map(p, d_in);
@@ -301,11 +309,6 @@ int sar_slab_launch(sar_plan *p, int stage, const void *d_in, void *d_out, void 
     }
     SAR_CHECK(launch_k1(vk, static_cast<const float2 *>(d_in), true, s, tm_s, p->tma_ap ? &p->tm_ap : nullptr,
                         p->k1_br, p->k1_regacc, p->num_sms));
-    // pack for exchange #1: block h = columns [h nx', (h+1) nx') of every row
-    const long long hs1 = (long long)nyl * nxl * v.nk * c8;
-    SAR_CHECK(block_copy(peers ? dst_peers(peers, G, r, hs1) : dst_packed(d_out, G, hs1), v.w0, G, nyl,
-                         (long long)nxl * v.nk * c8, (long long)nxl * v.nk * c8, (long long)v.nx * v.nk * c8,
-                         (long long)nxl * v.nk * c8, p->num_sms, s));
     return SAR_OK;
   }
   if (stage == 2) {
@@ -326,13 +329,22 @@ int sar_slab_launch(sar_plan *p, int stage, const void *d_in, void *d_out, void 
     vk.ncls = p->slab_ncls;
     vk.w0 = xs;
     SAR_CHECK(launch_k3(vk, true, s, p->num_sms));
-    SAR_CHECK(launch_mid<+1>(v.w1, v.tw_y, 1, v.ny, nxl, v.nz, s, p->tma_w1x ? &p->tm_w1x_mid : nullptr,
-                             p->num_sms));
-    // pack for exchange #2: block h = z-slots [h nz', (h+1) nz') of every column
+    // y-IFFT; exchange #2 takes block h = z-slots [h nz', (h+1) nz') of every
+    // column: stored there by the y-IFFT's own epilogue when a 16-wide z chunk
+    // never straddles two blocks, else packed by a copy
     const long long hs2 = (long long)v.ny * nxl * nzl * c8;
-    SAR_CHECK(block_copy(peers ? dst_peers(peers, G, r, hs2) : dst_packed(d_out, G, hs2), v.w1, G,
-                         (long long)v.ny * nxl, (long long)nzl * c8, (long long)nzl * c8, (long long)v.nz * c8,
-                         (long long)nzl * c8, p->num_sms, s));
+    const BlockDst bd2 = peers ? dst_peers(peers, G, r, hs2) : dst_packed(d_out, G, hs2);
+    if (p->tma_w1x && nzl % KC == 0 && v.ny <= 512) {
+      MidSlabOut so{};
+      so.nzl = nzl;
+      for (int h = 0; h < G; ++h) so.d[h] = bd2.d[h];
+      SAR_CHECK(launch_mid<+1>(v.w1, v.tw_y, 1, v.ny, nxl, v.nz, s, &p->tm_w1x_mid, p->num_sms, &so));
+    } else {
+      SAR_CHECK(launch_mid<+1>(v.w1, v.tw_y, 1, v.ny, nxl, v.nz, s, p->tma_w1x ? &p->tm_w1x_mid : nullptr,
+                               p->num_sms));
+      SAR_CHECK(block_copy(bd2, v.w1, G, (long long)v.ny * nxl, (long long)nzl * c8, (long long)nzl * c8,
+                           (long long)v.nz * c8, (long long)nzl * c8, p->num_sms, s));
+    }
     return SAR_OK;
   }
   // stage 3: unpack [G][ny][nx'][nz'] (block g = columns [g nx', (g+1) nx'))

@@ -548,6 +548,7 @@ int sar_plan_create(sar_plan **out, const sar_geom_desc *g, const sar_image_desc
   v.zroll = v.mode2d ? 0 : p->nz / 2;
   v.vy0 = 0;
   v.nvy = p->ny;
+  v.slab_lg = -1;
   v.ncls = (p->nx / 2 + 1) * (p->ny / 2 + 1);
   v.z_off = 0;
   v.nz_img = p->nz;

@@ -39,6 +39,8 @@ struct SarDeviceView {
   int roll_x, roll_y;
   // slab decomposition (sar_slab_*; whole-image plans: 0, ny, (nx/2+1)(ny/2+1), 0, nz)
   int vy0, nvy;         // K1: virtual rows [vy0, vy0 + nvy) written as rows 0.. of w0
+  int slab_lg;          // K1 slab epilogue: -1 off, else log2(nx'); column a of row vyl goes to
+  float2 *slab_dst[SAR_MAX_SLAB];  //   slab_dst[a >> slab_lg] + (vyl nx' + a % nx') nk (packed or a peer)
   int ncls;             // K3: entries of cls
   int z_off, nz_img;    // K4b: the nz z-slots are z_off.. of an nz_img-plane image
   int zroll;            // output z roll: nz/2 (3-D, reading R8), 0 (2-D planes)
