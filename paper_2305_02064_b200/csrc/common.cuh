@@ -246,7 +246,7 @@ cudaError_t launch_k3_plane(const SarDeviceView &v, cudaStream_t s);
 cudaError_t launch_stolt_index(const SarDeviceView &v, const int32_t *cols, int n, int32_t *i0, float *tau,
                                cudaStream_t s);
 cudaError_t launch_k4b(const SarDeviceView &v, void *img, bool cplx, cudaStream_t s, const CUtensorMap *tm,
-                       int num_sms);
+                       int num_sms, bool slab4d = false);
 bool passb_supported(const SarDeviceView &v);
 cudaError_t launch_passb(const SarDeviceView &v, const CUtensorMap *tm0, const CUtensorMap *tm1, const int4 *items,
                          int nitems, int *cnt, int stop, bool discard, cudaStream_t s, int num_sms);

@@ -46,7 +46,10 @@ constexpr int k4b2_ctas() {
   return (int)((200 * 1024) / k4b2_smem<NX, false>()) < 1 ? 1 : (int)((200 * 1024) / k4b2_smem<NX, false>());
 }
 
-template <int NX, bool CPLX>
+// SLAB: tm is a 4-D map over the received blocks [G][ny][nx'][nz'] of the
+// slab exchange #2 (box {16 z, nx', 1, G} = one [nx][16] tile), so stage 3
+// needs no unpack pass.
+template <int NX, bool CPLX, bool SLAB>
 __global__ void __launch_bounds__(sarfft2::nt_fft<NX, KC>() + 32)
     k4_xifft_mag2(const SarDeviceView v, const __grid_constant__ CUtensorMap tm, void *__restrict__ img, int nzc,
                   int nitems) {
@@ -79,9 +82,13 @@ __global__ void __launch_bounds__(sarfft2::nt_fft<NX, KC>() + 32)
         if (n >= S) sartma::mbar_wait(&empty[st], ((n / S) - 1) & 1);
         const int zc = item % nzc, fy = item / nzc;  // fy = f*ny + y
         sartma::mbar_arrive_expect_tx(&full[st], TILE_BYTES);
+        if constexpr (SLAB) {
+          sartma::tma_load_4d(ring + (size_t)st * NX * KC, &tm, zc * KC, 0, fy, 0, &full[st]);
+        } else {
 #pragma unroll
-        for (int bx = 0; bx < NBOX; ++bx)
-          sartma::tma_load_3d(ring + (size_t)st * NX * KC + bx * ROWS * KC, &tm, zc * KC, bx * ROWS, fy, &full[st]);
+          for (int bx = 0; bx < NBOX; ++bx)
+            sartma::tma_load_3d(ring + (size_t)st * NX * KC + bx * ROWS * KC, &tm, zc * KC, bx * ROWS, fy, &full[st]);
+        }
       }
     }
     return;
@@ -203,14 +210,16 @@ cudaError_t launch_img(K kernel, dim3 grid, int nt, size_t smem, cudaStream_t s,
 }  // namespace
 
 cudaError_t launch_k4b(const SarDeviceView &v, void *img, bool cplx, cudaStream_t s, const CUtensorMap *tm,
-                       int num_sms) {
+                       int num_sms, bool slab4d) {
+  if (slab4d && !(tm && v.nx <= 512)) return cudaErrorInvalidValue;
   if (tm && v.nx <= 512) {
     const int nzc = (v.nz + KC - 1) / KC;
     const int nitems = nzc * v.ny * v.F;
     switch (v.nx) {
 #define X(N)                                                                                           \
   case N: {                                                                                            \
-    auto kern = cplx ? k4_xifft_mag2<N, true> : k4_xifft_mag2<N, false>;                               \
+    auto kern = cplx ? k4_xifft_mag2<N, true, false> : k4_xifft_mag2<N, false, false>;                 \
+    if (slab4d) kern = cplx ? k4_xifft_mag2<N, true, true> : k4_xifft_mag2<N, false, true>;            \
     constexpr size_t smem = k4b2_smem<N, false>();                                                     \
     if (smem > 40 * 1024) {                                                                            \
       cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \

@@ -150,6 +150,21 @@ bool encode3d(CUtensorMap *m, void *base, uint64_t d0, uint64_t d1, uint64_t d2,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
+// 4-D map over a complex64 array [d3][d2][d1][d0] (d0 fastest)
+bool encode4d(CUtensorMap *m, const void *base, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t d3, uint32_t b0,
+              uint32_t b1, uint32_t b2, uint32_t b3) {
+  auto enc = get_encode();
+  if (!enc) return false;
+  if ((d0 * 8) % 16 != 0 || (reinterpret_cast<uintptr_t>(base) & 15) != 0) return false;
+  cuuint64_t dims[4] = {d0, d1, d2, d3};
+  cuuint64_t strides[3] = {d0 * 8, d0 * d1 * 8, d0 * d1 * d2 * 8};
+  cuuint32_t box[4] = {b0, b1, b2, b3};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<void *>(base), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
 }  // namespace
 
 // 2-D map over a row-major [d1][d0] array of `esize`-byte elements
@@ -347,8 +362,24 @@ int sar_slab_launch(sar_plan *p, int stage, const void *d_in, void *d_out, void 
     }
     return SAR_OK;
   }
-  // stage 3: unpack [G][ny][nx'][nz'] (block g = columns [g nx', (g+1) nx'))
-  // into the z-slab [ny][nx][nz'] (in W0), then x-IFFT + magnitude
+  // stage 3: x-IFFT + magnitude of the received [G][ny][nx'][nz'] (block g =
+  // columns [g nx', (g+1) nx')): read in place through a 4-D tensor map
+  // (one box = one [nx][16] tile), or unpacked into the z-slab [ny][nx][nz']
+  // (in W0) when the map does not apply
+  if (!getenv("SAR_NO_TMA") && nxl <= 256 && v.nx <= 512 && nzl % 2 == 0) {
+    if (p->tm_r2_ptr != d_in) {
+      p->tma_r2 = encode4d(&p->tm_r2_4d, d_in, nzl, nxl, v.ny, G, KC, nxl, 1, G);
+      p->tm_r2_ptr = d_in;
+    }
+    if (p->tma_r2) {
+      SarDeviceView vk = v;
+      vk.nz = nzl;
+      vk.z_off = r * nzl;
+      vk.nz_img = v.nz;
+      SAR_CHECK(launch_k4b(vk, d_image, (p->flags & SAR_OUTPUT_COMPLEX) != 0, s, &p->tm_r2_4d, p->num_sms, true));
+      return SAR_OK;
+    }
+  }
   float2 *zs = v.w0;
   SAR_CHECK(block_copy(dst_packed(zs, G, (long long)nxl * nzl * c8), d_in, G, v.ny, (long long)nxl * nzl * c8,
                        (long long)v.ny * nxl * nzl * c8, (long long)nxl * nzl * c8, (long long)v.nx * nzl * c8,

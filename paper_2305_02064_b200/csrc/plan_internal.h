@@ -120,9 +120,9 @@ struct sar_plan {
   int slab_rank = 0, slab_world = 0;
   SarClass *d_slab_cls = nullptr;
   int slab_ncls = 0;
-  CUtensorMap tm_w1x_mid, tm_w1z_rows, tm_r1_mid;
-  bool tma_w1x = false, tma_w1z = false, tma_r1 = false;
-  const void *tm_r1_ptr = nullptr;
+  CUtensorMap tm_w1x_mid, tm_w1z_rows, tm_r1_mid, tm_r2_4d;
+  bool tma_w1x = false, tma_w1z = false, tma_r1 = false, tma_r2 = false;
+  const void *tm_r1_ptr = nullptr, *tm_r2_ptr = nullptr;
   // NUFFT mode tables and the half-transformed fine grid
   void *d_nu = nullptr;
   unsigned *d_peak = nullptr;   // SAR_REPORT_PEAK
