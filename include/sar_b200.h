@@ -204,13 +204,16 @@ int sar_plan_launches_per_call(const sar_plan *p, int32_t *n);
  *     [h nz', (h+1) nz').
  *   exchange #2: rank h receives block h of every rank g in order of g:
  *     complex64 [G][ny][nx'][nz'].
- *   stage 3 (rank r): x-IFFT + magnitude of the z-slots [r nz', (r+1) nz'],
+ *   stage 3 (rank r): x-IFFT + magnitude of the z-slots [r nz', (r+1) nz']
+ *     (d_in = the exchange-#2 receive buffer, read in place, not modified),
  *     written into d_image = float32 (complex64 with SAR_OUTPUT_COMPLEX)
  *     [nz][ny][nx], the same rolled layout as sar_reconstruct; only the nz'
  *     planes this rank owns are written (plane m = (z + nz/2) mod nz of
  *     z-slot z, reading R8), the others are left untouched.
- * Every element is computed by the same kernel code as sar_reconstruct, so
- * the assembled image equals the whole-image result bit for bit.  All three
+ * Stages 1 and 2 store their blocks from the kernels' own epilogues (no
+ * separate pack pass).  Every element is computed by the same arithmetic as
+ * sar_reconstruct, so the assembled image equals the whole-image result bit
+ * for bit.  All three
  * calls are asynchronous on `stream`; d_in / d_out / d_image are device
  * pointers owned by the caller, 16-byte aligned, and must not alias.  The
  * plan also works as a whole-image plan (sar_reconstruct). */
