@@ -176,6 +176,11 @@ constexpr int K3P_G = K3P_GEOM_[0];
 constexpr int K3P_NG = K3P_GEOM_[1];
 constexpr int K3P_S = K3P_GEOM_[2];
 constexpr int K3P_CL = K3P_GEOM_[3];
+// group g takes items n = g (mod NG), which use stage n mod S: with NG | S
+// every stage belongs to one group, so a group waiting on a stage's full
+// barrier can never see the phase of another group's item (mbarrier parity
+// waits cannot tell phases two apart)
+static_assert(K3P_S % K3P_NG == 0, "K3 ring: the stage count must be a multiple of the group count");
 template <int NZ, int CL>
 size_t k3pp_smem(int nk) {
   const size_t hdr = (sizeof(K3Hdr<CL>) + 15) & ~(size_t)15;
