@@ -437,7 +437,8 @@ def test_plane2d_edge_cases(kw, planes):
 @pytest.mark.parametrize("name,world,flags", [("small", 1, 0), ("small", 2, 0), ("small", 4, 0),
                                               ("small", 2, sar.SAR_OUTPUT_COMPLEX),
                                               ("small", 2, sar.SAR_NO_COMPENSATION),
-                                              ("freehand", 4, 0), ("large", 2, 0), ("large", 8, 0)])
+                                              ("freehand", 4, 0), ("large", 2, 0), ("large", 8, 0),
+                                              ("large", 16, 0)])
 def test_slab_emulated_equals_whole_image(name, world, flags):
     """All G ranks run in this process (exchanges by tensor indexing, the same
     block permutation NCCL's all_to_all_single performs -- test_multiproc.py
