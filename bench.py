@@ -48,9 +48,7 @@ def _peaks():
 def stage_alg_bytes(sc):
     """Algorithmic bytes per launch of each kernel slot:
     the compulsory read of its input and write of its output, 8 B per complex64
-    element, 4 B per float32 voxel.  With the fused pass B (K2+K3+K4a in one
-    kernel, reported in the K3 slot) that slot reads W0 once and writes W1
-    once, the same bytes as K3 alone."""
+    element, 4 B per float32 voxel."""
     F, ny, nx, nk, nz = sc.n_frames, sc.ny, sc.nx, sc.n_k, sc.nz
     planar = 8 * F * ny * nx * nk
     vol = 8 * F * ny * nx * nz
@@ -59,10 +57,7 @@ def stage_alg_bytes(sc):
 
 
 def stage_slots(plan, sar):
-    """(slot index, name) of the kernels one call launches."""
-    if plan.launches_per_call() == 3:
-        return [(0, sar.STAGE_NAMES[0]), (2, "K2+K3+K4a fused pass B (y-FFT, filter+Stolt+z-IFFT, y-IFFT)"),
-                (4, sar.STAGE_NAMES[4])]
+    """(slot index, name) of the kernel slots one call times."""
     return list(enumerate(sar.STAGE_NAMES))
 
 
@@ -137,7 +132,11 @@ def oracle_sample(sc, s_host, max_pairs=1, planes=None, nufft=False):
     geo = oracle.decompose(sc.tx[:1], sc.rx[:max_pairs], sc.scan, sc.npx, sc.npy, sc.x0, sc.y0, sc.dx, sc.dy,
                            sc.z0, sc.k, sc.nx, sc.ny, sc.nz, sc.dz_img, sc.z_ref)
     t0 = time.perf_counter()
-    if nufft:
+    if nufft and planes:
+        sc1 = dataclasses.replace(sc, tx=sc.tx[:1], rx=sc.rx[:max_pairs])
+        S, g1 = oracle.nufft.spectrum_nufft(sub, sc1)
+        oracle.magnitude_planes(oracle.ifft2_planes(oracle.plane_sum(oracle.rma_filter(S, g1), g1, planes)), g1)
+    elif nufft:
         sc1 = dataclasses.replace(sc, tx=sc.tx[:1], rx=sc.rx[:max_pairs])
         oracle.nufft.reconstruct_nufft(sub, sc1)
     elif planes:

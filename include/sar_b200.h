@@ -66,7 +66,11 @@ enum sar_flags {
                                     from their TRUE (x', y') positions (fast Gaussian gridding,
                                     oversampling 2, half width 6 fine cells) instead of the RASTER
                                     lattice + FFT.  Needs nx <= 512, npx <= 512; debug stage 1 is
-                                    not available (there is no lattice) */
+                                    not available (there is no lattice).  Combines with
+                                    SAR_IMAGE_2D (NUFFT spectrum, then the plane sums) */,
+  SAR_FORCE_PLAIN = 1u << 6      /* testing: run the plain (non-TMA, non-persistent) kernel of every
+                                    stage instead of the TMA-pipelined ones; same arithmetic, results
+                                    equal to fp32 rounding (the coverage of the fallback kernels) */
 };
 
 /* Limits of this build. */
@@ -131,7 +135,8 @@ int sar_plan_describe(const sar_geom_desc *g, const sar_image_desc *im, uint32_t
 /* Create a plan: validates the geometry, runs the fp64 decomposition of
  * Eqs. (3),(4),(7),(12) on the host (virtual-node offsets j_tr, beta terms,
  * k_x/k_y/k_z tables), allocates the device workspace
- * (F*ny*nx*(n_k+nz)*8 bytes) and uploads the tables.  *out receives the plan
+ * (F*ny*nx*(n_k+nz)*8 bytes; + F*4*ny*nx*n_k*8 for the SAR_GRID_NUFFT fine
+ * grid) and uploads the tables.  *out receives the plan
  * (NULL on failure).  Errors: INVALID_ARG, GEOMETRY, UNSUPPORTED, OOM, CUDA. */
 int sar_plan_create(sar_plan **out, const sar_geom_desc *g, const sar_image_desc *im,
                     uint32_t flags);
@@ -141,10 +146,10 @@ int sar_plan_create(sar_plan **out, const sar_geom_desc *g, const sar_image_desc
  * 8-byte aligned, read only, caller-owned.  d_image: device, float32
  * [F][nz][ny][nx] (complex64 with SAR_OUTPUT_COMPLEX), caller-owned, fully
  * overwritten.  Voxel (m,iy,ix) is at world (x_first+ix*dx, y_first+iy*dy,
- * z_first+m*dz), see sar_plan_get_axes.  Enqueues 5 kernels on `stream` and
- * returns without synchronising; no allocation.  Not re-entrant per plan (the
+ * z_first+m*dz), see sar_plan_get_axes.  Enqueues 5 kernels (6 with
+ * SAR_GRID_NUFFT) on `stream` and returns without synchronising; no allocation.  Not re-entrant per plan (the
  * workspace is shared): use one plan per concurrent stream.
- * Errors: INVALID_ARG (null pointers), CUDA. */
+ * Errors: INVALID_ARG (null pointers, a slab plan), CUDA. */
 int sar_reconstruct(sar_plan *p, const void *d_data, void *d_image, sar_stream stream);
 
 /* End-to-end variant with HOST buffers: copies h_data (same layout as d_data)
@@ -179,7 +184,8 @@ int sar_plan_profile_reset(sar_plan *p);
  * NULL), CUDA. */
 int sar_plan_peaks(sar_plan *p, float *h_peaks);
 
-/* Number of kernel launches one sar_reconstruct call enqueues (5; 0 if F = 0). */
+/* Number of kernel launches one sar_reconstruct call enqueues (5, 6 with
+ * SAR_GRID_NUFFT; 0 if F = 0). */
 int sar_plan_launches_per_call(const sar_plan *p, int32_t *n);
 
 /* ---- single-image slab decomposition over G GPUs ----
@@ -215,8 +221,10 @@ int sar_plan_launches_per_call(const sar_plan *p, int32_t *n);
  * sar_reconstruct, so the assembled image equals the whole-image result bit
  * for bit.  All three
  * calls are asynchronous on `stream`; d_in / d_out / d_image are device
- * pointers owned by the caller, 16-byte aligned, and must not alias.  The
- * plan also works as a whole-image plan (sar_reconstruct). */
+ * pointers owned by the caller, 16-byte aligned, and must not alias.  A slab
+ * plan's workspace holds only its slabs (2 * ny*nx*nz/G*8 bytes), so it does
+ * not run the whole-image entry points (sar_reconstruct, sar_reconstruct_host,
+ * sar_debug_stage return INVALID_ARG). */
 #define SAR_MAX_SLAB 16 /* world <= 16 */
 
 typedef struct {

@@ -1,5 +1,5 @@
 // common.cuh -- device helpers, constants and launcher declarations shared by
-// the kernel translation units (k1.cu, fft_mid.cu, k3.cu, k4.cu, passb.cu,
+// the kernel translation units (k1.cu, fft_mid.cu, k3.cu, k4.cu,
 // nufft.cu) and the pipeline (pipeline.cu).  Citation keys: P:n = PAPER.md
 // line n; readings R1..R19 are in DESIGN.md section 3.
 #pragma once
@@ -193,39 +193,6 @@ __device__ __forceinline__ void stolt_range(const SarDeviceView &v, double kr2, 
   *jlo = lo;
   *jhi = hi < lo ? lo - 1 : hi;
 }
-constexpr int PB_NT = 256;    // consumer threads (+1 producer warp)
-constexpr int PB_S = 2;       // ring stages
-constexpr int PB_CL = 2;      // mirror classes per S item (<= 8 columns)
-constexpr int PB_KC = 8;      // tile width of the Y / I items ([ny][8], 64-byte rows)
-
-template <int NY, int NZ>
-__host__ __device__ size_t passb_stage_bytes(int nk) {
-  const size_t hdr = (sizeof(K3Hdr<PB_CL>) + 15) & ~(size_t)15;
-  const size_t a = (size_t)NY * PB_KC * sizeof(float2), b = hdr + (size_t)4 * PB_CL * nk * sizeof(float2);
-  return ((a > b ? a : b) + 127) & ~(size_t)127;
-}
-template <int NY, int NZ>
-constexpr int passb_work() {
-  return NY * PB_KC > NZ * (4 * PB_CL + 1) ? NY * PB_KC : NZ * (4 * PB_CL + 1);
-}
-template <int NY, int NZ>
-size_t passb_smem(int nk) {
-  return PB_S * passb_stage_bytes<NY, NZ>(nk) + (size_t)passb_work<NY, NZ>() * sizeof(float2) +
-         (size_t)(NY + NZ) * sizeof(float2);
-}
-
-__device__ __forceinline__ int ld_acquire(const int *p) {
-  int v;
-  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void fence_proxy_async_global() {
-  asm volatile("fence.proxy.async.global;" ::: "memory");
-}
-__device__ __forceinline__ void discard_l2(const void *p) {
-  asm volatile("discard.global.L2 [%0], 128;" ::"l"(p) : "memory");
-}
-
 #define SAR_SIZES(X) X(2) X(4) X(8) X(16) X(32) X(64) X(128) X(256) X(512) X(1024)
 
 // ---- launchers (one translation unit each) ----
@@ -247,9 +214,6 @@ cudaError_t launch_stolt_index(const SarDeviceView &v, const int32_t *cols, int 
                                cudaStream_t s);
 cudaError_t launch_k4b(const SarDeviceView &v, void *img, bool cplx, cudaStream_t s, const CUtensorMap *tm,
                        int num_sms, bool slab4d = false);
-bool passb_supported(const SarDeviceView &v);
-cudaError_t launch_passb(const SarDeviceView &v, const CUtensorMap *tm0, const CUtensorMap *tm1, const int4 *items,
-                         int nitems, int *cnt, int stop, bool discard, cudaStream_t s, int num_sms);
 cudaError_t launch_nufft(const SarDeviceView &v, const float2 *data, cudaStream_t s, const CUtensorMap *tm_fine,
                          int num_sms, int part);
 

@@ -214,7 +214,7 @@ __device__ __forceinline__ void k3pp_consume(const SarDeviceView &v, int nitems_
     int tot = 0;
 #pragma unroll
     for (int cl = 0; cl < CL; ++cl) tot += h.jhi[cl] - h.jlo[cl] + 1;
-    for (int idx = (v.dbg & 2) ? tot : gt; idx < tot; idx += K3P_G) {
+    for (int idx = gt; idx < tot; idx += K3P_G) {
       int cl = 0, j = idx;
 #pragma unroll
       for (int q = 0; q < CL - 1; ++q) {
@@ -258,7 +258,7 @@ __device__ __forceinline__ void k3pp_consume(const SarDeviceView &v, int nitems_
     auto load = [&](int c, int m) {
       return (m >= slo[c] && m <= shi[c]) ? fout[m * LD + c] : make_float2(0.f, 0.f);
     };
-    if (DO_IFFT && !(v.dbg & 4)) {
+    if (DO_IFFT) {
       // the output column's pointer is resolved once per butterfly, so every
       // store is one STG with an immediate offset
       // pass 2 split between thread pairs where C R1 butterflies would leave
@@ -521,7 +521,7 @@ bool try_k3pp(const SarDeviceView &v, bool ifft, cudaStream_t s, int num_sms, cu
 }  // namespace
 
 cudaError_t launch_k3(const SarDeviceView &v, bool ifft, cudaStream_t s, int num_sms) {
-  if ((v.nk & 1) == 0 && v.nz >= 128 && !getenv("SAR_K3_PLAIN")) {
+  if ((v.nk & 1) == 0 && v.nz >= 128 && !v.force_plain) {
     // n_z >= 256: 2 classes (<= 8 columns) per item; n_z = 128: 4 classes
     // (Freehand 0.065 -> 0.055 ms; at n_z = 64 k3_class stays faster:
     // Realtime 0.37 vs 0.43 ms with 8 classes per item)

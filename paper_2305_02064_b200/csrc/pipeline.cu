@@ -59,48 +59,26 @@ int sar_launch_pipeline(sar_plan *p, const void *d_data, void *d_image, cudaStre
     SAR_CHECK(launch_nufft(v, data, s, tmf, p->num_sms, 1));
     if (ev) SAR_CHECK(cudaEventRecord(ev[1], s));
     SAR_CHECK(launch_nufft(v, data, s, tmf, p->num_sms, 2));
-    if (ev) SAR_CHECK(cudaEventRecord(ev[2], s));
-    if (stop_stage == 2) return SAR_OK;
-    SAR_CHECK(launch_k3(v, stop_stage != 3, s, p->num_sms));
-    if (ev) SAR_CHECK(cudaEventRecord(ev[3], s));
-    if (stop_stage == 3) return SAR_OK;
-    SAR_CHECK(launch_mid<+1>(v.w1, v.tw_y, v.F, v.ny, v.nx, v.nz, s, p->tma_mid1 ? &p->tm_w1_mid : nullptr,
-                             p->num_sms));
-    if (ev) SAR_CHECK(cudaEventRecord(ev[4], s));
-    if (v.peak) SAR_CHECK(cudaMemsetAsync(v.peak, 0, (size_t)v.F * sizeof(unsigned), s));
-    SAR_CHECK(launch_k4b(v, d_image, complex_out != 0, s, p->tma_rows1 ? &p->tm_w1_rows : nullptr, p->num_sms));
-    if (ev) SAR_CHECK(cudaEventRecord(ev[5], s));
-    return SAR_OK;
-  }
-  SAR_CHECK(launch_k1(v, data, stop_stage != 1, s, tm_s, p->tma_ap ? &p->tm_ap : nullptr, p->k1_br, p->k1_regacc,
-                      p->num_sms));
-  if (ev) SAR_CHECK(cudaEventRecord(ev[1], s));
-  if (stop_stage == 1) return SAR_OK;
-  if (p->fused) {
-    // K2 + K3 + K4a as one kernel (its time is reported in the K3 slot)
-    if (ev) SAR_CHECK(cudaEventRecord(ev[2], s));
-    SAR_CHECK(launch_passb(v, &p->tm_w0_pb, &p->tm_w1_pb, p->d_items, p->n_items, p->d_cnt,
-                           stop_stage == 2 || stop_stage == 3 ? stop_stage : 0,
-                           stop_stage == 0 && p->passb_discard, s, p->num_sms));
-    if (ev) SAR_CHECK(cudaEventRecord(ev[3], s));
-    if (stop_stage == 2 || stop_stage == 3) return SAR_OK;
-    if (ev) SAR_CHECK(cudaEventRecord(ev[4], s));
   } else {
+    SAR_CHECK(launch_k1(v, data, stop_stage != 1, s, tm_s, p->tma_ap ? &p->tm_ap : nullptr, p->k1_br,
+                        p->k1_regacc, p->num_sms));
+    if (ev) SAR_CHECK(cudaEventRecord(ev[1], s));
+    if (stop_stage == 1) return SAR_OK;
     SAR_CHECK(launch_mid<-1>(v.w0, v.tw_y, v.F, v.ny, v.nx, v.nk, s, p->tma_mid0 ? &p->tm_w0_mid : nullptr,
                              p->num_sms));
-    if (ev) SAR_CHECK(cudaEventRecord(ev[2], s));
-    if (stop_stage == 2) return SAR_OK;
-    if (v.mode2d) {
-      SAR_CHECK(launch_k3_plane(v, s));
-    } else {
-      SAR_CHECK(launch_k3(v, stop_stage != 3, s, p->num_sms));
-    }
-    if (ev) SAR_CHECK(cudaEventRecord(ev[3], s));
-    if (stop_stage == 3) return SAR_OK;
-    SAR_CHECK(launch_mid<+1>(v.w1, v.tw_y, v.F, v.ny, v.nx, v.nz, s, p->tma_mid1 ? &p->tm_w1_mid : nullptr,
-                             p->num_sms));
-    if (ev) SAR_CHECK(cudaEventRecord(ev[4], s));
   }
+  if (ev) SAR_CHECK(cudaEventRecord(ev[2], s));
+  if (stop_stage == 2) return SAR_OK;
+  if (v.mode2d) {
+    SAR_CHECK(launch_k3_plane(v, s));
+  } else {
+    SAR_CHECK(launch_k3(v, stop_stage != 3, s, p->num_sms));
+  }
+  if (ev) SAR_CHECK(cudaEventRecord(ev[3], s));
+  if (stop_stage == 3) return SAR_OK;
+  SAR_CHECK(launch_mid<+1>(v.w1, v.tw_y, v.F, v.ny, v.nx, v.nz, s, p->tma_mid1 ? &p->tm_w1_mid : nullptr,
+                           p->num_sms));
+  if (ev) SAR_CHECK(cudaEventRecord(ev[4], s));
   if (v.peak) SAR_CHECK(cudaMemsetAsync(v.peak, 0, (size_t)v.F * sizeof(unsigned), s));
   SAR_CHECK(launch_k4b(v, d_image, complex_out != 0, s, p->tma_rows1 ? &p->tm_w1_rows : nullptr, p->num_sms));
   if (ev) SAR_CHECK(cudaEventRecord(ev[5], s));
@@ -194,12 +172,10 @@ bool sar_encode_input_map(sar_plan *p, const void *d_data) {
 int sar_build_tensor_maps(sar_plan *p) {
   const SarDeviceView &v = p->v;
   p->tma_mid0 = p->tma_mid1 = p->tma_rows1 = false;
-  if (v.F == 0 || getenv("SAR_NO_TMA")) return SAR_OK;
+  if (v.F == 0 || v.force_plain) return SAR_OK;
   const uint32_t rows = v.ny < 256 ? v.ny : 256;
   p->tma_mid0 = encode3d(&p->tm_w0_mid, v.w0, v.nk, v.nx, (uint64_t)v.F * v.ny, KC, 1, rows);
   p->tma_mid1 = encode3d(&p->tm_w1_mid, v.w1, v.nz, v.nx, (uint64_t)v.F * v.ny, KC, 1, rows);
-  p->tma_pb = encode3d(&p->tm_w0_pb, v.w0, v.nk, v.nx, (uint64_t)v.F * v.ny, PB_KC, 1, rows) &&
-              encode3d(&p->tm_w1_pb, v.w1, v.nz, v.nx, (uint64_t)v.F * v.ny, PB_KC, 1, rows);
   if (v.nufft) {
     // fine grid [F*2ny][2nx][nk]: x-FFT boxes {16 k, 1, <=256 fine columns}
     const uint32_t rx = 2 * v.nx, fr = rx < 256 ? rx : 256;
@@ -285,13 +261,9 @@ BlockDst dst_peers(void *const *peers, int G, int rank, long long hs) {
 int sar_slab_setup(sar_plan *p) {
   const SarDeviceView &v = p->v;
   const int G = p->slab_world, nxl = v.nx / G, nzl = v.nz / G;
-  if ((size_t)v.nk < (size_t)nzl) {
-    sar_set_error("slab plans need n_k >= nz / world (the z-slab reuses the lattice buffer)");
-    return SAR_ERR_UNSUPPORTED;
-  }
   p->tma_w1x = p->tma_w1z = p->tma_r1 = false;
   p->tm_r1_ptr = nullptr;
-  if (getenv("SAR_NO_TMA")) return SAR_OK;
+  if (v.force_plain) return SAR_OK;
   const uint32_t rows = v.ny < 256 ? v.ny : 256, xr = v.nx < 256 ? v.nx : 256;
   p->tma_w1x = encode3d(&p->tm_w1x_mid, v.w1, v.nz, nxl, v.ny, KC, 1, rows);
   p->tma_w1z = encode3d(&p->tm_w1z_rows, v.w0, nzl, v.nx, v.ny, KC, xr, 1);
@@ -329,7 +301,7 @@ int sar_slab_launch(sar_plan *p, int stage, const void *d_in, void *d_out, void 
   if (stage == 2) {
     float2 *xs = static_cast<float2 *>(const_cast<void *>(d_in));   // the x-slab [ny][nx'][nk], overwritten
     const CUtensorMap *tm = nullptr;
-    if (!getenv("SAR_NO_TMA")) {
+    if (!v.force_plain) {
       if (p->tm_r1_ptr != d_in) {
         const uint32_t rows = v.ny < 256 ? v.ny : 256;
         p->tma_r1 = encode3d(&p->tm_r1_mid, xs, v.nk, nxl, v.ny, KC, 1, rows);
@@ -366,7 +338,7 @@ int sar_slab_launch(sar_plan *p, int stage, const void *d_in, void *d_out, void 
   // columns [g nx', (g+1) nx')): read in place through a 4-D tensor map
   // (one box = one [nx][16] tile), or unpacked into the z-slab [ny][nx][nz']
   // (in W0) when the map does not apply
-  if (!getenv("SAR_NO_TMA") && nxl <= 256 && v.nx <= 512 && nzl % 2 == 0) {
+  if (!v.force_plain && nxl <= 256 && v.nx <= 512 && nzl % 2 == 0) {
     if (p->tm_r2_ptr != d_in) {
       p->tma_r2 = encode4d(&p->tm_r2_4d, d_in, nzl, nxl, v.ny, G, KC, nxl, 1, G);
       p->tm_r2_ptr = d_in;

@@ -46,8 +46,9 @@ struct DeviceGuard {
 void free_plan(sar_plan *p) {
   if (!p) return;
   DeviceGuard g(p->device);
-  if (p->last_stream) cudaStreamSynchronize(p->last_stream);
-  cudaDeviceSynchronize();
+  // the plan's work was enqueued on last_stream (NULL = the legacy default
+  // stream, whose synchronisation is what that stream promises)
+  cudaStreamSynchronize(p->last_stream);
   if (p->prof_events)
     for (int i = 0; i < SAR_PROFILE_RING; ++i)
       for (int j = 0; j <= SAR_N_STAGES; ++j) cudaEventDestroy(p->ev[i][j]);
@@ -56,8 +57,6 @@ void free_plan(sar_plan *p) {
   cudaFree(p->d_w1);
   cudaFree(p->d_in);
   cudaFree(p->d_img);
-  cudaFree(p->d_items);
-  cudaFree(p->d_cnt);
   cudaFree(p->d_wh);
   cudaFree(p->d_peak);
   cudaFree(p->d_slab_cls);
@@ -142,7 +141,10 @@ int host_decompose(const sar_geom_desc *g, const sar_image_desc *im, uint32_t fl
     return fail(SAR_ERR_UNSUPPORTED, "SAR_GRID_NUFFT needs 32 <= nx <= 512, ny <= 512, npx <= 512");
   if (!(g->dx > 0) || !(g->dy > 0) || (!mode2d && !(im->dz > 0)))
     return fail(SAR_ERR_INVALID_ARG, "pitches must be > 0");
-  if ((long long)g->n_frames * g->npx * g->npy > (1LL << 31)) return fail(SAR_ERR_UNSUPPORTED, "too many poses");
+  // K1's TMA row coordinate and the NUFFT spread entries index raw sample rows
+  // (frame, pair, pose) with 32-bit ints
+  if ((long long)g->n_frames * g->n_tx * g->n_rx * g->npx * g->npy >= (1LL << 31))
+    return fail(SAR_ERR_UNSUPPORTED, "n_frames * n_tx * n_rx * poses >= 2^31 sample rows");
   if (g->n_frames > 65535) return fail(SAR_ERR_UNSUPPORTED, "n_frames > 65535");
 
   const int F = g->n_frames, nt = g->n_tx, nr = g->n_rx, nk = g->n_k;
@@ -371,7 +373,8 @@ int host_decompose(const sar_geom_desc *g, const sar_image_desc *im, uint32_t fl
   p->axes[3] = g->dx;
   p->axes[4] = g->dy;
   p->axes[5] = mode2d ? (p->nz > 1 ? im->z_planes[1] - im->z_planes[0] : 0.0) : im->dz;
-  p->ws_bytes = ((size_t)F * p->ny * p->nx * ((size_t)nk + p->nz + ((flags & SAR_GRID_NUFFT) ? 2 * (size_t)nk : 0))) *
+  // W0 [F][ny][nx][nk] + W1 [F][ny][nx][nz] (+ the NUFFT fine grid [F][2ny][2nx][nk])
+  p->ws_bytes = ((size_t)F * p->ny * p->nx * ((size_t)nk + p->nz + ((flags & SAR_GRID_NUFFT) ? 4 * (size_t)nk : 0))) *
                 sizeof(float2);
   return SAR_OK;
 }
@@ -410,7 +413,14 @@ int sar_plan_describe(const sar_geom_desc *g, const sar_image_desc *im, uint32_t
   return SAR_OK;
 }
 
-int sar_plan_create(sar_plan **out, const sar_geom_desc *g, const sar_image_desc *im, uint32_t flags) {
+}  // extern "C"
+
+namespace {
+// slab_world > 0: the plan of one rank of a slab decomposition, whose
+// workspace holds only the slab volumes: W1 = the x-slab [ny][nx/G][nz] and
+// W0 = the z-slab [ny][nx][nz/G] (the stage-3 unpack target)
+int plan_create_impl(sar_plan **out, const sar_geom_desc *g, const sar_image_desc *im, uint32_t flags,
+                     int slab_world) {
   if (!out) return fail(SAR_ERR_INVALID_ARG, "out is NULL");
   *out = nullptr;
   sar_plan *p = new (std::nothrow) sar_plan();
@@ -491,7 +501,12 @@ int sar_plan_create(sar_plan **out, const sar_geom_desc *g, const sar_image_desc
     free_plan(p);
     return cuda_fail(ce, "table upload");
   }
-  const size_t n0 = (size_t)F * p->ny * p->nx * nk, n1 = (size_t)F * p->ny * p->nx * p->nz;
+  size_t n0 = (size_t)F * p->ny * p->nx * nk, n1 = (size_t)F * p->ny * p->nx * p->nz;
+  if (slab_world > 0) {
+    n0 = n1 = (size_t)p->ny * p->nx * (p->nz / slab_world);
+    p->ws_bytes = (n0 + n1) * sizeof(float2);
+    p->slab_world = slab_world;
+  }
   if (F > 0) {
     if (cudaMalloc(&p->d_w0, n0 * sizeof(float2)) != cudaSuccess ||
         cudaMalloc(&p->d_w1, n1 * sizeof(float2)) != cudaSuccess ||
@@ -570,16 +585,11 @@ int sar_plan_create(sar_plan **out, const sar_geom_desc *g, const sar_image_desc
   v.peak = p->d_peak;
   v.w0 = p->d_w0;
   v.wh = p->d_wh;
-  v.dbg = getenv("SAR_DBG") ? atoi(getenv("SAR_DBG")) : 0;
+  v.force_plain = (flags & SAR_FORCE_PLAIN) ? 1 : 0;
   v.w1 = p->d_w1;
 
   p->num_sms = prop.multiProcessorCount;
-  sar_build_tensor_maps(p);
-  st = sar_setup_passb(p);
-  if (st != SAR_OK) {
-    free_plan(p);
-    return fail(st, "pass-B work list allocation failed");
-  }
+  if (slab_world == 0) sar_build_tensor_maps(p);
   if (flags & SAR_PROFILE_STAGES) {
     for (int i = 0; i < SAR_PROFILE_RING; ++i)
       for (int j = 0; j <= SAR_N_STAGES; ++j) cudaEventCreate(&p->ev[i][j]);
@@ -587,6 +597,13 @@ int sar_plan_create(sar_plan **out, const sar_geom_desc *g, const sar_image_desc
   }
   *out = p;
   return SAR_OK;
+}
+}  // namespace
+
+extern "C" {
+
+int sar_plan_create(sar_plan **out, const sar_geom_desc *g, const sar_image_desc *im, uint32_t flags) {
+  return plan_create_impl(out, g, im, flags, 0);
 }
 
 int sar_plan_create_slab(sar_plan **out, const sar_geom_desc *g, const sar_image_desc *im, uint32_t flags,
@@ -602,11 +619,10 @@ int sar_plan_create_slab(sar_plan **out, const sar_geom_desc *g, const sar_image
   if (im->nx % G || im->ny % G || im->nz % G || im->nx / G < 1 || im->nz / G < 1)
     return fail(SAR_ERR_INVALID_ARG, "world must divide nx, ny and nz");
   sar_plan *p = nullptr;
-  int st = sar_plan_create(&p, g, im, flags);
+  int st = plan_create_impl(&p, g, im, flags, G);
   if (st != SAR_OK) return st;
   DeviceGuard guard(p->device);
   p->slab_rank = r;
-  p->slab_world = G;
   // the x-slab's Stolt classes: every mirror class restricted to the member
   // columns a in [r nx', (r+1) nx'), local column index b nx' + (a - r nx');
   // k_r^2 and the in-band range are the whole-image class's (bit-identical)
@@ -682,6 +698,7 @@ int sar_slab_stage_peers(sar_plan *p, int32_t stage, const void *d_in, void *con
 
 int sar_reconstruct(sar_plan *p, const void *d_data, void *d_image, sar_stream stream) {
   if (!p) return fail(SAR_ERR_INVALID_ARG, "plan is NULL");
+  if (p->slab_world) return fail(SAR_ERR_INVALID_ARG, "slab plans run sar_slab_stage");
   if (p->F == 0) return SAR_OK;
   if (!d_data || !d_image) return fail(SAR_ERR_INVALID_ARG, "data or image pointer is NULL");
   DeviceGuard g(p->device);
@@ -694,6 +711,7 @@ int sar_reconstruct(sar_plan *p, const void *d_data, void *d_image, sar_stream s
 
 int sar_reconstruct_host(sar_plan *p, const void *h_data, void *h_image, sar_stream stream) {
   if (!p) return fail(SAR_ERR_INVALID_ARG, "plan is NULL");
+  if (p->slab_world) return fail(SAR_ERR_INVALID_ARG, "slab plans run sar_slab_stage");
   if (p->F == 0) return SAR_OK;
   if (!h_data || !h_image) return fail(SAR_ERR_INVALID_ARG, "data or image pointer is NULL");
   DeviceGuard g(p->device);
@@ -701,9 +719,16 @@ int sar_reconstruct_host(sar_plan *p, const void *h_data, void *h_image, sar_str
   const size_t in_b = (size_t)p->F * p->npair * p->P * p->nk * sizeof(float2);
   const size_t img_b = (size_t)p->F * p->nz * p->ny * p->nx *
                        ((p->flags & SAR_OUTPUT_COMPLEX) ? sizeof(float2) : sizeof(float));
-  if (!p->d_in) {
+  if (!p->d_in || !p->d_img) {
+    // both staging buffers or neither (a failed call leaves no half state)
+    cudaFree(p->d_in);
+    cudaFree(p->d_img);
+    p->d_in = p->d_img = nullptr;
     if (cudaMalloc(&p->d_in, in_b) != cudaSuccess || cudaMalloc(&p->d_img, img_b) != cudaSuccess) {
       cudaGetLastError();
+      cudaFree(p->d_in);
+      cudaFree(p->d_img);
+      p->d_in = p->d_img = nullptr;
       return fail(SAR_ERR_OOM, "staging allocation failed");
     }
     p->in_bytes = in_b;
@@ -749,7 +774,8 @@ int sar_plan_workspace_bytes(const sar_plan *p, size_t *bytes) {
 
 int sar_plan_launches_per_call(const sar_plan *p, int32_t *n) {
   if (!p || !n) return fail(SAR_ERR_INVALID_ARG, "NULL argument");
-  *n = p->F > 0 ? (p->fused ? 3 : SAR_N_STAGES) : 0;
+  // K1 (or the NUFFT spread + fine x-FFT + K2n), K2, K3, K4a, K4b
+  *n = p->F > 0 ? ((p->flags & SAR_GRID_NUFFT) ? SAR_N_STAGES + 1 : SAR_N_STAGES) : 0;
   return SAR_OK;
 }
 
@@ -782,6 +808,7 @@ int sar_debug_stage(sar_plan *p, int32_t stage, const void *d_data, void *d_out,
   if (!p) return fail(SAR_ERR_INVALID_ARG, "plan is NULL");
   if (stage < 1 || stage > 4) return fail(SAR_ERR_INVALID_ARG, "stage must be 1..4");
   if (stage == 1 && (p->flags & SAR_GRID_NUFFT)) return fail(SAR_ERR_INVALID_ARG, "no planar lattice in NUFFT mode");
+  if (p->slab_world) return fail(SAR_ERR_INVALID_ARG, "slab plans run sar_slab_stage");
   if (p->F == 0) return SAR_OK;
   if (!d_data || !d_out) return fail(SAR_ERR_INVALID_ARG, "NULL pointer");
   DeviceGuard g(p->device);

@@ -74,7 +74,7 @@ struct SarDeviceView {
   double kz_top, kz_step;  // k_z[nz-1] = 2 k_max and the k_z bin width (reading R5)
   double stolt_delta;   // decision guard band of the fast Stolt path (common.cuh)
   int k1_step_ok;       // max |dk * beta| <= 0.25: K1 may use the Taylor step phasor
-  int dbg;              // ablation switches (env SAR_DBG; 0 in production)
+  int force_plain;      // SAR_FORCE_PLAIN: the plain (non-TMA, non-persistent) kernels
   float img_scale;      // 1/(nx ny nz)
   unsigned *peak;       // [F] max |voxel| bits per frame (SAR_REPORT_PEAK) or nullptr
   float2 *w0;           // [F][ny][nx][nk]  planar lattice -> spectrum
@@ -110,12 +110,6 @@ struct sar_plan {
   int k1_br = 0;                   // pose rows per K1 TMA box
   bool k1_regacc = false;          // every j^x offset is 0: K1 sums in registers
   int num_sms = 148;
-  // fused pass B (K2 + K3 + K4a): work list and dependency counters
-  bool fused = false, passb_discard = false, tma_pb = false;
-  CUtensorMap tm_w0_pb, tm_w1_pb;  // [ny][8] boxes over W0 / W1
-  int4 *d_items = nullptr;
-  int n_items = 0;
-  int *d_cnt = nullptr;
   // slab decomposition (sar_plan_create_slab); slab_world == 0: whole image
   int slab_rank = 0, slab_world = 0;
   SarClass *d_slab_cls = nullptr;
@@ -139,5 +133,4 @@ int sar_build_tensor_maps(sar_plan *p);
 int sar_slab_setup(sar_plan *p);
 int sar_slab_launch(sar_plan *p, int stage, const void *d_in, void *d_out, void *d_image, cudaStream_t s,
                     void *const *peers = nullptr);
-int sar_setup_passb(sar_plan *p);
 bool sar_encode_input_map(sar_plan *p, const void *d_data);

@@ -282,12 +282,10 @@ def test_bad_tensor_arguments():
 
 
 @pytest.mark.parametrize("name", ["small", "realtime"])
-def test_non_tma_fallback_path(name, monkeypatch):
+def test_non_tma_fallback_path(name):
     """The plain (non-TMA) kernels used for odd n_k / unaligned rasters are
-    forced with SAR_NO_TMA and must meet the same bar."""
-    monkeypatch.setenv("SAR_NO_TMA", "1")
-    monkeypatch.setenv("SAR_K3_PLAIN", "1")
-    _check_e2e(scenes.make_scene(name))
+    forced with the SAR_FORCE_PLAIN plan flag and must meet the same bar."""
+    _check_e2e(scenes.make_scene(name), flags=sar.SAR_FORCE_PLAIN)
 
 
 def test_tma_and_plain_paths_agree():
@@ -295,33 +293,10 @@ def test_tma_and_plain_paths_agree():
     d, _ = _data(sc)
     with sar.Plan.from_scene(sc) as plan:
         a = plan.reconstruct(d).cpu().numpy()
-    import os
-    os.environ["SAR_NO_TMA"] = "1"
-    try:
-        with sar.Plan.from_scene(sc) as plan:
-            b = plan.reconstruct(d).cpu().numpy()
-    finally:
-        del os.environ["SAR_NO_TMA"]
+    with sar.Plan.from_scene(sc, flags=sar.SAR_FORCE_PLAIN) as plan:
+        b = plan.reconstruct(d).cpu().numpy()
     e2, _ = errs(a, b.astype(np.float64))
     assert e2 < 1e-5
-
-
-@pytest.mark.parametrize("name", ["small", "freehand", "realtime"])
-def test_fused_pass_b_parity(name, monkeypatch):
-    """The opt-in fused K2+K3+K4a kernel (SAR_FUSE=1, dependency counters and
-    L2 discards) meets the same bar, per stage and end to end."""
-    monkeypatch.setenv("SAR_FUSE", "1")
-    sc = scenes.make_scene(name)
-    with sar.Plan.from_scene(sc) as plan:
-        assert plan.launches_per_call() == 3
-    _check_e2e(sc)
-    if name == "small":
-        d, s = _data(sc)
-        _, _, st = oracle.reconstruct(s, sc, complex_out=True, return_stages=True)
-        with sar.Plan.from_scene(sc) as plan:
-            for stage, key in ((2, "spectrum"), (3, "stolt")):
-                e2, _ = errs(plan.debug_stage(stage, d).cpu().numpy(), st[key])
-                assert e2 <= STAGE_BAR, (key, e2)
 
 
 # ---- 2-D single-plane images (SAR_IMAGE_2D, reading R18) -------------------
@@ -370,6 +345,24 @@ def test_nufft_parity(name):
             plan.debug_stage(1, d)
     e2s, _ = errs(g2, S)
     assert e2s <= STAGE_BAR, e2s
+    e2, einf = errs(got, want)
+    assert e2 <= E2_BAR and einf <= EINF_BAR, (name, e2, einf)
+
+
+@pytest.mark.parametrize("name,planes", [("small", [0.2, 0.25, 0.3]), ("tiny", [0.25])])
+def test_nufft_plane2d_parity(name, planes):
+    """SAR_GRID_NUFFT | SAR_IMAGE_2D: the NUFFT spectrum (reading R19) followed
+    by the plane sums of reading R18 (oracle: nufft.spectrum_nufft, then the
+    2-D steps O4, O5'-O7')."""
+    from oracle import nufft
+    sc = scenes.make_scene(name)
+    d, s = _data(sc)
+    S, geo = nufft.spectrum_nufft(s, sc)
+    want = oracle.magnitude_planes(oracle.ifft2_planes(oracle.plane_sum(oracle.rma_filter(S, geo), geo, planes)),
+                                   geo)
+    with sar.Plan.from_scene(sc, flags=sar.SAR_GRID_NUFFT, z_planes=planes) as plan:
+        assert plan.launches_per_call() == 6
+        got = plan.reconstruct(d).cpu().numpy()
     e2, einf = errs(got, want)
     assert e2 <= E2_BAR and einf <= EINF_BAR, (name, e2, einf)
 
@@ -483,6 +476,10 @@ def test_slab_rank_writes_only_its_planes_and_errors():
             plane = img[0, m]
             assert bool((plane == 0).all()) if m in mine else bool((plane == -1).all())
         assert s1.shape == (4, sc.ny // 4, sc.nx // 4, sc.k.size) and s2.shape == (4, sc.ny, sc.nx // 4, sc.nz // 4)
+        # the slab workspace holds only the slabs, so the whole-image entry points refuse
+        assert p.workspace_bytes() == 2 * 8 * sc.ny * sc.nx * (sc.nz // 4)
+        with pytest.raises(sar.SarError):
+            p.reconstruct(d)
     with pytest.raises(sar.SarError):
         sar.SlabPlan.from_scene(sc, rank=0, world=3)            # 3 does not divide 128
     with pytest.raises(sar.SarError):
@@ -513,15 +510,14 @@ def test_slab_nonsquare_small_z_slots(world):
             p.close()
 
 
-def test_slab_without_tma_equals_whole_image(monkeypatch):
-    """The slab stages on the non-TMA fallback kernels (SAR_NO_TMA)."""
+def test_slab_without_tma_equals_whole_image():
+    """The slab stages on the non-TMA fallback kernels (SAR_FORCE_PLAIN)."""
     from paper_2305_02064_b200 import slab
     sc = scenes.make_scene("small")
     d, _ = _data(sc)
     with sar.Plan.from_scene(sc) as p0:
         want = p0.reconstruct(d)
-    monkeypatch.setenv("SAR_NO_TMA", "1")
-    plans = [sar.SlabPlan.from_scene(sc, rank=r, world=4) for r in range(4)]
+    plans = [sar.SlabPlan.from_scene(sc, rank=r, world=4, flags=sar.SAR_FORCE_PLAIN) for r in range(4)]
     try:
         got = torch.full_like(want, float("nan"))
         slab.emulate(plans, d, got)
