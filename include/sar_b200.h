@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define SAR_B200_VERSION 3
+#define SAR_B200_VERSION 4
 
 typedef struct sar_plan sar_plan;       /* opaque */
 typedef struct CUstream_st *sar_stream; /* == cudaStream_t; NULL = legacy default stream */
@@ -131,6 +131,18 @@ typedef struct {
 int sar_plan_describe(const sar_geom_desc *g, const sar_image_desc *im, uint32_t flags,
                       sar_plan_info *info, int32_t *jx, int32_t *jy, double *kx, double *ky,
                       double *kz, float *apose, float *bpair);
+
+/* Host-only export of the Stolt bin range step 3 computes for every spectral
+ * column (Eqs. (13)-(14); readings R5, R9): ranges[(b*nx + a)*2]
+ * = jlo, [+1] = jhi, a superset of the k_z bins j whose pull can be in band
+ * (the bit-exact fp64 decision runs only there, every other bin is zero).
+ * jhi < jlo marks a column with no bin in band, whose Stolt output is zero:
+ * evanescent (k_r^2 >= 4 k_max^2) or its band below the k_z window; the plan
+ * skips such columns (no read, no write) except where the inverse y-FFT reads
+ * them as part of a 32-row box.  ranges: host int32 [ny][nx][2].  Errors: as
+ * sar_plan_describe. */
+int sar_plan_describe_stolt_ranges(const sar_geom_desc *g, const sar_image_desc *im, uint32_t flags,
+                                   int32_t *ranges);
 
 /* Create a plan: validates the geometry, runs the fp64 decomposition of
  * Eqs. (3),(4),(7),(12) on the host (virtual-node offsets j_tr, beta terms,

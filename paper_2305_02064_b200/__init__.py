@@ -5,8 +5,11 @@ Public API: :class:`Plan` (``sar_plan_create`` / ``sar_reconstruct`` /
 in-tree CUDA library ``libsar_b200.so``; PyTorch provides device memory and
 streams only.  There is no CPU fallback.
 """
-from .sar import (Plan, SlabPlan, SarError, describe, describe_scene, load_library, LIB_PATH, SAR_NO_COMPENSATION,  # noqa: F401
-                  SAR_OUTPUT_COMPLEX, SAR_PROFILE_STAGES, SAR_IMAGE_2D, SAR_GRID_NUFFT, SAR_REPORT_PEAK, STAGE_NAMES)
+from .sar import (Plan, SlabPlan, SarError, describe, describe_scene, describe_stolt_ranges,  # noqa: F401
+                  describe_stolt_ranges_scene, load_library, LIB_PATH, SAR_NO_COMPENSATION, SAR_OUTPUT_COMPLEX,
+                  SAR_PROFILE_STAGES, SAR_IMAGE_2D, SAR_GRID_NUFFT, SAR_REPORT_PEAK, SAR_FORCE_PLAIN, STAGE_NAMES)
 
-__all__ = ["Plan", "SlabPlan", "SarError", "describe", "describe_scene", "load_library", "LIB_PATH", "SAR_NO_COMPENSATION",
-           "SAR_OUTPUT_COMPLEX", "SAR_PROFILE_STAGES", "SAR_IMAGE_2D", "SAR_GRID_NUFFT", "SAR_REPORT_PEAK", "STAGE_NAMES"]
+__all__ = ["Plan", "SlabPlan", "SarError", "describe", "describe_scene", "describe_stolt_ranges",
+           "describe_stolt_ranges_scene", "load_library", "LIB_PATH", "SAR_NO_COMPENSATION", "SAR_OUTPUT_COMPLEX",
+           "SAR_PROFILE_STAGES", "SAR_IMAGE_2D", "SAR_GRID_NUFFT", "SAR_REPORT_PEAK", "SAR_FORCE_PLAIN",
+           "STAGE_NAMES"]

@@ -32,14 +32,14 @@ def _newer(target, deps):
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def _compile(src, force, verbose):
+def _compile(src, force, verbose, bdir=BUILD, defines=()):
     s = os.path.join(CSRC, src)
-    o = os.path.join(BUILD, src + ".o")
+    o = os.path.join(bdir, src + ".o")
     if force or _newer(o, [s] + HEADERS):
         if src.endswith(".cpp"):
-            cmd = [NVCC, *FLAGS, "-x", "c++", "-c", s, "-o", o]
+            cmd = [NVCC, *FLAGS, *defines, "-x", "c++", "-c", s, "-o", o]
         else:
-            cmd = [NVCC, *ARCH, *FLAGS, "-x", "cu", "-c", s, "-o", o]
+            cmd = [NVCC, *ARCH, *FLAGS, *defines, "-x", "cu", "-c", s, "-o", o]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if verbose or r.returncode:
             sys.stderr.write(r.stdout + r.stderr)
@@ -50,20 +50,27 @@ def _compile(src, force, verbose):
     return o
 
 
-def build(verbose: bool = False, force: bool = False) -> str:
-    """Compile every translation unit (in parallel) and link the library."""
+def build(verbose: bool = False, force: bool = False, variant: str = "", defines=()) -> str:
+    """Compile every translation unit (in parallel) and link the library.
+    ``variant`` + ``defines`` (e.g. ["-DK4A_ROWS=256"]) build an experiment
+    copy, ``libsar_b200_<variant>.so``, from objects of its own (A/B timing
+    of compile-time alternatives; the product library is never affected)."""
     from concurrent.futures import ThreadPoolExecutor
-    os.makedirs(BUILD, exist_ok=True)
+    bdir = BUILD + ("_" + variant if variant else "")
+    lib = LIB if not variant else LIB.replace(".so", "_" + variant + ".so")
+    os.makedirs(bdir, exist_ok=True)
     with ThreadPoolExecutor(max_workers=min(len(SOURCES), os.cpu_count() or 1)) as ex:
-        objs = list(ex.map(lambda src: _compile(src, force, verbose), SOURCES))
-    if force or _newer(LIB, objs):
-        cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lcudart_static", "-lrt", "-ldl", "-lpthread"]
+        objs = list(ex.map(lambda src: _compile(src, force, verbose, bdir, list(defines)), SOURCES))
+    if force or _newer(lib, objs):
+        cmd = [NVCC, *ARCH, "-shared", "-o", lib, *objs, "-lcudart_static", "-lrt", "-ldl", "-lpthread"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode:
             sys.stderr.write(r.stdout + r.stderr)
             raise RuntimeError("link failed")
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(verbose="-v" in sys.argv, force="-f" in sys.argv))
+    var = [a.split("=", 1)[1] for a in sys.argv if a.startswith("--variant=")]
+    defs = [a for a in sys.argv if a.startswith("-D")]
+    print(build(verbose="-v" in sys.argv, force="-f" in sys.argv, variant=var[0] if var else "", defines=defs))

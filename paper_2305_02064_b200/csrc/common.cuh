@@ -26,8 +26,14 @@ constexpr int nt_for(int n) { return n <= 32 ? 32 : (n < 512 ? n : 512); }
 // thread) except for the 1024-point tiles, whose 32 elements per thread need more
 constexpr int minb_for(int n) { return n >= 1024 ? 1 : 1024 / nt_for(n); }
 
-constexpr int K1_STAGES = 4;
-constexpr int K1_BOX_BYTES = 32768;
+#ifndef K1_STAGES_
+#define K1_STAGES_ 4
+#endif
+#ifndef K1_BOX_BYTES_
+#define K1_BOX_BYTES_ 32768
+#endif
+constexpr int K1_STAGES = K1_STAGES_;        // TMA ring stages of K1
+constexpr int K1_BOX_BYTES = K1_BOX_BYTES_;  // raw-sample bytes per TMA box
 constexpr int K1_NT = 512;   // consumer threads (+1 producer warp)
 constexpr int K1_KT = 4;  // consecutive k per thread
 
@@ -205,9 +211,13 @@ struct MidSlabOut {
   char *d[SAR_MAX_SLAB];
   int nzl;   // 0: off (in place)
 };
+// liveb (or nullptr = every row): [nx] live-row bound of each column a, the
+// rows |m_s| <= liveb[a].  Forward (K2): only live rows
+// are stored.  Inverse (K4a): only live rows are read, the others are zero.
 template <int DIR>
 cudaError_t launch_mid(float2 *data, const float2 *tw, int F, int ny, int nx, int inner, cudaStream_t s,
-                       const CUtensorMap *tm, int num_sms, const MidSlabOut *so = nullptr);
+                       const CUtensorMap *tm, int num_sms, const MidSlabOut *so = nullptr,
+                       const int *liveb = nullptr);
 cudaError_t launch_k3(const SarDeviceView &v, bool ifft, cudaStream_t s, int num_sms);
 cudaError_t launch_k3_plane(const SarDeviceView &v, cudaStream_t s);
 cudaError_t launch_stolt_index(const SarDeviceView &v, const int32_t *cols, int n, int32_t *i0, float *tau,

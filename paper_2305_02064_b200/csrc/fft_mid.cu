@@ -17,9 +17,15 @@ namespace {
 // ------------------------------------------------------------ K2 / K4a ----
 // FFT along the middle (y) axis of a [F][N][nx][inner] complex volume for one
 // (chunk of 16 along `inner`, column a, frame f).
+// live(m, lb): spectral row m (signed index m_s) of a column whose live rows
+// are |m_s| <= lb (lb < 0: none); the rows of evanescent / out-of-window
+// columns (host class table) are never read
+__device__ __forceinline__ bool row_live(int m, int n, int lb) { return m <= lb || n - m <= lb; }
+
 template <int N, int DIR>
 __global__ void __launch_bounds__(nt_for(N), minb_for(N))
-    k_fft_mid(float2 *__restrict__ data, const float2 *__restrict__ tw, int nx, int inner) {
+    k_fft_mid(float2 *__restrict__ data, const float2 *__restrict__ tw, int nx, int inner,
+              const int *__restrict__ liveb) {
   constexpr int NT = nt_for(N);
   constexpr int ITEMS = N * KC;
   constexpr int E = (ITEMS + NT - 1) / NT;
@@ -30,13 +36,15 @@ __global__ void __launch_bounds__(nt_for(N), minb_for(N))
   const int f = blockIdx.z;
   float2 *base = data + ((size_t)f * N * nx + a) * (size_t)inner;
   const size_t row = (size_t)nx * inner;
+  const int lb = liveb ? liveb[a] : N;
 #pragma unroll
   for (int e = 0; e < E; ++e) {
     const int item = tid + e * NT;
     if (ITEMS % NT != 0 && item >= ITEMS) continue;
     const int cc = item & (KC - 1), b = item >> 4;
     const int c = cbase + cc;
-    tile[item] = c < inner ? base[b * row + c] : make_float2(0.f, 0.f);
+    // inverse (K4a): rows of skipped columns are zero; forward (K2): all rows read
+    tile[item] = c < inner && (DIR < 0 || row_live(b, N, lb)) ? base[b * row + c] : make_float2(0.f, 0.f);
   }
   __syncthreads();
   sarfft::tile_fft<N, KC, KC, NT, DIR>(tile, tw, tid);
@@ -46,7 +54,8 @@ __global__ void __launch_bounds__(nt_for(N), minb_for(N))
     if (ITEMS % NT != 0 && item >= ITEMS) continue;
     const int cc = item & (KC - 1), b = item >> 4;
     const int c = cbase + cc;
-    if (c < inner) base[b * row + c] = tile[item];
+    // forward (K2): rows no later stage reads are not stored
+    if (c < inner && (DIR > 0 || row_live(b, N, lb))) base[b * row + c] = tile[item];
   }
 }
 
@@ -72,13 +81,19 @@ constexpr int mid2_ctas() {
 template <int N>
 constexpr int mid2_ntc() { return N == 512 ? 512 : sarfft2::nt_fft<N, KC>(); }
 
+// TMA box rows: the forward transform (K2) reads whole columns in <= 256-row
+// boxes; the inverse (K4a) reads only the boxes of 32 rows that hold live rows
+template <int N, int DIR>
+constexpr int mid2_rows() { return DIR < 0 ? (N < 256 ? N : 256) : (N < K4A_ROWS ? N : K4A_ROWS); }
+
 template <int N, int DIR, bool SLAB>
 __global__ void __launch_bounds__(mid2_ntc<N>() + 32)
     k_fft_mid2(const __grid_constant__ CUtensorMap tm, float2 *__restrict__ data, const float2 *__restrict__ twg,
-               int nx, int inner, int nchunk, int nitems, const MidSlabOut so) {
+               int nx, int inner, int nchunk, int nitems, const MidSlabOut so, const int *__restrict__ liveb,
+               int oob_row) {
   constexpr int NTC = mid2_ntc<N>();
   constexpr int S = mid2_stages<N>();
-  constexpr int ROWS = N < 256 ? N : 256;
+  constexpr int ROWS = mid2_rows<N, DIR>();
   constexpr int NBOX = N / ROWS;
   constexpr uint32_t TILE_BYTES = N * KC * sizeof(float2);
   extern __shared__ __align__(128) float2 smm[];
@@ -104,11 +119,26 @@ __global__ void __launch_bounds__(mid2_ntc<N>() + 32)
         if (n >= S) sartma::mbar_wait(&empty[st], ((n / S) - 1) & 1);
         const int chunk = item % nchunk, rest = item / nchunk;
         const int a = rest % nx, f = rest / nx;
-        sartma::mbar_arrive_expect_tx(&full[st], TILE_BYTES);
+        if (DIR > 0 && liveb) {
+          // boxes that hold a live row (|m_s| <= lb) are read; the others are
+          // requested out of bounds (row F*N), which TMA fills with zeros
+          // without touching memory.  Every row of a box read here was
+          // written by K3 (its class list covers whole boxes, plan.cpp).
+          const int lb = liveb[a];
+          sartma::mbar_arrive_expect_tx(&full[st], TILE_BYTES);
 #pragma unroll
-        for (int bx = 0; bx < NBOX; ++bx)
-          sartma::tma_load_3d(ring + (size_t)st * N * KC + bx * ROWS * KC, &tm, chunk * KC, a, f * N + bx * ROWS,
-                              &full[st]);
+          for (int bx = 0; bx < NBOX; ++bx) {
+            const bool live = lb >= 0 && (bx * ROWS <= lb || (bx + 1) * ROWS - 1 >= N - lb);
+            sartma::tma_load_3d(ring + (size_t)st * N * KC + bx * ROWS * KC, &tm, chunk * KC, a,
+                                live ? f * N + bx * ROWS : oob_row, &full[st]);
+          }
+        } else {
+          sartma::mbar_arrive_expect_tx(&full[st], TILE_BYTES);
+#pragma unroll
+          for (int bx = 0; bx < NBOX; ++bx)
+            sartma::tma_load_3d(ring + (size_t)st * N * KC + bx * ROWS * KC, &tm, chunk * KC, a,
+                                f * N + bx * ROWS, &full[st]);
+        }
       }
     }
     return;
@@ -129,6 +159,11 @@ __global__ void __launch_bounds__(mid2_ntc<N>() + 32)
       base = data + ((size_t)f * N * nx + a) * (size_t)inner + chunk * KC;
     }
     const int cmax = inner - chunk * KC;
+    // forward (K2): the live rows (m + lb) mod N < 2 lb + 1 are stored (one
+    // add, and, compare per store; the two-sided test costs spills)
+    const int lb = (DIR < 0 && liveb) ? liveb[a] : N;
+    const unsigned span = lb < 0 ? 0u : (2 * lb + 1 >= N ? (unsigned)N : (unsigned)(2 * lb + 1));
+    const int lbo = lb < 0 ? 0 : lb;
     sarfft2::fft_ctx<N, KC, KC, NTC, DIR, 1, false, (N == 512 ? 16 : 0), (N == 512)>(
         work, tw, tid, [&](int c, int m) { return stage[m * KC + c]; },
         [&] {
@@ -136,7 +171,7 @@ __global__ void __launch_bounds__(mid2_ntc<N>() + 32)
         },
         [](int c) { return c; },
         [&](int c, int m, float2 v) {
-          if (c < cmax) __stcs(base + (size_t)m * row + c, v);
+          if (c < cmax && (DIR > 0 || (unsigned)((m + lbo) & (N - 1)) < span)) __stcs(base + (size_t)m * row + c, v);
         });
   }
 }
@@ -146,7 +181,7 @@ __global__ void __launch_bounds__(mid2_ntc<N>() + 32)
 
 template <int DIR>
 cudaError_t launch_mid(float2 *data, const float2 *tw, int F, int ny, int nx, int inner, cudaStream_t s,
-                       const CUtensorMap *tm, int num_sms, const MidSlabOut *so) {
+                       const CUtensorMap *tm, int num_sms, const MidSlabOut *so, const int *liveb) {
   const MidSlabOut off{};
   if (so && !(tm && ny <= 512 && F == 1 && so->nzl % KC == 0)) return cudaErrorInvalidValue;
   if (tm && ny <= 512) {
@@ -155,7 +190,8 @@ cudaError_t launch_mid(float2 *data, const float2 *tw, int F, int ny, int nx, in
     switch (ny) {
 #define X(N)                                                                                       \
   case N: {                                                                                        \
-    void (*kern)(const CUtensorMap, float2 *, const float2 *, int, int, int, int, const MidSlabOut) =   \
+    void (*kern)(const CUtensorMap, float2 *, const float2 *, int, int, int, int, const MidSlabOut,    \
+                 const int *, int) =                                                              \
         k_fft_mid2<N, DIR, false>;                                                                 \
     if (so) kern = k_fft_mid2<N, DIR, true>;                                                       \
     constexpr size_t smem = mid2_smem<N>();                                                        \
@@ -165,7 +201,7 @@ cudaError_t launch_mid(float2 *data, const float2 *tw, int F, int ny, int nx, in
     }                                                                                              \
     const int maxg = num_sms * mid2_ctas<N>();                                                     \
     kern<<<nitems < maxg ? nitems : maxg, mid2_ntc<N>() + 32, smem, s>>>(*tm, data, tw, nx, inner,   \
-                                                                                  nchunk, nitems, so ? *so : off); \
+                                                   nchunk, nitems, so ? *so : off, liveb, F * ny); \
     return cudaGetLastError();                                                                     \
   }
       X(2) X(4) X(8) X(16) X(32) X(64) X(128) X(256) X(512)
@@ -183,7 +219,7 @@ cudaError_t launch_mid(float2 *data, const float2 *tw, int F, int ny, int nx, in
       cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
       if (e != cudaSuccess) return e;                                                              \
     }                                                                                              \
-    kern<<<grid, nt_for(N), smem, s>>>(data, tw, nx, inner);                                       \
+    kern<<<grid, nt_for(N), smem, s>>>(data, tw, nx, inner, liveb);                                \
     return cudaGetLastError();                                                                     \
   }
     SAR_SIZES(X)
@@ -194,8 +230,8 @@ cudaError_t launch_mid(float2 *data, const float2 *tw, int F, int ny, int nx, in
 
 
 template cudaError_t launch_mid<-1>(float2 *, const float2 *, int, int, int, int, cudaStream_t, const CUtensorMap *, int,
-                                    const MidSlabOut *);
+                                    const MidSlabOut *, const int *);
 template cudaError_t launch_mid<+1>(float2 *, const float2 *, int, int, int, int, cudaStream_t, const CUtensorMap *, int,
-                                    const MidSlabOut *);
+                                    const MidSlabOut *, const int *);
 
 }  // namespace sark

@@ -200,13 +200,40 @@ __device__ __forceinline__ void sync(int rbar = 0) {
 //   g_r = W_N^{r i'} (y[i + r R1] + W_{2 R1}^{i'} y[i + (r + R2/2) R1]),
 //   X[i' + 2 q R1] = DFT_{R2/2}(g)_q,          r, q < R2/2,
 // so both halves run the same code (W_{2R1}^{R1} = -1 supplies the sign).
+// TW2: `tw` is the pass-2 table laid out by rows, tw[r * tw2_ld + i] =
+// W_N^{r i} (r < R2, i < tw2_ld = 2 R1 with SPLIT2, else R1; build_tw2), so
+// that the threads of a warp, which take consecutive butterflies i when
+// I_FAST2, read consecutive words instead of a stride-r pattern (a 32-way
+// bank conflict at r = 16 with the plain table).
+template <int N, int R1SEL, bool SPLIT2>
+constexpr int tw2_ld() {
+  return (R1SEL ? R1SEL : Split<N>::R1) * (SPLIT2 ? 2 : 1);
+}
+template <int N, int R1SEL, bool SPLIT2>
+constexpr int tw2_size() {
+  return N <= 32 ? 1 : (N / (R1SEL ? R1SEL : Split<N>::R1)) * tw2_ld<N, R1SEL, SPLIT2>();
+}
+// tw2[r * L + i] = tw[(r * i) mod N] (tw: exp(-2 pi i m / N), any memory), by
+// threads [tid, ..., nthreads)
+template <int N, int R1SEL, bool SPLIT2>
+__device__ __forceinline__ void build_tw2(float2 *tw2, const float2 *tw, int tid, int nthreads) {
+  constexpr int L = tw2_ld<N, R1SEL, SPLIT2>();
+  if constexpr (N > 32) {
+    for (int e = tid; e < tw2_size<N, R1SEL, SPLIT2>(); e += nthreads) {
+      const int r = e / L, i = e - r * L;
+      tw2[e] = tw[(r * i) & (N - 1)];
+    }
+  }
+}
+
 template <int N, int C, int LDW, int NT, int DIR, int BARID, bool I_FAST2, int R1SEL = 0, bool SPLIT2 = false,
-          typename Load, typename Loaded, typename Prep, typename Store>
+          bool TW2 = false, typename Load, typename Loaded, typename Prep, typename Store>
 __device__ __forceinline__ void fft_ctx(float2 *__restrict__ work, const float2 *__restrict__ tw, int tid,
                                         Load &&load, Loaded &&loaded, Prep &&prep, Store &&store, int rbar = 0) {
   static_assert((N & (N - 1)) == 0 && N >= 2 && N <= 1024, "power-of-two length in [2, 1024]");
   constexpr int R1 = R1SEL ? R1SEL : Split<N>::R1, R2 = N / R1;
   static_assert(R1 <= 32 && R2 <= 32, "two passes of radix <= 32");
+  constexpr int TL = TW2 ? tw2_ld<N, R1SEL, SPLIT2>() : 0;   // pass-2 table row length (0: plain table)
   if constexpr (R2 == 1) {
     // single pass: one thread per column
     constexpr int IT = (C + NT - 1) / NT;
@@ -274,7 +301,7 @@ __device__ __forceinline__ void fft_ctx(float2 *__restrict__ work, const float2 
           const int c = I_FAST2 ? b / (2 * R1) : b % C;
           const int ip = I_FAST2 ? b % (2 * R1) : b / C;
           const int i = ip & (R1 - 1);
-          float2 e = tw[H * ip];
+          float2 e = TW2 ? tw[H * TL + ip] : tw[H * ip];
           if (DIR > 0) e.y = -e.y;
           float2 g[H];
 #pragma unroll
@@ -283,7 +310,7 @@ __device__ __forceinline__ void fft_ctx(float2 *__restrict__ work, const float2 
             if (r == 0) {
               g[0] = t;
             } else {
-              float2 w = tw[r * ip];
+              float2 w = TW2 ? tw[r * TL + ip] : tw[r * ip];
               if (DIR > 0) w.y = -w.y;
               g[r] = mul(t, w);
             }
@@ -311,7 +338,7 @@ __device__ __forceinline__ void fft_ctx(float2 *__restrict__ work, const float2 
         u[0] = work[i * LDW + c];
 #pragma unroll
         for (int r = 1; r < R2; ++r) {
-          float2 w = tw[r * i];
+          float2 w = TW2 ? tw[r * TL + i] : tw[r * i];
           if (DIR > 0) w.y = -w.y;
           u[r] = mul(work[(i + r * R1) * LDW + c], w);
         }

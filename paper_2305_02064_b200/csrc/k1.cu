@@ -296,6 +296,11 @@ __global__ void __launch_bounds__(K1_NT + 32, 1)
     // tile) with the transformed rows stored straight to W0
     float2 *out = v.w0 + ((size_t)(f * v.nvy + vyl) * NX) * (size_t)v.nk + kc * C;
     const int cmax = v.nk - kc * C;
+#ifdef K1_NO_FFT   // timing experiment only (scripts/ab_variants.py): the x-FFT left out
+    for (int i = tid; i < NX * C; i += K1_NT)
+      if (i % C < cmax) __stcs(out + (size_t)(i / C) * v.nk + i % C, tile[i]);
+    if (false)
+#endif
     sarfft2::fft<NX, C, C, K1_NT, -1, 1, false, (NX == 512 ? 16 : 0)>(
         tile, tws, tid, [&](int c, int m) { return tile[m * C + c]; }, [] {},
         [&](int c, int m, float2 x) {

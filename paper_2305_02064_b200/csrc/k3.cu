@@ -35,7 +35,8 @@ constexpr int k3c_cl() {
 }
 template <int NZ, int CL>
 size_t k3c_smem(int nk) {
-  return ((size_t)4 * CL * nk + (size_t)NZ * (4 * CL + 1)) * sizeof(float2);
+  return ((size_t)4 * CL * nk + (size_t)NZ * (4 * CL + 1) +
+          sarfft2::tw2_size<NZ, (NZ == 512 ? 16 : 0), false>()) * sizeof(float2);
 }
 
 // CL classes per CTA: k3c_cl<NZ>() normally, 1 when n_k is so large that
@@ -50,11 +51,13 @@ __global__ void __launch_bounds__(K3C_NT, 8) k3_class(const SarDeviceView v) {
   const int nk = v.nk;
   float2 *fin = sm3;                                 // [CC][nk]  source spectrum
   float2 *fout = fin + (size_t)CC * nk;              // [NZ][LD]  Stolt output / FFT work
+  float2 *tw2 = fout + (size_t)NZ * LD;              // pass-2 twiddle rows
   const int tid = threadIdx.x;
   const int ncol = v.nx * v.ny;
   const int nclass = v.ncls;
   const int q0 = blockIdx.x * CL;
   const int f = blockIdx.y;
+  if constexpr (DO_IFFT) sarfft2::build_tw2<NZ, (NZ == 512 ? 16 : 0), false>(tw2, v.tw_z, tid, K3C_NT);
   if (tid < CL) {
     const int q = q0 + tid;
     if (q < nclass) {
@@ -85,7 +88,7 @@ __global__ void __launch_bounds__(K3C_NT, 8) k3_class(const SarDeviceView v) {
       for (int u = 0; u < U; ++u) {
         const int e = base + u * K3C_NT;
         const int sl = e / h2, i = e - sl * h2;
-        t[u] = (e < tot && colof[sl] >= 0)
+        t[u] = (e < tot && colof[sl] >= 0 && jhis[sl >> 2] >= jlos[sl >> 2])
                    ? __ldcs(reinterpret_cast<const float4 *>(wf + (size_t)colof[sl] * nk) + i)
                    : make_float4(0.f, 0.f, 0.f, 0.f);
       }
@@ -99,7 +102,7 @@ __global__ void __launch_bounds__(K3C_NT, 8) k3_class(const SarDeviceView v) {
   } else {
     for (int e = tid; e < CC * nk; e += K3C_NT) {
       const int sl = e / nk, i = e - sl * nk;
-      if (colof[sl] >= 0) fin[e] = __ldcs(wf + (size_t)colof[sl] * nk + i);
+      if (colof[sl] >= 0 && jhis[sl >> 2] >= jlos[sl >> 2]) fin[e] = __ldcs(wf + (size_t)colof[sl] * nk + i);
     }
   }
   __syncthreads();
@@ -149,8 +152,8 @@ __global__ void __launch_bounds__(K3C_NT, 8) k3_class(const SarDeviceView v) {
     return (m >= jlos[cl] && m <= jhis[cl]) ? fout[m * LD + c] : make_float2(0.f, 0.f);
   };
   if constexpr (DO_IFFT) {
-    sarfft2::fft_ctx<NZ, CC, LD, K3C_NT, +1, 0, true, (NZ == 512 ? 16 : 0)>(
-        fout, v.tw_z, tid, load, [] {},
+    sarfft2::fft_ctx<NZ, CC, LD, K3C_NT, +1, 0, true, (NZ == 512 ? 16 : 0), false, (NZ > 32)>(
+        fout, NZ > 32 ? tw2 : v.tw_z, tid, load, [] {},
         [&](int c) {
           const int col = colof[c];
           return col >= 0 ? dst + (size_t)col * NZ : nullptr;
@@ -181,12 +184,22 @@ constexpr int K3P_CL = K3P_GEOM_[3];
 // barrier can never see the phase of another group's item (mbarrier parity
 // waits cannot tell phases two apart)
 static_assert(K3P_S % K3P_NG == 0, "K3 ring: the stage count must be a multiple of the group count");
+// pass-2 split and row-major twiddle table of k3_pp's z-IFFT
+template <int NZ, int CL>
+struct K3PFft {
+  static constexpr int R1S = NZ == 512 ? 16 : 0;
+  static constexpr int R1 = R1S ? R1S : sarfft2::Split<NZ>::R1;
+  // pass 2 split between thread pairs where C R1 butterflies would leave
+  // half the group idle (N = 512 as 16 x 32, N = 256)
+  static constexpr bool SPL = NZ / R1 >= 4 && 2 * (4 * CL) * R1 <= K3P_G;
+  static constexpr int TWN = sarfft2::tw2_size<NZ, R1S, SPL>();
+};
 template <int NZ, int CL>
 size_t k3pp_smem(int nk) {
   const size_t hdr = (sizeof(K3Hdr<CL>) + 15) & ~(size_t)15;
   return K3P_S * (hdr + (size_t)4 * CL * nk * sizeof(float2)) +
          K3P_NG * ((size_t)NZ * (4 * CL + 1)) * sizeof(float2) +
-         ((size_t)NZ + nk) * sizeof(double) + (size_t)NZ * sizeof(float2);
+         ((size_t)NZ + nk) * sizeof(double) + (size_t)K3PFft<NZ, CL>::TWN * sizeof(float2);
 }
 
 template <int NZ, int CL, bool DO_IFFT>
@@ -261,12 +274,8 @@ __device__ __forceinline__ void k3pp_consume(const SarDeviceView &v, int nitems_
     if (DO_IFFT) {
       // the output column's pointer is resolved once per butterfly, so every
       // store is one STG with an immediate offset
-      // pass 2 split between thread pairs where C R1 butterflies would leave
-      // half the group idle (N = 512 as 16 x 32, N = 256)
-      constexpr int R1S = NZ == 512 ? 16 : 0;
-      constexpr int R1 = R1S ? R1S : sarfft2::Split<NZ>::R1;
-      constexpr bool SPL = NZ / R1 >= 4 && 2 * CC * R1 <= K3P_G;
-      sarfft2::fft_ctx<NZ, CC, LD, K3P_G, +1, -1, true, R1S, SPL>(
+      using FT = K3PFft<NZ, CL>;
+      sarfft2::fft_ctx<NZ, CC, LD, K3P_G, +1, -1, true, FT::R1S, FT::SPL, (NZ > 32)>(
           fout, tw, gt, load, [] {},
           [&](int c) {
             const int col = colofs[c];
@@ -300,15 +309,13 @@ __global__ void __launch_bounds__(K3P_NG * K3P_G + 32, 1) k3_pp(const SarDeviceV
   const size_t grp_elems = (size_t)NZ * LD;                      // fout per group
   double *ks = reinterpret_cast<double *>(grp + K3P_NG * grp_elems);  // [nk]
   double *kzs = ks + nk;                                          // [NZ]
-  float2 *tw = reinterpret_cast<float2 *>(kzs + NZ);              // [NZ]
+  float2 *tw = reinterpret_cast<float2 *>(kzs + NZ);              // pass-2 rows (K3PFft::TWN)
   __shared__ __align__(8) uint64_t full[K3P_S], empty[K3P_S];
   __shared__ int colofs[K3P_NG][CC], slo[K3P_NG][CC], shi[K3P_NG][CC];
   const int tid = threadIdx.x;
   for (int i = tid; i < nk; i += NTH) ks[i] = v.k[i];
-  for (int i = tid; i < NZ; i += NTH) {
-    kzs[i] = v.kz[i];
-    tw[i] = v.tw_z[i];
-  }
+  for (int i = tid; i < NZ; i += NTH) kzs[i] = v.kz[i];
+  sarfft2::build_tw2<NZ, K3PFft<NZ, CL>::R1S, K3PFft<NZ, CL>::SPL>(tw, v.tw_z, tid, NTH);
   if (tid == 0) {
     for (int i = 0; i < K3P_S; ++i) {
       sartma::mbar_init(&full[i], 1);
@@ -376,10 +383,14 @@ __global__ void __launch_bounds__(K3P_NG * K3P_G + 32, 1) k3_pp(const SarDeviceV
         h.rr = v.rref[f] * (1.0 / TWO_PI);
       }
       __syncwarp();
-      if (lane == 0) sartma::mbar_arrive_expect_tx(&full[st], (uint32_t)cnt * (uint32_t)nk * 8u);
+      // members of classes with no bin in band (jhi < jlo: zero output, kept
+      // only to fill K4a's row boxes) are never read by the consumers: not loaded
+      const bool ld = lane < cnt && h.jhi[h.clof[lane]] >= h.jlo[h.clof[lane]];
+      const int nld = __popc(__ballot_sync(0xffffffffu, ld));
+      if (lane == 0) sartma::mbar_arrive_expect_tx(&full[st], (uint32_t)nld * (uint32_t)nk * 8u);
       __syncwarp();
       const float2 *wf = v.w0 + (size_t)f * ncol * (size_t)nk;
-      if (lane < cnt) sartma::bulk_g2s(fin + lane * nk, wf + (size_t)h.colof[lane] * nk, (uint32_t)nk * 8u, &full[st]);
+      if (ld) sartma::bulk_g2s(fin + lane * nk, wf + (size_t)h.colof[lane] * nk, (uint32_t)nk * 8u, &full[st]);
       cur = nxt;
     }
     return;
@@ -520,7 +531,11 @@ bool try_k3pp(const SarDeviceView &v, bool ifft, cudaStream_t s, int num_sms, cu
 }
 }  // namespace
 
+namespace {
+}  // namespace
+
 cudaError_t launch_k3(const SarDeviceView &v, bool ifft, cudaStream_t s, int num_sms) {
+  if (v.ncls == 0) return cudaSuccess;   // every column skipped (zero Stolt output)
   if ((v.nk & 1) == 0 && v.nz >= 128 && !v.force_plain) {
     // n_z >= 256: 2 classes (<= 8 columns) per item; n_z = 128: 4 classes
     // (Freehand 0.065 -> 0.055 ms; at n_z = 64 k3_class stays faster:
@@ -570,6 +585,7 @@ cudaError_t launch_k3(const SarDeviceView &v, bool ifft, cudaStream_t s, int num
 
 cudaError_t launch_k3_plane(const SarDeviceView &v, cudaStream_t s) {
   const int nclass = v.ncls;
+  if (nclass == 0) return cudaSuccess;
   const int cpb = K3P2_NT / 32;
   k3_plane<<<dim3((nclass + cpb - 1) / cpb, v.F), K3P2_NT, 0, s>>>(v);
   return cudaGetLastError();

@@ -65,7 +65,7 @@ __global__ void __launch_bounds__(sarfft2::nt_fft<NX, KC>() + 32)
   float2 *tw = work + (size_t)NX * (KC + 1);   // [NX]
   __shared__ __align__(8) uint64_t full[S], empty[S];
   const int tid = threadIdx.x;
-  for (int i = tid; i < NX; i += NTC + 32) tw[i] = v.tw_x[i];
+  sarfft2::build_tw2<NX, 0, false>(tw, v.tw_x, tid, NTC + 32);   // [NX] pass-2 rows
   if (tid == 0) {
     for (int i = 0; i < S; ++i) {
       sartma::mbar_init(&full[i], 1);
@@ -111,7 +111,7 @@ __global__ void __launch_bounds__(sarfft2::nt_fft<NX, KC>() + 32)
     float pk = 0.f;
     // the image row of z-slot c is resolved once per butterfly (prep), so a
     // store is the x roll plus one STG
-    sarfft2::fft_ctx<NX, KC, KC + 1, NTC, +1, 1, true>(
+    sarfft2::fft_ctx<NX, KC, KC + 1, NTC, +1, 1, true, 0, false, (NX > 32)>(
         work, tw, tid, [&](int c, int m) { return stage[m * KC + c]; },
         [&] {
           if (tid == 0) sartma::mbar_arrive(&empty[st]);

@@ -64,11 +64,16 @@ int sar_launch_pipeline(sar_plan *p, const void *d_data, void *d_image, cudaStre
                         p->k1_regacc, p->num_sms));
     if (ev) SAR_CHECK(cudaEventRecord(ev[1], s));
     if (stop_stage == 1) return SAR_OK;
+    // debug stage 2 dumps the whole spectrum; otherwise rows of skipped
+    // columns are not stored
     SAR_CHECK(launch_mid<-1>(v.w0, v.tw_y, v.F, v.ny, v.nx, v.nk, s, p->tma_mid0 ? &p->tm_w0_mid : nullptr,
-                             p->num_sms));
+                             p->num_sms, nullptr, stop_stage == 2 ? nullptr : v.liveb));
   }
   if (ev) SAR_CHECK(cudaEventRecord(ev[2], s));
   if (stop_stage == 2) return SAR_OK;
+  // skipped columns are not written by K3: zero them for the stage-3 dump
+  if (stop_stage == 3 && v.liveb)
+    SAR_CHECK(cudaMemsetAsync(v.w1, 0, (size_t)v.F * v.ny * v.nx * v.nz * sizeof(float2), s));
   if (v.mode2d) {
     SAR_CHECK(launch_k3_plane(v, s));
   } else {
@@ -77,7 +82,7 @@ int sar_launch_pipeline(sar_plan *p, const void *d_data, void *d_image, cudaStre
   if (ev) SAR_CHECK(cudaEventRecord(ev[3], s));
   if (stop_stage == 3) return SAR_OK;
   SAR_CHECK(launch_mid<+1>(v.w1, v.tw_y, v.F, v.ny, v.nx, v.nz, s, p->tma_mid1 ? &p->tm_w1_mid : nullptr,
-                           p->num_sms));
+                           p->num_sms, nullptr, v.liveb));
   if (ev) SAR_CHECK(cudaEventRecord(ev[4], s));
   if (v.peak) SAR_CHECK(cudaMemsetAsync(v.peak, 0, (size_t)v.F * sizeof(unsigned), s));
   SAR_CHECK(launch_k4b(v, d_image, complex_out != 0, s, p->tma_rows1 ? &p->tm_w1_rows : nullptr, p->num_sms));
@@ -169,20 +174,24 @@ bool sar_encode_input_map(sar_plan *p, const void *d_data) {
   return encode2d(&p->tm_s, d_data, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, v.nk, rows, k1c_for(v.nx), p->k1_br);
 }
 
+// Slab plans (workspace = the slabs only) skip the whole-image workspace maps
+// and build K1's.
 int sar_build_tensor_maps(sar_plan *p) {
   const SarDeviceView &v = p->v;
-  p->tma_mid0 = p->tma_mid1 = p->tma_rows1 = false;
+  p->tma_mid0 = p->tma_mid1 = p->tma_rows1 = p->tma_fine = p->tma_ap = false;
   if (v.F == 0 || v.force_plain) return SAR_OK;
-  const uint32_t rows = v.ny < 256 ? v.ny : 256;
-  p->tma_mid0 = encode3d(&p->tm_w0_mid, v.w0, v.nk, v.nx, (uint64_t)v.F * v.ny, KC, 1, rows);
-  p->tma_mid1 = encode3d(&p->tm_w1_mid, v.w1, v.nz, v.nx, (uint64_t)v.F * v.ny, KC, 1, rows);
-  if (v.nufft) {
-    // fine grid [F*2ny][2nx][nk]: x-FFT boxes {16 k, 1, <=256 fine columns}
-    const uint32_t rx = 2 * v.nx, fr = rx < 256 ? rx : 256;
-    p->tma_fine = encode3d(&p->tm_fine, v.wh, v.nk, 1, (uint64_t)v.F * 2 * v.ny * rx, KC, 1, fr);
+  if (p->slab_world == 0) {
+    const uint32_t rows = v.ny < 256 ? v.ny : 256, rows1 = v.ny < K4A_ROWS ? v.ny : K4A_ROWS;   // K2 / K4a boxes
+    p->tma_mid0 = encode3d(&p->tm_w0_mid, v.w0, v.nk, v.nx, (uint64_t)v.F * v.ny, KC, 1, rows);
+    p->tma_mid1 = encode3d(&p->tm_w1_mid, v.w1, v.nz, v.nx, (uint64_t)v.F * v.ny, KC, 1, rows1);
+    if (v.nufft) {
+      // fine grid [F*2ny][2nx][nk]: x-FFT boxes {16 k, 1, <=256 fine columns}
+      const uint32_t rx = 2 * v.nx, fr = rx < 256 ? rx : 256;
+      p->tma_fine = encode3d(&p->tm_fine, v.wh, v.nk, 1, (uint64_t)v.F * 2 * v.ny * rx, KC, 1, fr);
+    }
+    const uint32_t xr = v.nx < 256 ? v.nx : 256;
+    p->tma_rows1 = encode3d(&p->tm_w1_rows, v.w1, v.nz, v.nx, (uint64_t)v.F * v.ny, KC, xr, 1);
   }
-  const uint32_t xr = v.nx < 256 ? v.nx : 256;
-  p->tma_rows1 = encode3d(&p->tm_w1_rows, v.w1, v.nz, v.nx, (uint64_t)v.F * v.ny, KC, xr, 1);
   // K1: -2 d_z table [F*npy][npx] float32 with box [1][br]; input map per call
   const int brmax = K1_BOX_BYTES / (k1c_for(v.nx) * 8);
   p->k1_br = v.npx < brmax ? v.npx : brmax;
@@ -264,8 +273,8 @@ int sar_slab_setup(sar_plan *p) {
   p->tma_w1x = p->tma_w1z = p->tma_r1 = false;
   p->tm_r1_ptr = nullptr;
   if (v.force_plain) return SAR_OK;
-  const uint32_t rows = v.ny < 256 ? v.ny : 256, xr = v.nx < 256 ? v.nx : 256;
-  p->tma_w1x = encode3d(&p->tm_w1x_mid, v.w1, v.nz, nxl, v.ny, KC, 1, rows);
+  const uint32_t rows1 = v.ny < K4A_ROWS ? v.ny : K4A_ROWS, xr = v.nx < 256 ? v.nx : 256;
+  p->tma_w1x = encode3d(&p->tm_w1x_mid, v.w1, v.nz, nxl, v.ny, KC, 1, rows1);
   p->tma_w1z = encode3d(&p->tm_w1z_rows, v.w0, nzl, v.nx, v.ny, KC, xr, 1);
   return SAR_OK;
 }
@@ -309,7 +318,8 @@ int sar_slab_launch(sar_plan *p, int stage, const void *d_in, void *d_out, void 
       }
       if (p->tma_r1) tm = &p->tm_r1_mid;
     }
-    SAR_CHECK(launch_mid<-1>(xs, v.tw_y, 1, v.ny, nxl, v.nk, s, tm, p->num_sms));
+    const int *lbx = v.liveb ? v.liveb + r * nxl : nullptr;   // this x-slab's columns
+    SAR_CHECK(launch_mid<-1>(xs, v.tw_y, 1, v.ny, nxl, v.nk, s, tm, p->num_sms, nullptr, lbx));
     SarDeviceView vk = v;
     vk.nx = nxl;
     vk.cls = p->d_slab_cls;
@@ -325,10 +335,10 @@ int sar_slab_launch(sar_plan *p, int stage, const void *d_in, void *d_out, void 
       MidSlabOut so{};
       so.nzl = nzl;
       for (int h = 0; h < G; ++h) so.d[h] = bd2.d[h];
-      SAR_CHECK(launch_mid<+1>(v.w1, v.tw_y, 1, v.ny, nxl, v.nz, s, &p->tm_w1x_mid, p->num_sms, &so));
+      SAR_CHECK(launch_mid<+1>(v.w1, v.tw_y, 1, v.ny, nxl, v.nz, s, &p->tm_w1x_mid, p->num_sms, &so, lbx));
     } else {
       SAR_CHECK(launch_mid<+1>(v.w1, v.tw_y, 1, v.ny, nxl, v.nz, s, p->tma_w1x ? &p->tm_w1x_mid : nullptr,
-                               p->num_sms));
+                               p->num_sms, nullptr, lbx));
       SAR_CHECK(block_copy(bd2, v.w1, G, (long long)v.ny * nxl, (long long)nzl * c8, (long long)nzl * c8,
                            (long long)v.nz * c8, (long long)nzl * c8, p->num_sms, s));
     }

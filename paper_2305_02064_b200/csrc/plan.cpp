@@ -101,6 +101,10 @@ namespace {
 struct HostTables {
   std::vector<float> apose, bpair, kturn, pinv, tw;
   std::vector<SarClass> cls;
+  // the classes K3 computes and the live-row bound of every spectral column
+  // (empty liveb: every column is computed)
+  std::vector<SarClass> live;
+  std::vector<int> liveb;
   // NUFFT mode
   std::vector<float> nu_decx, nu_decy;
   // NUFFT spread blocks (K1s): CSR of entries per (frame, 4 x 8 fine-cell block)
@@ -298,6 +302,68 @@ int host_decompose(const sar_geom_desc *g, const sar_image_desc *im, uint32_t fl
       }
   }
 
+  // Columns whose Stolt output is provably zero are skipped by K3 (not read,
+  // not written), their rows are not stored by K2 and read as zero by K4a:
+  // evanescent columns, k_r^2 >= 4 k_max^2, where H = 0 for every k_i (Eq. (13),
+  // P:211; reading R4), and, in 3-D, columns none of whose k_z bins can be in
+  // band (jhi < jlo: the band lies below the k_z window).  Both conditions grow
+  // with k_r^2, so the live rows of column a are |b_s| <= liveb[a]; the table
+  // is checked for that shape and the skip is dropped if it does not hold.
+  {
+    const int hx = p->nx / 2 + 1, hy = p->ny / 2 + 1;
+    const double kmax = T.k0 + (double)(nk - 1) * T.dk;
+    auto dead = [&](const SarClass &c) {
+      const double qhi = 4.0 * kmax * kmax - c.kr2;
+      return !(qhi > 0.0) || (!mode2d && c.jhi < c.jlo);
+    };
+    std::vector<int> lb(p->nx, -1);
+    for (int b = 0; b < hy; ++b)
+      for (int a = 0; a < hx; ++a) {
+        const SarClass &c = T.cls[(size_t)b * hx + a];
+        if (dead(c)) continue;
+        for (int m = 0; m < c.nmem; ++m) {
+          const int ca = c.col[m] % p->nx;
+          lb[ca] = std::max(lb[ca], b);
+        }
+      }
+    bool shaped = true;
+    for (int b = 0; b < hy; ++b)
+      for (int a = 0; a < hx; ++a) {
+        const SarClass &c = T.cls[(size_t)b * hx + a];
+        if ((b <= lb[a]) == dead(c)) shaped = false;
+      }
+    // K4a reads whole boxes of R rows (those with a live row, the others are
+    // zero-filled), so K3 also writes every row of those boxes: the classes it
+    // computes are |b_s| <= lbk[a] (the extra ones are dead: zero output)
+    const int R = std::min(p->ny, K4A_ROWS), N = p->ny;
+    std::vector<int> lbk(p->nx, -1);
+    for (int a = 0; a < p->nx; ++a)
+      for (int bx = 0; bx < N / R; ++bx) {
+        const bool live = lb[a] >= 0 && (bx * R <= lb[a] || (bx + 1) * R - 1 >= N - lb[a]);
+        if (!live) continue;
+        for (int m = bx * R; m < (bx + 1) * R; ++m) lbk[a] = std::max(lbk[a], m <= N / 2 ? m : N - m);
+      }
+    T.live.clear();
+    p->col_range.assign((size_t)p->ny * p->nx * 2, 0);
+    for (int b = 0; b < hy; ++b)
+      for (int a = 0; a < hx; ++a) {
+        const SarClass &c = T.cls[(size_t)b * hx + a];
+        const bool skip = shaped && b > lbk[a];
+        if (!skip) T.live.push_back(c);
+        for (int m = 0; m < c.nmem; ++m) {
+          p->col_range[2 * (size_t)c.col[m]] = skip ? 0 : c.jlo;
+          p->col_range[2 * (size_t)c.col[m] + 1] = skip ? -1 : c.jhi;
+        }
+      }
+#ifdef SAR_EXPERIMENT_NO_SKIP
+    shaped = false;   // A/B experiments only (scripts/ab_variants.py)
+    T.live = T.cls;
+    for (size_t i = 0; i < p->col_range.size(); i += 2) p->col_range[i] = 0, p->col_range[i + 1] = p->nz - 1;
+#endif
+    if (shaped) T.liveb = lb;
+    else T.liveb.clear();
+  }
+
   // NUFFT placement tables (reading R19; must match oracle/nufft.py): fine
   // grid 2N per axis, Gaussian of half width W = 6 fine cells, variance
   // s2 = W / (2 pi (1 - 1/(2 sigma))), deconvolution 1/Phi(a) with
@@ -468,7 +534,8 @@ int plan_create_impl(sar_plan **out, const sar_geom_desc *g, const sar_image_des
   const size_t o_rr = off; off += al(T.rref.size() * 8 + 8);
   const size_t o_pi = off; off += al(T.pinv.size() * 4);
   const size_t o_tw = off; off += al(T.tw.size() * 4);
-  const size_t o_cl = off; off += al(T.cls.size() * sizeof(SarClass));
+  const size_t o_cl = off; off += al(T.live.size() * sizeof(SarClass));
+  const size_t o_lb = off; off += al(T.liveb.size() * 4);
   const size_t o_nu_dx = off; off += al(T.nu_decx.size() * 4);
   const size_t o_nu_dy = off; off += al(T.nu_decy.size() * 4);
   const size_t o_sp_off = off; off += al(T.sp_off.size() * 4);
@@ -493,7 +560,8 @@ int plan_create_impl(sar_plan **out, const sar_geom_desc *g, const sar_image_des
       (ce = up(o_rr, T.rref.data(), T.rref.size() * 8)) != cudaSuccess ||
       (ce = up(o_pi, T.pinv.data(), T.pinv.size() * 4)) != cudaSuccess ||
       (ce = up(o_tw, T.tw.data(), T.tw.size() * 4)) != cudaSuccess ||
-      (ce = up(o_cl, T.cls.data(), T.cls.size() * sizeof(SarClass))) != cudaSuccess ||
+      (ce = up(o_cl, T.live.data(), T.live.size() * sizeof(SarClass))) != cudaSuccess ||
+      (ce = up(o_lb, T.liveb.data(), T.liveb.size() * 4)) != cudaSuccess ||
       (ce = up(o_nu_dx, T.nu_decx.data(), T.nu_decx.size() * 4)) != cudaSuccess ||
       (ce = up(o_nu_dy, T.nu_decy.data(), T.nu_decy.size() * 4)) != cudaSuccess ||
       (ce = up(o_sp_off, T.sp_off.data(), T.sp_off.size() * 4)) != cudaSuccess ||
@@ -544,6 +612,7 @@ int plan_create_impl(sar_plan **out, const sar_geom_desc *g, const sar_image_des
   v.sp_ent = (const SarSpreadEntry *)(base + o_sp_ent);
   v.tw_f = (const float2 *)(base + o_tw) + T.tw_f_off;
   v.cls = (const SarClass *)(base + o_cl);
+  v.liveb = T.liveb.empty() ? nullptr : (const int *)(base + o_lb);
   v.pinv = T.pinv.empty() ? nullptr : (const float2 *)(base + o_pi);
   v.tw_x = (const float2 *)(base + o_tw);
   v.tw_y = (const float2 *)(base + o_tw) + T.tw_y_off;
@@ -564,7 +633,7 @@ int plan_create_impl(sar_plan **out, const sar_geom_desc *g, const sar_image_des
   v.vy0 = 0;
   v.nvy = p->ny;
   v.slab_lg = -1;
-  v.ncls = (p->nx / 2 + 1) * (p->ny / 2 + 1);
+  v.ncls = (int)T.live.size();
   v.z_off = 0;
   v.nz_img = p->nz;
   v.img_scale = (float)(1.0 / ((double)p->nx * p->ny * (v.mode2d ? 1 : p->nz)));
@@ -589,7 +658,7 @@ int plan_create_impl(sar_plan **out, const sar_geom_desc *g, const sar_image_des
   v.w1 = p->d_w1;
 
   p->num_sms = prop.multiProcessorCount;
-  if (slab_world == 0) sar_build_tensor_maps(p);
+  sar_build_tensor_maps(p);
   if (flags & SAR_PROFILE_STAGES) {
     for (int i = 0; i < SAR_PROFILE_RING; ++i)
       for (int j = 0; j <= SAR_N_STAGES; ++j) cudaEventCreate(&p->ev[i][j]);
@@ -604,6 +673,17 @@ extern "C" {
 
 int sar_plan_create(sar_plan **out, const sar_geom_desc *g, const sar_image_desc *im, uint32_t flags) {
   return plan_create_impl(out, g, im, flags, 0);
+}
+
+int sar_plan_describe_stolt_ranges(const sar_geom_desc *g, const sar_image_desc *im, uint32_t flags,
+                                   int32_t *ranges) {
+  if (!ranges) return fail(SAR_ERR_INVALID_ARG, "ranges is NULL");
+  sar_plan tmp;
+  HostTables T;
+  int st = host_decompose(g, im, flags, &tmp, T);
+  if (st != SAR_OK) return st;
+  memcpy(ranges, tmp.col_range.data(), tmp.col_range.size() * sizeof(int32_t));
+  return SAR_OK;
 }
 
 int sar_plan_create_slab(sar_plan **out, const sar_geom_desc *g, const sar_image_desc *im, uint32_t flags,

@@ -11,6 +11,12 @@
 
 #include "../../include/sar_b200.h"
 
+// rows per TMA box of the inverse y-FFT (K4a, fft_mid.cu): K4a reads only the
+// boxes that hold live rows, so K3's class list covers whole boxes (plan.cpp)
+#ifndef K4A_ROWS
+#define K4A_ROWS 32
+#endif
+
 #define SAR_PROFILE_RING 1024
 #define SAR_N_STAGES 5
 
@@ -65,7 +71,10 @@ struct SarDeviceView {
   const double *ky;     // [ny]
   const double *kz;     // [nz]        uniform Stolt grid (reading R5)
   const double *rref;   // [F]         R_ref = z_ref - Z_0
-  const SarClass *cls;  // [(ny/2+1)*(nx/2+1)] mirror classes, q = b*(nx/2+1) + a
+  const SarClass *cls;  // [ncls] the mirror classes K3 computes (those with a non-zero column,
+                        // DESIGN.md section 6; all classes when liveb == nullptr)
+  const int *liveb;     // [nx] live rows |b_s| <= liveb[a] of spectral column a (-1: none), or
+                        // nullptr: every column is computed
   const float2 *pinv;   // [nk] 1/P(f) or nullptr (P == 1)
   const float2 *tw_x;   // [nx] exp(-2 pi i m/nx)
   const float2 *tw_y;   // [ny]
@@ -89,6 +98,7 @@ struct sar_plan {
   double dx = 0, dy = 0, dz = 0, z_ref = 0;
   double axes[6] = {0, 0, 0, 0, 0, 0};
   std::vector<int> jx, jy;
+  std::vector<int32_t> col_range;   // [ny][nx][2] K3's in-band bin range of each column ({0,-1}: skipped)
   int jx_min = 0, jy_min = 0, nvx = 0, nvy = 0;
   SarDeviceView v{};
   // device allocations

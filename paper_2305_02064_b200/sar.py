@@ -77,6 +77,7 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         "sar_plan_create": (C.c_int, [C.POINTER(vp), C.POINTER(GeomDesc), C.POINTER(ImageDesc), u32]),
         "sar_reconstruct": (C.c_int, [vp, vp, vp, vp]),
         "sar_reconstruct_host": (C.c_int, [vp, vp, vp, vp]),
+        "sar_plan_describe_stolt_ranges": (C.c_int, [C.POINTER(GeomDesc), C.POINTER(ImageDesc), u32, vp]),
         "sar_plan_destroy": (C.c_int, [vp]),
         "sar_plan_get_axes": (C.c_int, [vp, C.POINTER(C.c_double)]),
         "sar_plan_workspace_bytes": (C.c_int, [vp, C.POINTER(C.c_size_t)]),
@@ -106,7 +107,7 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
 
 def exported_symbols():
     """Names of the C entry points this binding expects (the header's API)."""
-    return ["sar_plan_describe", "sar_plan_create", "sar_reconstruct", "sar_reconstruct_host", "sar_plan_destroy",
+    return ["sar_plan_describe", "sar_plan_describe_stolt_ranges", "sar_plan_create", "sar_reconstruct", "sar_reconstruct_host", "sar_plan_destroy",
             "sar_plan_get_axes", "sar_plan_workspace_bytes", "sar_plan_profile_read",
             "sar_plan_profile_reset", "sar_plan_launches_per_call", "sar_plan_peaks", "sar_debug_stage",
             "sar_debug_node_offsets", "sar_debug_stolt_index", "sar_plan_create_slab", "sar_slab_buffer_bytes",
@@ -185,9 +186,28 @@ def describe(tx, rx, scan, npx, npy, x0, y0, dx, dy, z0, k, nx, ny, nz, dz, z_re
                 apose=ap[:F * P].reshape(F, P), bpair=bp[:F * npair].reshape(F, *shp))
 
 
+def describe_stolt_ranges(tx, rx, scan, npx, npy, x0, y0, dx, dy, z0, k, nx, ny, nz, dz, z_ref, pulse=None,
+                          flags=0):
+    """Host-only (``sar_plan_describe_stolt_ranges``): int32 [ny, nx, 2] = the
+    (jlo, jhi) k_z bin range step 3 evaluates for every spectral column,
+    (0, -1) for a column the plan skips (zero Stolt output)."""
+    lib = load_library()
+    g, im, keep = _descriptors(tx, rx, scan, npx, npy, x0, y0, dx, dy, z0, k, nx, ny, nz, dz, z_ref, pulse, 0)
+    out = np.zeros((int(ny), int(nx), 2), np.int32)
+    _check(lib.sar_plan_describe_stolt_ranges(C.byref(g), C.byref(im), C.c_uint32(flags),
+                                              C.c_void_p(out.ctypes.data)))
+    del keep
+    return out
+
+
 def describe_scene(sc, flags=0):
     return describe(sc.tx, sc.rx, sc.scan, sc.npx, sc.npy, sc.x0, sc.y0, sc.dx, sc.dy, sc.z0, sc.k,
                     sc.nx, sc.ny, sc.nz, sc.dz_img, sc.z_ref, flags=flags)
+
+
+def describe_stolt_ranges_scene(sc, flags=0):
+    return describe_stolt_ranges(sc.tx, sc.rx, sc.scan, sc.npx, sc.npy, sc.x0, sc.y0, sc.dx, sc.dy, sc.z0, sc.k,
+                                 sc.nx, sc.ny, sc.nz, sc.dz_img, sc.z_ref, flags=flags)
 
 
 class Plan:

@@ -41,7 +41,7 @@ def test_library_exports_every_declared_symbol():
     for d in declared:
         assert hasattr(lib, d)
     assert sorted(sarmod.exported_symbols()) == declared
-    assert lib.sar_version() == 3
+    assert lib.sar_version() == 4
 
 
 def test_no_oracle_in_product_path():
@@ -119,3 +119,45 @@ def test_plan_create_without_gpu_fails_loudly():
     with pytest.raises(sar.SarError) as ei:
         sar.Plan.from_scene(scenes.make_scene("tiny"))
     assert ei.value.status == 3
+
+
+@pytest.mark.parametrize("name,n_sample", [("tiny", None), ("small", None), ("freehand", None),
+                                           ("realtime", None), ("large", 8192)])
+def test_stolt_ranges_cover_every_oracle_in_band_bin(name, n_sample):
+    """The k_z bin range K3 evaluates per spectral column (the host class table
+    it uploads, sar_plan_describe_stolt_ranges) contains every bin the oracle's
+    pull puts in band (oracle.stolt_index_table, readings R5/R9), so the bins
+    outside it -- and the columns the plan skips, (0, -1) -- are exactly zero
+    in the oracle too.  Large: a random sample of columns plus the DC and
+    Nyquist rows/columns, where the range widens to the whole axis."""
+    sc = scenes.make_scene(name)
+    geo = oracle.rma.geometry_of(sc)
+    rng_tab = sar.describe_stolt_ranges_scene(sc)
+    b, a = np.meshgrid(np.arange(sc.ny), np.arange(sc.nx), indexing="ij")
+    a, b = a.ravel(), b.ravel()
+    if n_sample:
+        pick = np.random.default_rng(1).choice(a.size, n_sample, replace=False)
+        extra_a = np.concatenate([np.arange(sc.nx), np.zeros(sc.ny, int), np.full(sc.ny, sc.nx // 2)])
+        extra_b = np.concatenate([np.zeros(sc.nx, int), np.arange(sc.ny), np.arange(sc.ny)])
+        a, b = np.concatenate([a[pick], extra_a]), np.concatenate([b[pick], extra_b])
+    i0, _ = oracle.stolt_index_table(geo, a, b)
+    lo, hi = rng_tab[b, a, 0], rng_tab[b, a, 1]
+    j = np.arange(sc.nz)[None, :]
+    inband = i0 >= 0
+    inside = (j >= lo[:, None]) & (j <= hi[:, None])
+    assert not (inband & ~inside).any(), np.argwhere(inband & ~inside)[:5]
+    skipped = hi < lo
+    assert not inband[skipped].any()
+    # the range is a tight superset: at most 2 bins of margin on each side of
+    # the in-band run (reading R9's widening), except where an edge nears k_z = 0
+    live = inband.any(axis=1)
+    first = np.where(live, inband.argmax(axis=1), 0)
+    last = np.where(live, sc.nz - 1 - inband[:, ::-1].argmax(axis=1), 0)
+    tight = live & (hi - lo < sc.nz - 1)
+    assert (first[tight] - lo[tight] <= 3).all() and (hi[tight] - last[tight] <= 3).all()
+    if name in ("freehand", "large", "realtime"):
+        # the evanescent corners of the (k_x, k_y) plane (~18% of the columns at
+        # lambda/4 sampling) and, with a shallow k_z window (Realtime), the
+        # columns whose band lies below it are skipped
+        frac = (rng_tab[:, :, 1] < rng_tab[:, :, 0]).mean()
+        assert 0.17 < frac < 0.5, frac

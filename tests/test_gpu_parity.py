@@ -73,6 +73,24 @@ def test_stage_parity(name):
         assert e2 <= STAGE_BAR, (k, e2, einf)
 
 
+@pytest.mark.parametrize("kw", [dict(npx=24, npy=16, nx=32, ny=32, nk=64, nz=256, dz=2e-3, z_ref=0.25),
+                                dict(npx=20, npy=12, nx=32, ny=16, nk=600, nz=512, dz=2e-3, z_ref=0.3),
+                                dict(npx=30, npy=9, nx=32, ny=32, nk=40, nz=128, dz=4e-3, z_ref=0.2)],
+                         ids=lambda kw: f"nz{kw['nz']}")
+def test_stage_parity_k3_warp(kw):
+    """Per-stage parity where K3 runs the warp-per-column kernel (n_z = 128,
+    256, 512): the Stolt output before the z-IFFT and the complex image."""
+    sc = _custom(**kw)
+    d, s = _data(sc, gpu_gen=False)
+    img, geo, st = oracle.reconstruct(s, sc, complex_out=True, return_stages=True)
+    with sar.Plan.from_scene(sc) as plan:
+        g3 = plan.debug_stage(3, d).cpu().numpy()
+        g4 = plan.debug_stage(4, d).cpu().numpy()
+    for key, g, w in (("stolt", g3, st["stolt"]), ("complex", g4, img)):
+        e2, _ = errs(g, w)
+        assert e2 <= STAGE_BAR, (key, e2)
+
+
 def _check_e2e(sc, flags=0, gpu_gen=None, geo=None, pulse=None):
     d, s = _data(sc, gpu_gen)
     want, _ = oracle.reconstruct(s, geo if geo is not None else sc,
@@ -91,12 +109,45 @@ def test_end_to_end(name):
     _check_e2e(scenes.make_scene(name))
 
 
+@pytest.fixture(scope="module")
+def large_case():
+    """Large (configs[3]): device input and the full fp64 oracle image, computed
+    once for the tests that compare against it."""
+    sc = scenes.make_scene("large")
+    d, s = _data(sc, True)
+    want, _ = oracle.reconstruct(s, sc)
+    del s
+    return sc, d, want
+
+
 @pytest.mark.slow
-def test_end_to_end_large_bench_configuration():
+def test_end_to_end_large_bench_configuration(large_case):
     """Large (configs[3]) at full size in the launch configuration bench.py
     times (plan with SAR_PROFILE_STAGES), full oracle on the host."""
-    sc = scenes.make_scene("large")
-    _check_e2e(sc, flags=sar.SAR_PROFILE_STAGES, gpu_gen=True)
+    sc, d, want = large_case
+    with sar.Plan.from_scene(sc, flags=sar.SAR_PROFILE_STAGES) as plan:
+        got = plan.reconstruct(d).cpu().numpy()
+    e2, einf = errs(got, want)
+    assert e2 <= E2_BAR and einf <= EINF_BAR, (e2, einf)
+
+
+@pytest.mark.slow
+def test_slab_large_g8_against_oracle(large_case):
+    """The single-image slab decomposition (8 ranks emulated in this process)
+    against the fp64 oracle directly, not only against the whole-image CUDA
+    path."""
+    from paper_2305_02064_b200 import slab
+    sc, d, want = large_case
+    plans = [sar.SlabPlan.from_scene(sc, rank=r, world=8) for r in range(8)]
+    try:
+        got = torch.full(sc.image_shape, float("nan"), device="cuda")
+        slab.emulate(plans, d, got)
+        got = got.cpu().numpy()
+    finally:
+        for p in plans:
+            p.close()
+    e2, einf = errs(got, want)
+    assert e2 <= E2_BAR and einf <= EINF_BAR, (e2, einf)
 
 
 def test_node_offsets_match_oracle():
@@ -175,6 +226,10 @@ EDGE = [
     dict(npx=8, npy=6, nx=8, ny=8, nk=2048, nz=512, dz=2e-3, z_ref=0.25),
     # SAR_MAX_PAIRS = 64 Tx/Rx pairs (16 Tx x 4 Rx: a 64-row virtual array)
     dict(npx=16, npy=12, nx=16, ny=128, nk=16, nz=16, dz=5e-3, z_ref=0.25, n_tx=16),
+    # the warp-per-column K3 (k3_warp) at every n_z it covers, n_k below / above n_z
+    dict(npx=24, npy=16, nx=32, ny=32, nk=64, nz=256, dz=2e-3, z_ref=0.25),
+    dict(npx=20, npy=12, nx=32, ny=16, nk=600, nz=512, dz=2e-3, z_ref=0.3),
+    dict(npx=30, npy=9, nx=32, ny=32, nk=40, nz=128, dz=4e-3, z_ref=0.2),
 ]
 
 
@@ -299,6 +354,53 @@ def test_tma_and_plain_paths_agree():
     assert e2 < 1e-5
 
 
+# ---- Tx/Rx layouts with x baselines (j^x != 0; Eq. (3)) --------
+def _xlayout(n_tx=2):
+    """Tx along x (x = 0, 2 lambda[, 4 lambda]) and the 4 Rx along y: the
+    virtual midpoints ((tx + rx)/2, Eq. (3)) span both lattice axes, j^x in
+    {0, 4, 8} and j^y in {0..3}.  Every pair with j^x != 0 lands on other
+    lattice columns than its pose, so K1 accumulates in the shared x-tile
+    instead of registers (k1_correct_xfft_tma<N, false, *>)."""
+    lam = scenes.LAMBDA_C
+    tx = np.zeros((n_tx, 3))
+    tx[:, 0] = [2.0 * lam * i for i in range(n_tx)]
+    rx = np.zeros((4, 3))
+    rx[:, 1] = [0.0, lam / 2.0, lam, 1.5 * lam]
+    return tx, rx
+
+
+XLAYOUT = [
+    # TMA K1 with the shared accumulation tile (nx >= 64, npx % 4 == 0, even n_k), no wrap
+    dict(npx=48, npy=24, nx=64, ny=32, nk=32, nz=32, dz=5e-3, z_ref=0.2),
+    # x-wrap: npx + max j^x > nx, the virtual aperture wraps 8 columns (3 Tx)
+    dict(npx=64, npy=24, nx=64, ny=32, nk=48, nz=32, dz=5e-3, z_ref=0.2, n_tx=3),
+    # nx = 512 (the Large x-FFT tile), wrap of 4 columns, ragged last k chunk
+    dict(npx=512, npy=8, nx=512, ny=16, nk=40, nz=16, dz=5e-3, z_ref=0.25),
+    # the plain (non-TMA) K1: odd n_k
+    dict(npx=30, npy=10, nx=32, ny=16, nk=17, nz=16, dz=5e-3, z_ref=0.2),
+]
+
+
+@pytest.mark.parametrize("kw", XLAYOUT, ids=lambda kw: "x".join(str(kw[k]) for k in ("npx", "npy", "nx", "nk")))
+def test_x_baseline_layouts(kw):
+    """Tx/Rx layouts with x baselines against the oracle, per stage (planar
+    lattice, spectrum) and end to end."""
+    sc = _custom(**kw)
+    sc.tx, sc.rx = _xlayout(kw.get("n_tx", 2))
+    info = sar.describe_scene(sc)
+    assert info["jx"].max() > 0 and info["jy"].max() > 0
+    d, s = _data(sc, gpu_gen=False)
+    img, geo, st = oracle.reconstruct(s, sc, complex_out=True, return_stages=True)
+    assert np.array_equal(geo.jx, info["jx"])
+    with sar.Plan.from_scene(sc) as plan:
+        g1 = plan.debug_stage(1, d).cpu().numpy()
+        g2 = plan.debug_stage(2, d).cpu().numpy()
+    for key, g in (("planar", g1), ("spectrum", g2)):
+        e2, _ = errs(g, st[key])
+        assert e2 <= STAGE_BAR, (key, e2)
+    _check_e2e(sc, gpu_gen=False)
+
+
 # ---- 2-D single-plane images (SAR_IMAGE_2D, reading R18) -------------------
 @pytest.mark.parametrize("name,planes", [("tiny", [0.25]), ("small", [0.2, 0.25, 0.3]),
                                          ("freehand", [0.30]), ("realtime", [0.25, 0.3])])
@@ -400,6 +502,29 @@ NUFFT_EDGE = [
     dict(npx=24, npy=20, nx=32, ny=32, nk=32, nz=32, dz=5e-3, z_ref=0.2, n_frames=3, n_tx=3),  # frames, wrap
     dict(npx=8, npy=6, nx=32, ny=16, nk=2048, nz=32, dz=5e-3, z_ref=0.2),          # SAR_MAX_NK: 8 k chunks
 ]
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("n_k,pairs", [(136, (1, 2)), (24, (2, 4))])
+def test_nufft_freehand_geometry(n_k, pairs):
+    """NUFFT placement at the Freehand geometry (BJ.configs[2]: 256 x 256
+    free-hand poses, 256^2 image -> the 512^2 fine grid, the 512-point fine
+    x-FFT and k2n_yfft_crop<512>), against the FGG oracle.  n_k = 136 (> 128)
+    runs the 256-thread spread; the full 2 x 4 array at n_k = 24 keeps the
+    oracle to ~1 minute."""
+    from oracle import nufft
+    sc = scenes.make_scene("freehand", n_k=n_k)
+    sc.tx, sc.rx = sc.tx[:pairs[0]], sc.rx[:pairs[1]]
+    d, s = _data(sc, gpu_gen=True)
+    S, geo = nufft.spectrum_nufft(s, sc)
+    want = oracle.magnitude_image(oracle.ifft3(oracle.stolt(oracle.rma_filter(S, geo), geo)), geo)
+    with sar.Plan.from_scene(sc, flags=sar.SAR_GRID_NUFFT) as plan:
+        g2 = plan.debug_stage(2, d).cpu().numpy()
+        got = plan.reconstruct(d).cpu().numpy()
+    e2s, _ = errs(g2, S)
+    assert e2s <= STAGE_BAR, e2s
+    e2, einf = errs(got, want)
+    assert e2 <= E2_BAR and einf <= EINF_BAR, (n_k, e2, einf)
 
 
 @pytest.mark.parametrize("kw", NUFFT_EDGE, ids=lambda kw: "x".join(str(kw[k]) for k in ("npx", "npy", "nx", "ny", "nk")))
@@ -527,6 +652,25 @@ def test_slab_without_tma_equals_whole_image():
     finally:
         for p in plans:
             p.close()
+
+
+@pytest.mark.parametrize("world,flags", [(2, 0), (4, 0), (4, sar.SAR_NO_COMPENSATION)])
+def test_slab_small_against_oracle(world, flags):
+    """Small, G = 2 and 4 emulated ranks, compared with the fp64 oracle."""
+    from paper_2305_02064_b200 import slab
+    sc = scenes.make_scene("small")
+    d, s = _data(sc)
+    want, _ = oracle.reconstruct(s, sc, no_compensation=bool(flags & sar.SAR_NO_COMPENSATION))
+    plans = [sar.SlabPlan.from_scene(sc, rank=r, world=world, flags=flags) for r in range(world)]
+    try:
+        got = torch.full(sc.image_shape, float("nan"), device="cuda")
+        slab.emulate(plans, d, got)
+        got = got.cpu().numpy()
+    finally:
+        for p in plans:
+            p.close()
+    e2, einf = errs(got, want)
+    assert e2 <= E2_BAR and einf <= EINF_BAR, (world, e2, einf)
 
 
 @pytest.mark.parametrize("name,world", [("small", 2), ("small", 4), ("large", 8)])
