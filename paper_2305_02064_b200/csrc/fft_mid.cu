@@ -196,12 +196,14 @@ cudaError_t launch_mid(float2 *data, const float2 *tw, int F, int ny, int nx, in
     if (so) kern = k_fft_mid2<N, DIR, true>;                                                       \
     constexpr size_t smem = mid2_smem<N>();                                                        \
     if (smem > 40 * 1024) {                                                                        \
-      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
-      if (e != cudaSuccess) return e;                                                              \
+      cudaError_t e0 = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+      if (e0 != cudaSuccess) return e0;                                                            \
     }                                                                                              \
-    const int maxg = num_sms * mid2_ctas<N>();                                                     \
-    kern<<<nitems < maxg ? nitems : maxg, mid2_ntc<N>() + 32, smem, s>>>(*tm, data, tw, nx, inner,   \
-                                                   nchunk, nitems, so ? *so : off, liveb, F * ny); \
+    const int occ = resident_ctas((const void *)kern, mid2_ntc<N>() + 32, smem);                  \
+    const int maxg = num_sms * (occ < mid2_ctas<N>() ? occ : mid2_ctas<N>());                                                     \
+    cudaError_t e = launch_ex(kern, dim3(nitems < maxg ? nitems : maxg), dim3(mid2_ntc<N>() + 32), smem, s, \
+                               *tm, data, tw, nx, inner, nchunk, nitems, so ? *so : off, liveb, F * ny); \
+    if (e != cudaSuccess) return e;                                                                \
     return cudaGetLastError();                                                                     \
   }
       X(2) X(4) X(8) X(16) X(32) X(64) X(128) X(256) X(512)

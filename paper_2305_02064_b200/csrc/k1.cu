@@ -234,17 +234,34 @@ __global__ void __launch_bounds__(K1_NT + 32, 1)
         ++jobctr;
         const float2 *sv = reinterpret_cast<const float2 *>(stages + st * STAGE);
         const float *sap = reinterpret_cast<const float *>(stages + st * STAGE + K1_BOX_BYTES);
+        // the warp's rows of the box go to registers and the stage is handed
+        // back before the rotation, so the producer refills it meanwhile
+        float4 r01[UPB], r23[UPB];
+        float rbeta[UPB];
+#pragma unroll
+        for (int w = 0; w < UPB; ++w) {
+          const int il = r0 + w * RPP;
+          const int ix = b * br + il;
+          r01[w] = r23[w] = make_float4(0.f, 0.f, 0.f, 0.f);
+          rbeta[w] = 0.f;
+          if (il < br && ix < v.npx) {
+            r01[w] = *reinterpret_cast<const float4 *>(sv + il * C + kq);
+            r23[w] = *reinterpret_cast<const float4 *>(sv + il * C + kq + 2);
+            rbeta[w] = sap[il];
+          }
+        }
+        __syncwarp();
+        if (lane == 0) sartma::mbar_arrive(&empty[st]);
 #pragma unroll
         for (int w = 0; w < UPB; ++w) {
           const int il = r0 + w * RPP;
           const int ix = b * br + il;
           if (il < br && ix < v.npx) {
-            const float4 v01 = *reinterpret_cast<const float4 *>(sv + il * C + kq);
-            const float4 v23 = *reinterpret_cast<const float4 *>(sv + il * C + kq + 2);
+            const float4 v01 = r01[w], v23 = r23[w];
             float2 val[4] = {make_float2(v01.x, v01.y), make_float2(v01.z, v01.w), make_float2(v23.x, v23.y),
                              make_float2(v23.z, v23.w)};
             if (!v.no_comp) {
-              const float beta = sap[il] + bp;
+              const float beta = rbeta[w] + bp;
               float turns = beta * kt;
               turns -= rintf(turns);
               float2 rot;
@@ -271,8 +288,6 @@ __global__ void __launch_bounds__(K1_NT + 32, 1)
             }
           }
         }
-        __syncwarp();
-        if (lane == 0) sartma::mbar_arrive(&empty[st]);
         if (!REGACC) sarfft::tile_sync<1, K1_NT>();  // tile updates of this job complete
       }
     }
@@ -296,11 +311,6 @@ __global__ void __launch_bounds__(K1_NT + 32, 1)
     // tile) with the transformed rows stored straight to W0
     float2 *out = v.w0 + ((size_t)(f * v.nvy + vyl) * NX) * (size_t)v.nk + kc * C;
     const int cmax = v.nk - kc * C;
-#ifdef K1_NO_FFT   // timing experiment only (scripts/ab_variants.py): the x-FFT left out
-    for (int i = tid; i < NX * C; i += K1_NT)
-      if (i % C < cmax) __stcs(out + (size_t)(i / C) * v.nk + i % C, tile[i]);
-    if (false)
-#endif
     sarfft2::fft<NX, C, C, K1_NT, -1, 1, false, (NX == 512 ? 16 : 0)>(
         tile, tws, tid, [&](int c, int m) { return tile[m * C + c]; }, [] {},
         [&](int c, int m, float2 x) {
@@ -353,7 +363,8 @@ cudaError_t launch_k1(const SarDeviceView &v, const float2 *data, bool fft, cuda
                                : (regacc ? k1_correct_xfft_tma<N, true, false> : k1_correct_xfft_tma<N, false, false>); \
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
     if (e != cudaSuccess) return e;                                                                   \
-    kern<<<grid, K1_NT + 32, smem, s>>>(v, *tm_s, *tm_ap, br, nbox, nitems);                               \
+    e = launch_ex(kern, dim3(grid), dim3(K1_NT + 32), smem, s, v, *tm_s, *tm_ap, br, nbox, nitems);       \
+    if (e != cudaSuccess) return e;                                                                   \
     return cudaGetLastError();                                                                        \
   }
       X(64) X(128) X(256) X(512)

@@ -169,16 +169,24 @@ __global__ void __launch_bounds__(K3C_NT, 8) k3_class(const SarDeviceView v) {
   }
 }
 
-#ifndef K3P_GEOM
-#define K3P_GEOM 256, 3, 3, 2
-#endif
 // threads per consumer group, consumer groups (round-robin items), ring
-// stages, mirror classes per item
-constexpr int K3P_GEOM_[4] = {K3P_GEOM};
-constexpr int K3P_G = K3P_GEOM_[0];
-constexpr int K3P_NG = K3P_GEOM_[1];
-constexpr int K3P_S = K3P_GEOM_[2];
-constexpr int K3P_CL = K3P_GEOM_[3];
+// stages, mirror classes per item (compile-time overridable for A/B runs)
+#ifndef K3P_G_
+#define K3P_G_ 256
+#endif
+#ifndef K3P_NG_
+#define K3P_NG_ 3
+#endif
+#ifndef K3P_S_
+#define K3P_S_ 3
+#endif
+#ifndef K3P_CL_
+#define K3P_CL_ 2
+#endif
+constexpr int K3P_G = K3P_G_;
+constexpr int K3P_NG = K3P_NG_;
+constexpr int K3P_S = K3P_S_;
+constexpr int K3P_CL = K3P_CL_;
 // group g takes items n = g (mod NG), which use stage n mod S: with NG | S
 // every stage belongs to one group, so a group waiting on a stage's full
 // barrier can never see the phase of another group's item (mbarrier parity
@@ -525,8 +533,8 @@ bool try_k3pp(const SarDeviceView &v, bool ifft, cudaStream_t s, int num_sms, cu
   auto kern = ifft ? k3_pp<N, CL, true> : k3_pp<N, CL, false>;
   *err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (*err != cudaSuccess) return true;
-  kern<<<grid, K3P_NG * K3P_G + 32, smem, s>>>(v, nitems_f);
-  *err = cudaGetLastError();
+  *err = launch_ex(kern, dim3(grid), dim3(K3P_NG * K3P_G + 32), smem, s, v, nitems_f);
+  if (*err == cudaSuccess) *err = cudaGetLastError();
   return true;
 }
 }  // namespace

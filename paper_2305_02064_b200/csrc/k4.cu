@@ -37,9 +37,19 @@ __device__ __forceinline__ void report_peak(const SarDeviceView &v, int f, float
 // write |o|/(nx ny nz) (or the scaled complex value) straight into the rolled
 // image rows (reading R8, R11): coalesced 128-byte segments, no transpose
 // buffer.
+// consumer threads and pass split of the x-IFFT: one thread per pass-1
+// butterfly (512 threads with the split pass 2, as in K2, measured slower:
+// 0.347 vs 0.314 ms on Large)
+template <int NX>
+struct K4bFft {
+  static constexpr bool BIG = false;
+  static constexpr int NTC = BIG ? 512 : sarfft2::nt_fft<NX, KC>();
+  static constexpr int R1S = BIG ? 16 : 0;
+  static constexpr int TWN = sarfft2::tw2_size<NX, R1S, BIG>() > NX ? sarfft2::tw2_size<NX, R1S, BIG>() : NX;
+};
 template <int NX, bool CPLX>
 constexpr size_t k4b2_smem() {
-  return ((size_t)2 * NX * KC + (size_t)NX * (KC + 1) + NX) * sizeof(float2);
+  return ((size_t)2 * NX * KC + (size_t)NX * (KC + 1) + K4bFft<NX>::TWN) * sizeof(float2);
 }
 template <int NX>
 constexpr int k4b2_ctas() {
@@ -50,10 +60,11 @@ constexpr int k4b2_ctas() {
 // slab exchange #2 (box {16 z, nx', 1, G} = one [nx][16] tile), so stage 3
 // needs no unpack pass.
 template <int NX, bool CPLX, bool SLAB>
-__global__ void __launch_bounds__(sarfft2::nt_fft<NX, KC>() + 32)
+__global__ void __launch_bounds__(K4bFft<NX>::NTC + 32)
     k4_xifft_mag2(const SarDeviceView v, const __grid_constant__ CUtensorMap tm, void *__restrict__ img, int nzc,
                   int nitems) {
-  constexpr int NTC = sarfft2::nt_fft<NX, KC>();
+  using FT = K4bFft<NX>;
+  constexpr int NTC = FT::NTC;
   constexpr int S = 2;
   constexpr int ROWS = NX < 256 ? NX : 256;
   constexpr int NBOX = NX / ROWS;
@@ -65,7 +76,7 @@ __global__ void __launch_bounds__(sarfft2::nt_fft<NX, KC>() + 32)
   float2 *tw = work + (size_t)NX * (KC + 1);   // [NX]
   __shared__ __align__(8) uint64_t full[S], empty[S];
   const int tid = threadIdx.x;
-  sarfft2::build_tw2<NX, 0, false>(tw, v.tw_x, tid, NTC + 32);   // [NX] pass-2 rows
+  sarfft2::build_tw2<NX, FT::R1S, FT::BIG>(tw, v.tw_x, tid, NTC + 32);   // pass-2 rows
   if (tid == 0) {
     for (int i = 0; i < S; ++i) {
       sartma::mbar_init(&full[i], 1);
@@ -111,7 +122,7 @@ __global__ void __launch_bounds__(sarfft2::nt_fft<NX, KC>() + 32)
     float pk = 0.f;
     // the image row of z-slot c is resolved once per butterfly (prep), so a
     // store is the x roll plus one STG
-    sarfft2::fft_ctx<NX, KC, KC + 1, NTC, +1, 1, true, 0, false, (NX > 32)>(
+    sarfft2::fft_ctx<NX, KC, KC + 1, NTC, +1, 1, true, FT::R1S, FT::BIG, (NX > 32)>(
         work, tw, tid, [&](int c, int m) { return stage[m * KC + c]; },
         [&] {
           if (tid == 0) sartma::mbar_arrive(&empty[st]);
@@ -222,11 +233,14 @@ cudaError_t launch_k4b(const SarDeviceView &v, void *img, bool cplx, cudaStream_
     if (slab4d) kern = cplx ? k4_xifft_mag2<N, true, true> : k4_xifft_mag2<N, false, true>;            \
     constexpr size_t smem = k4b2_smem<N, false>();                                                     \
     if (smem > 40 * 1024) {                                                                            \
-      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
-      if (e != cudaSuccess) return e;                                                                  \
+      cudaError_t e0 = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+      if (e0 != cudaSuccess) return e0;                                                                \
     }                                                                                                  \
-    const int maxg = num_sms * k4b2_ctas<N>();                                                         \
-    kern<<<nitems < maxg ? nitems : maxg, sarfft2::nt_fft<N, KC>() + 32, smem, s>>>(v, *tm, img, nzc, nitems); \
+    const int occ = resident_ctas((const void *)kern, K4bFft<N>::NTC + 32, smem);                      \
+    const int maxg = num_sms * (occ < k4b2_ctas<N>() ? occ : k4b2_ctas<N>());                                                         \
+    cudaError_t e = launch_ex(kern, dim3(nitems < maxg ? nitems : maxg), dim3(K4bFft<N>::NTC + 32), smem, s, \
+                               v, *tm, img, nzc, nitems);                                              \
+    if (e != cudaSuccess) return e;                                                                    \
     return cudaGetLastError();                                                                         \
   }
       X(2) X(4) X(8) X(16) X(32) X(64) X(128) X(256) X(512)

@@ -23,13 +23,35 @@
 #include <stdint.h>
 #include <stdlib.h>
 
+#include <map>
+#include <mutex>
 #include <string>
+#include <tuple>
 #include <type_traits>
 #include <vector>
 
 #include "common.cuh"
 
 using namespace sark;
+
+namespace sark {
+int resident_ctas(const void *kern, int threads, size_t smem) {
+  static std::mutex mu;
+  static std::map<std::tuple<const void *, int, size_t>, int> cache;
+  std::lock_guard<std::mutex> lock(mu);
+  const auto key = std::make_tuple(kern, threads, smem);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  int n = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, threads, smem) != cudaSuccess) {
+    cudaGetLastError();
+    n = 1;
+  }
+  n = n < 1 ? 1 : n;
+  cache[key] = n;
+  return n;
+}
+}  // namespace sark
 
 // Enqueue the path.  stop_stage: 0 = full; 1 = K1 without the x-FFT; 2 = K1+K2;
 // 3 = K1+K2+K3 without the z-IFFT.  ev (optional, 6 events) brackets the kernels.
