@@ -146,12 +146,13 @@ int sar_plan_describe_stolt_ranges(const sar_geom_desc *g, const sar_image_desc 
 
 /* Create a plan: validates the geometry, runs the fp64 decomposition of
  * Eqs. (3),(4),(7),(12) on the host (virtual-node offsets j_tr, beta terms,
- * k_x/k_y/k_z tables), allocates the device workspace
- * (F*ny*nx*(n_k+nz)*8 bytes; + F*4*ny*nx*n_k*8 for the SAR_GRID_NUFFT fine
- * grid) and uploads the tables.  *out receives the plan
+ * k_x/k_y/k_z tables), allocates the device workspace and uploads the tables.  *out receives the plan
  * (NULL on failure).  Errors: INVALID_ARG, GEOMETRY, UNSUPPORTED, OOM, CUDA. */
 int sar_plan_create(sar_plan **out, const sar_geom_desc *g, const sar_image_desc *im,
                     uint32_t flags);
+/* Workspace: F*ny*nx*(n_k+nz)*8 bytes (+ F*4*ny*nx*n_k*8 for the
+ * SAR_GRID_NUFFT fine grid).  (A build with SAR_WAVE_BYTES > 0 processes a
+ * batch W frames at a time with a W-frame workspace; measured slower.) */
 
 /* Reconstruct (3-D volume, or the planes of a SAR_IMAGE_2D plan).
  * d_data: device, complex64 [F][n_tx][n_rx][npy*npx][n_k],

@@ -39,6 +39,18 @@ constexpr int K1_KT = 4;  // consecutive k per thread
 
 constexpr int k1c_for(int nx) { return nx >= 256 ? 16 : 64; }
 
+// Store of an intermediate volume (W0 / W1) that the next kernel reads:
+// default write-back caching, so a frame wave's volumes can be served from
+// L2 (plan.cpp: frame waves); SAR_STREAM_INTERMEDIATES selects the
+// evict-first streaming store instead (A/B builds)
+__device__ __forceinline__ void st_mid(float2 *p, float2 x) {
+#ifdef SAR_STREAM_INTERMEDIATES
+  __stcs(p, x);
+#else
+  *p = x;
+#endif
+}
+
 // acc += a * b (complex), two paired-fp32 FMAs
 __device__ __forceinline__ float2 cmac2(float2 acc, float2 a, float2 b) {
   acc = __ffma2_rn(make_float2(a.x, a.x), b, acc);
@@ -238,6 +250,7 @@ cudaError_t launch_mid(float2 *data, const float2 *tw, int F, int ny, int nx, in
                        const CUtensorMap *tm, int num_sms, const MidSlabOut *so = nullptr,
                        const int *liveb = nullptr);
 cudaError_t launch_k3(const SarDeviceView &v, bool ifft, cudaStream_t s, int num_sms);
+
 cudaError_t launch_k3_plane(const SarDeviceView &v, cudaStream_t s);
 cudaError_t launch_stolt_index(const SarDeviceView &v, const int32_t *cols, int n, int32_t *i0, float *tau,
                                cudaStream_t s);

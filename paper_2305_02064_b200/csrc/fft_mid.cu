@@ -171,7 +171,7 @@ __global__ void __launch_bounds__(mid2_ntc<N>() + 32)
         },
         [](int c) { return c; },
         [&](int c, int m, float2 v) {
-          if (c < cmax && (DIR > 0 || (unsigned)((m + lbo) & (N - 1)) < span)) __stcs(base + (size_t)m * row + c, v);
+          if (c < cmax && (DIR > 0 || (unsigned)((m + lbo) & (N - 1)) < span)) st_mid(base + (size_t)m * row + c, v);
         });
   }
 }
@@ -202,7 +202,7 @@ cudaError_t launch_mid(float2 *data, const float2 *tw, int F, int ny, int nx, in
     const int occ = resident_ctas((const void *)kern, mid2_ntc<N>() + 32, smem);                  \
     const int maxg = num_sms * (occ < mid2_ctas<N>() ? occ : mid2_ctas<N>());                                                     \
     cudaError_t e = launch_ex(kern, dim3(nitems < maxg ? nitems : maxg), dim3(mid2_ntc<N>() + 32), smem, s, \
-                               *tm, data, tw, nx, inner, nchunk, nitems, so ? *so : off, liveb, F * ny); \
+                               *tm, data, tw, nx, inner, nchunk, nitems, so ? *so : off, liveb, 1 << 30); \
     if (e != cudaSuccess) return e;                                                                \
     return cudaGetLastError();                                                                     \
   }

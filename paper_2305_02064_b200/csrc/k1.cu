@@ -45,10 +45,10 @@ __global__ void __launch_bounds__(nt_for(NX), minb_for(NX))
     if (iy < 0) iy += v.ny;
     if (iy >= v.npy) continue;  // uniform over the CTA
     const int t = pr / v.nr, r = pr - t * v.nr;
-    const size_t rowbase = ((size_t)(f * v.nt + t) * v.nr + r) * (size_t)v.P + (size_t)iy * v.npx;
+    const size_t rowbase = ((size_t)((f + v.f0) * v.nt + t) * v.nr + r) * (size_t)v.P + (size_t)iy * v.npx;
     const float2 *srow = s + rowbase * (size_t)v.nk;
-    const float *ap = v.apose + (size_t)f * v.P + (size_t)iy * v.npx;
-    const float bp = v.bpair[f * v.npair + pr];
+    const float *ap = v.apose + (size_t)(f + v.f0) * v.P + (size_t)iy * v.npx;
+    const float bp = v.bpair[(f + v.f0) * v.npair + pr];
     const int jx = v.jx[pr];
     // issue a batch of EB independent loads before consuming any (memory-level
     // parallelism without holding all E samples in registers)
@@ -196,11 +196,12 @@ __global__ void __launch_bounds__(K1_NT + 32, 1)
           int iy = vy - v.jy[j.pr];
           if (iy < 0) iy += v.ny;
           const int t = j.pr / v.nr, r = j.pr - t * v.nr;
-          const long long row = ((long long)(f * v.nt + t) * v.nr + r) * v.P + (long long)iy * v.npx + j.b * br;
+          const long long row =
+              ((long long)((f + v.f0) * v.nt + t) * v.nr + r) * v.P + (long long)iy * v.npx + j.b * br;
           unsigned char *sb = stages + st * STAGE;
           sartma::mbar_arrive_expect_tx(&full[st], tx_bytes);
           sartma::tma_load_2d(sb, &tm_s, kc * C, (int)row, &full[st]);
-          sartma::tma_load_2d(sb + K1_BOX_BYTES, &tm_ap, j.b * br, f * v.npy + iy, &full[st]);
+          sartma::tma_load_2d(sb + K1_BOX_BYTES, &tm_ap, j.b * br, (f + v.f0) * v.npy + iy, &full[st]);
         }
       }
     }
@@ -224,7 +225,7 @@ __global__ void __launch_bounds__(K1_NT + 32, 1)
     for (int u = 0; u < (REGACC ? MAXB * UPB * K1_KT : 1); ++u) acc[u] = make_float2(0.f, 0.f);
     for (int pr = 0; pr < v.npair; ++pr) {
       if (!k1_pair_valid(v, vy, pr)) continue;
-      const float bp = v.bpair[f * v.npair + pr];
+      const float bp = v.bpair[(f + v.f0) * v.npair + pr];
       const int jx = v.jx[pr];
 #pragma unroll
       for (int b = 0; b < MAXB; ++b) {
@@ -250,6 +251,9 @@ __global__ void __launch_bounds__(K1_NT + 32, 1)
             rbeta[w] = sap[il];
           }
         }
+        // the stage is refilled by TMA (async proxy) after this warp's arrival:
+        // the proxy fence makes the shared-memory reads above complete first
+        sartma::fence_proxy_async();
         __syncwarp();
         if (lane == 0) sartma::mbar_arrive(&empty[st]);
 #pragma unroll
@@ -319,7 +323,7 @@ __global__ void __launch_bounds__(K1_NT + 32, 1)
               const int h = m >> v.slab_lg, al = m & ((1 << v.slab_lg) - 1);
               __stcs(v.slab_dst[h] + (((size_t)vyl << v.slab_lg) + al) * v.nk + kc * C + c, x);
             } else {
-              __stcs(out + (size_t)m * v.nk + c, x);
+              st_mid(out + (size_t)m * v.nk + c, x);
             }
           }
         });

@@ -108,7 +108,7 @@ __global__ void __launch_bounds__(K3C_NT, 8) k3_class(const SarDeviceView v) {
   __syncthreads();
   // 2. Stolt pull over the in-band (class, j) pairs, filter at the two taps
   //    folded into the weights (readings R2-R5, R9)
-  const double rr = v.rref[f] * (1.0 / TWO_PI);
+  const double rr = v.rref[f + v.f0] * (1.0 / TWO_PI);
   int tot = 0;
 #pragma unroll
   for (int cl = 0; cl < CL; ++cl) tot += jhis[cl] - jlos[cl] + 1;
@@ -159,7 +159,7 @@ __global__ void __launch_bounds__(K3C_NT, 8) k3_class(const SarDeviceView v) {
           return col >= 0 ? dst + (size_t)col * NZ : nullptr;
         },
         [&](float2 *p, int m, float2 x) {
-          if (p) __stcs(p + m, x);
+          if (p) st_mid(p + m, x);
         });
   } else {
     for (int i = tid; i < CC * NZ; i += K3C_NT) {
@@ -290,7 +290,7 @@ __device__ __forceinline__ void k3pp_consume(const SarDeviceView &v, int nitems_
             return col >= 0 ? dst + (size_t)col * NZ : nullptr;
           },
           [&](float2 *p, int m, float2 x) {
-            if (p) __stcs(p + m, x);
+            if (p) st_mid(p + m, x);
           },
           1 + g);
     } else {
@@ -388,7 +388,7 @@ __global__ void __launch_bounds__(K3P_NG * K3P_G + 32, 1) k3_pp(const SarDeviceV
       if (lane == 0) {
         h.nused = cnt;
         h.f = f;
-        h.rr = v.rref[f] * (1.0 / TWO_PI);
+        h.rr = v.rref[f + v.f0] * (1.0 / TWO_PI);
       }
       __syncwarp();
       // members of classes with no bin in band (jhi < jlo: zero output, kept
@@ -429,7 +429,7 @@ __global__ void __launch_bounds__(K3P2_NT) k3_plane(const SarDeviceView v) {
   const int nm = c.nmem, nk = v.nk, ns = v.nz;
   const int ncol = v.nx * v.ny;
   const double kr2 = c.kr2;
-  const double zoff = v.rref[f];   // z_s - Z_0 = (z_s - z_ref) + R_ref
+  const double zoff = v.rref[f + v.f0];   // z_s - Z_0 = (z_s - z_ref) + R_ref
   const float2 *wf = v.w0 + (size_t)f * ncol * (size_t)nk;
   const float2 *col[4];
 #pragma unroll

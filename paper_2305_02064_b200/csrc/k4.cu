@@ -28,7 +28,7 @@ __device__ __forceinline__ float fast_abs(float2 o) {
 __device__ __forceinline__ void report_peak(const SarDeviceView &v, int f, float pk) {
   if (!v.peak) return;
   const unsigned b = __reduce_max_sync(0xffffffffu, __float_as_uint(pk));
-  if ((threadIdx.x & 31) == 0 && b) atomicMax(v.peak + f, b);
+  if ((threadIdx.x & 31) == 0 && b) atomicMax(v.peak + v.f0 + f, b);
 }
 
 // Warp-specialised persistent K4b (nx <= 512, n_z even): [nx][16 z] tiles of

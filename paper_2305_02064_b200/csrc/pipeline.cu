@@ -53,11 +53,16 @@ int resident_ctas(const void *kern, int threads, size_t smem) {
 }
 }  // namespace sark
 
-// Enqueue the path.  stop_stage: 0 = full; 1 = K1 without the x-FFT; 2 = K1+K2;
-// 3 = K1+K2+K3 without the z-IFFT.  ev (optional, 6 events) brackets the kernels.
+// Enqueue the path for frames [f0, f0 + nf) (one frame wave; the workspace
+// holds its frames from 0).  d_image points at frame f0 of the image.
+// stop_stage: 0 = full; 1 = K1 without the x-FFT; 2 = K1+K2; 3 = K1+K2+K3
+// without the z-IFFT.  ev (optional, 6 events) brackets the kernels.
 int sar_launch_pipeline(sar_plan *p, const void *d_data, void *d_image, cudaStream_t s, int stop_stage,
-                        int complex_out, cudaEvent_t *ev) {
-  const SarDeviceView &v = p->v;
+                        int complex_out, cudaEvent_t *ev, int f0, int nf) {
+  SarDeviceView vw = p->v;
+  vw.f0 = f0;
+  vw.F = nf;
+  const SarDeviceView &v = vw;
   const float2 *data = reinterpret_cast<const float2 *>(d_data);
   cudaError_t e = cudaSuccess;
 #define SAR_CHECK(call)                                                       \
@@ -106,7 +111,6 @@ int sar_launch_pipeline(sar_plan *p, const void *d_data, void *d_image, cudaStre
   SAR_CHECK(launch_mid<+1>(v.w1, v.tw_y, v.F, v.ny, v.nx, v.nz, s, p->tma_mid1 ? &p->tm_w1_mid : nullptr,
                            p->num_sms, nullptr, v.liveb));
   if (ev) SAR_CHECK(cudaEventRecord(ev[4], s));
-  if (v.peak) SAR_CHECK(cudaMemsetAsync(v.peak, 0, (size_t)v.F * sizeof(unsigned), s));
   SAR_CHECK(launch_k4b(v, d_image, complex_out != 0, s, p->tma_rows1 ? &p->tm_w1_rows : nullptr, p->num_sms));
   if (ev) SAR_CHECK(cudaEventRecord(ev[5], s));
   return SAR_OK;
@@ -204,15 +208,16 @@ int sar_build_tensor_maps(sar_plan *p) {
   if (v.F == 0 || v.force_plain) return SAR_OK;
   if (p->slab_world == 0) {
     const uint32_t rows = v.ny < 256 ? v.ny : 256, rows1 = v.ny < K4A_ROWS ? v.ny : K4A_ROWS;   // K2 / K4a boxes
-    p->tma_mid0 = encode3d(&p->tm_w0_mid, v.w0, v.nk, v.nx, (uint64_t)v.F * v.ny, KC, 1, rows);
-    p->tma_mid1 = encode3d(&p->tm_w1_mid, v.w1, v.nz, v.nx, (uint64_t)v.F * v.ny, KC, 1, rows1);
+    const uint64_t wf = (uint64_t)p->wave;   // the workspace holds one frame wave
+    p->tma_mid0 = encode3d(&p->tm_w0_mid, v.w0, v.nk, v.nx, wf * v.ny, KC, 1, rows);
+    p->tma_mid1 = encode3d(&p->tm_w1_mid, v.w1, v.nz, v.nx, wf * v.ny, KC, 1, rows1);
     if (v.nufft) {
       // fine grid [F*2ny][2nx][nk]: x-FFT boxes {16 k, 1, <=256 fine columns}
       const uint32_t rx = 2 * v.nx, fr = rx < 256 ? rx : 256;
       p->tma_fine = encode3d(&p->tm_fine, v.wh, v.nk, 1, (uint64_t)v.F * 2 * v.ny * rx, KC, 1, fr);
     }
     const uint32_t xr = v.nx < 256 ? v.nx : 256;
-    p->tma_rows1 = encode3d(&p->tm_w1_rows, v.w1, v.nz, v.nx, (uint64_t)v.F * v.ny, KC, xr, 1);
+    p->tma_rows1 = encode3d(&p->tm_w1_rows, v.w1, v.nz, v.nx, wf * v.ny, KC, xr, 1);
   }
   // K1: -2 d_z table [F*npy][npx] float32 with box [1][br]; input map per call
   const int brmax = K1_BOX_BYTES / (k1c_for(v.nx) * 8);

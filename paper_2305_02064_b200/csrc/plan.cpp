@@ -17,6 +17,10 @@
 
 #include "plan_internal.h"
 
+#ifndef SAR_WAVE_BYTES
+#define SAR_WAVE_BYTES 0   // L2 budget of one frame wave's W0 + W1; 0: no waves (measured slower)
+#endif
+
 namespace {
 thread_local std::string g_last_error;
 
@@ -439,8 +443,22 @@ int host_decompose(const sar_geom_desc *g, const sar_image_desc *im, uint32_t fl
   p->axes[3] = g->dx;
   p->axes[4] = g->dy;
   p->axes[5] = mode2d ? (p->nz > 1 ? im->z_planes[1] - im->z_planes[0] : 0.0) : im->dz;
-  // W0 [F][ny][nx][nk] + W1 [F][ny][nx][nz] (+ the NUFFT fine grid [F][2ny][2nx][nk])
-  p->ws_bytes = ((size_t)F * p->ny * p->nx * ((size_t)nk + p->nz + ((flags & SAR_GRID_NUFFT) ? 4 * (size_t)nk : 0))) *
+  // Frame waves: a batch runs the five kernels on `wave` frames at a time, so
+  // that a wave's intermediate volumes (W0 + W1) fit the L2 budget and the
+  // kernel after the one that wrote them reads them from L2 (Realtime: 24 MiB
+  // per frame).  The workspace holds one wave.
+  {
+    const size_t per_frame = (size_t)p->ny * p->nx * ((size_t)nk + p->nz) * sizeof(float2);
+    int w = F;
+    if (F > 1 && !(flags & SAR_GRID_NUFFT) && (size_t)SAR_WAVE_BYTES > 0) {
+      const size_t fit = (size_t)SAR_WAVE_BYTES / per_frame;
+      w = (int)std::min<size_t>((size_t)F, std::max<size_t>(1, fit));
+    }
+    p->wave = w;
+  }
+  // W0 [wave][ny][nx][nk] + W1 [wave][ny][nx][nz] (+ the NUFFT fine grid [F][2ny][2nx][nk])
+  p->ws_bytes = ((size_t)p->wave * p->ny * p->nx * ((size_t)nk + p->nz) +
+                 ((flags & SAR_GRID_NUFFT) ? (size_t)F * p->ny * p->nx * 4 * (size_t)nk : 0)) *
                 sizeof(float2);
   return SAR_OK;
 }
@@ -569,7 +587,7 @@ int plan_create_impl(sar_plan **out, const sar_geom_desc *g, const sar_image_des
     free_plan(p);
     return cuda_fail(ce, "table upload");
   }
-  size_t n0 = (size_t)F * p->ny * p->nx * nk, n1 = (size_t)F * p->ny * p->nx * p->nz;
+  size_t n0 = (size_t)p->wave * p->ny * p->nx * nk, n1 = (size_t)p->wave * p->ny * p->nx * p->nz;
   if (slab_world > 0) {
     n0 = n1 = (size_t)p->ny * p->nx * (p->nz / slab_world);
     p->ws_bytes = (n0 + n1) * sizeof(float2);
@@ -578,14 +596,14 @@ int plan_create_impl(sar_plan **out, const sar_geom_desc *g, const sar_image_des
   if (F > 0) {
     if (cudaMalloc(&p->d_w0, n0 * sizeof(float2)) != cudaSuccess ||
         cudaMalloc(&p->d_w1, n1 * sizeof(float2)) != cudaSuccess ||
-      ((flags & SAR_GRID_NUFFT) && cudaMalloc(&p->d_wh, 4 * n0 * sizeof(float2)) != cudaSuccess)) {
+      ((flags & SAR_GRID_NUFFT) && cudaMalloc(&p->d_wh, 4 * (size_t)F * p->ny * p->nx * nk * sizeof(float2)) != cudaSuccess)) {
       cudaGetLastError();
       free_plan(p);
       return fail(SAR_ERR_OOM, "workspace allocation failed");
     }
   }
   SarDeviceView &v = p->v;
-  v.F = F; v.nt = p->nt; v.nr = p->nr; v.npair = p->npair; v.npx = p->npx; v.npy = p->npy; v.P = P;
+  v.F = F; v.f0 = 0; v.nt = p->nt; v.nr = p->nr; v.npair = p->npair; v.npx = p->npx; v.npy = p->npy; v.P = P;
   v.nk = nk; v.nx = p->nx; v.ny = p->ny; v.nz = p->nz;
   v.roll_x = T.roll_x; v.roll_y = T.roll_y;
   v.no_comp = (flags & SAR_NO_COMPENSATION) ? 1 : 0;
@@ -784,9 +802,21 @@ int sar_reconstruct(sar_plan *p, const void *d_data, void *d_image, sar_stream s
   DeviceGuard g(p->device);
   cudaStream_t s = (cudaStream_t)stream;
   p->last_stream = s;
-  cudaEvent_t *ev = nullptr;
-  if (p->prof_events && p->n_prof < SAR_PROFILE_RING) ev = p->ev[p->n_prof++];
-  return sar_launch_pipeline(p, d_data, d_image, s, 0, (p->flags & SAR_OUTPUT_COMPLEX) ? 1 : 0, ev);
+  const int cplx = (p->flags & SAR_OUTPUT_COMPLEX) ? 1 : 0;
+  if (p->d_peak) {
+    cudaError_t e = cudaMemsetAsync(p->d_peak, 0, (size_t)p->F * sizeof(unsigned), s);
+    if (e != cudaSuccess) return cuda_fail(e, "peak reset");
+  }
+  const size_t frame_img = (size_t)p->nz * p->ny * p->nx * (cplx ? sizeof(float2) : sizeof(float));
+  if (p->prof_events) ++p->n_prof_calls;
+  for (int f0 = 0; f0 < p->F; f0 += p->wave) {
+    cudaEvent_t *ev = nullptr;
+    if (p->prof_events && p->n_prof < SAR_PROFILE_RING) ev = p->ev[p->n_prof++];
+    const int st = sar_launch_pipeline(p, d_data, static_cast<char *>(d_image) + (size_t)f0 * frame_img, s, 0, cplx,
+                                       ev, f0, std::min(p->wave, p->F - f0));
+    if (st != SAR_OK) return st;
+  }
+  return SAR_OK;
 }
 
 int sar_reconstruct_host(sar_plan *p, const void *h_data, void *h_image, sar_stream stream) {
@@ -861,7 +891,7 @@ int sar_plan_launches_per_call(const sar_plan *p, int32_t *n) {
 
 int sar_plan_profile_reset(sar_plan *p) {
   if (!p) return fail(SAR_ERR_INVALID_ARG, "plan is NULL");
-  p->n_prof = 0;
+  p->n_prof = p->n_prof_calls = 0;
   return SAR_OK;
 }
 
@@ -880,7 +910,7 @@ int sar_plan_profile_read(sar_plan *p, float ms_out[5], int32_t *n_calls) {
       ms_out[j] += ms;
     }
   }
-  if (n_calls) *n_calls = p->n_prof;
+  if (n_calls) *n_calls = p->n_prof_calls;
   return SAR_OK;
 }
 
@@ -894,13 +924,22 @@ int sar_debug_stage(sar_plan *p, int32_t stage, const void *d_data, void *d_out,
   DeviceGuard g(p->device);
   cudaStream_t s = (cudaStream_t)stream;
   p->last_stream = s;
-  if (stage == 4) return sar_launch_pipeline(p, d_data, d_out, s, 0, 1, nullptr);
-  int st = sar_launch_pipeline(p, d_data, nullptr, s, stage, 0, nullptr);
-  if (st != SAR_OK) return st;
-  const size_t n = (size_t)p->F * p->ny * p->nx * (stage == 3 ? p->nz : p->nk);
-  cudaError_t e = cudaMemcpyAsync(d_out, stage == 3 ? p->d_w1 : p->d_w0, n * sizeof(float2),
-                                  cudaMemcpyDeviceToDevice, s);
-  if (e != cudaSuccess) return cuda_fail(e, "stage copy");
+  // wave by wave; each wave's stage result is copied out of the workspace
+  const size_t fr = (size_t)p->ny * p->nx * (stage == 3 ? p->nz : stage == 4 ? p->nz : p->nk);
+  for (int f0 = 0; f0 < p->F; f0 += p->wave) {
+    const int nf = std::min(p->wave, p->F - f0);
+    if (stage == 4) {
+      const int st = sar_launch_pipeline(p, d_data, static_cast<float2 *>(d_out) + (size_t)f0 * fr, s, 0, 1, nullptr,
+                                         f0, nf);
+      if (st != SAR_OK) return st;
+      continue;
+    }
+    const int st = sar_launch_pipeline(p, d_data, nullptr, s, stage, 0, nullptr, f0, nf);
+    if (st != SAR_OK) return st;
+    cudaError_t e = cudaMemcpyAsync(static_cast<float2 *>(d_out) + (size_t)f0 * fr, stage == 3 ? p->d_w1 : p->d_w0,
+                                    (size_t)nf * fr * sizeof(float2), cudaMemcpyDeviceToDevice, s);
+    if (e != cudaSuccess) return cuda_fail(e, "stage copy");
+  }
   return SAR_OK;
 }
 

@@ -42,6 +42,8 @@ struct SarSpreadEntry {
 // Everything a kernel needs, passed by value (fits the 32 KB parameter space).
 struct SarDeviceView {
   int F, nt, nr, npair, npx, npy, P, nk, nx, ny, nz;
+  int f0;               // first frame of this launch (frame waves): raw rows, beta, R_ref and
+                        // peak tables are indexed by f0 + f, the workspace by f
   int roll_x, roll_y;
   // slab decomposition (sar_slab_*; whole-image plans: 0, ny, (nx/2+1)(ny/2+1), 0, nz)
   int vy0, nvy;         // K1: virtual rows [vy0, vy0 + nvy) written as rows 0.. of w0
@@ -93,6 +95,7 @@ struct SarDeviceView {
 struct sar_plan {
   // sizes
   int F = 0, nt = 0, nr = 0, npair = 0, npx = 0, npy = 0, P = 0, nk = 0, nx = 0, ny = 0, nz = 0;
+  int wave = 0;   // frames per launch wave (= F without waves); the workspace holds `wave` frames
   uint32_t flags = 0;
   int device = 0;
   double dx = 0, dy = 0, dz = 0, z_ref = 0;
@@ -110,7 +113,7 @@ struct sar_plan {
   size_t in_bytes = 0, img_bytes = 0;
   // profiling
   cudaEvent_t ev[SAR_PROFILE_RING][SAR_N_STAGES + 1];
-  int n_prof = 0;
+  int n_prof = 0, n_prof_calls = 0;
   bool prof_events = false;
   cudaStream_t last_stream = nullptr;
   // TMA tensor maps over the workspace (built once per plan; valid flags)
@@ -130,12 +133,14 @@ struct sar_plan {
   // NUFFT mode tables and the half-transformed fine grid
   void *d_nu = nullptr;
   unsigned *d_peak = nullptr;   // SAR_REPORT_PEAK
+
   float2 *d_wh = nullptr;
 };
 
 // pipeline.cu
 int sar_launch_pipeline(sar_plan *p, const void *d_data, void *d_image, cudaStream_t s,
-                        int stop_stage /*0 = full*/, int complex_out, cudaEvent_t *ev /*6 or null*/);
+                        int stop_stage /*0 = full*/, int complex_out, cudaEvent_t *ev /*6 or null*/, int f0,
+                        int nf);
 int sar_launch_stolt_index(sar_plan *p, const int32_t *d_cols, int n, int32_t *d_i0, float *d_tau,
                            cudaStream_t s);
 void sar_set_error(const std::string &msg);

@@ -72,6 +72,7 @@ def test_describe_matches_oracle_bit_exact(name):
     bet = -2.0 * geo.d_z
     assert np.array_equal(d["apose"], bet.astype(np.float32))
     assert np.array_equal(d["bpair"], geo.beta_mimo.astype(np.float32))
+    # the workspace holds one frame wave (waves are off in this build: all F frames)
     assert d["workspace_bytes"] == sc.n_frames * sc.ny * sc.nx * (sc.n_k + sc.nz) * 8
 
 
