@@ -14,12 +14,13 @@
 namespace sark {
 namespace {
 
-// |o| as p * rsqrt(p): one MUFU and a multiply instead of the IEEE sqrtf
-// sequence with its slow-path call (relative error ~2^-22, far inside the
-// 1e-4 parity tolerance)
+// |o| by the SFU square root (sqrt.approx: one MUFU, relative error <= 2^-23,
+// exact 0 at 0) instead of the IEEE sqrtf sequence with its slow-path call
 __device__ __forceinline__ float fast_abs(float2 o) {
   const float p = fmaf(o.x, o.x, o.y * o.y);
-  return p > 0.f ? p * rsqrtf(p) : 0.f;
+  float r;
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(p));
+  return r;
 }
 
 
@@ -59,7 +60,8 @@ constexpr int k4b2_ctas() {
 // SLAB: tm is a 4-D map over the received blocks [G][ny][nx'][nz'] of the
 // slab exchange #2 (box {16 z, nx', 1, G} = one [nx][16] tile), so stage 3
 // needs no unpack pass.
-template <int NX, bool CPLX, bool SLAB>
+// PEAK: SAR_REPORT_PEAK plans (the running max costs one instruction per voxel)
+template <int NX, bool CPLX, bool SLAB, bool PEAK>
 __global__ void __launch_bounds__(K4bFft<NX>::NTC + 32)
     k4_xifft_mag2(const SarDeviceView v, const __grid_constant__ CUtensorMap tm, void *__restrict__ img, int nzc,
                   int nitems) {
@@ -138,7 +140,7 @@ __global__ void __launch_bounds__(K4bFft<NX>::NTC + 32)
           if (rowp) {
             const int ix = (a - rx) & (NX - 1);
             const float mag = fast_abs(o) * sc;
-            pk = fmaxf(pk, mag);
+            if constexpr (PEAK) pk = fmaxf(pk, mag);
             if constexpr (CPLX) {
               __stcs(reinterpret_cast<float2 *>(rowp) + ix, make_float2(o.x * sc, o.y * sc));
             } else {
@@ -146,7 +148,7 @@ __global__ void __launch_bounds__(K4bFft<NX>::NTC + 32)
             }
           }
         });
-    report_peak(v, f, pk);
+    if constexpr (PEAK) report_peak(v, f, pk);
   }
 }
 
@@ -229,8 +231,9 @@ cudaError_t launch_k4b(const SarDeviceView &v, void *img, bool cplx, cudaStream_
     switch (v.nx) {
 #define X(N)                                                                                           \
   case N: {                                                                                            \
-    auto kern = cplx ? k4_xifft_mag2<N, true, false> : k4_xifft_mag2<N, false, false>;                 \
-    if (slab4d) kern = cplx ? k4_xifft_mag2<N, true, true> : k4_xifft_mag2<N, false, true>;            \
+    auto kern = cplx ? k4_xifft_mag2<N, true, false, false> : k4_xifft_mag2<N, false, false, false>;   \
+    if (v.peak) kern = cplx ? k4_xifft_mag2<N, true, false, true> : k4_xifft_mag2<N, false, false, true>; \
+    if (slab4d) kern = cplx ? k4_xifft_mag2<N, true, true, false> : k4_xifft_mag2<N, false, true, false>; \
     constexpr size_t smem = k4b2_smem<N, false>();                                                     \
     if (smem > 40 * 1024) {                                                                            \
       cudaError_t e0 = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
