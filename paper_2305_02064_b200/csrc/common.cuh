@@ -245,10 +245,12 @@ struct MidSlabOut {
 // liveb (or nullptr = every row): [nx] live-row bound of each column a, the
 // rows |m_s| <= liveb[a].  Forward (K2): only live rows
 // are stored.  Inverse (K4a): only live rows are read, the others are zero.
+// tm_st (or nullptr): a [32 rows][16] box map over `data` for TMA stores of
+// the transformed tiles (ny >= 256)
 template <int DIR>
 cudaError_t launch_mid(float2 *data, const float2 *tw, int F, int ny, int nx, int inner, cudaStream_t s,
                        const CUtensorMap *tm, int num_sms, const MidSlabOut *so = nullptr,
-                       const int *liveb = nullptr);
+                       const int *liveb = nullptr, const CUtensorMap *tm_st = nullptr);
 cudaError_t launch_k3(const SarDeviceView &v, bool ifft, cudaStream_t s, int num_sms);
 
 cudaError_t launch_k3_plane(const SarDeviceView &v, cudaStream_t s);

@@ -86,11 +86,15 @@ constexpr int mid2_ntc() { return N == 512 ? 512 : sarfft2::nt_fft<N, KC>(); }
 template <int N, int DIR>
 constexpr int mid2_rows() { return DIR < 0 ? (N < 256 ? N : 256) : (N < K4A_ROWS ? N : K4A_ROWS); }
 
-template <int N, int DIR, bool SLAB>
+// TST: the transformed tile is written back by TMA bulk-tensor stores of
+// [32 rows][16] boxes (tm_st) from the work tile instead of one STG per
+// element (the per-element 64-bit address arithmetic was a fifth of the
+// kernel's instructions); K2 stores only the boxes that hold live rows.
+template <int N, int DIR, bool SLAB, bool TST>
 __global__ void __launch_bounds__(mid2_ntc<N>() + 32)
     k_fft_mid2(const __grid_constant__ CUtensorMap tm, float2 *__restrict__ data, const float2 *__restrict__ twg,
                int nx, int inner, int nchunk, int nitems, const MidSlabOut so, const int *__restrict__ liveb,
-               int oob_row) {
+               int oob_row, const __grid_constant__ CUtensorMap tm_st) {
   constexpr int NTC = mid2_ntc<N>();
   constexpr int S = mid2_stages<N>();
   constexpr int ROWS = mid2_rows<N, DIR>();
@@ -164,15 +168,41 @@ __global__ void __launch_bounds__(mid2_ntc<N>() + 32)
     const int lb = (DIR < 0 && liveb) ? liveb[a] : N;
     const unsigned span = lb < 0 ? 0u : (2 * lb + 1 >= N ? (unsigned)N : (unsigned)(2 * lb + 1));
     const int lbo = lb < 0 ? 0 : lb;
-    sarfft2::fft_ctx<N, KC, KC, NTC, DIR, 1, false, (N == 512 ? 16 : 0), (N == 512)>(
+    if constexpr (TST) {
+      // the previous tile's bulk stores have finished reading `work` before
+      // this tile's pass 1 (after its barrier) writes it
+      if (tid == 0) sartma::bulk_wait_read0();
+    }
+    sarfft2::fft_ctx<N, KC, KC, NTC, DIR, 1, false, (N == 512 ? 16 : 0), (N == 512), false, TST>(
         work, tw, tid, [&](int c, int m) { return stage[m * KC + c]; },
         [&] {
           if (tid == 0) sartma::mbar_arrive(&empty[st]);
         },
         [](int c) { return c; },
         [&](int c, int m, float2 v) {
-          if (c < cmax && (DIR > 0 || (unsigned)((m + lbo) & (N - 1)) < span)) st_mid(base + (size_t)m * row + c, v);
+          if constexpr (TST) {
+            work[m * KC + c] = v;
+          } else {
+            if (c < cmax && (DIR > 0 || (unsigned)((m + lbo) & (N - 1)) < span))
+              st_mid(base + (size_t)m * row + c, v);
+          }
         });
+    if constexpr (TST) {
+      constexpr int SR = N < 32 ? N : 32;
+      sartma::fence_proxy_async();   // the tile's generic writes, then the bulk (async proxy) reads
+      sarfft2::sync<1, NTC>();
+      if (tid == 0) {
+#pragma unroll
+        for (int bx = 0; bx < N / SR; ++bx) {
+          const bool live = DIR > 0 || (lb >= 0 && (bx * SR <= lb || (bx + 1) * SR - 1 >= N - lb));
+          if (live) sartma::tma_store_3d(&tm_st, chunk * KC, a, f * N + bx * SR, work + bx * SR * KC);
+        }
+        sartma::bulk_commit();
+      }
+    }
+  }
+  if constexpr (TST) {
+    if (tid == 0) sartma::bulk_wait0();
   }
 }
 
@@ -181,7 +211,8 @@ __global__ void __launch_bounds__(mid2_ntc<N>() + 32)
 
 template <int DIR>
 cudaError_t launch_mid(float2 *data, const float2 *tw, int F, int ny, int nx, int inner, cudaStream_t s,
-                       const CUtensorMap *tm, int num_sms, const MidSlabOut *so, const int *liveb) {
+                       const CUtensorMap *tm, int num_sms, const MidSlabOut *so, const int *liveb,
+                       const CUtensorMap *tm_st) {
   const MidSlabOut off{};
   if (so && !(tm && ny <= 512 && F == 1 && so->nzl % KC == 0)) return cudaErrorInvalidValue;
   if (tm && ny <= 512) {
@@ -191,9 +222,9 @@ cudaError_t launch_mid(float2 *data, const float2 *tw, int F, int ny, int nx, in
 #define X(N)                                                                                       \
   case N: {                                                                                        \
     void (*kern)(const CUtensorMap, float2 *, const float2 *, int, int, int, int, const MidSlabOut,    \
-                 const int *, int) =                                                              \
-        k_fft_mid2<N, DIR, false>;                                                                 \
-    if (so) kern = k_fft_mid2<N, DIR, true>;                                                       \
+                 const int *, int, const CUtensorMap) = k_fft_mid2<N, DIR, false, false>;           \
+    if (so) kern = k_fft_mid2<N, DIR, true, false>;                                                \
+    else if (tm_st && N >= 256) kern = k_fft_mid2<N, DIR, false, (N >= 256)>;                      \
     constexpr size_t smem = mid2_smem<N>();                                                        \
     if (smem > 40 * 1024) {                                                                        \
       cudaError_t e0 = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
@@ -202,7 +233,8 @@ cudaError_t launch_mid(float2 *data, const float2 *tw, int F, int ny, int nx, in
     const int occ = resident_ctas((const void *)kern, mid2_ntc<N>() + 32, smem);                  \
     const int maxg = num_sms * (occ < mid2_ctas<N>() ? occ : mid2_ctas<N>());                                                     \
     cudaError_t e = launch_ex(kern, dim3(nitems < maxg ? nitems : maxg), dim3(mid2_ntc<N>() + 32), smem, s, \
-                               *tm, data, tw, nx, inner, nchunk, nitems, so ? *so : off, liveb, 1 << 30); \
+                               *tm, data, tw, nx, inner, nchunk, nitems, so ? *so : off, liveb, 1 << 30, \
+                               tm_st ? *tm_st : *tm);                                              \
     if (e != cudaSuccess) return e;                                                                \
     return cudaGetLastError();                                                                     \
   }
@@ -232,8 +264,8 @@ cudaError_t launch_mid(float2 *data, const float2 *tw, int F, int ny, int nx, in
 
 
 template cudaError_t launch_mid<-1>(float2 *, const float2 *, int, int, int, int, cudaStream_t, const CUtensorMap *, int,
-                                    const MidSlabOut *, const int *);
+                                    const MidSlabOut *, const int *, const CUtensorMap *);
 template cudaError_t launch_mid<+1>(float2 *, const float2 *, int, int, int, int, cudaStream_t, const CUtensorMap *, int,
-                                    const MidSlabOut *, const int *);
+                                    const MidSlabOut *, const int *, const CUtensorMap *);
 
 }  // namespace sark

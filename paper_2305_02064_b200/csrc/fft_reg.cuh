@@ -226,8 +226,11 @@ __device__ __forceinline__ void build_tw2(float2 *tw2, const float2 *tw, int tid
   }
 }
 
+// SYNC_STORE: a barrier over the NT threads between the last read of `work`
+// and the first store() (one pass-2 butterfly per thread), so that store()
+// may write into `work` itself (e.g. a tile for a TMA store).
 template <int N, int C, int LDW, int NT, int DIR, int BARID, bool I_FAST2, int R1SEL = 0, bool SPLIT2 = false,
-          bool TW2 = false, typename Load, typename Loaded, typename Prep, typename Store>
+          bool TW2 = false, bool SYNC_STORE = false, typename Load, typename Loaded, typename Prep, typename Store>
 __device__ __forceinline__ void fft_ctx(float2 *__restrict__ work, const float2 *__restrict__ tw, int tid,
                                         Load &&load, Loaded &&loaded, Prep &&prep, Store &&store, int rbar = 0) {
   static_assert((N & (N - 1)) == 0 && N >= 2 && N <= 1024, "power-of-two length in [2, 1024]");
@@ -316,6 +319,10 @@ __device__ __forceinline__ void fft_ctx(float2 *__restrict__ work, const float2 
             }
           }
           dft<H, DIR>(g);
+          if constexpr (SYNC_STORE) {
+            static_assert(NB2 == NT, "SYNC_STORE: one pass-2 butterfly per thread");
+            sync<BARID, NT>(rbar);
+          }
           const auto ctx = prep(c);
           static_for<0, H>([&](auto P) {
             constexpr int p = decltype(P)::value;
@@ -343,6 +350,10 @@ __device__ __forceinline__ void fft_ctx(float2 *__restrict__ work, const float2 
           u[r] = mul(work[(i + r * R1) * LDW + c], w);
         }
         dft<R2, DIR>(u);
+        if constexpr (SYNC_STORE) {
+          static_assert(SPLIT2 || NB2 == NT, "SYNC_STORE: one pass-2 butterfly per thread");
+          sync<BARID, NT>(rbar);
+        }
         const auto ctx = prep(c);
         static_for<0, R2>([&](auto P) {
           constexpr int p = decltype(P)::value;
