@@ -122,29 +122,74 @@ def _dist():
     return rank, world, local
 
 
-def oracle_sample(sc, s_host, max_pairs=1, planes=None, nufft=False):
+def host_info():
+    """CPU model, logical cores and RAM of this host (for the cpu_baseline line)."""
+    model = None
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    ram = None
+    try:
+        import psutil
+        ram = round(psutil.virtual_memory().total / 2**30, 1)
+    except ImportError:
+        pass
+    return {"cpu_model": model, "cores": os.cpu_count(), "ram_GiB": ram}
+
+
+def oracle_sample(sc, s_host, planes=None, nufft=False):
     """Time the fp64 oracle (as it stands) on a bounded sample of the workload:
-    the first Tx/Rx channel(s) through the whole O1..O7 pipeline (the full-size
-    3-D RMA included; O5'-O7' for 2-D planes).  ``sc`` is the 3-D scene.
-    Returns (seconds, samples processed, cores)."""
+    Tx/Rx channel (0,0) through the whole path.  The oracle's per-channel
+    work (O1-O2 compensation + lattice accumulation; the NUFFT spread) and
+    its once-per-image work (FT_2D, filter, Stolt, IFT_3D, magnitude) are
+    timed separately, so the full image's oracle time is projected as
+    n_channels * t_channel + t_image.  ``sc`` is the 3-D scene, ``s_host``
+    its channel (0,0).  Returns a dict of the times (s) and the projection."""
     import oracle
-    sub = s_host[:, :1, :max_pairs]
-    geo = oracle.decompose(sc.tx[:1], sc.rx[:max_pairs], sc.scan, sc.npx, sc.npy, sc.x0, sc.y0, sc.dx, sc.dy,
+    geo = oracle.decompose(sc.tx[:1], sc.rx[:1], sc.scan, sc.npx, sc.npy, sc.x0, sc.y0, sc.dx, sc.dy,
                            sc.z0, sc.k, sc.nx, sc.ny, sc.nz, sc.dz_img, sc.z_ref)
+    sc1 = dataclasses.replace(sc, tx=sc.tx[:1], rx=sc.rx[:1])
     t0 = time.perf_counter()
-    if nufft and planes:
-        sc1 = dataclasses.replace(sc, tx=sc.tx[:1], rx=sc.rx[:max_pairs])
-        S, g1 = oracle.nufft.spectrum_nufft(sub, sc1)
-        oracle.magnitude_planes(oracle.ifft2_planes(oracle.plane_sum(oracle.rma_filter(S, g1), g1, planes)), g1)
-    elif nufft:
-        sc1 = dataclasses.replace(sc, tx=sc.tx[:1], rx=sc.rx[:max_pairs])
-        oracle.nufft.reconstruct_nufft(sub, sc1)
-    elif planes:
-        oracle.reconstruct_planes(sub, geo, planes)
+    if nufft:
+        S, g1 = oracle.nufft.spectrum_nufft(s_host, sc1)
+        t1 = time.perf_counter()
+        Fk = oracle.rma_filter(S, g1)
+        if planes:
+            oracle.magnitude_planes(oracle.ifft2_planes(oracle.plane_sum(Fk, g1, planes)), g1)
+        else:
+            oracle.magnitude_image(oracle.ifft3(oracle.stolt(Fk, g1)), g1)
     else:
-        oracle.reconstruct(sub, geo)
-    dt = time.perf_counter() - t0
-    return dt, int(np.prod(sub.shape)), os.cpu_count()
+        planar = oracle.compensate(s_host, geo)
+        t1 = time.perf_counter()
+        Fk = oracle.rma_filter(oracle.fft2(planar), geo)
+        if planes:
+            oracle.magnitude_planes(oracle.ifft2_planes(oracle.plane_sum(Fk, geo, planes)), geo)
+        else:
+            oracle.magnitude_image(oracle.ifft3(oracle.stolt(Fk, geo)), geo)
+    t2 = time.perf_counter()
+    nch = sc.n_tx * sc.n_rx
+    return {"t_channel": t1 - t0, "t_image": t2 - t1, "t_sample": t2 - t0, "n_channels": nch,
+            "t_projected": nch * (t1 - t0) + (t2 - t1), "samples_sample": int(np.prod(s_host.shape)),
+            "samples_image": sc.n_samples}
+
+
+def oracle_line(sc, name, res, planes=None, nufft=False):
+    """cpu_baseline object for an oracle_sample result."""
+    what = ("NUFFT spectrum + " if nufft else "O1-O2 + ") + \
+        (f"O3-O4, O5'-O7' on {len(planes)} plane(s)" if planes else
+         f"O3-O7 incl. the {sc.nx}x{sc.ny}x{sc.nz} RMA")
+    return dict(value=res["samples_image"] / res["t_projected"] / 1e9, unit=UNIT, kind="oracle",
+                **host_info(),
+                sample=(f"{name}: fp64 oracle ({what}) timed on Tx/Rx channel (0,0) "
+                        f"({res['samples_sample']} of {res['samples_image']} samples): per-channel part "
+                        f"{res['t_channel']:.3g} s, once-per-image part {res['t_image']:.3g} s; the full image "
+                        f"projected as {res['n_channels']} x {res['t_channel']:.3g} + {res['t_image']:.3g} = "
+                        f"{res['t_projected']:.3g} s (value = image samples / projected time)"),
+                seconds_measured=res["t_sample"], seconds_projected_full_image=res["t_projected"])
 
 
 def run_reference(args):
@@ -164,22 +209,21 @@ def run_reference(args):
         scenes.gpu.build()
         s = scenes.gpu.synthesize_gpu(sub).cpu().numpy()
     for _ in range(args.warmup):
-        oracle_sample(sub, s)
-    times = []
-    n = 0
+        oracle_sample(sc, s)
+    res = None
+    tproj = []
     for _ in range(args.steps):
-        dt, n, cores = oracle_sample(sub, s)
-        times.append(dt)
-    t = float(np.sum(times))
-    val = n * args.steps / t / 1e9
-    sample = (f"{args.config}: Tx/Rx channel (0,0) only ({n} of {sc.n_samples} samples) through the full "
-              f"oracle O1..O7 incl. the {sc.nx}x{sc.ny}x{sc.nz} RMA, per step")
+        res = oracle_sample(sc, s)
+        tproj.append(res["t_projected"])
+    t = float(np.sum(tproj))
+    val = sc.n_samples * args.steps / t / 1e9
+    cpu = oracle_line(sc, args.config, res)
+    sample = cpu["sample"]
     line = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": {"workload": args.config, "sample": sample},
-            "cpu_baseline": {"value": val, "unit": UNIT, "cores": os.cpu_count(), "kind": "oracle",
-                             "sample": sample},
+            "cpu_baseline": dict(cpu, value=val),
             "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -326,13 +370,15 @@ def run_ours(args):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         s_host = data[:, :1, :1].cpu().numpy()
-        sub = dataclasses.replace(sc3, tx=sc3.tx[:1], rx=sc3.rx[:1])
-        dt, n, cores = oracle_sample(sub, s_host, planes=planes, nufft=bool(gflag))
-        what = f"O1..O4 + O5'..O7' on {len(planes)} plane(s)" if planes else \
-            f"O1..O7 incl. the {sc.nx}x{sc.ny}x{sc.nz} RMA"
-        cpu = {"value": n / dt / 1e9, "unit": UNIT, "cores": cores, "kind": "oracle",
-               "sample": f"Tx/Rx channel (0,0) of {args.config} ({n} of {samples} samples) through the full "
-                         f"fp64 oracle {what}: {dt:.1f} s"}
+        res = oracle_sample(sc3, s_host, planes=planes, nufft=bool(gflag))
+        cpu = oracle_line(sc3, args.config, res, planes=planes, nufft=bool(gflag))
+
+    # parity of this configuration as last measured by the GPU parity suite
+    # (the full fp64 oracle on the host takes minutes: tests, not the bench)
+    parity = None
+    pp = os.path.join(ROOT, "profiles", f"{args.config}_parity.json")
+    if os.path.exists(pp) and not planes and not gflag:
+        parity = json.load(open(pp))
 
     if rank == 0:
         line = {
@@ -355,7 +401,7 @@ def run_ours(args):
             "roofline": roof,
             "stages": {n: {"ms": avg[i], "share": avg[i] / max(tot, 1e-12),
                            "alg_GBps": alg[i] / (max(avg[i], 1e-9) * 1e-3) / 1e9} for i, n in slots},
-            "cpu_baseline": cpu, "e2e": e2e,
+            "cpu_baseline": cpu, "e2e": e2e, "parity": parity,
             "gpu_launches": plan.launches_per_call() * args.steps,
             "clocks": clk.summary(),
         }

@@ -104,9 +104,27 @@ def _check_e2e(sc, flags=0, gpu_gen=None, geo=None, pulse=None):
     return got, want, e2, einf
 
 
+def _record_parity(name, e2, einf):
+    """profiles/<config>_parity.json: the config's last measured GPU-vs-oracle
+    errors (bench.py reports them with its line); a copy goes to gpurun_out/."""
+    import json
+    import os
+    import time
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    rec = {"config": name, "eps2": float(e2), "epsinf": float(einf), "bar": {"eps2": E2_BAR, "epsinf": EINF_BAR},
+           "source": "tests/test_gpu_parity.py (full fp64 oracle on the host, same input bytes)",
+           "gpu": torch.cuda.get_device_name(0), "when": time.strftime("%Y-%m-%dT%H:%M:%SZ", time.gmtime())}
+    for d in ("profiles", "gpurun_out"):
+        path = os.path.join(root, d)
+        if os.path.isdir(path):
+            with open(os.path.join(path, f"{name}_parity.json"), "w") as fh:
+                json.dump(rec, fh, indent=1)
+
+
 @pytest.mark.parametrize("name", ["tiny", "small", "freehand", "realtime"])
 def test_end_to_end(name):
-    _check_e2e(scenes.make_scene(name))
+    _, _, e2, einf = _check_e2e(scenes.make_scene(name))
+    _record_parity(name, e2, einf)
 
 
 @pytest.fixture(scope="module")
@@ -129,6 +147,7 @@ def test_end_to_end_large_bench_configuration(large_case):
         got = plan.reconstruct(d).cpu().numpy()
     e2, einf = errs(got, want)
     assert e2 <= E2_BAR and einf <= EINF_BAR, (e2, einf)
+    _record_parity("large", e2, einf)
 
 
 @pytest.mark.slow
