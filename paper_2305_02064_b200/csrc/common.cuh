@@ -35,7 +35,10 @@ constexpr int minb_for(int n) { return n >= 1024 ? 1 : 1024 / nt_for(n); }
 constexpr int K1_STAGES = K1_STAGES_;        // TMA ring stages of K1
 constexpr int K1_BOX_BYTES = K1_BOX_BYTES_;  // raw-sample bytes per TMA box
 constexpr int K1_NT = 512;   // consumer threads (+1 producer warp)
-constexpr int K1_KT = 4;  // consecutive k per thread
+#ifndef K1_KT_
+#define K1_KT_ 4
+#endif
+constexpr int K1_KT = K1_KT_;  // consecutive k per thread (one SFU sincos + step phasor per K1_KT samples)
 
 constexpr int k1c_for(int nx) { return nx >= 256 ? 16 : 64; }
 

@@ -209,7 +209,7 @@ __global__ void __launch_bounds__(K1_NT + 32, 1)
   }
 
   // ---------------- consumers: 512 threads ----------------
-  const int kq = (tid % TPR) * K1_KT;   // first of this thread's 4 k within the chunk
+  const int kq = (tid % TPR) * K1_KT;   // first of this thread's K1_KT k within the chunk
   const int r0 = tid / TPR;            // first of this thread's box rows
   const int lane = tid & 31, warp = tid >> 5;
   const float dkt = (float)(v.dk);
@@ -237,17 +237,19 @@ __global__ void __launch_bounds__(K1_NT + 32, 1)
         const float *sap = reinterpret_cast<const float *>(stages + st * STAGE + K1_BOX_BYTES);
         // the warp's rows of the box go to registers and the stage is handed
         // back before the rotation, so the producer refills it meanwhile
-        float4 r01[UPB], r23[UPB];
+        constexpr int NV = K1_KT / 2;   // float4 (2 samples) per row and thread
+        float4 rv[UPB][NV];
         float rbeta[UPB];
 #pragma unroll
         for (int w = 0; w < UPB; ++w) {
           const int il = r0 + w * RPP;
           const int ix = b * br + il;
-          r01[w] = r23[w] = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+          for (int q = 0; q < NV; ++q) rv[w][q] = make_float4(0.f, 0.f, 0.f, 0.f);
           rbeta[w] = 0.f;
           if (il < br && ix < v.npx) {
-            r01[w] = *reinterpret_cast<const float4 *>(sv + il * C + kq);
-            r23[w] = *reinterpret_cast<const float4 *>(sv + il * C + kq + 2);
+#pragma unroll
+            for (int q = 0; q < NV; ++q) rv[w][q] = *reinterpret_cast<const float4 *>(sv + il * C + kq + 2 * q);
             rbeta[w] = sap[il];
           }
         }
@@ -261,9 +263,12 @@ __global__ void __launch_bounds__(K1_NT + 32, 1)
           const int il = r0 + w * RPP;
           const int ix = b * br + il;
           if (il < br && ix < v.npx) {
-            const float4 v01 = r01[w], v23 = r23[w];
-            float2 val[4] = {make_float2(v01.x, v01.y), make_float2(v01.z, v01.w), make_float2(v23.x, v23.y),
-                             make_float2(v23.z, v23.w)};
+            float2 val[K1_KT];
+#pragma unroll
+            for (int q = 0; q < NV; ++q) {
+              val[2 * q] = make_float2(rv[w][q].x, rv[w][q].y);
+              val[2 * q + 1] = make_float2(rv[w][q].z, rv[w][q].w);
+            }
             if (!v.no_comp) {
               const float beta = rbeta[w] + bp;
               float turns = beta * kt;
