@@ -65,8 +65,11 @@ __global__ void __launch_bounds__(nt_for(N), minb_for(N))
 // the two-pass register FFT (fft_reg.cuh), hand the stage back right after
 // the pass-1 loads, and store the transformed rows straight to global memory
 // (each warp store = two full 128-byte lines).
+#ifndef MID_S_SMALL
+#define MID_S_SMALL 6   // ring stages of the mid-axis FFT below N = 256 (Realtime K2 0.41 -> 0.38 ms, K4a 0.20 -> 0.17)
+#endif
 template <int N>
-constexpr int mid2_stages() { return N >= 256 ? 2 : 4; }
+constexpr int mid2_stages() { return N >= 256 ? 2 : MID_S_SMALL; }
 template <int N>
 constexpr size_t mid2_smem() {
   return ((size_t)mid2_stages<N>() * N * KC + (size_t)N * KC + N) * sizeof(float2);
