@@ -68,9 +68,15 @@ enum sar_flags {
                                     lattice + FFT.  Needs nx <= 512, npx <= 512; debug stage 1 is
                                     not available (there is no lattice).  Combines with
                                     SAR_IMAGE_2D (NUFFT spectrum, then the plane sums) */,
-  SAR_FORCE_PLAIN = 1u << 6      /* testing: run the plain (non-TMA, non-persistent) kernel of every
+  SAR_FORCE_PLAIN = 1u << 6,     /* testing: run the plain (non-TMA, non-persistent) kernel of every
                                     stage instead of the TMA-pipelined ones; same arithmetic, results
                                     equal to fp32 rounding (the coverage of the fallback kernels) */
+  SAR_CUDA_GRAPH = 1u << 7       /* replay the call's launches as one CUDA graph (for small, launch-bound
+                                    configurations): the first sar_reconstruct with a given
+                                    (d_data, d_image) pair records the path into a graph on a stream of
+                                    the plan's own, later calls with the same pair launch that graph on
+                                    the caller's stream (a new pair re-records); same kernels, same
+                                    results.  Not combined with SAR_PROFILE_STAGES */
 };
 
 /* Limits of this build. */

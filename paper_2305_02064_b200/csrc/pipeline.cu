@@ -194,6 +194,97 @@ static bool encode2d(CUtensorMap *m, const void *base, CUtensorMapDataType dt, u
   return r == CUDA_SUCCESS;
 }
 
+// ------------------------------------------------------- CUDA graphs ----
+// SAR_CUDA_GRAPH.  The library links the static CUDA runtime while PyTorch
+// loads its own shared one, and the runtime's stream capture failed in that
+// arrangement (round 1); the capture and the graph calls here go straight to
+// the driver (entry points looked up once), on a non-blocking stream of the
+// plan, so the legacy default stream of the caller is never captured.
+namespace {
+struct GraphApi {
+  CUresult (*begin)(CUstream, CUstreamCaptureMode) = nullptr;
+  CUresult (*end)(CUstream, CUgraph *) = nullptr;
+  CUresult (*inst)(CUgraphExec *, CUgraph, unsigned long long) = nullptr;
+  CUresult (*launch)(CUgraphExec, CUstream) = nullptr;
+  CUresult (*gdestroy)(CUgraph) = nullptr;
+  CUresult (*edestroy)(CUgraphExec) = nullptr;
+  bool ok = false;
+};
+const GraphApi &graph_api() {
+  static GraphApi g;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    auto get = [](const char *name, void **fn) {
+      cudaDriverEntryPointQueryResult q;
+      return cudaGetDriverEntryPoint(name, fn, cudaEnableDefault, &q) == cudaSuccess &&
+             q == cudaDriverEntryPointSuccess && *fn;
+    };
+    g.ok = get("cuStreamBeginCapture", (void **)&g.begin) && get("cuStreamEndCapture", (void **)&g.end) &&
+           get("cuGraphInstantiateWithFlags", (void **)&g.inst) && get("cuGraphLaunch", (void **)&g.launch) &&
+           get("cuGraphDestroy", (void **)&g.gdestroy) && get("cuGraphExecDestroy", (void **)&g.edestroy);
+  }
+  return g;
+}
+}  // namespace
+
+void sar_graph_destroy(sar_plan *p) {
+  if (p->graph_exec) {
+    const GraphApi &g = graph_api();
+    if (g.ok) g.edestroy(static_cast<CUgraphExec>(p->graph_exec));
+    p->graph_exec = nullptr;
+  }
+}
+
+int sar_graph_reconstruct(sar_plan *p, const void *d_data, void *d_image, cudaStream_t s) {
+  const GraphApi &g = graph_api();
+  if (!g.ok) {
+    sar_set_error("CUDA graph driver entry points unavailable");
+    return SAR_ERR_UNSUPPORTED;
+  }
+  if (!p->graph_exec || p->g_data != d_data || p->g_image != d_image) {
+    sar_graph_destroy(p);
+    // the capture stream must not overlap work the caller's stream still
+    // has in flight on the plan's workspace
+    cudaError_t e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) {
+      sar_set_error(std::string("CUDA: ") + cudaGetErrorString(e));
+      return SAR_ERR_CUDA;
+    }
+    CUstream cs = reinterpret_cast<CUstream>(p->cap_stream);
+    if (g.begin(cs, CU_STREAM_CAPTURE_MODE_THREAD_LOCAL) != CUDA_SUCCESS) {
+      sar_set_error("cuStreamBeginCapture failed");
+      return SAR_ERR_CUDA;
+    }
+    const int st = sar_enqueue_call(p, d_data, d_image, p->cap_stream);
+    CUgraph graph = nullptr;
+    const CUresult ce = g.end(cs, &graph);
+    if (st != SAR_OK) {
+      if (graph) g.gdestroy(graph);
+      return st;
+    }
+    if (ce != CUDA_SUCCESS || !graph) {
+      sar_set_error("cuStreamEndCapture failed");
+      return SAR_ERR_CUDA;
+    }
+    CUgraphExec exec = nullptr;
+    const CUresult ie = g.inst(&exec, graph, 0);
+    g.gdestroy(graph);
+    if (ie != CUDA_SUCCESS) {
+      sar_set_error("cuGraphInstantiate failed");
+      return SAR_ERR_CUDA;
+    }
+    p->graph_exec = exec;
+    p->g_data = d_data;
+    p->g_image = d_image;
+  }
+  if (g.launch(static_cast<CUgraphExec>(p->graph_exec), reinterpret_cast<CUstream>(s)) != CUDA_SUCCESS) {
+    sar_set_error("cuGraphLaunch failed");
+    return SAR_ERR_CUDA;
+  }
+  return SAR_OK;
+}
+
 // raw samples viewed as [F*n_tx*n_rx*P rows][n_k] complex64, box [br rows][16]
 bool sar_encode_input_map(sar_plan *p, const void *d_data) {
   const SarDeviceView &v = p->v;

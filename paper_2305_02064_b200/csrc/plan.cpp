@@ -53,6 +53,8 @@ void free_plan(sar_plan *p) {
   // the plan's work was enqueued on last_stream (NULL = the legacy default
   // stream, whose synchronisation is what that stream promises)
   cudaStreamSynchronize(p->last_stream);
+  sar_graph_destroy(p);
+  if (p->cap_stream) cudaStreamDestroy(p->cap_stream);
   if (p->prof_events)
     for (int i = 0; i < SAR_PROFILE_RING; ++i)
       for (int j = 0; j <= SAR_N_STAGES; ++j) cudaEventDestroy(p->ev[i][j]);
@@ -677,6 +679,13 @@ int plan_create_impl(sar_plan **out, const sar_geom_desc *g, const sar_image_des
 
   p->num_sms = prop.multiProcessorCount;
   sar_build_tensor_maps(p);
+  if (flags & SAR_CUDA_GRAPH) {
+    if (cudaStreamCreateWithFlags(&p->cap_stream, cudaStreamNonBlocking) != cudaSuccess) {
+      cudaGetLastError();
+      free_plan(p);
+      return fail(SAR_ERR_CUDA, "capture stream creation failed");
+    }
+  }
   if (flags & SAR_PROFILE_STAGES) {
     for (int i = 0; i < SAR_PROFILE_RING; ++i)
       for (int j = 0; j <= SAR_N_STAGES; ++j) cudaEventCreate(&p->ev[i][j]);
@@ -711,7 +720,7 @@ int sar_plan_create_slab(sar_plan **out, const sar_geom_desc *g, const sar_image
   if (!slab || !g || !im) return fail(SAR_ERR_INVALID_ARG, "slab, geometry or image descriptor is NULL");
   const int G = slab->world, r = slab->rank;
   if (G < 1 || G > SAR_MAX_SLAB || r < 0 || r >= G) return fail(SAR_ERR_INVALID_ARG, "slab rank/world out of range");
-  if (flags & (SAR_IMAGE_2D | SAR_GRID_NUFFT | SAR_REPORT_PEAK))
+  if (flags & (SAR_IMAGE_2D | SAR_GRID_NUFFT | SAR_REPORT_PEAK | SAR_CUDA_GRAPH))
     return fail(SAR_ERR_UNSUPPORTED, "slab plans support the 3-D RASTER path only");
   if (g->n_frames != 1) return fail(SAR_ERR_INVALID_ARG, "slab plans reconstruct one image (n_frames == 1)");
   if (im->nx % G || im->ny % G || im->nz % G || im->nx / G < 1 || im->nz / G < 1)
@@ -794,6 +803,26 @@ int sar_slab_stage_peers(sar_plan *p, int32_t stage, const void *d_in, void *con
   return sar_slab_launch(p, stage, d_in, nullptr, nullptr, s, peer_recv);
 }
 
+}  // extern "C"
+
+// the launches of one call (all frame waves) on s
+int sar_enqueue_call(sar_plan *p, const void *d_data, void *d_image, cudaStream_t s) {
+  const int cplx = (p->flags & SAR_OUTPUT_COMPLEX) ? 1 : 0;
+  if (p->d_peak) {
+    cudaError_t e = cudaMemsetAsync(p->d_peak, 0, (size_t)p->F * sizeof(unsigned), s);
+    if (e != cudaSuccess) return cuda_fail(e, "peak reset");
+  }
+  const size_t frame_img = (size_t)p->nz * p->ny * p->nx * (cplx ? sizeof(float2) : sizeof(float));
+  for (int f0 = 0; f0 < p->F; f0 += p->wave) {
+    const int st = sar_launch_pipeline(p, d_data, static_cast<char *>(d_image) + (size_t)f0 * frame_img, s, 0, cplx,
+                                       nullptr, f0, std::min(p->wave, p->F - f0));
+    if (st != SAR_OK) return st;
+  }
+  return SAR_OK;
+}
+
+extern "C" {
+
 int sar_reconstruct(sar_plan *p, const void *d_data, void *d_image, sar_stream stream) {
   if (!p) return fail(SAR_ERR_INVALID_ARG, "plan is NULL");
   if (p->slab_world) return fail(SAR_ERR_INVALID_ARG, "slab plans run sar_slab_stage");
@@ -802,6 +831,7 @@ int sar_reconstruct(sar_plan *p, const void *d_data, void *d_image, sar_stream s
   DeviceGuard g(p->device);
   cudaStream_t s = (cudaStream_t)stream;
   p->last_stream = s;
+  if ((p->flags & SAR_CUDA_GRAPH) && !p->prof_events) return sar_graph_reconstruct(p, d_data, d_image, s);
   const int cplx = (p->flags & SAR_OUTPUT_COMPLEX) ? 1 : 0;
   if (p->d_peak) {
     cudaError_t e = cudaMemsetAsync(p->d_peak, 0, (size_t)p->F * sizeof(unsigned), s);

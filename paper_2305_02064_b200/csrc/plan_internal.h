@@ -123,7 +123,12 @@ struct sar_plan {
   int k1_br = 0;                   // pose rows per K1 TMA box
   bool k1_regacc = false;          // every j^x offset is 0: K1 sums in registers
   int num_sms = 148;
-  // slab decomposition (sar_plan_create_slab); slab_world == 0: whole image
+  // SAR_CUDA_GRAPH: the recorded call and the (data, image) pair it was recorded for
+  cudaStream_t cap_stream = nullptr;
+  void *graph_exec = nullptr;   // CUgraphExec
+  const void *g_data = nullptr;
+  void *g_image = nullptr;
+  // slab decomposition (sar_slab_create_slab); slab_world == 0: whole image
   int slab_rank = 0, slab_world = 0;
   SarClass *d_slab_cls = nullptr;
   int slab_ncls = 0;
@@ -138,6 +143,12 @@ struct sar_plan {
 };
 
 // pipeline.cu
+// SAR_CUDA_GRAPH: record the whole call (all frame waves) on p->cap_stream and
+// launch it on s
+int sar_graph_reconstruct(sar_plan *p, const void *d_data, void *d_image, cudaStream_t s);
+// plan.cpp: the launches of one call (all frame waves) on s
+int sar_enqueue_call(sar_plan *p, const void *d_data, void *d_image, cudaStream_t s);
+void sar_graph_destroy(sar_plan *p);
 int sar_launch_pipeline(sar_plan *p, const void *d_data, void *d_image, cudaStream_t s,
                         int stop_stage /*0 = full*/, int complex_out, cudaEvent_t *ev /*6 or null*/, int f0,
                         int nf);

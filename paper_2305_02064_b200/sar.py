@@ -23,6 +23,7 @@ SAR_IMAGE_2D = 8
 SAR_GRID_NUFFT = 16
 SAR_REPORT_PEAK = 32
 SAR_FORCE_PLAIN = 64
+SAR_CUDA_GRAPH = 128
 STAGE_NAMES = ("K1 correct+x-FFT", "K2 y-FFT", "K3 filter+Stolt+z-IFFT", "K4a y-IFFT", "K4b x-IFFT+|.|")
 
 

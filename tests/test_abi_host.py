@@ -44,6 +44,16 @@ def test_library_exports_every_declared_symbol():
     assert lib.sar_version() == 4
 
 
+def test_library_has_no_unresolved_own_symbols():
+    """Every symbol the library needs comes from libc/libstdc++/libdl (the CUDA
+    runtime is linked statically): a C/C++ linkage mismatch between two
+    translation units would otherwise only fail at load time on the GPU box."""
+    out = subprocess.run(["nm", "-D", "--undefined-only", sar.LIB_PATH], capture_output=True, text=True).stdout
+    bad = [ln.split()[-1] for ln in out.splitlines()
+           if ln.strip() and not ln.strip().startswith("w ") and "@" not in ln.split()[-1]]
+    assert not bad, bad
+
+
 def test_no_oracle_in_product_path():
     """The product package never imports the oracle (test infrastructure)."""
     pkg = os.path.join(ROOT, "paper_2305_02064_b200")
