@@ -12,6 +12,10 @@
 
 #include "common.cuh"
 
+#ifndef K1_GROUPS
+#define K1_GROUPS 2
+#endif
+
 namespace sark {
 namespace {
 
@@ -150,17 +154,24 @@ __device__ __forceinline__ bool k1_next(const SarDeviceView &v, K1Job &j, int ni
   }
 }
 
-template <int NX, bool REGACC, bool SLAB>
+// NG = 2 (REGACC with two boxes per pose row): the consumer warps form two
+// groups, group g takes the jobs of box g (every other job, its own two ring
+// stages), so the halves of a row advance independently instead of every
+// stage waiting for all 16 warps.
+template <int NX, bool REGACC, bool SLAB, int NG>
 __global__ void __launch_bounds__(K1_NT + 32, 1)
     k1_correct_xfft_tma(const SarDeviceView v, const __grid_constant__ CUtensorMap tm_s,
                         const __grid_constant__ CUtensorMap tm_ap, int br, int nbox, int nitems) {
   constexpr int C = k1c_for(NX);
   constexpr int BRMAX = K1_BOX_BYTES / (C * 8);
   constexpr int TPR = C / K1_KT;                 // consumer threads per box row
-  constexpr int RPP = K1_NT / TPR;               // box rows per consumer pass
+  constexpr int GT = K1_NT / NG;                 // consumer threads per group
+  constexpr int RPP = GT / TPR;                  // box rows per consumer pass
   constexpr int UPB = BRMAX / RPP;               // box rows per consumer thread
   constexpr int MAXB = NX / BRMAX > 0 ? NX / BRMAX : 1;  // boxes per pose row (<= 2)
-  constexpr int NWARP = K1_NT / 32;
+  constexpr int NB = NG == 2 ? 1 : MAXB;         // boxes a thread accumulates
+  static_assert(NG == 1 || (REGACC && MAXB == 2 && K1_STAGES % 2 == 0), "two groups: REGACC, two boxes");
+  constexpr int NWARP = K1_NT / 32 / NG;         // arrivals per stage
   extern __shared__ __align__(128) unsigned char smraw[];
   float2 *tile = reinterpret_cast<float2 *>(smraw);                       // [NX][C]
   unsigned char *stages = smraw + (size_t)NX * C * sizeof(float2);
@@ -209,9 +220,11 @@ __global__ void __launch_bounds__(K1_NT + 32, 1)
   }
 
   // ---------------- consumers: 512 threads ----------------
-  const int kq = (tid % TPR) * K1_KT;   // first of this thread's K1_KT k within the chunk
-  const int r0 = tid / TPR;            // first of this thread's box rows
-  const int lane = tid & 31, warp = tid >> 5;
+  const int g = NG == 2 ? tid / GT : 0;        // group: the box it accumulates (NG = 2)
+  const int gtid = tid - g * GT;
+  const int kq = (gtid % TPR) * K1_KT;  // first of this thread's K1_KT k within the chunk
+  const int r0 = gtid / TPR;           // first of this thread's box rows
+  const int lane = tid & 31;
   const float dkt = (float)(v.dk);
   unsigned jobctr = 0;
   for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
@@ -220,9 +233,9 @@ __global__ void __launch_bounds__(K1_NT + 32, 1)
     const int vy = v.vy0 + vyl;
     const int k0 = kc * C + kq;
     const float kt = k0 < v.nk ? __ldg(v.kturn + k0) : 0.f;
-    float2 acc[REGACC ? MAXB * UPB * K1_KT : 1];
+    float2 acc[REGACC ? NB * UPB * K1_KT : 1];
 #pragma unroll
-    for (int u = 0; u < (REGACC ? MAXB * UPB * K1_KT : 1); ++u) acc[u] = make_float2(0.f, 0.f);
+    for (int u = 0; u < (REGACC ? NB * UPB * K1_KT : 1); ++u) acc[u] = make_float2(0.f, 0.f);
     for (int pr = 0; pr < v.npair; ++pr) {
       if (!k1_pair_valid(v, vy, pr)) continue;
       const float bp = v.bpair[(f + v.f0) * v.npair + pr];
@@ -231,8 +244,10 @@ __global__ void __launch_bounds__(K1_NT + 32, 1)
       for (int b = 0; b < MAXB; ++b) {
         if (b >= nbox) break;
         const int st = jobctr % K1_STAGES;
-        sartma::mbar_wait(&full[st], (jobctr / K1_STAGES) & 1);
+        const unsigned ph = (jobctr / K1_STAGES) & 1;
         ++jobctr;
+        if (NG == 2 && b != g) continue;   // the other group's job
+        sartma::mbar_wait(&full[st], ph);
         const float2 *sv = reinterpret_cast<const float2 *>(stages + st * STAGE);
         const float *sap = reinterpret_cast<const float *>(stages + st * STAGE + K1_BOX_BYTES);
         // the warp's rows of the box go to registers and the stage is handed
@@ -287,7 +302,8 @@ __global__ void __launch_bounds__(K1_NT + 32, 1)
             if constexpr (REGACC) {
 #pragma unroll
               for (int u = 0; u < K1_KT; ++u)
-                acc[(b * UPB + w) * K1_KT + u] = __fadd2_rn(acc[(b * UPB + w) * K1_KT + u], val[u]);
+                acc[((NG == 2 ? 0 : b) * UPB + w) * K1_KT + u] =
+                    __fadd2_rn(acc[((NG == 2 ? 0 : b) * UPB + w) * K1_KT + u], val[u]);
             } else {
               int vx = ix + jx;
               if (vx >= NX) vx -= NX;
@@ -303,14 +319,15 @@ __global__ void __launch_bounds__(K1_NT + 32, 1)
     if constexpr (REGACC) {
       // vx = ix for every pair: scatter the register sums into the tile
 #pragma unroll
-      for (int b = 0; b < MAXB; ++b)
+      for (int bb = 0; bb < NB; ++bb)
 #pragma unroll
         for (int w = 0; w < UPB; ++w) {
+          const int b = NG == 2 ? g : bb;
           const int il = r0 + w * RPP;
           const int ix = b * br + il;
           if (b < nbox && il < br && ix < NX)
 #pragma unroll
-            for (int u = 0; u < K1_KT; ++u) tile[ix * C + kq + u] = acc[(b * UPB + w) * K1_KT + u];
+            for (int u = 0; u < K1_KT; ++u) tile[ix * C + kq + u] = acc[(bb * UPB + w) * K1_KT + u];
         }
       // rows not covered by any box (npx < NX) are zero
       for (int i = nbox * br * C + tid; i < NX * C; i += K1_NT) tile[i] = make_float2(0.f, 0.f);
@@ -368,8 +385,10 @@ cudaError_t launch_k1(const SarDeviceView &v, const float2 *data, bool fft, cuda
     switch (v.nx) {
 #define X(N)                                                                                          \
   case N: {                                                                                           \
-    auto kern = v.slab_lg >= 0 ? (regacc ? k1_correct_xfft_tma<N, true, true> : k1_correct_xfft_tma<N, false, true>) \
-                               : (regacc ? k1_correct_xfft_tma<N, true, false> : k1_correct_xfft_tma<N, false, false>); \
+    auto kern = v.slab_lg >= 0 ? (regacc ? k1_correct_xfft_tma<N, true, true, 1> : k1_correct_xfft_tma<N, false, true, 1>) \
+                               : (regacc ? k1_correct_xfft_tma<N, true, false, 1> : k1_correct_xfft_tma<N, false, false, 1>); \
+    if (K1_GROUPS == 2 && N == 512 && k1c_for(N) == 16 && regacc && nbox == 2 && v.slab_lg < 0)     \
+      kern = k1_correct_xfft_tma<N, true, false, (N == 512 && K1_GROUPS == 2) ? 2 : 1>;               \
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
     if (e != cudaSuccess) return e;                                                                   \
     e = launch_ex(kern, dim3(grid), dim3(K1_NT + 32), smem, s, v, *tm_s, *tm_ap, br, nbox, nitems);       \
