@@ -13,8 +13,9 @@ from scenes import gpu as sgpu  # noqa: E402
 import paper_2305_02064_b200 as sar  # noqa: E402
 from paper_2305_02064_b200 import sar as sarmod  # noqa: E402
 
-name = sys.argv[1]
+name, _, mode = sys.argv[1].partition(":")   # CONFIG or CONFIG:nufft
 sc = scenes.make_scene(name)
+mflags = sar.SAR_GRID_NUFFT if mode == "nufft" else 0
 sgpu.build()
 d = sgpu.synthesize_gpu(sc)
 ref = None
@@ -22,7 +23,7 @@ for spec in sys.argv[2:]:
     tag, _, path = spec.partition(":")
     sarmod._lib = None
     sarmod.load_library(path or sarmod.LIB_PATH)
-    with sar.Plan.from_scene(sc, flags=sar.SAR_PROFILE_STAGES) as plan:
+    with sar.Plan.from_scene(sc, flags=sar.SAR_PROFILE_STAGES | mflags) as plan:
         for _ in range(3):
             img = plan.reconstruct(d)
         torch.cuda.synchronize()
