@@ -387,8 +387,8 @@ cudaError_t launch_k1(const SarDeviceView &v, const float2 *data, bool fft, cuda
   case N: {                                                                                           \
     auto kern = v.slab_lg >= 0 ? (regacc ? k1_correct_xfft_tma<N, true, true, 1> : k1_correct_xfft_tma<N, false, true, 1>) \
                                : (regacc ? k1_correct_xfft_tma<N, true, false, 1> : k1_correct_xfft_tma<N, false, false, 1>); \
-    if (K1_GROUPS == 2 && N == 512 && k1c_for(N) == 16 && regacc && nbox == 2 && v.slab_lg < 0)     \
-      kern = k1_correct_xfft_tma<N, true, false, (N == 512 && K1_GROUPS == 2) ? 2 : 1>;               \
+    if (K1_GROUPS == 2 && (N == 512 || N == 128) && regacc && nbox == 2 && v.slab_lg < 0)            \
+      kern = k1_correct_xfft_tma<N, true, false, ((N == 512 || N == 128) && K1_GROUPS == 2) ? 2 : 1>; \
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
     if (e != cudaSuccess) return e;                                                                   \
     e = launch_ex(kern, dim3(grid), dim3(K1_NT + 32), smem, s, v, *tm_s, *tm_ap, br, nbox, nitems);       \

@@ -544,12 +544,18 @@ namespace {
 
 cudaError_t launch_k3(const SarDeviceView &v, bool ifft, cudaStream_t s, int num_sms) {
   if (v.ncls == 0) return cudaSuccess;   // every column skipped (zero Stolt output)
-  if ((v.nk & 1) == 0 && v.nz >= 128 && !v.force_plain) {
+#ifndef K3PP_64
+#define K3PP_64 0   // classes per item of k3_pp at n_z = 64 (0: k3_class there)
+#endif
+  if ((v.nk & 1) == 0 && (v.nz >= 128 || (K3PP_64 && v.nz == 64)) && !v.force_plain) {
     // n_z >= 256: 2 classes (<= 8 columns) per item; n_z = 128: 4 classes
     // (Freehand 0.065 -> 0.055 ms; at n_z = 64 k3_class stays faster:
     // Realtime 0.37 vs 0.43 ms with 8 classes per item)
     cudaError_t e = cudaSuccess;
     switch (v.nz) {
+      case 64:
+        if (try_k3pp<64, (K3PP_64 ? K3PP_64 : 4)>(v, ifft, s, num_sms, &e)) return e;
+        break;
       case 128:
         if (try_k3pp<128, 4>(v, ifft, s, num_sms, &e)) return e;
         break;
