@@ -408,6 +408,287 @@ __global__ void __launch_bounds__(K3P_NG * K3P_G + 32, 1) k3_pp(const SarDeviceV
                                 full, empty, colofs[g], slo[g], shi[g]);
 }
 
+// ------------------------------------------- K3, warp-specialised ----
+// k3_ws (n_z = 512): the same arithmetic as k3_pp, split over three roles
+// that run concurrently on every SM and hand work to each other through
+// mbarriers only (no CTA-wide barrier on the data path):
+//   * a producer warp fills an S-stage ring with the columns of the next
+//     items (2 Stolt mirror classes = up to 8 columns, one cp.async.bulk per
+//     column, as in k3_pp);
+//   * KW_WS "Stolt" warps take every item: the bit-exact fp64 pull and the
+//     filter at the two taps (readings R2-R5, R9), then the interpolated
+//     in-band rows of each member column into one of KW_B column buffers
+//     (out-of-band rows are masked later, never written); they hand the ring
+//     stage back and the buffer on;
+//   * 8 "FFT" warps, one per column slot of the buffer: each transforms its
+//     column along z on its own (two-pass register FFT, 16 x 32, only
+//     __syncwarp between the passes, pass 2 split over the lane halves) and
+//     stores it to W1 [col][z] with 256-byte warp stores.
+// A role waits only for the item it needs next, so the fp64 latency of the
+// Stolt warps, the FFT warps' shared-memory round trips and the ring's
+// transfer latency overlap instead of adding up behind barriers.
+#ifndef KW_S_
+#define KW_S_ 4
+#endif
+#ifndef KW_B_
+#define KW_B_ 2
+#endif
+#ifndef KW_WS_
+#define KW_WS_ 10
+#endif
+constexpr int KW_S = KW_S_;    // ring stages
+constexpr int KW_B = KW_B_;    // column buffers
+constexpr int KW_WS = KW_WS_;  // Stolt warps
+#ifndef KW_FS_
+#define KW_FS_ 1
+#endif
+constexpr int KW_WF = 8;    // FFT warps per set (= column slots of an item)
+constexpr int KW_FS = KW_FS_;   // FFT warp sets; set s takes the items n = s (mod KW_FS)
+constexpr int KW_CL = 2;    // mirror classes per item
+constexpr int KW_NT = 32 * (1 + KW_WS + KW_WF * KW_FS);
+// a buffer is always consumed by the same set (mbarrier parity waits cannot
+// tell phases two apart)
+static_assert(KW_B % KW_FS == 0, "k3_ws: the buffer count must be a multiple of the FFT set count");
+template <int NZ>
+struct KwGeom {
+  static constexpr int R1 = 16, R2 = NZ / 16;         // pass 1 radix 16 (R2 = 32 butterflies)
+  static constexpr int NZP = NZ + NZ / 16;             // padded column: m -> m + m/16
+  static constexpr int TW2 = sarfft2::tw2_size<NZ, 16, true>();
+  static constexpr size_t META = 128;                  // colof[8], slo[8], shi[8], f
+  static constexpr size_t BUF = META + (size_t)KW_WF * NZP * sizeof(float2);
+};
+__device__ __forceinline__ int kw_pad(int m) { return m + (m >> 4); }
+
+template <int NZ>
+size_t k3ws_smem(int nk) {
+  using G = KwGeom<NZ>;
+  const size_t hdr = (sizeof(K3Hdr<KW_CL>) + 15) & ~(size_t)15;
+  return KW_S * (hdr + (size_t)4 * KW_CL * nk * sizeof(float2)) + KW_B * G::BUF +
+         ((size_t)NZ + nk) * sizeof(double) + (size_t)G::TW2 * sizeof(float2);
+}
+
+template <int NZ>
+__global__ void __launch_bounds__(KW_NT, 1) k3_ws(const SarDeviceView v, int nitems_f) {
+  using G = KwGeom<NZ>;
+  constexpr int CL = KW_CL, CC = 4 * CL;
+  static_assert(CC == KW_WF, "one FFT warp per column slot");
+  static_assert(G::R2 == 32, "pass 1: one radix-16 butterfly per lane");
+  extern __shared__ __align__(16) unsigned char smw[];
+  const int nk = v.nk;
+  const size_t hdr_bytes = (sizeof(K3Hdr<CL>) + 15) & ~(size_t)15;
+  const size_t stage_bytes = hdr_bytes + (size_t)CC * nk * sizeof(float2);
+  unsigned char *ring = smw;
+  unsigned char *bufs = smw + KW_S * stage_bytes;
+  double *ks = reinterpret_cast<double *>(bufs + KW_B * G::BUF);   // [nk]
+  double *kzs = ks + nk;                                           // [NZ]
+  float2 *tw = reinterpret_cast<float2 *>(kzs + NZ);               // pass-2 rows
+  __shared__ __align__(8) uint64_t full[KW_S], empty[KW_S], full2[KW_B], empty2[KW_B];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  for (int i = tid; i < nk; i += KW_NT) ks[i] = v.k[i];
+  for (int i = tid; i < NZ; i += KW_NT) kzs[i] = v.kz[i];
+  sarfft2::build_tw2<NZ, 16, true>(tw, v.tw_z, tid, KW_NT);
+  if (tid == 0) {
+    for (int i = 0; i < KW_S; ++i) {
+      sartma::mbar_init(&full[i], 1);
+      sartma::mbar_init(&empty[i], 32 * KW_WS);
+    }
+    for (int i = 0; i < KW_B; ++i) {
+      sartma::mbar_init(&full2[i], 32 * KW_WS);
+      sartma::mbar_init(&empty2[i], 32 * KW_WF);
+    }
+    sartma::fence_barrier_init();
+  }
+  __syncthreads();
+  const int ncol = v.nx * v.ny;
+  const int nitems = nitems_f * v.F;
+  if (warp == 0) {
+    // ---- producer: as k3_pp (class entries one item ahead, one bulk copy per member column)
+    const int nclass = v.ncls;
+    auto fetch = [&](int item, SarClass &c) {
+      const int f = item / nitems_f;
+      const int q = (item - f * nitems_f) * CL + lane;
+      if (item < nitems && lane < CL && q < nclass) {
+        c = v.cls[q];
+      } else {
+        c.kr2 = 0.0;
+        c.jlo = 0;
+        c.jhi = -1;
+        c.nmem = 0;
+      }
+    };
+    SarClass cur, nxt;
+    fetch(blockIdx.x, cur);
+    unsigned n = 0;
+    for (int item = blockIdx.x; item < nitems; item += gridDim.x, ++n) {
+      fetch(item + gridDim.x, nxt);
+      const int st = n % KW_S;
+      if (lane == 0 && n >= KW_S) sartma::mbar_wait(&empty[st], ((n / KW_S) - 1) & 1);
+      __syncwarp();
+      unsigned char *sb = ring + st * stage_bytes;
+      K3Hdr<CL> &h = *reinterpret_cast<K3Hdr<CL> *>(sb);
+      float2 *fin = reinterpret_cast<float2 *>(sb + hdr_bytes);
+      const int f = item / nitems_f;
+      const int mine = lane < CL ? cur.nmem : 0;
+      int base = mine;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, base, o);
+        if (lane >= o) base += y;
+      }
+      const int cnt = __shfl_sync(0xffffffffu, base, CL - 1);
+      base -= mine;
+      if (lane < CL) {
+        h.kr2[lane] = cur.kr2;
+        h.jlo[lane] = cur.jlo;
+        h.jhi[lane] = cur.jhi;
+        h.nmem[lane] = cur.nmem;
+        for (int m = 0; m < cur.nmem; ++m) {
+          h.mslot[lane][m] = base + m;
+          h.clof[base + m] = lane;
+          h.colof[base + m] = cur.col[m];
+        }
+      }
+      if (lane == 0) {
+        h.nused = cnt;
+        h.f = f;
+        h.rr = v.rref[f + v.f0] * (1.0 / TWO_PI);
+      }
+      __syncwarp();
+      const bool ld = lane < cnt && h.jhi[h.clof[lane]] >= h.jlo[h.clof[lane]];
+      const int nld = __popc(__ballot_sync(0xffffffffu, ld));
+      if (lane == 0) sartma::mbar_arrive_expect_tx(&full[st], (uint32_t)nld * (uint32_t)nk * 8u);
+      __syncwarp();
+      const float2 *wf = v.w0 + (size_t)f * ncol * (size_t)nk;
+      if (ld) sartma::bulk_g2s(fin + lane * nk, wf + (size_t)h.colof[lane] * nk, (uint32_t)nk * 8u, &full[st]);
+      cur = nxt;
+    }
+    return;
+  }
+  if (warp <= KW_WS) {
+    // ---- Stolt warps: every item, (class, j) pairs strided over the KW_WS warps
+    const int st_t = tid - 32;
+    unsigned n = 0;
+    for (int item = blockIdx.x; item < nitems; item += gridDim.x, ++n) {
+      const int st = n % KW_S, b = n % KW_B;
+      sartma::mbar_wait(&full[st], (n / KW_S) & 1);
+      if (n >= KW_B) sartma::mbar_wait(&empty2[b], ((n / KW_B) - 1) & 1);
+      const unsigned char *sb = ring + st * stage_bytes;
+      const K3Hdr<CL> &h = *reinterpret_cast<const K3Hdr<CL> *>(sb);
+      const float2 *fin = reinterpret_cast<const float2 *>(sb + hdr_bytes);
+      unsigned char *bb = bufs + b * G::BUF;
+      int *meta = reinterpret_cast<int *>(bb);
+      float2 *cols = reinterpret_cast<float2 *>(bb + G::META);
+      const double rr = h.rr;
+      int tot = 0;
+#pragma unroll
+      for (int cl = 0; cl < CL; ++cl) tot += h.jhi[cl] - h.jlo[cl] + 1;
+      // an item has ~2 x 54 in-band pairs at Large (far fewer than Stolt
+      // threads): the first pair goes to a thread that rotates by 3 warps per
+      // item, so the fp64 chains of consecutive items run on different warps
+      // (each warp runs ahead to the items it has work in)
+      constexpr int NTS = 32 * KW_WS;
+      const int rot = (int)((n * 96u) % (unsigned)NTS);
+      const int t0 = st_t >= rot ? st_t - rot : st_t - rot + NTS;
+      for (int idx = t0; idx < tot; idx += NTS) {
+        int cl = 0, j = idx;
+#pragma unroll
+        for (int q = 0; q < CL - 1; ++q) {
+          const int len = h.jhi[cl] - h.jlo[cl] + 1;
+          if (j >= len) {
+            j -= len;
+            ++cl;
+          }
+        }
+        j += h.jlo[cl];
+        const double kr2 = h.kr2[cl];
+        int i0 = 0;
+        double tau = 0.0;
+        const bool ok = stolt_pull(kzs[j], kr2, v.k0, v.inv_dk, v.dk, nk, v.stolt_delta, &i0, &tau);
+        float2 wl = make_float2(0.f, 0.f), wu = wl;
+        if (ok) {
+          const float t = (float)tau;
+          const float2 hl = filter_h(v, ks[i0], kr2, rr, i0);
+          const float2 hu = filter_h(v, ks[i0 + 1], kr2, rr, i0 + 1);
+          wl = make_float2((1.f - t) * hl.x, (1.f - t) * hl.y);
+          wu = make_float2(t * hu.x, t * hu.y);
+        }
+        const int nm = h.nmem[cl];
+        for (int m = 0; m < nm; ++m) {
+          const int sl = h.mslot[cl][m];
+          float2 o = make_float2(0.f, 0.f);
+          if (ok) o = cmac2(cmul2(wl, fin[sl * nk + i0]), wu, fin[sl * nk + i0 + 1]);
+          cols[sl * G::NZP + kw_pad(j)] = o;
+        }
+      }
+      if (st_t < CC) {
+        const bool used = st_t < h.nused;
+        meta[st_t] = used ? h.colof[st_t] : -1;
+        meta[CC + st_t] = used ? h.jlo[h.clof[st_t]] : NZ;
+        meta[2 * CC + st_t] = used ? h.jhi[h.clof[st_t]] : -1;
+      }
+      if (st_t == 0) meta[3 * CC] = h.f;
+      // every lane's stage reads were consumed by its stores above; arrive
+      // (release) on both barriers
+      sartma::mbar_arrive(&empty[st]);
+      sartma::mbar_arrive(&full2[b]);
+    }
+    return;
+  }
+  // ---- FFT warps: warp w of set fs transforms column slot w of the set's items
+  const int fw = warp - 1 - KW_WS, fs = fw / KW_WF, w = fw - fs * KW_WF;
+  unsigned n = fs;
+  for (int item = blockIdx.x + fs * gridDim.x; item < nitems; item += KW_FS * gridDim.x, n += KW_FS) {
+    const int b = n % KW_B;
+    sartma::mbar_wait(&full2[b], (n / KW_B) & 1);
+    unsigned char *bb = bufs + b * G::BUF;
+    const int *meta = reinterpret_cast<const int *>(bb);
+    float2 *col = reinterpret_cast<float2 *>(bb + G::META) + w * G::NZP;
+    const int colof = meta[w], slo = meta[CC + w], shi = meta[2 * CC + w], f = meta[3 * CC];
+    if (colof >= 0) {
+      // pass 1: lane i, radix 16 over m = i + 32 r (rows outside [slo, shi] are zero)
+      float2 x[16];
+#pragma unroll
+      for (int r = 0; r < 16; ++r) {
+        const int m = lane + 32 * r;
+        x[r] = (m >= slo && m <= shi) ? col[kw_pad(m)] : make_float2(0.f, 0.f);
+      }
+      __syncwarp();
+      sarfft2::dft<16, +1>(x);
+      sarfft2::static_for<0, 16>([&](auto P) {
+        constexpr int p = decltype(P)::value;
+        col[kw_pad(lane * 16 + sarfft2::freq_at(16, p))] = x[p];
+      });
+      __syncwarp();
+      // pass 2, split over the lane halves (fft_ctx SPLIT2 with the row-major
+      // twiddle table): ip = lane, i = ip mod 16
+      constexpr int H = 16, TL = 32;
+      const int ip = lane, i = ip & 15;
+      float2 e = tw[H * TL + ip];
+      e.y = -e.y;
+      float2 g[H];
+#pragma unroll
+      for (int r = 0; r < H; ++r) {
+        const float2 t = sarfft2::add(col[kw_pad(i + r * 16)], sarfft2::mul(col[kw_pad(i + (r + H) * 16)], e));
+        if (r == 0) {
+          g[0] = t;
+        } else {
+          float2 tw_ = tw[r * TL + ip];
+          tw_.y = -tw_.y;
+          g[r] = sarfft2::mul(t, tw_);
+        }
+      }
+      sarfft2::dft<H, +1>(g);
+      float2 *dst = v.w1 + ((size_t)f * ncol + colof) * (size_t)NZ;
+      sarfft2::static_for<0, H>([&](auto P) {
+        constexpr int p = decltype(P)::value;
+        st_mid(dst + ip + 2 * sarfft2::freq_at(H, p) * 16, g[p]);
+      });
+    }
+    // the pass-2 reads of the buffer were consumed by the stores above
+    sartma::mbar_arrive(&empty2[b]);
+  }
+}
+
 // ------------------------------------------------------- K3, 2-D mode ----
 // SAR_IMAGE_2D (reading R18): per Stolt mirror class (the <= 4 columns that
 // share k_r^2), k_z,i = sqrt(4 k_i^2 - k_r^2) once, then for every plane s the
@@ -542,8 +823,21 @@ bool try_k3pp(const SarDeviceView &v, bool ifft, cudaStream_t s, int num_sms, cu
 namespace {
 }  // namespace
 
+#ifndef K3_WS
+#define K3_WS 1   // warp-specialised k3_ws at n_z = 512
+#endif
 cudaError_t launch_k3(const SarDeviceView &v, bool ifft, cudaStream_t s, int num_sms) {
   if (v.ncls == 0) return cudaSuccess;   // every column skipped (zero Stolt output)
+  if (K3_WS && ifft && v.nz == 512 && (v.nk & 1) == 0 && !v.force_plain && k3ws_smem<512>(v.nk) <= 225 * 1024) {
+    const size_t smem = k3ws_smem<512>(v.nk);
+    const int nitems_f = (v.ncls + KW_CL - 1) / KW_CL;
+    const int nitems = nitems_f * v.F;
+    const int grid = nitems < num_sms ? nitems : num_sms;
+    cudaError_t e = cudaFuncSetAttribute(k3_ws<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    e = launch_ex(k3_ws<512>, dim3(grid), dim3(KW_NT), smem, s, v, nitems_f);
+    return e == cudaSuccess ? cudaGetLastError() : e;
+  }
 #ifndef K3PP_64
 #define K3PP_64 0   // classes per item of k3_pp at n_z = 64 (0: k3_class there)
 #endif
