@@ -445,6 +445,18 @@ constexpr int KW_WS = KW_WS_;  // Stolt warps
 constexpr int KW_WF = 8;    // FFT warps per set (= column slots of an item)
 constexpr int KW_FS = KW_FS_;   // FFT warp sets; set s takes the items n = s (mod KW_FS)
 constexpr int KW_CL = 2;    // mirror classes per item
+#ifndef KW_ARR_
+#define KW_ARR_ 32
+#endif
+constexpr int KW_ARR = KW_ARR_;
+#ifndef KW_SLEEP
+#define KW_SLEEP 1
+#endif
+#if KW_SLEEP
+#define KW_WAIT sartma::mbar_wait_sleep
+#else
+#define KW_WAIT sartma::mbar_wait
+#endif   // arrivals per warp on the hand-off barriers (1: lane 0 after __syncwarp)
 constexpr int KW_NT = 32 * (1 + KW_WS + KW_WF * KW_FS);
 // a buffer is always consumed by the same set (mbarrier parity waits cannot
 // tell phases two apart)
@@ -490,11 +502,11 @@ __global__ void __launch_bounds__(KW_NT, 1) k3_ws(const SarDeviceView v, int nit
   if (tid == 0) {
     for (int i = 0; i < KW_S; ++i) {
       sartma::mbar_init(&full[i], 1);
-      sartma::mbar_init(&empty[i], 32 * KW_WS);
+      sartma::mbar_init(&empty[i], KW_ARR * KW_WS);
     }
     for (int i = 0; i < KW_B; ++i) {
-      sartma::mbar_init(&full2[i], 32 * KW_WS);
-      sartma::mbar_init(&empty2[i], 32 * KW_WF);
+      sartma::mbar_init(&full2[i], KW_ARR * KW_WS);
+      sartma::mbar_init(&empty2[i], KW_ARR * KW_WF);
     }
     sartma::fence_barrier_init();
   }
@@ -570,8 +582,8 @@ __global__ void __launch_bounds__(KW_NT, 1) k3_ws(const SarDeviceView v, int nit
     unsigned n = 0;
     for (int item = blockIdx.x; item < nitems; item += gridDim.x, ++n) {
       const int st = n % KW_S, b = n % KW_B;
-      sartma::mbar_wait(&full[st], (n / KW_S) & 1);
-      if (n >= KW_B) sartma::mbar_wait(&empty2[b], ((n / KW_B) - 1) & 1);
+      KW_WAIT(&full[st], (n / KW_S) & 1);
+      if (n >= KW_B) KW_WAIT(&empty2[b], ((n / KW_B) - 1) & 1);
       const unsigned char *sb = ring + st * stage_bytes;
       const K3Hdr<CL> &h = *reinterpret_cast<const K3Hdr<CL> *>(sb);
       const float2 *fin = reinterpret_cast<const float2 *>(sb + hdr_bytes);
@@ -628,9 +640,13 @@ __global__ void __launch_bounds__(KW_NT, 1) k3_ws(const SarDeviceView v, int nit
       }
       if (st_t == 0) meta[3 * CC] = h.f;
       // every lane's stage reads were consumed by its stores above; arrive
-      // (release) on both barriers
-      sartma::mbar_arrive(&empty[st]);
-      sartma::mbar_arrive(&full2[b]);
+      // (release) on both barriers, one arrival per warp after __syncwarp
+      // (which orders the lanes' shared-memory writes before lane 0's release)
+      if (KW_ARR == 1) __syncwarp();
+      if (KW_ARR == 32 || lane == 0) {
+        sartma::mbar_arrive(&empty[st]);
+        sartma::mbar_arrive(&full2[b]);
+      }
     }
     return;
   }
@@ -639,7 +655,7 @@ __global__ void __launch_bounds__(KW_NT, 1) k3_ws(const SarDeviceView v, int nit
   unsigned n = fs;
   for (int item = blockIdx.x + fs * gridDim.x; item < nitems; item += KW_FS * gridDim.x, n += KW_FS) {
     const int b = n % KW_B;
-    sartma::mbar_wait(&full2[b], (n / KW_B) & 1);
+    KW_WAIT(&full2[b], (n / KW_B) & 1);
     unsigned char *bb = bufs + b * G::BUF;
     const int *meta = reinterpret_cast<const int *>(bb);
     float2 *col = reinterpret_cast<float2 *>(bb + G::META) + w * G::NZP;
@@ -685,7 +701,8 @@ __global__ void __launch_bounds__(KW_NT, 1) k3_ws(const SarDeviceView v, int nit
       });
     }
     // the pass-2 reads of the buffer were consumed by the stores above
-    sartma::mbar_arrive(&empty2[b]);
+    if (KW_ARR == 1) __syncwarp();
+    if (KW_ARR == 32 || lane == 0) sartma::mbar_arrive(&empty2[b]);
   }
 }
 
