@@ -42,9 +42,21 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t *bar, uint32_t parity) {
   return ok != 0;
 }
 
+// SAR_WAIT_HINT_NS > 0: waits pass a suspend-time hint to try_wait, so a
+// waiting warp sleeps until the phase completes instead of re-polling (the
+// spinning issue slots cost power, and under the power cap clock)
+#ifndef SAR_WAIT_HINT_NS
+#define SAR_WAIT_HINT_NS 0
+#endif
+__device__ __forceinline__ bool mbar_try_wait_hint(uint64_t *bar, uint32_t parity, uint32_t ns);
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+#if SAR_WAIT_HINT_NS > 0
+  while (!mbar_try_wait_hint(bar, parity, (uint32_t)SAR_WAIT_HINT_NS)) {
+  }
+#else
   while (!mbar_try_wait(bar, parity)) {
   }
+#endif
 }
 
 // try_wait with a suspend-time hint: a waiting warp sleeps until the phase

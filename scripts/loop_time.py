@@ -3,6 +3,7 @@ plans with and without per-kernel profiling events, per library:
     python scripts/loop_time.py CONFIG NAME[:LIBPATH] ..."""
 import os
 import sys
+import time
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402
@@ -27,10 +28,18 @@ for spec in sys.argv[2:]:
             for _ in range(3):
                 plan.reconstruct(d, out)
             torch.cuda.synchronize()
+            if flags:
+                plan.profile_reset()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
+            t0 = time.perf_counter()
             for _ in range(K):
                 plan.reconstruct(d, out)
+            t1 = time.perf_counter()
             e1.record()
             torch.cuda.synchronize()
-            print(f"{name} {tag:>8} {'profiled' if flags else 'plain   '} {e0.elapsed_time(e1) / K:.4f} ms/call", flush=True)
+            print(f"{name} {tag:>8} {'profiled' if flags else 'plain   '} {e0.elapsed_time(e1) / K:.4f} ms/call"
+                  f" (host enqueue {(t1 - t0) * 1e3 / K:.4f} ms/call)", flush=True)
+            if flags:
+                ms, n = plan.profile_read()
+                print("   stages over the loop:", " ".join(f"{m / n:.3f}" for m in ms), f"sum {sum(ms) / n:.4f} ms (n={n})")
