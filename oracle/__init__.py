@@ -23,6 +23,8 @@ O6     IFT_3D                                                         Eq. (14) P
 O7     magnitude, axes                                               (reading)
 O5'-7' 2-D single-plane image: back-propagate to z_s, sum over k,    Table I 2-D rows
        IFT_2D, magnitude (oracle/plane2d.py)                          P:394, P:602-609
+O2''   NEAREST placement: pose -> lattice node nearest to its true   P:239 (reading
+       (x', y') position, collisions summed (oracle/rma.py)            R20)
 O3''   NUFFT mode: type-1 transform from the true (x', y') positions
        (direct sum and FGG, oracle/nufft.py)
 =====  ==========================================================  ===========
@@ -40,7 +42,8 @@ circular-shift (phase-ramp) formulation of the lattice placement, single
 scatterers landing on their voxel, and back-projection brute force.
 """
 from .rma import (Geometry, decompose, compensate, fft2, rma_filter, stolt,  # noqa: F401
-                  ifft3, magnitude_image, reconstruct, stolt_index_table, BAND_EPS)
+                  ifft3, magnitude_image, reconstruct, stolt_index_table, BAND_EPS,
+                  nearest_nodes)
 from .bpa import bpa  # noqa: F401
 from .plane2d import plane_sum, ifft2_planes, magnitude_planes, reconstruct_planes  # noqa: F401
 from . import nufft  # noqa: F401

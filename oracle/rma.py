@@ -144,17 +144,37 @@ def beta(geo: Geometry, f: int, t: int, r: int) -> np.ndarray:
     return -2.0 * geo.d_z[f] + geo.beta_mimo[f, t, r]
 
 
-def compensate(s, geo: Geometry, no_compensation=False, rows_per_chunk=None) -> np.ndarray:
+def nearest_nodes(scan, x0, y0, dx, dy):
+    """NEAREST placement (reading R20; SURVEY 8(b) SAR_GRID_NEAREST, the
+    in-plane irregularity of P:239 snapped to the lambda/4 lattice instead of
+    interpolated): the planar node of pose p is the lattice point nearest to
+    its TRUE in-plane position,
+        ix = rint((x_p - x0)/dx),  iy = rint((y_p - y0)/dy)
+    (fp64, the division first, round-half-even).  Returns int64 [F, P] arrays
+    (ix, iy); they may be negative or beyond the raster (placement is modulo
+    the FFT grid, reading R6)."""
+    scan = np.asarray(scan, float)
+    ix = np.rint((scan[:, :, 0] - x0) / dx).astype(np.int64)
+    iy = np.rint((scan[:, :, 1] - y0) / dy).astype(np.int64)
+    return ix, iy
+
+
+def compensate(s, geo: Geometry, no_compensation=False, rows_per_chunk=None, nodes=None) -> np.ndarray:
     """O2: s_hat = s * exp(+j k beta) (Eq. (11)), accumulated onto the
     virtual planar lattice (reading R6: coherent sum of every (t,r,p) landing
     on a node; placement modulo the FFT grid).  Empty nodes stay 0 (the zero
-    padding).  Returns complex128 [F, ny, nx, n_k]."""
+    padding).  ``nodes`` = (ix, iy) [F, P] from ``nearest_nodes`` selects the
+    NEAREST placement (reading R20: several poses may land on one node, their
+    samples are summed; nodes no pose reaches stay 0); default RASTER
+    (pose (ix, iy) -> node (ix, iy), reading R7).  Returns complex128
+    [F, ny, nx, n_k]."""
     F, nt, nr, P, nk = s.shape
     assert P == geo.npx * geo.npy
     out = np.zeros((F, geo.ny, geo.nx, nk), complex)
-    iy, ix = np.divmod(np.arange(P), geo.npx)
+    iy_r, ix_r = np.divmod(np.arange(P), geo.npx)
     chunk = rows_per_chunk or max(1, (1 << 22) // max(nk, 1))
     for f in range(F):
+        ix, iy = (ix_r, iy_r) if nodes is None else (nodes[0][f], nodes[1][f])
         for t in range(nt):
             for r in range(nr):
                 vy = (iy + geo.jy[t, r]) % geo.ny
@@ -164,8 +184,12 @@ def compensate(s, geo: Geometry, no_compensation=False, rows_per_chunk=None) -> 
                     sl = slice(p0, p0 + chunk)
                     val = s[f, t, r, sl].astype(complex)
                     val = val * np.exp(1j * geo.k[None, :] * b[sl, None])
-                    # nodes are distinct within one pair (npx<=nx, npy<=ny)
-                    out[f, vy[sl], vx[sl]] += val
+                    if nodes is None:
+                        # nodes are distinct within one pair (npx<=nx, npy<=ny)
+                        out[f, vy[sl], vx[sl]] += val
+                    else:
+                        # NEAREST: poses of one pair may share a node
+                        np.add.at(out[f], (vy[sl], vx[sl]), val)
     return out
 
 
@@ -251,14 +275,19 @@ def magnitude_image(o: np.ndarray, geo: Geometry, complex_out=False) -> np.ndarr
     return v if complex_out else np.abs(v)
 
 
-def reconstruct(s, sc_or_geo, no_compensation=False, complex_out=False, return_stages=False):
+def reconstruct(s, sc_or_geo, no_compensation=False, complex_out=False, return_stages=False, nearest=False):
     """Whole path O1..O7 for a ``scenes.Scene`` (or an explicit Geometry).
 
     ``s`` is the complex64 input s[F, n_tx, n_rx, P, n_k] (the same bytes the
-    GPU receives).  Returns (image, geometry[, stages]).
+    GPU receives).  ``nearest`` (a Scene only): NEAREST placement (reading
+    R20) instead of RASTER.  Returns (image, geometry[, stages]).
     """
     geo = sc_or_geo if isinstance(sc_or_geo, Geometry) else geometry_of(sc_or_geo)
-    planar = compensate(s, geo, no_compensation)
+    nodes = None
+    if nearest:
+        sc = sc_or_geo
+        nodes = nearest_nodes(sc.scan, sc.x0, sc.y0, sc.dx, sc.dy)
+    planar = compensate(s, geo, no_compensation, nodes=nodes)
     S = fft2(planar)
     Fk = rma_filter(S, geo)
     O = stolt(Fk, geo)
