@@ -141,7 +141,7 @@ def host_info():
     return {"cpu_model": model, "cores": os.cpu_count(), "ram_GiB": ram}
 
 
-def oracle_sample(sc, s_host, planes=None, nufft=False):
+def oracle_sample(sc, s_host, planes=None, nufft=False, nearest=False):
     """Time the fp64 oracle (as it stands) on a bounded sample of the workload:
     Tx/Rx channel (0,0) through the whole path.  The oracle's per-channel
     work (O1-O2 compensation + lattice accumulation; the NUFFT spread) and
@@ -163,7 +163,8 @@ def oracle_sample(sc, s_host, planes=None, nufft=False):
         else:
             oracle.magnitude_image(oracle.ifft3(oracle.stolt(Fk, g1)), g1)
     else:
-        planar = oracle.compensate(s_host, geo)
+        nodes = oracle.nearest_nodes(sc.scan, sc.x0, sc.y0, sc.dx, sc.dy) if nearest else None
+        planar = oracle.compensate(s_host, geo, nodes=nodes)
         t1 = time.perf_counter()
         Fk = oracle.rma_filter(oracle.fft2(planar), geo)
         if planes:
@@ -262,7 +263,7 @@ def run_ours(args):
     sc3 = sc
     if planes:
         sc = dataclasses.replace(sc, nz=len(planes))       # image [F][planes][ny][nx]
-    gflag = sar.SAR_GRID_NUFFT if args.grid == "nufft" else 0
+    gflag = {"nufft": sar.SAR_GRID_NUFFT, "nearest": sar.SAR_GRID_NEAREST}.get(args.grid, 0)
     # the timed plan records no per-kernel events (they would sit between the
     # programmatically dependent launches); a second, profiled plan measures
     # the per-kernel times after the timed region
@@ -314,7 +315,7 @@ def run_ours(args):
     path_gbs = sc.alg_bytes() / (ms_step * 1e-3) / 1e9
     roof = {"bound": "hbm", "kernel": dom_name, "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
             "traffic": traffic, "alg_bytes": alg[dom], "ms": avg[dom], "peak_source": peak_src}
-    if gflag and dom == 0:
+    if args.grid == "nufft" and dom == 0:
         # NUFFT spread (K1s) is FP32-FMA bound, not HBM bound: algorithmic
         # flops = samples x (2W+1)^2 taps x 4 (complex sample x real weight =
         # 2 FMA), W = 6; peak = 148 SMs x 128 FP32 lanes x 2 flop x the max SM
@@ -370,8 +371,8 @@ def run_ours(args):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         s_host = data[:, :1, :1].cpu().numpy()
-        res = oracle_sample(sc3, s_host, planes=planes, nufft=bool(gflag))
-        cpu = oracle_line(sc3, args.config, res, planes=planes, nufft=bool(gflag))
+        res = oracle_sample(sc3, s_host, planes=planes, nufft=args.grid == "nufft", nearest=args.grid == "nearest")
+        cpu = oracle_line(sc3, args.config, res, planes=planes, nufft=args.grid == "nufft")
 
     # parity of this configuration as last measured by the GPU parity suite
     # (the full fp64 oracle on the host takes minutes: tests, not the bench)
@@ -387,7 +388,7 @@ def run_ours(args):
             "scaling": "strong" if sharded else "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded scenes, GPU-synthesised Eq. (9) echo)",
             "config": {"workload": args.config + (f" 2-D planes {planes}" if planes else "") +
-                       (" NUFFT placement" if gflag else ""),
+                       {"nufft": " NUFFT placement", "nearest": " NEAREST placement"}.get(args.grid, ""),
                        "frames": sc.n_frames, "tx": sc.n_tx, "rx": sc.n_rx,
                        "poses": sc.n_pos, "n_k": sc.n_k, "image": [sc.nx, sc.ny, sc.nz],
                        "samples_per_step": samples, "raw_GiB_per_gpu": sc.raw_bytes() / 2**30,
@@ -518,8 +519,9 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="large", choices=["tiny", "small", "freehand", "large", "realtime"])
-    ap.add_argument("--grid", default="raster", choices=["raster", "nufft"],
-                    help="in-plane placement: RASTER lattice (reading R7) or FGG-NUFFT from the true positions (R19)")
+    ap.add_argument("--grid", default="raster", choices=["raster", "nufft", "nearest"],
+                    help="in-plane placement: RASTER lattice (reading R7), FGG-NUFFT from the true positions (R19) "
+                         "or the lattice node nearest the true position (NEAREST, R20)")
     ap.add_argument("--planes", type=str, default=None,
                     help="comma-separated z planes (m): 2-D single-plane images (SAR_IMAGE_2D, Table I '2-D' rows) "
                          "instead of the 3-D volume")

@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define SAR_B200_VERSION 4
+#define SAR_B200_VERSION 5
 
 typedef struct sar_plan sar_plan;       /* opaque */
 typedef struct CUstream_st *sar_stream; /* == cudaStream_t; NULL = legacy default stream */
@@ -71,6 +71,15 @@ enum sar_flags {
   SAR_FORCE_PLAIN = 1u << 6,     /* testing: run the plain (non-TMA, non-persistent) kernel of every
                                     stage instead of the TMA-pipelined ones; same arithmetic, results
                                     equal to fp32 rounding (the coverage of the fallback kernels) */
+  SAR_GRID_NEAREST = 1u << 8,    /* NEAREST placement (reading R20): step 1 puts every
+                                    pose on the lambda/4 lattice node NEAREST its true in-plane
+                                    position, (ix, iy) = (rint((x - x0)/dx), rint((y - y0)/dy)) in
+                                    fp64, instead of its raster index (RASTER, reading R7); poses
+                                    that land on one node are summed, nodes no pose reaches are 0,
+                                    placement is modulo the FFT grid (reading R6).  The in-plane
+                                    error is then <= pitch/2 instead of the jitter (the paper's
+                                    FGG-NUFFT treatment of P:239-242 is SAR_GRID_NUFFT).  Not with
+                                    SAR_GRID_NUFFT (INVALID_ARG) or slab plans (UNSUPPORTED) */
   SAR_CUDA_GRAPH = 1u << 7       /* replay the call's launches as one CUDA graph (for small, launch-bound
                                     configurations): the first sar_reconstruct with a given
                                     (d_data, d_image) pair records the path into a graph on a stream of
@@ -149,6 +158,15 @@ int sar_plan_describe(const sar_geom_desc *g, const sar_image_desc *im, uint32_t
  * sar_plan_describe. */
 int sar_plan_describe_stolt_ranges(const sar_geom_desc *g, const sar_image_desc *im, uint32_t flags,
                                    int32_t *ranges);
+
+/* Host-only export of the SAR_GRID_NEAREST pose nodes (reading R20):
+ * ix[f*P + p] = rint((x - x0)/dx), iy[f*P + p] = rint((y - y0)/dy) of pose p
+ * of frame f (fp64, round-half-even; before the pair offsets j_tr and the
+ * modulo of the FFT grid).  ix, iy: host int32 [F*npy*npx].  The same table
+ * step 1 uses when SAR_GRID_NEAREST is set (flags need not include it).
+ * Errors: as sar_plan_describe; UNSUPPORTED if a node does not fit 32 bits. */
+int sar_plan_describe_nearest(const sar_geom_desc *g, const sar_image_desc *im, uint32_t flags,
+                              int32_t *ix, int32_t *iy);
 
 /* Create a plan: validates the geometry, runs the fp64 decomposition of
  * Eqs. (3),(4),(7),(12) on the host (virtual-node offsets j_tr, beta terms,

@@ -114,6 +114,65 @@ __global__ void __launch_bounds__(nt_for(NX), minb_for(NX))
   }
 }
 
+// SAR_GRID_NEAREST (reading R20): K1 with the plan's node lists instead of
+// the raster rows.  One CTA = (k chunk, lattice row vy, frame f), thread item
+// (vx, kk) as in k1_correct_xfft; item (vx, kk) sums, in list order, every
+// (pair, pose) sample row the plan put on node (f, vy, vx), rotated by
+// exp(+j k beta) with beta = -2 d_z + beta_MIMO (Eqs. (11)-(12)); then the same
+// x-FFT and store.  With every pose on its raster node the lists hold one
+// row per pair in pair order, so the result equals k1_correct_xfft's bit for
+// bit (same rotation code, same order).
+template <int NX, bool DO_FFT>
+__global__ void __launch_bounds__(nt_for(NX), minb_for(NX))
+    k1_nearest(const SarDeviceView v, const float2 *__restrict__ s) {
+  constexpr int NT = nt_for(NX);
+  constexpr int ITEMS = NX * KC;
+  constexpr int E = (ITEMS + NT - 1) / NT;
+  extern __shared__ float2 tile[];  // [NX][16]
+  const int tid = threadIdx.x;
+  const int kbase = blockIdx.x * KC;
+  const int vy = blockIdx.y;
+  const int f = blockIdx.z;
+  static_assert(NT % KC == 0, "k lane of a thread is fixed: kk = tid % 16");
+  const int k = kbase + (tid & (KC - 1));
+  const float kt = k < v.nk ? __ldg(v.kturn + k) : 0.f;
+  const int *off = v.nn_off + ((size_t)(f + v.f0) * v.ny + vy) * NX;
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int item = tid + e * NT;
+    if (ITEMS % NT != 0 && item >= ITEMS) continue;
+    const int vx = item >> 4;
+    float2 acc = make_float2(0.f, 0.f);
+    if (k < v.nk) {
+      const int q1 = __ldg(off + vx + 1);
+      for (int q = __ldg(off + vx); q < q1; ++q) {
+        const SarNearEntry en = v.nn_ent[q];
+        const float2 val = __ldcs(s + (size_t)en.row * v.nk + k);
+        if (v.no_comp) {
+          acc = cadd(acc, val);
+        } else {
+          float turns = en.beta * kt;
+          turns -= rintf(turns);
+          float sn, cs;
+          __sincosf(turns * 6.28318530717958647692f, &sn, &cs);
+          acc = cadd(acc, cmul(val, make_float2(cs, sn)));
+        }
+      }
+    }
+    tile[item] = acc;  // tile[vx*16 + kk]
+  }
+  __syncthreads();
+  if constexpr (DO_FFT) sarfft::tile_fft<NX, KC, KC, NT, -1>(tile, v.tw_x, tid);
+  float2 *out = v.w0 + ((size_t)(f * v.nvy + vy) * NX) * (size_t)v.nk;
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int item = tid + e * NT;
+    if (ITEMS % NT != 0 && item >= ITEMS) continue;
+    const int kk = item & (KC - 1), vx = item >> 4;
+    if (kbase + kk < v.nk) out[(size_t)vx * v.nk + kbase + kk] = tile[item];
+  }
+}
+
 // Persistent, TMA-pipelined K1 (used when n_k is even, npx % 4 == 0 and the
 // step phasor below is accurate).  One CTA (1024 threads) per SM walks a flat
 // sequence of "jobs" = (work item (frame, vy, k chunk of K1C), valid pair, box
@@ -373,6 +432,19 @@ cudaError_t launch(K kernel, dim3 grid, int nt, size_t smem, cudaStream_t s, con
 
 cudaError_t launch_k1(const SarDeviceView &v, const float2 *data, bool fft, cudaStream_t s,
                       const CUtensorMap *tm_s, const CUtensorMap *tm_ap, int br, bool regacc, int num_sms) {
+  if (v.nearest) {
+    dim3 grid((v.nk + KC - 1) / KC, v.ny, v.F);
+    const size_t smem = (size_t)v.nx * KC * sizeof(float2);
+    switch (v.nx) {
+#define X(N)                                                                                   \
+  case N:                                                                                      \
+    return fft ? launch(k1_nearest<N, true>, grid, nt_for(N), smem, s, v, data)               \
+               : launch(k1_nearest<N, false>, grid, nt_for(N), smem, s, v, data);
+      SAR_SIZES(X)
+#undef X
+    }
+    return cudaErrorInvalidValue;
+  }
   if (fft && tm_s && tm_ap && v.nx >= 64 && v.nx <= 512 && v.k1_step_ok) {
     const int C = k1c_for(v.nx);
     const int nchunk = (v.nk + C - 1) / C;

@@ -116,6 +116,10 @@ struct HostTables {
   // NUFFT spread blocks (K1s): CSR of entries per (frame, 4 x 8 fine-cell block)
   std::vector<int> sp_off;
   std::vector<SarSpreadEntry> sp_ent;
+  // SAR_GRID_NEAREST: pose nodes [F*P] and the CSR of entries per lattice node
+  std::vector<int32_t> nn_ix, nn_iy;
+  std::vector<int> nn_off;
+  std::vector<SarNearEntry> nn_ent;
   int sp_nbx = 0, sp_nby = 0;
   size_t tw_f_off = 0;
   std::vector<double> kx, ky, kz, kd, rref;
@@ -149,6 +153,8 @@ int host_decompose(const sar_geom_desc *g, const sar_image_desc *im, uint32_t fl
   if (g->npx > im->nx || g->npy > im->ny) return fail(SAR_ERR_INVALID_ARG, "raster larger than the FFT grid");
   if ((flags & SAR_GRID_NUFFT) && (im->nx > 512 || im->ny > 512 || g->npx > 512 || im->nx < 32))
     return fail(SAR_ERR_UNSUPPORTED, "SAR_GRID_NUFFT needs 32 <= nx <= 512, ny <= 512, npx <= 512");
+  if ((flags & SAR_GRID_NUFFT) && (flags & SAR_GRID_NEAREST))
+    return fail(SAR_ERR_INVALID_ARG, "SAR_GRID_NEAREST and SAR_GRID_NUFFT are exclusive");
   if (!(g->dx > 0) || !(g->dy > 0) || (!mode2d && !(im->dz > 0)))
     return fail(SAR_ERR_INVALID_ARG, "pitches must be > 0");
   // K1's TMA row coordinate and the NUFFT spread entries index raw sample rows
@@ -436,6 +442,54 @@ int host_decompose(const sar_geom_desc *g, const sar_image_desc *im, uint32_t fl
     twiddles(T.tw, Rx);
   }
 
+  // NEAREST placement (reading R20; must match oracle.nearest_nodes): pose
+  // node (rint((x - x0)/dx), rint((y - y0)/dy)) in fp64 (division first,
+  // round-half-even), then + j_tr modulo the FFT grid (reading R6); the
+  // entries of a node in (pair, pose) order, so with every pose on its raster
+  // node the summation order is K1's (pairs in order)
+  T.nn_ix.clear();
+  T.nn_iy.clear();
+  if (F > 0) {
+    T.nn_ix.resize((size_t)F * P);
+    T.nn_iy.resize((size_t)F * P);
+    for (size_t i = 0; i < (size_t)F * P; ++i) {
+      const double *sp = g->scan_xyz + i * 3;
+      const double fx = nearbyint((sp[0] - g->x0) / g->dx), fy = nearbyint((sp[1] - g->y0) / g->dy);
+      if (!(fabs(fx) < 1e9 && fabs(fy) < 1e9))
+        return fail(SAR_ERR_UNSUPPORTED, "a NEAREST pose node does not fit 32 bits");
+      T.nn_ix[i] = (int32_t)fx;
+      T.nn_iy[i] = (int32_t)fy;
+    }
+  }
+  if ((flags & SAR_GRID_NEAREST) && F > 0) {
+    const size_t nnode = (size_t)F * p->ny * p->nx;
+    auto wmod = [](long long a, long long b) { return (int)(((a % b) + b) % b); };
+    T.nn_off.assign(nnode + 1, 0);
+    for (int pass = 0; pass < 2; ++pass) {
+      std::vector<int> fill;
+      if (pass == 1) {
+        for (size_t i = 0; i < nnode; ++i) T.nn_off[i + 1] += T.nn_off[i];
+        T.nn_ent.resize((size_t)T.nn_off[nnode]);
+        fill.assign(T.nn_off.begin(), T.nn_off.end() - 1);
+      }
+      for (int f = 0; f < F; ++f)
+        for (int pr = 0; pr < p->npair; ++pr)
+          for (int q = 0; q < P; ++q) {
+            const size_t i = (size_t)f * P + q;
+            const int vx = wmod((long long)T.nn_ix[i] + p->jx[pr], p->nx);
+            const int vy = wmod((long long)T.nn_iy[i] + p->jy[pr], p->ny);
+            const size_t node = ((size_t)f * p->ny + vy) * p->nx + vx;
+            if (pass == 0) {
+              ++T.nn_off[node + 1];
+            } else {
+              SarNearEntry &e = T.nn_ent[(size_t)fill[node]++];
+              e.row = (int)(((size_t)f * p->npair + pr) * P + q);
+              e.beta = T.apose[i] + T.bpair[(size_t)f * p->npair + pr];
+            }
+          }
+    }
+  }
+
   // O7 rolls and axes (reading R8)
   T.roll_x = p->nvx / 2 - p->nx / 2;
   T.roll_y = p->nvy / 2 - p->ny / 2;
@@ -560,6 +614,8 @@ int plan_create_impl(sar_plan **out, const sar_geom_desc *g, const sar_image_des
   const size_t o_nu_dy = off; off += al(T.nu_decy.size() * 4);
   const size_t o_sp_off = off; off += al(T.sp_off.size() * 4);
   const size_t o_sp_ent = off; off += al(T.sp_ent.size() * sizeof(SarSpreadEntry));
+  const size_t o_nn_off = off; off += al(T.nn_off.size() * 4);
+  const size_t o_nn_ent = off; off += al(T.nn_ent.size() * sizeof(SarNearEntry));
   ce = cudaMalloc(&p->d_tables, off);
   if (ce != cudaSuccess) {
     cudaGetLastError();
@@ -585,7 +641,9 @@ int plan_create_impl(sar_plan **out, const sar_geom_desc *g, const sar_image_des
       (ce = up(o_nu_dx, T.nu_decx.data(), T.nu_decx.size() * 4)) != cudaSuccess ||
       (ce = up(o_nu_dy, T.nu_decy.data(), T.nu_decy.size() * 4)) != cudaSuccess ||
       (ce = up(o_sp_off, T.sp_off.data(), T.sp_off.size() * 4)) != cudaSuccess ||
-      (ce = up(o_sp_ent, T.sp_ent.data(), T.sp_ent.size() * sizeof(SarSpreadEntry))) != cudaSuccess) {
+      (ce = up(o_sp_ent, T.sp_ent.data(), T.sp_ent.size() * sizeof(SarSpreadEntry))) != cudaSuccess ||
+      (ce = up(o_nn_off, T.nn_off.data(), T.nn_off.size() * 4)) != cudaSuccess ||
+      (ce = up(o_nn_ent, T.nn_ent.data(), T.nn_ent.size() * sizeof(SarNearEntry))) != cudaSuccess) {
     free_plan(p);
     return cuda_fail(ce, "table upload");
   }
@@ -631,6 +689,9 @@ int plan_create_impl(sar_plan **out, const sar_geom_desc *g, const sar_image_des
   v.sp_off = (const int *)(base + o_sp_off);
   v.sp_ent = (const SarSpreadEntry *)(base + o_sp_ent);
   v.tw_f = (const float2 *)(base + o_tw) + T.tw_f_off;
+  v.nearest = (flags & SAR_GRID_NEAREST) ? 1 : 0;
+  v.nn_off = (const int *)(base + o_nn_off);
+  v.nn_ent = (const SarNearEntry *)(base + o_nn_ent);
   v.cls = (const SarClass *)(base + o_cl);
   v.liveb = T.liveb.empty() ? nullptr : (const int *)(base + o_lb);
   v.pinv = T.pinv.empty() ? nullptr : (const float2 *)(base + o_pi);
@@ -713,6 +774,20 @@ int sar_plan_describe_stolt_ranges(const sar_geom_desc *g, const sar_image_desc 
   return SAR_OK;
 }
 
+int sar_plan_describe_nearest(const sar_geom_desc *g, const sar_image_desc *im, uint32_t flags, int32_t *ix,
+                              int32_t *iy) {
+  if (!ix || !iy) return fail(SAR_ERR_INVALID_ARG, "ix or iy is NULL");
+  sar_plan tmp;
+  HostTables T;
+  int st = host_decompose(g, im, flags & ~(uint32_t)SAR_GRID_NEAREST, &tmp, T);
+  if (st != SAR_OK) return st;
+  if (!T.nn_ix.empty()) {
+    memcpy(ix, T.nn_ix.data(), T.nn_ix.size() * sizeof(int32_t));
+    memcpy(iy, T.nn_iy.data(), T.nn_iy.size() * sizeof(int32_t));
+  }
+  return SAR_OK;
+}
+
 int sar_plan_create_slab(sar_plan **out, const sar_geom_desc *g, const sar_image_desc *im, uint32_t flags,
                          const sar_slab_desc *slab) {
   if (!out) return fail(SAR_ERR_INVALID_ARG, "out is NULL");
@@ -720,7 +795,7 @@ int sar_plan_create_slab(sar_plan **out, const sar_geom_desc *g, const sar_image
   if (!slab || !g || !im) return fail(SAR_ERR_INVALID_ARG, "slab, geometry or image descriptor is NULL");
   const int G = slab->world, r = slab->rank;
   if (G < 1 || G > SAR_MAX_SLAB || r < 0 || r >= G) return fail(SAR_ERR_INVALID_ARG, "slab rank/world out of range");
-  if (flags & (SAR_IMAGE_2D | SAR_GRID_NUFFT | SAR_REPORT_PEAK | SAR_CUDA_GRAPH))
+  if (flags & (SAR_IMAGE_2D | SAR_GRID_NUFFT | SAR_GRID_NEAREST | SAR_REPORT_PEAK | SAR_CUDA_GRAPH))
     return fail(SAR_ERR_UNSUPPORTED, "slab plans support the 3-D RASTER path only");
   if (g->n_frames != 1) return fail(SAR_ERR_INVALID_ARG, "slab plans reconstruct one image (n_frames == 1)");
   if (im->nx % G || im->ny % G || im->nz % G || im->nx / G < 1 || im->nz / G < 1)

@@ -39,6 +39,13 @@ struct SarSpreadEntry {
   float beta;   // -2 d_z + beta_MIMO (m); phase = beta * k
 };
 
+// SAR_GRID_NEAREST (reading R20): one (frame, pair, pose) sample row landing
+// on a lattice node; the plan lists them per node (CSR) in (pair, pose) order.
+struct SarNearEntry {
+  int row;      // sample row (f * npair + pair) * P + pose of the raw input
+  float beta;   // -2 d_z + beta_MIMO (m), the fp32 sum K1 forms; phase = beta * k
+};
+
 // Everything a kernel needs, passed by value (fits the 32 KB parameter space).
 struct SarDeviceView {
   int F, nt, nr, npair, npx, npy, P, nk, nx, ny, nz;
@@ -65,6 +72,9 @@ struct SarDeviceView {
   const int *sp_off;               // [F*sp_nby*sp_nbx + 1] CSR offsets
   const SarSpreadEntry *sp_ent;    // entries
   const float2 *tw_f;              // [2 nx] exp(-2 pi i m / (2 nx)) (fine x-FFT)
+  int nearest;                     // SAR_GRID_NEAREST
+  const int *nn_off;               // [F*ny*nx + 1] CSR offsets per lattice node (frame, vy, vx)
+  const SarNearEntry *nn_ent;      // entries
   const float *apose;   // [F][P]      -2 d_z (m), fp32
   const float *bpair;   // [F][npair]  (d_x^2+d_y^2)/(4 R_ref) (m), fp32
   const float *kturn;   // [nk]        k_i / (2 pi) (turns per metre), fp32

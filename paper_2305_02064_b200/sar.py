@@ -24,6 +24,7 @@ SAR_GRID_NUFFT = 16
 SAR_REPORT_PEAK = 32
 SAR_FORCE_PLAIN = 64
 SAR_CUDA_GRAPH = 128
+SAR_GRID_NEAREST = 256
 STAGE_NAMES = ("K1 correct+x-FFT", "K2 y-FFT", "K3 filter+Stolt+z-IFFT", "K4a y-IFFT", "K4b x-IFFT+|.|")
 
 
@@ -79,6 +80,7 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         "sar_reconstruct": (C.c_int, [vp, vp, vp, vp]),
         "sar_reconstruct_host": (C.c_int, [vp, vp, vp, vp]),
         "sar_plan_describe_stolt_ranges": (C.c_int, [C.POINTER(GeomDesc), C.POINTER(ImageDesc), u32, vp]),
+        "sar_plan_describe_nearest": (C.c_int, [C.POINTER(GeomDesc), C.POINTER(ImageDesc), u32, vp, vp]),
         "sar_plan_destroy": (C.c_int, [vp]),
         "sar_plan_get_axes": (C.c_int, [vp, C.POINTER(C.c_double)]),
         "sar_plan_workspace_bytes": (C.c_int, [vp, C.POINTER(C.c_size_t)]),
@@ -108,7 +110,7 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
 
 def exported_symbols():
     """Names of the C entry points this binding expects (the header's API)."""
-    return ["sar_plan_describe", "sar_plan_describe_stolt_ranges", "sar_plan_create", "sar_reconstruct", "sar_reconstruct_host", "sar_plan_destroy",
+    return ["sar_plan_describe", "sar_plan_describe_stolt_ranges", "sar_plan_describe_nearest", "sar_plan_create", "sar_reconstruct", "sar_reconstruct_host", "sar_plan_destroy",
             "sar_plan_get_axes", "sar_plan_workspace_bytes", "sar_plan_profile_read",
             "sar_plan_profile_reset", "sar_plan_launches_per_call", "sar_plan_peaks", "sar_debug_stage",
             "sar_debug_node_offsets", "sar_debug_stolt_index", "sar_plan_create_slab", "sar_slab_buffer_bytes",
@@ -199,6 +201,24 @@ def describe_stolt_ranges(tx, rx, scan, npx, npy, x0, y0, dx, dy, z0, k, nx, ny,
                                               C.c_void_p(out.ctypes.data)))
     del keep
     return out
+
+
+def describe_nearest(tx, rx, scan, npx, npy, x0, y0, dx, dy, z0, k, nx, ny, nz, dz, z_ref, pulse=None, flags=0):
+    """Host-only (``sar_plan_describe_nearest``): the SAR_GRID_NEAREST pose
+    nodes (ix, iy), int32 [F, P] each (reading R20)."""
+    lib = load_library()
+    g, im, keep = _descriptors(tx, rx, scan, npx, npy, x0, y0, dx, dy, z0, k, nx, ny, nz, dz, z_ref, pulse, 0)
+    F, P = g.n_frames, g.npx * g.npy
+    ix, iy = np.zeros((max(F, 1), P), np.int32), np.zeros((max(F, 1), P), np.int32)
+    _check(lib.sar_plan_describe_nearest(C.byref(g), C.byref(im), C.c_uint32(flags), C.c_void_p(ix.ctypes.data),
+                                         C.c_void_p(iy.ctypes.data)))
+    del keep
+    return ix[:F], iy[:F]
+
+
+def describe_nearest_scene(sc, flags=0):
+    return describe_nearest(sc.tx, sc.rx, sc.scan, sc.npx, sc.npy, sc.x0, sc.y0, sc.dx, sc.dy, sc.z0, sc.k,
+                            sc.nx, sc.ny, sc.nz, sc.dz_img, sc.z_ref, flags=flags)
 
 
 def describe_scene(sc, flags=0):

@@ -41,7 +41,7 @@ def test_library_exports_every_declared_symbol():
     for d in declared:
         assert hasattr(lib, d)
     assert sorted(sarmod.exported_symbols()) == declared
-    assert lib.sar_version() == 4
+    assert lib.sar_version() == 5
 
 
 def test_library_has_no_unresolved_own_symbols():
@@ -172,3 +172,24 @@ def test_stolt_ranges_cover_every_oracle_in_band_bin(name, n_sample):
         # columns whose band lies below it are skipped
         frac = (rng_tab[:, :, 1] < rng_tab[:, :, 0]).mean()
         assert 0.17 < frac < 0.5, frac
+
+
+@pytest.mark.parametrize("name", ["tiny", "small", "freehand", "large", "realtime"])
+def test_nearest_nodes_match_oracle_bit_exact(name):
+    """SAR_GRID_NEAREST node table (reading R20): the host's fp64 rint of the
+    true in-plane position equals the oracle's for every pose of every frame
+    (integer work, bit-exact); Freehand's cumulative spacing walks poses
+    several nodes away from their raster index, which this exercises."""
+    sc = scenes.make_scene(name)
+    ix, iy = sar.describe_nearest_scene(sc)
+    ox, oy = oracle.nearest_nodes(sc.scan, sc.x0, sc.y0, sc.dx, sc.dy)
+    assert np.array_equal(ix, ox) and np.array_equal(iy, oy)
+    if name == "freehand":
+        iy_r, ix_r = np.divmod(np.arange(sc.n_pos), sc.npx)
+        assert np.abs(ix[0] - ix_r).max() >= 3
+
+
+def test_nearest_with_nufft_is_rejected():
+    with pytest.raises(sar.SarError) as ei:
+        sar.describe(**_args(), flags=sar.SAR_GRID_NEAREST | sar.SAR_GRID_NUFFT)
+    assert ei.value.status == 1

@@ -798,3 +798,84 @@ def test_slab_peer_stores_ipc_two_processes():
         pr.join(timeout=120)
         assert pr.exitcode == 0
     assert res == {0: True, 1: True}
+
+
+# ---- NEAREST placement (SAR_GRID_NEAREST, reading R20) ---------------------
+@pytest.mark.parametrize("name", ["tiny", "small", "freehand"])
+def test_nearest_parity(name):
+    """Planar lattice (stage 1, before the x-FFT) and image against the oracle
+    with the NEAREST node table; Freehand's cumulative spacing puts poses
+    several nodes from their raster index, with collisions and holes."""
+    sc = scenes.make_scene(name)
+    d, s = _data(sc)
+    want, geo, st = oracle.reconstruct(s, sc, nearest=True, return_stages=True)
+    with sar.Plan.from_scene(sc, flags=sar.SAR_GRID_NEAREST) as plan:
+        assert plan.launches_per_call() == 5
+        g1 = plan.debug_stage(1, d).cpu().numpy()
+        got = plan.reconstruct(d)
+        torch.cuda.synchronize()
+        got = got.cpu().numpy()
+    e1, _ = errs(g1, st["planar"])
+    assert e1 <= STAGE_BAR, e1
+    e2, einf = errs(got, want)
+    assert e2 <= E2_BAR and einf <= EINF_BAR, (name, e2, einf)
+    if name == "freehand":
+        raster, _ = oracle.reconstruct(s, sc)
+        assert errs(raster, want)[0] > 0.1    # the placements really differ here
+
+
+def test_nearest_equals_raster_bitwise_on_the_lattice():
+    """Every pose on its raster node: the node lists hold one row per pair in
+    pair order, so NEAREST runs exactly the plain K1's arithmetic -- the
+    images of the two plain paths are bit-identical."""
+    sc = scenes.with_geometry(scenes.make_scene("small"), jitter_xy=0.0)
+    d = torch.from_numpy(scenes.synthesize_cpu(sc)).cuda()
+    fp = sar.SAR_FORCE_PLAIN
+    with sar.Plan.from_scene(sc, flags=fp) as p0, sar.Plan.from_scene(sc, flags=fp | sar.SAR_GRID_NEAREST) as p1:
+        assert torch.equal(p0.reconstruct(d), p1.reconstruct(d))
+    with sar.Plan.from_scene(sc) as p0, sar.Plan.from_scene(sc, flags=sar.SAR_GRID_NEAREST) as p1:
+        e2, _ = errs(p1.reconstruct(d).cpu().numpy(), p0.reconstruct(d).cpu().numpy().astype(np.float64))
+    assert e2 <= 2e-5
+
+
+NEAREST_EDGE = [
+    # poses pushed 0.6..3 pitches off the raster: collisions, holes, and
+    # nodes beyond the raster and below 0 (modulo the FFT grid)
+    dict(npx=24, npy=16, nx=32, ny=32, nk=16, nz=16, jit=2.5e-3, seed=3),
+    # odd n_k, several frames, 3 Tx, nx = 512 with the x-FFT of the Large tile
+    dict(npx=500, npy=6, nx=512, ny=16, nk=13, nz=8, jit=1.5e-3, seed=4, n_tx=3, frames=2),
+    # NO_COMPENSATION with NEAREST
+    dict(npx=16, npy=12, nx=16, ny=16, nk=8, nz=8, jit=1e-3, seed=5, nocomp=True),
+]
+
+
+@pytest.mark.parametrize("kw", NEAREST_EDGE, ids=lambda kw: f"{kw['npx']}x{kw['npy']}_nk{kw['nk']}")
+def test_nearest_edge_cases(kw):
+    sc = scenes.raster_scene(kw["npx"], kw["npy"], kw["nx"], kw["ny"], kw["nk"], kw["nz"], 5e-3, 0.15,
+                             n_tx=kw.get("n_tx", 2), jitter_xy=kw["jit"], jitter_z=1e-3,
+                             n_frames=kw.get("frames", 1), seed=kw["seed"])
+    rng = np.random.default_rng(kw["seed"])
+    sc.scat_pos = [np.column_stack([rng.uniform(-0.01, 0.01, 3), rng.uniform(-0.01, 0.01, 3),
+                                    rng.uniform(0.12, 0.18, 3)]) for _ in range(sc.n_frames)]
+    sc.scat_amp = [np.ones(3, complex) for _ in range(sc.n_frames)]
+    d, s = _data(sc)
+    nocomp = kw.get("nocomp", False)
+    flags = sar.SAR_GRID_NEAREST | (sar.SAR_NO_COMPENSATION if nocomp else 0)
+    want, _ = oracle.reconstruct(s, sc, no_compensation=nocomp, nearest=True)
+    ix, _ = oracle.nearest_nodes(sc.scan, sc.x0, sc.y0, sc.dx, sc.dy)
+    assert ix.min() < 0 or ix.max() >= sc.npx   # nodes leave the raster
+    with sar.Plan.from_scene(sc, flags=flags) as plan:
+        got = plan.reconstruct(d).cpu().numpy()
+    e2, einf = errs(got, want)
+    assert e2 <= E2_BAR and einf <= EINF_BAR, (kw, e2, einf)
+
+
+def test_nearest_deterministic_and_rejections():
+    sc = scenes.make_scene("small")
+    d, _ = _data(sc)
+    with sar.Plan.from_scene(sc, flags=sar.SAR_GRID_NEAREST) as plan:
+        a = plan.reconstruct(d).clone()
+        assert torch.equal(plan.reconstruct(d), a)
+    with pytest.raises(sar.SarError) as ei:
+        sar.Plan.from_scene(sc, flags=sar.SAR_GRID_NEAREST | sar.SAR_GRID_NUFFT)
+    assert ei.value.status == 1
