@@ -145,17 +145,27 @@ __global__ void __launch_bounds__(nt_for(NX), minb_for(NX))
     float2 acc = make_float2(0.f, 0.f);
     if (k < v.nk) {
       const int q1 = __ldg(off + vx + 1);
-      for (int q = __ldg(off + vx); q < q1; ++q) {
-        const SarNearEntry en = v.nn_ent[q];
-        const float2 val = __ldcs(s + (size_t)en.row * v.nk + k);
-        if (v.no_comp) {
-          acc = cadd(acc, val);
-        } else {
-          float turns = en.beta * kt;
-          turns -= rintf(turns);
-          float sn, cs;
-          __sincosf(turns * 6.28318530717958647692f, &sn, &cs);
-          acc = cadd(acc, cmul(val, make_float2(cs, sn)));
+      // up to 4 entries' samples in flight, summed in list order
+      for (int q = __ldg(off + vx); q < q1; q += 4) {
+        SarNearEntry en[4];
+        float2 val[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          en[u] = q + u < q1 ? v.nn_ent[q + u] : SarNearEntry{0, 0.f};
+          val[u] = q + u < q1 ? __ldcs(s + (size_t)en[u].row * v.nk + k) : make_float2(0.f, 0.f);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if (q + u >= q1) break;
+          if (v.no_comp) {
+            acc = cadd(acc, val[u]);
+          } else {
+            float turns = en[u].beta * kt;
+            turns -= rintf(turns);
+            float sn, cs;
+            __sincosf(turns * 6.28318530717958647692f, &sn, &cs);
+            acc = cadd(acc, cmul(val[u], make_float2(cs, sn)));
+          }
         }
       }
     }
