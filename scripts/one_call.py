@@ -11,6 +11,9 @@ import paper_2305_02064_b200 as sar  # noqa: E402
 
 name = sys.argv[1] if len(sys.argv) > 1 else "large"
 calls = int(sys.argv[2]) if len(sys.argv) > 2 else 3
+if len(sys.argv) > 3:   # a library variant (scripts/ab_variants.py)
+    from paper_2305_02064_b200 import sar as sarmod
+    sarmod.load_library(sys.argv[3])
 sc = scenes.make_scene(name)
 sgpu.build()
 d = sgpu.synthesize_gpu(sc)
