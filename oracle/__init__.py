@@ -27,6 +27,8 @@ O2''   NEAREST placement: pose -> lattice node nearest to its true   P:239 (read
        (x', y') position, collisions summed (oracle/rma.py)            R20)
 O3''   NUFFT mode: type-1 transform from the true (x', y') positions
        (direct sum and FGG, oracle/nufft.py)
+O5*    NUFFT Stolt: each filtered column transformed along z from its   P:239-242 (reading
+       non-uniform k_z,i by a 1-D type-1 NUFFT (oracle/stolt_nufft.py)  R21)
 =====  ==========================================================  ===========
 
 The readings taken where the paper is silent or inconsistent (sign of the 2d_z
@@ -47,3 +49,4 @@ from .rma import (Geometry, decompose, compensate, fft2, rma_filter, stolt,  # n
 from .bpa import bpa  # noqa: F401
 from .plane2d import plane_sum, ifft2_planes, magnitude_planes, reconstruct_planes  # noqa: F401
 from . import nufft  # noqa: F401
+from . import stolt_nufft  # noqa: F401
