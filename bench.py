@@ -141,7 +141,7 @@ def host_info():
     return {"cpu_model": model, "cores": os.cpu_count(), "ram_GiB": ram}
 
 
-def oracle_sample(sc, s_host, planes=None, nufft=False, nearest=False):
+def oracle_sample(sc, s_host, planes=None, nufft=False, nearest=False, stolt_nufft=False):
     """Time the fp64 oracle (as it stands) on a bounded sample of the workload:
     Tx/Rx channel (0,0) through the whole path.  The oracle's per-channel
     work (O1-O2 compensation + lattice accumulation; the NUFFT spread) and
@@ -169,6 +169,10 @@ def oracle_sample(sc, s_host, planes=None, nufft=False, nearest=False):
         Fk = oracle.rma_filter(oracle.fft2(planar), geo)
         if planes:
             oracle.magnitude_planes(oracle.ifft2_planes(oracle.plane_sum(Fk, geo, planes)), geo)
+        elif stolt_nufft:
+            import scipy.fft
+            oz = oracle.stolt_nufft.stolt_nufft(Fk, geo)
+            oracle.magnitude_image(scipy.fft.ifft2(oz, axes=(1, 2), workers=os.cpu_count()), geo)
         else:
             oracle.magnitude_image(oracle.ifft3(oracle.stolt(Fk, geo)), geo)
     t2 = time.perf_counter()
@@ -264,6 +268,8 @@ def run_ours(args):
     if planes:
         sc = dataclasses.replace(sc, nz=len(planes))       # image [F][planes][ny][nx]
     gflag = {"nufft": sar.SAR_GRID_NUFFT, "nearest": sar.SAR_GRID_NEAREST}.get(args.grid, 0)
+    if args.stolt == "nufft":
+        gflag |= sar.SAR_STOLT_NUFFT
     # the timed plan records no per-kernel events (they would sit between the
     # programmatically dependent launches); a second, profiled plan measures
     # the per-kernel times after the timed region
@@ -371,7 +377,8 @@ def run_ours(args):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         s_host = data[:, :1, :1].cpu().numpy()
-        res = oracle_sample(sc3, s_host, planes=planes, nufft=args.grid == "nufft", nearest=args.grid == "nearest")
+        res = oracle_sample(sc3, s_host, planes=planes, nufft=args.grid == "nufft", nearest=args.grid == "nearest",
+                            stolt_nufft=args.stolt == "nufft")
         cpu = oracle_line(sc3, args.config, res, planes=planes, nufft=args.grid == "nufft")
 
     # parity of this configuration as last measured by the GPU parity suite
@@ -388,7 +395,8 @@ def run_ours(args):
             "scaling": "strong" if sharded else "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded scenes, GPU-synthesised Eq. (9) echo)",
             "config": {"workload": args.config + (f" 2-D planes {planes}" if planes else "") +
-                       {"nufft": " NUFFT placement", "nearest": " NEAREST placement"}.get(args.grid, ""),
+                       {"nufft": " NUFFT placement", "nearest": " NEAREST placement"}.get(args.grid, "") +
+                       (" NUFFT Stolt" if args.stolt == "nufft" else ""),
                        "frames": sc.n_frames, "tx": sc.n_tx, "rx": sc.n_rx,
                        "poses": sc.n_pos, "n_k": sc.n_k, "image": [sc.nx, sc.ny, sc.nz],
                        "samples_per_step": samples, "raw_GiB_per_gpu": sc.raw_bytes() / 2**30,
@@ -522,6 +530,9 @@ def main():
     ap.add_argument("--grid", default="raster", choices=["raster", "nufft", "nearest"],
                     help="in-plane placement: RASTER lattice (reading R7), FGG-NUFFT from the true positions (R19) "
                          "or the lattice node nearest the true position (NEAREST, R20)")
+    ap.add_argument("--stolt", default="linear", choices=["linear", "nufft"],
+                    help="Stolt step: linear pull onto the uniform k_z grid (reading R4) or the 1-D NUFFT from "
+                         "the non-uniform k_z (SAR_STOLT_NUFFT, reading R21)")
     ap.add_argument("--planes", type=str, default=None,
                     help="comma-separated z planes (m): 2-D single-plane images (SAR_IMAGE_2D, Table I '2-D' rows) "
                          "instead of the 3-D volume")

@@ -80,6 +80,15 @@ enum sar_flags {
                                     error is then <= pitch/2 instead of the jitter (the paper's
                                     FGG-NUFFT treatment of P:239-242 is SAR_GRID_NUFFT).  Not with
                                     SAR_GRID_NUFFT (INVALID_ARG) or slab plans (UNSUPPORTED) */
+  SAR_STOLT_NUFFT = 1u << 9,     /* NUFFT Stolt step (reading R21; "NUFFT ... for the Fourier
+                                    transforms and Stolt interpolation step"): step 3
+                                    takes every filtered column along z from its non-uniform
+                                    k_z,i = sqrt(4 k_i^2 - k_r^2) by a 1-D type-1 NUFFT (fast
+                                    Gaussian gridding, oversampling 2, half width 6; samples
+                                    weighted by the Jacobian 4 k_i dk / (k_z,i dk_z)) instead of
+                                    the linear pull onto the uniform k_z grid and the z-IFFT.
+                                    3-D only (INVALID_ARG with SAR_IMAGE_2D), nz <= 512
+                                    (UNSUPPORTED); debug stage 3 is not available */
   SAR_CUDA_GRAPH = 1u << 7       /* replay the call's launches as one CUDA graph (for small, launch-bound
                                     configurations): the first sar_reconstruct with a given
                                     (d_data, d_image) pair records the path into a graph on a stream of

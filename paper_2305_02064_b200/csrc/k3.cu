@@ -706,6 +706,146 @@ __global__ void __launch_bounds__(KW_NT, 1) k3_ws(const SarDeviceView v, int nit
   }
 }
 
+// ------------------------------------------------- K3, NUFFT Stolt ----
+// SAR_STOLT_NUFFT (reading R21): each filtered column is taken
+// along z from its NON-uniform k_z,i = sqrt(4 k_i^2 - k_r^2) by a 1-D type-1
+// NUFFT (fast Gaussian gridding, sigma = 2, W = 6) instead of the linear pull
+// onto the uniform k_z grid + the z-IFFT.  One CTA per Stolt mirror class
+// (the <= 4 columns sharing k_r^2, so the positions, the filter H and the
+// Jacobian 4 k dk / (k_z dk_z) are computed once for the class):
+//   1. member columns -> shared memory;
+//   2. per sample i: in band iff 4 k_i^2 > k_r^2 and k_z,i >= k_z,0 (fp64, the
+//      oracle's IEEE sequence), fine position sigma (k_z,i - k_z,0)/dk_z as
+//      integer cell + fp32 fraction, weight H_i w_i;
+//   3. gather onto the R = 2 n_z fine cells (periodic): cell l sums, in sample
+//      order, weight_i F_i phi(l + kR - pos_i) over the contiguous sample
+//      range with |l + kR - pos_i| <= W for every image k (positions increase
+//      with i: binary search) -- deterministic, no atomics on the data;
+//   4. inverse R-point FFT of the 4 fine columns (two-pass register FFT),
+//      keep the n_z signed depths m, times 1/Phi(m) (host table), store
+//      W1 [col][m mod n_z] (K4b applies 1/(nx ny nz)).
+constexpr int K3N_NT = 256;
+constexpr int K3N_W = 6;       // Gaussian half width (fine cells)
+constexpr int K3N_LDW = 5;     // fine-grid row stride (4 members + pad)
+template <int NZ>
+size_t k3n_smem(int nk) {
+  constexpr int R = 2 * NZ;
+  return ((size_t)4 * nk + (size_t)R * K3N_LDW + nk + R) * sizeof(float2) + (size_t)nk * (sizeof(float) + sizeof(int));
+}
+
+template <int NZ>
+__global__ void __launch_bounds__(K3N_NT) k3_nufft(const SarDeviceView v) {
+  constexpr int R = 2 * NZ;
+  constexpr int LDW = K3N_LDW;
+  constexpr int NIMG = (K3N_W + R) / R + 1;   // images l + kR, |k| <= NIMG, that can reach [0, R)
+  extern __shared__ __align__(16) float2 smn[];
+  const int nk = v.nk;
+  float2 *fin = smn;                                       // [4][nk]
+  float2 *grid = fin + (size_t)4 * nk;                     // [R][LDW] fine cells x members
+  float2 *wgt = grid + (size_t)R * LDW;                    // [nk] H_i w_i
+  float2 *tw = wgt + nk;                                   // [R] exp(-2 pi i n / R)
+  float *posf = reinterpret_cast<float *>(tw + R);         // [nk] fraction of the fine position
+  int *posb = reinterpret_cast<int *>(posf + nk);          // [nk] integer cell of the fine position
+  __shared__ int colof[4], first;
+  const int tid = threadIdx.x;
+  const int q = blockIdx.x, f = blockIdx.y;
+  const SarClass &c = v.cls[q];
+  const int nm = c.nmem;
+  const double kr2 = c.kr2;
+  const int ncol = v.nx * v.ny;
+  if (tid < 4) colof[tid] = tid < nm ? c.col[tid] : -1;
+  if (tid == 0) first = nk;
+  for (int i = tid; i < R; i += K3N_NT) {
+    float sn, cs;
+    sincospif(-2.0f * (float)i / (float)R, &sn, &cs);
+    tw[i] = make_float2(cs, sn);
+  }
+  __syncthreads();
+  // 1-2. columns and per-sample terms
+  const float2 *wf = v.w0 + (size_t)f * ncol * (size_t)nk;
+  for (int e = tid; e < 4 * nk; e += K3N_NT) {
+    const int m = e / nk, i = e - m * nk;
+    fin[e] = colof[m] >= 0 ? __ldcs(wf + (size_t)colof[m] * nk + i) : make_float2(0.f, 0.f);
+  }
+  const double rr = v.rref[f + v.f0] * (1.0 / TWO_PI);
+  const double kz0 = v.kz[0];
+  for (int i = tid; i < nk; i += K3N_NT) {
+    const double ki = v.k[i];
+    const double qq = __dsub_rn(__dmul_rn(__dmul_rn(4.0, ki), ki), kr2);
+    float2 w = make_float2(0.f, 0.f);
+    int pb = 0;
+    float pf = 0.f;
+    if (qq > 0.0) {
+      const double kz = __dsqrt_rn(qq);
+      if (kz >= kz0) {
+        const double t = 2.0 * __ddiv_rn(__dsub_rn(kz, kz0), v.kz_step);
+        const double tb = floor(t);
+        pb = (int)tb;
+        pf = (float)(t - tb);
+        const float2 h = filter_h(v, ki, kr2, rr, i);
+        const float jac = (float)(4.0 * ki * v.dk / (kz * v.kz_step));
+        w = make_float2(h.x * jac, h.y * jac);
+        atomicMin(&first, i);
+      }
+    }
+    wgt[i] = w;
+    posb[i] = pb;
+    posf[i] = pf;
+  }
+  __syncthreads();
+  // 3. gather (in-band samples are the suffix [first, nk), positions increasing)
+  const int i0 = first;
+  const float inv2s2 = 0.5f / v.nu_s2;
+  for (int l = tid; l < R; l += K3N_NT) {
+    float2 acc[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+    if (i0 < nk) {
+      const int pmin = posb[i0], pmax = posb[nk - 1] + 1;
+#pragma unroll 1
+      for (int k = -NIMG; k <= NIMG; ++k) {
+        const int lc = l + k * R;
+        if (lc + K3N_W < pmin || lc - K3N_W > pmax) continue;
+        // first sample with pos >= lc - W - 1 (cell resolution; the exact
+        // truncation |d| <= W is applied below)
+        int lo = i0, hi = nk;
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          if (posb[mid] < lc - K3N_W - 1) lo = mid + 1;
+          else hi = mid;
+        }
+        for (int i = lo; i < nk; ++i) {
+          const int db = lc - posb[i];
+          if (db < -K3N_W - 1) break;
+          const float d = (float)db - posf[i];
+          if (fabsf(d) > (float)K3N_W) continue;
+          const float ph = __expf(-d * d * inv2s2);
+          const float2 wi = wgt[i];
+          const float2 cw = make_float2(wi.x * ph, wi.y * ph);
+#pragma unroll
+          for (int m = 0; m < 4; ++m) acc[m] = cmac2(acc[m], cw, fin[m * nk + i]);
+        }
+      }
+    }
+#pragma unroll
+    for (int m = 0; m < 4; ++m) grid[l * LDW + m] = acc[m];
+  }
+  __syncthreads();
+  // 4. inverse fine FFT, deconvolution, signed depths -> W1 [col][m mod nz]
+  float2 *dst = v.w1 + (size_t)f * ncol * (size_t)NZ;
+  sarfft2::fft_ctx<R, 4, LDW, K3N_NT, +1, 0, true>(
+      grid, tw, tid, [&](int cc, int n) { return grid[n * LDW + cc]; }, [] {},
+      [&](int cc) {
+        const int col = colof[cc];
+        return col >= 0 ? dst + (size_t)col * NZ : nullptr;
+      },
+      [&](float2 *p, int n, float2 x) {
+        if (p && (n < NZ / 2 || n >= R - NZ / 2)) {
+          const int qz = n < NZ / 2 ? n : n - R + NZ;
+          const float d = __ldg(v.sn_dec + qz);
+          st_mid(p + qz, make_float2(x.x * d, x.y * d));
+        }
+      });
+}
+
 // ------------------------------------------------------- K3, 2-D mode ----
 // SAR_IMAGE_2D (reading R18): per Stolt mirror class (the <= 4 columns that
 // share k_r^2), k_z,i = sqrt(4 k_i^2 - k_r^2) once, then for every plane s the
@@ -845,6 +985,23 @@ namespace {
 #endif
 cudaError_t launch_k3(const SarDeviceView &v, bool ifft, cudaStream_t s, int num_sms) {
   if (v.ncls == 0) return cudaSuccess;   // every column skipped (zero Stolt output)
+  if (v.stolt_nufft) {
+    if (!ifft) return cudaErrorInvalidValue;
+    switch (v.nz) {
+#define X(N)                                                                                           \
+  case N: {                                                                                            \
+    const size_t smem = k3n_smem<N>(v.nk);                                                             \
+    if (smem > 227 * 1024) return cudaErrorInvalidValue;                                               \
+    cudaError_t e = cudaFuncSetAttribute(k3_nufft<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+    if (e != cudaSuccess) return e;                                                                    \
+    k3_nufft<N><<<dim3(v.ncls, v.F), K3N_NT, smem, s>>>(v);                                            \
+    return cudaGetLastError();                                                                         \
+  }
+      X(2) X(4) X(8) X(16) X(32) X(64) X(128) X(256) X(512)
+#undef X
+    }
+    return cudaErrorInvalidValue;
+  }
   if (K3_WS && ifft && v.nz == 512 && (v.nk & 1) == 0 && !v.force_plain && k3ws_smem<512>(v.nk) <= 225 * 1024) {
     const size_t smem = k3ws_smem<512>(v.nk);
     const int nitems_f = (v.ncls + KW_CL - 1) / KW_CL;

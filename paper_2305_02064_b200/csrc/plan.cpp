@@ -118,6 +118,7 @@ struct HostTables {
   std::vector<SarSpreadEntry> sp_ent;
   // SAR_GRID_NEAREST: pose nodes [F*P] and the CSR of entries per lattice node
   std::vector<int32_t> nn_ix, nn_iy;
+  std::vector<float> sn_dec;     // SAR_STOLT_NUFFT deconvolution table [nz]
   std::vector<int> nn_off;
   std::vector<SarNearEntry> nn_ent;
   int sp_nbx = 0, sp_nby = 0;
@@ -155,6 +156,9 @@ int host_decompose(const sar_geom_desc *g, const sar_image_desc *im, uint32_t fl
     return fail(SAR_ERR_UNSUPPORTED, "SAR_GRID_NUFFT needs 32 <= nx <= 512, ny <= 512, npx <= 512");
   if ((flags & SAR_GRID_NUFFT) && (flags & SAR_GRID_NEAREST))
     return fail(SAR_ERR_INVALID_ARG, "SAR_GRID_NEAREST and SAR_GRID_NUFFT are exclusive");
+  if ((flags & SAR_STOLT_NUFFT) && mode2d)
+    return fail(SAR_ERR_INVALID_ARG, "SAR_STOLT_NUFFT needs the 3-D k_z grid (not SAR_IMAGE_2D)");
+  if ((flags & SAR_STOLT_NUFFT) && im->nz > 512) return fail(SAR_ERR_UNSUPPORTED, "SAR_STOLT_NUFFT needs nz <= 512");
   if (!(g->dx > 0) || !(g->dy > 0) || (!mode2d && !(im->dz > 0)))
     return fail(SAR_ERR_INVALID_ARG, "pitches must be > 0");
   // K1's TMA row coordinate and the NUFFT spread entries index raw sample rows
@@ -490,6 +494,21 @@ int host_decompose(const sar_geom_desc *g, const sar_image_desc *im, uint32_t fl
     }
   }
 
+  // NUFFT Stolt (reading R21; must match oracle/stolt_nufft.py): fine grid
+  // R = 2 nz, Gaussian of variance s2 = W / (2 pi (1 - 1/(2 sigma))), W = 6;
+  // storage slot q holds the signed depth m = q (q < nz/2) or q - nz, whose
+  // deconvolution is 1/Phi(m), Phi(m) = sqrt(2 pi s2) exp(-2 pi^2 s2 m^2 / R^2)
+  T.sn_dec.clear();
+  if (flags & SAR_STOLT_NUFFT) {
+    const double s2 = 6.0 / (2.0 * M_PI * (1.0 - 1.0 / 4.0));
+    const double R = 2.0 * p->nz;
+    T.sn_dec.resize(p->nz);
+    for (int qz = 0; qz < p->nz; ++qz) {
+      const double m = qz < p->nz / 2 ? qz : qz - p->nz;
+      T.sn_dec[qz] = (float)(1.0 / (sqrt(2.0 * M_PI * s2) * exp(-2.0 * M_PI * M_PI * s2 * m * m / (R * R))));
+    }
+  }
+
   // O7 rolls and axes (reading R8)
   T.roll_x = p->nvx / 2 - p->nx / 2;
   T.roll_y = p->nvy / 2 - p->ny / 2;
@@ -615,6 +634,7 @@ int plan_create_impl(sar_plan **out, const sar_geom_desc *g, const sar_image_des
   const size_t o_sp_off = off; off += al(T.sp_off.size() * 4);
   const size_t o_sp_ent = off; off += al(T.sp_ent.size() * sizeof(SarSpreadEntry));
   const size_t o_nn_off = off; off += al(T.nn_off.size() * 4);
+  const size_t o_sn = off; off += al(T.sn_dec.size() * 4);
   const size_t o_nn_ent = off; off += al(T.nn_ent.size() * sizeof(SarNearEntry));
   ce = cudaMalloc(&p->d_tables, off);
   if (ce != cudaSuccess) {
@@ -643,6 +663,7 @@ int plan_create_impl(sar_plan **out, const sar_geom_desc *g, const sar_image_des
       (ce = up(o_sp_off, T.sp_off.data(), T.sp_off.size() * 4)) != cudaSuccess ||
       (ce = up(o_sp_ent, T.sp_ent.data(), T.sp_ent.size() * sizeof(SarSpreadEntry))) != cudaSuccess ||
       (ce = up(o_nn_off, T.nn_off.data(), T.nn_off.size() * 4)) != cudaSuccess ||
+      (ce = up(o_sn, T.sn_dec.data(), T.sn_dec.size() * 4)) != cudaSuccess ||
       (ce = up(o_nn_ent, T.nn_ent.data(), T.nn_ent.size() * sizeof(SarNearEntry))) != cudaSuccess) {
     free_plan(p);
     return cuda_fail(ce, "table upload");
@@ -690,6 +711,8 @@ int plan_create_impl(sar_plan **out, const sar_geom_desc *g, const sar_image_des
   v.sp_ent = (const SarSpreadEntry *)(base + o_sp_ent);
   v.tw_f = (const float2 *)(base + o_tw) + T.tw_f_off;
   v.nearest = (flags & SAR_GRID_NEAREST) ? 1 : 0;
+  v.stolt_nufft = (flags & SAR_STOLT_NUFFT) ? 1 : 0;
+  v.sn_dec = (const float *)(base + o_sn);
   v.nn_off = (const int *)(base + o_nn_off);
   v.nn_ent = (const SarNearEntry *)(base + o_nn_ent);
   v.cls = (const SarClass *)(base + o_cl);
@@ -795,7 +818,7 @@ int sar_plan_create_slab(sar_plan **out, const sar_geom_desc *g, const sar_image
   if (!slab || !g || !im) return fail(SAR_ERR_INVALID_ARG, "slab, geometry or image descriptor is NULL");
   const int G = slab->world, r = slab->rank;
   if (G < 1 || G > SAR_MAX_SLAB || r < 0 || r >= G) return fail(SAR_ERR_INVALID_ARG, "slab rank/world out of range");
-  if (flags & (SAR_IMAGE_2D | SAR_GRID_NUFFT | SAR_GRID_NEAREST | SAR_REPORT_PEAK | SAR_CUDA_GRAPH))
+  if (flags & (SAR_IMAGE_2D | SAR_GRID_NUFFT | SAR_GRID_NEAREST | SAR_STOLT_NUFFT | SAR_REPORT_PEAK | SAR_CUDA_GRAPH))
     return fail(SAR_ERR_UNSUPPORTED, "slab plans support the 3-D RASTER path only");
   if (g->n_frames != 1) return fail(SAR_ERR_INVALID_ARG, "slab plans reconstruct one image (n_frames == 1)");
   if (im->nx % G || im->ny % G || im->nz % G || im->nx / G < 1 || im->nz / G < 1)
@@ -1023,6 +1046,8 @@ int sar_debug_stage(sar_plan *p, int32_t stage, const void *d_data, void *d_out,
   if (!p) return fail(SAR_ERR_INVALID_ARG, "plan is NULL");
   if (stage < 1 || stage > 4) return fail(SAR_ERR_INVALID_ARG, "stage must be 1..4");
   if (stage == 1 && (p->flags & SAR_GRID_NUFFT)) return fail(SAR_ERR_INVALID_ARG, "no planar lattice in NUFFT mode");
+  if (stage == 3 && (p->flags & SAR_STOLT_NUFFT))
+    return fail(SAR_ERR_INVALID_ARG, "no uniform k_z grid with SAR_STOLT_NUFFT (debug stage 3)");
   if (p->slab_world) return fail(SAR_ERR_INVALID_ARG, "slab plans run sar_slab_stage");
   if (p->F == 0) return SAR_OK;
   if (!d_data || !d_out) return fail(SAR_ERR_INVALID_ARG, "NULL pointer");

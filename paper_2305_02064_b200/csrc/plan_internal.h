@@ -72,6 +72,8 @@ struct SarDeviceView {
   const int *sp_off;               // [F*sp_nby*sp_nbx + 1] CSR offsets
   const SarSpreadEntry *sp_ent;    // entries
   const float2 *tw_f;              // [2 nx] exp(-2 pi i m / (2 nx)) (fine x-FFT)
+  int stolt_nufft;                 // SAR_STOLT_NUFFT (reading R21)
+  const float *sn_dec;             // [nz] 1/Phi(m) of the depth in storage slot m mod nz
   int nearest;                     // SAR_GRID_NEAREST
   const int *nn_off;               // [F*ny*nx + 1] CSR offsets per lattice node (frame, vy, vx)
   const SarNearEntry *nn_ent;      // entries

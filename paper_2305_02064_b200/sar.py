@@ -25,6 +25,7 @@ SAR_REPORT_PEAK = 32
 SAR_FORCE_PLAIN = 64
 SAR_CUDA_GRAPH = 128
 SAR_GRID_NEAREST = 256
+SAR_STOLT_NUFFT = 512
 STAGE_NAMES = ("K1 correct+x-FFT", "K2 y-FFT", "K3 filter+Stolt+z-IFFT", "K4a y-IFFT", "K4b x-IFFT+|.|")
 
 

@@ -879,3 +879,70 @@ def test_nearest_deterministic_and_rejections():
     with pytest.raises(sar.SarError) as ei:
         sar.Plan.from_scene(sc, flags=sar.SAR_GRID_NEAREST | sar.SAR_GRID_NUFFT)
     assert ei.value.status == 1
+
+
+# ---- NUFFT Stolt step (SAR_STOLT_NUFFT, reading R21) -----------------------
+@pytest.mark.parametrize("name", ["tiny", "small", "freehand"])
+def test_stolt_nufft_parity(name):
+    from oracle import stolt_nufft as sn
+    sc = scenes.make_scene(name)
+    d, s = _data(sc)
+    want, _ = sn.reconstruct_stolt_nufft(s, sc)
+    with sar.Plan.from_scene(sc, flags=sar.SAR_STOLT_NUFFT) as plan:
+        got = plan.reconstruct(d).cpu().numpy()
+        with pytest.raises(sar.SarError):
+            plan.debug_stage(3, d)
+    e2, einf = errs(got, want)
+    assert e2 <= E2_BAR and einf <= EINF_BAR, (name, e2, einf)
+
+
+STOLT_NUFFT_EDGE = [
+    # nz = 8: the fine grid (16 cells) is narrower than the Gaussian (13 cells): several images per cell
+    dict(npx=16, npy=12, nx=16, ny=16, nk=13, nz=8, dz=6e-3, frames=2),
+    dict(npx=12, npy=8, nx=16, ny=8, nk=40, nz=4, dz=1e-2, frames=1),
+    # n_k below n_z, window deeper than the band
+    dict(npx=24, npy=16, nx=32, ny=32, nk=24, nz=64, dz=3e-3, frames=1),
+]
+
+
+@pytest.mark.parametrize("kw", STOLT_NUFFT_EDGE, ids=lambda kw: f"nk{kw['nk']}_nz{kw['nz']}")
+def test_stolt_nufft_edge_cases(kw):
+    from oracle import stolt_nufft as sn
+    sc = scenes.raster_scene(kw["npx"], kw["npy"], kw["nx"], kw["ny"], kw["nk"], kw["nz"], kw["dz"], 0.15,
+                             jitter_xy=0.3e-3, jitter_z=1e-3, n_frames=kw["frames"], seed=9)
+    rng = np.random.default_rng(9)
+    sc.scat_pos = [np.column_stack([rng.uniform(-0.01, 0.01, 3), rng.uniform(-0.01, 0.01, 3),
+                                    rng.uniform(0.13, 0.17, 3)]) for _ in range(sc.n_frames)]
+    sc.scat_amp = [np.ones(3, complex) for _ in range(sc.n_frames)]
+    d, s = _data(sc)
+    want, _ = sn.reconstruct_stolt_nufft(s, sc)
+    with sar.Plan.from_scene(sc, flags=sar.SAR_STOLT_NUFFT) as plan:
+        got = plan.reconstruct(d).cpu().numpy()
+    e2, einf = errs(got, want)
+    assert e2 <= E2_BAR and einf <= EINF_BAR, (kw, e2, einf)
+
+
+def test_stolt_nufft_large_agrees_with_linear_and_is_deterministic(large_case):
+    """Large (the bench config): the full fp64 NUFFT-Stolt oracle is too slow
+    in Python, so the GPU image is checked against the linear-pull GPU image
+    (both approximate the same inversion: NCC >= 0.98, oracle property pinned
+    in tests/test_oracle_stolt_nufft.py) and for determinism."""
+    sc, d, want = large_case
+    with sar.Plan.from_scene(sc, flags=sar.SAR_STOLT_NUFFT) as plan:
+        a = plan.reconstruct(d)
+        b = plan.reconstruct(d)
+        assert torch.equal(a, b)
+        a = a.cpu().numpy().astype(np.float64)
+    ncc = float(np.sum(a * want) / (np.linalg.norm(a) * np.linalg.norm(want)))
+    assert ncc >= 0.98, ncc
+
+
+def test_stolt_nufft_rejections():
+    sc = scenes.make_scene("tiny")
+    with pytest.raises(sar.SarError) as ei:
+        sar.Plan.from_scene(sc, flags=sar.SAR_STOLT_NUFFT, z_planes=[0.25])
+    assert ei.value.status == 1
+    import dataclasses
+    with pytest.raises(sar.SarError) as ei:
+        sar.Plan.from_scene(dataclasses.replace(sc, nz=1024), flags=sar.SAR_STOLT_NUFFT)
+    assert ei.value.status == 3
