@@ -730,22 +730,22 @@ constexpr int K3N_LDW = 5;     // fine-grid row stride (4 members + pad)
 template <int NZ>
 size_t k3n_smem(int nk) {
   constexpr int R = 2 * NZ;
-  return ((size_t)4 * nk + (size_t)R * K3N_LDW + nk + R) * sizeof(float2) + (size_t)nk * (sizeof(float) + sizeof(int));
+  return ((size_t)R * K3N_LDW + 5 * (size_t)nk) * sizeof(float2) + (size_t)nk * (sizeof(float) + sizeof(int)) +
+         (size_t)(R + 4 * K3N_W + 8) * sizeof(int);
 }
 
 template <int NZ>
-__global__ void __launch_bounds__(K3N_NT) k3_nufft(const SarDeviceView v) {
+__global__ void __launch_bounds__(K3N_NT, 3) k3_nufft(const SarDeviceView v) {
   constexpr int R = 2 * NZ;
   constexpr int LDW = K3N_LDW;
-  constexpr int NIMG = (K3N_W + R) / R + 1;   // images l + kR, |k| <= NIMG, that can reach [0, R)
   extern __shared__ __align__(16) float2 smn[];
   const int nk = v.nk;
-  float2 *fin = smn;                                       // [4][nk]
-  float2 *grid = fin + (size_t)4 * nk;                     // [R][LDW] fine cells x members
-  float2 *wgt = grid + (size_t)R * LDW;                    // [nk] H_i w_i
-  float2 *tw = wgt + nk;                                   // [R] exp(-2 pi i n / R)
-  float *posf = reinterpret_cast<float *>(tw + R);         // [nk] fraction of the fine position
+  float2 *grid = smn;                                      // [R][LDW] fine cells x members
+  float2 *fin = grid + (size_t)R * LDW;                    // [4][nk] member columns
+  float2 *wgt = fin + (size_t)4 * nk;                      // [nk] H_i w_i
+  float *posf = reinterpret_cast<float *>(wgt + nk);       // [nk] fraction of the fine position
   int *posb = reinterpret_cast<int *>(posf + nk);          // [nk] integer cell of the fine position
+  int *cs = posb + nk;                                     // [<= R + 4W + 8] sample range starts
   __shared__ int colof[4], first;
   const int tid = threadIdx.x;
   const int q = blockIdx.x, f = blockIdx.y;
@@ -755,20 +755,18 @@ __global__ void __launch_bounds__(K3N_NT) k3_nufft(const SarDeviceView v) {
   const int ncol = v.nx * v.ny;
   if (tid < 4) colof[tid] = tid < nm ? c.col[tid] : -1;
   if (tid == 0) first = nk;
-  for (int i = tid; i < R; i += K3N_NT) {
-    float sn, cs;
-    sincospif(-2.0f * (float)i / (float)R, &sn, &cs);
-    tw[i] = make_float2(cs, sn);
-  }
   __syncthreads();
-  // 1-2. columns and per-sample terms
   const float2 *wf = v.w0 + (size_t)f * ncol * (size_t)nk;
+  // 1-2. columns and per-sample terms (the fine grid starts at zero: cells
+  //      no sample reaches are not written by the gather)
+  for (int e = tid; e < R * LDW; e += K3N_NT) grid[e] = make_float2(0.f, 0.f);
   for (int e = tid; e < 4 * nk; e += K3N_NT) {
     const int m = e / nk, i = e - m * nk;
     fin[e] = colof[m] >= 0 ? __ldcs(wf + (size_t)colof[m] * nk + i) : make_float2(0.f, 0.f);
   }
   const double rr = v.rref[f + v.f0] * (1.0 / TWO_PI);
   const double kz0 = v.kz[0];
+  const double inv_step = 1.0 / v.kz_step;
   for (int i = tid; i < nk; i += K3N_NT) {
     const double ki = v.k[i];
     const double qq = __dsub_rn(__dmul_rn(__dmul_rn(4.0, ki), ki), kr2);
@@ -776,15 +774,21 @@ __global__ void __launch_bounds__(K3N_NT) k3_nufft(const SarDeviceView v) {
     int pb = 0;
     float pf = 0.f;
     if (qq > 0.0) {
-      const double kz = __dsqrt_rn(qq);
+      const double kz = __dsqrt_rn(qq);   // IEEE: the in-band decision is the oracle's
       if (kz >= kz0) {
-        const double t = 2.0 * __ddiv_rn(__dsub_rn(kz, kz0), v.kz_step);
+        const double t = 2.0 * (kz - kz0) * inv_step;
         const double tb = floor(t);
         pb = (int)tb;
         pf = (float)(t - tb);
-        const float2 h = filter_h(v, ki, kr2, rr, i);
-        const float jac = (float)(4.0 * ki * v.dk / (kz * v.kz_step));
-        w = make_float2(h.x * jac, h.y * jac);
+        // filter H = k_z e^{+j k_z R_ref} / P (reading R2), phase in turns
+        double turns = kz * rr;
+        turns -= rint(turns);
+        float sn, cs;
+        __sincosf((float)turns * 6.28318530717958647692f, &sn, &cs);
+        // Jacobian 4 k dk / (k_z dk_z) times k_z of the filter: 4 k dk / dk_z
+        const float amp = (float)(4.0 * ki * v.dk * inv_step);
+        w = make_float2(amp * cs, amp * sn);
+        if (v.pinv) w = cmul(w, v.pinv[i]);
         atomicMin(&first, i);
       }
     }
@@ -793,29 +797,47 @@ __global__ void __launch_bounds__(K3N_NT) k3_nufft(const SarDeviceView v) {
     posf[i] = pf;
   }
   __syncthreads();
-  // 3. gather (in-band samples are the suffix [first, nk), positions increasing)
+  // 3. gather (in-band samples are the suffix [first, nk), positions
+  //    increasing).  cs[j] = first sample with cell >= vlo + j - W - 1, so the
+  //    samples within W of virtual cell lc are [cs[lc - vlo], cs[lc - vlo + 2W + 2]).
+  //    Work item = (fine cell touched by some sample, quarter of its sample
+  //    range): the touched cells are the circular range of the virtual cells
+  //    [pos_min - W, pos_max + W] mod R; four consecutive lanes take the four
+  //    quarters of one cell and sum all four members (positions, Gaussian and
+  //    weights shared), then add their partial sums in a fixed shuffle order
+  //    -- deterministic.  Every image p + kR of the cell is summed.
   const int i0 = first;
   const float inv2s2 = 0.5f / v.nu_s2;
-  for (int l = tid; l < R; l += K3N_NT) {
-    float2 acc[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
-    if (i0 < nk) {
-      const int pmin = posb[i0], pmax = posb[nk - 1] + 1;
-#pragma unroll 1
-      for (int k = -NIMG; k <= NIMG; ++k) {
-        const int lc = l + k * R;
-        if (lc + K3N_W < pmin || lc - K3N_W > pmax) continue;
-        // first sample with pos >= lc - W - 1 (cell resolution; the exact
-        // truncation |d| <= W is applied below)
-        int lo = i0, hi = nk;
-        while (lo < hi) {
-          const int mid = (lo + hi) >> 1;
-          if (posb[mid] < lc - K3N_W - 1) lo = mid + 1;
-          else hi = mid;
-        }
-        for (int i = lo; i < nk; ++i) {
-          const int db = lc - posb[i];
-          if (db < -K3N_W - 1) break;
-          const float d = (float)db - posf[i];
+  if (i0 < nk) {
+    const int pmin = posb[i0], pmax = posb[nk - 1];
+    const int vlo = pmin - K3N_W, vhi = pmax + 1 + K3N_W;
+    const int nvc = vhi - vlo + 1;                      // virtual cells
+    const int ncell = nvc < R ? nvc : R;                // physical cells touched
+    const int ncs = nvc + 2 * K3N_W + 3;
+    for (int j = tid; j < ncs; j += K3N_NT) {
+      const int key = vlo + j - K3N_W - 1;
+      int lo = i0, hi = nk;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (posb[mid] < key) lo = mid + 1;
+        else hi = mid;
+      }
+      cs[j] = lo;
+    }
+    __syncthreads();
+    const int nit = (4 * ncell + 31) & ~31;   // whole warps (shuffles below)
+    for (int it = tid; it < nit; it += K3N_NT) {
+      const int qt = it & 3, jc = it >> 2;
+      const bool live = jc < ncell;
+      const int p = live ? ((vlo + jc) % R + R) % R : 0;
+      float2 acc[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+      // images p + kR inside [vlo, vhi]: the first is vlo + ((p - vlo) mod R)
+      for (int lc = live ? vlo + ((p - vlo) % R + R) % R : vhi + 1; lc <= vhi; lc += R) {
+        const int j = lc - vlo;
+        const int lo = cs[j], n = cs[j + 2 * K3N_W + 2] - lo;
+        const int a0 = lo + (n * qt) / 4, a1 = lo + (n * (qt + 1)) / 4;
+        for (int i = a0; i < a1; ++i) {
+          const float d = (float)(lc - posb[i]) - posf[i];
           if (fabsf(d) > (float)K3N_W) continue;
           const float ph = __expf(-d * d * inv2s2);
           const float2 wi = wgt[i];
@@ -824,15 +846,24 @@ __global__ void __launch_bounds__(K3N_NT) k3_nufft(const SarDeviceView v) {
           for (int m = 0; m < 4; ++m) acc[m] = cmac2(acc[m], cw, fin[m * nk + i]);
         }
       }
-    }
 #pragma unroll
-    for (int m = 0; m < 4; ++m) grid[l * LDW + m] = acc[m];
+      for (int m = 0; m < 4; ++m) {
+        acc[m].x += __shfl_xor_sync(0xffffffffu, acc[m].x, 1);
+        acc[m].y += __shfl_xor_sync(0xffffffffu, acc[m].y, 1);
+        acc[m].x += __shfl_xor_sync(0xffffffffu, acc[m].x, 2);
+        acc[m].y += __shfl_xor_sync(0xffffffffu, acc[m].y, 2);
+      }
+      if (live && qt == 0) {
+#pragma unroll
+        for (int m = 0; m < 4; ++m) grid[p * LDW + m] = acc[m];
+      }
+    }
   }
   __syncthreads();
   // 4. inverse fine FFT, deconvolution, signed depths -> W1 [col][m mod nz]
   float2 *dst = v.w1 + (size_t)f * ncol * (size_t)NZ;
   sarfft2::fft_ctx<R, 4, LDW, K3N_NT, +1, 0, true>(
-      grid, tw, tid, [&](int cc, int n) { return grid[n * LDW + cc]; }, [] {},
+      grid, v.tw_z2, tid, [&](int cc, int n) { return grid[n * LDW + cc]; }, [] {},
       [&](int cc) {
         const int col = colof[cc];
         return col >= 0 ? dst + (size_t)col * NZ : nullptr;

@@ -124,7 +124,7 @@ struct HostTables {
   int sp_nbx = 0, sp_nby = 0;
   size_t tw_f_off = 0;
   std::vector<double> kx, ky, kz, kd, rref;
-  size_t tw_y_off = 0, tw_z_off = 0;
+  size_t tw_y_off = 0, tw_z_off = 0, tw_z2_off = 0;
   int roll_x = 0, roll_y = 0;
   double k0 = 0, dk = 0, dkz = 0;
 };
@@ -275,6 +275,8 @@ int host_decompose(const sar_geom_desc *g, const sar_image_desc *im, uint32_t fl
   twiddles(T.tw, p->ny);
   T.tw_z_off = T.tw.size() / 2;
   twiddles(T.tw, p->nz);
+  T.tw_z2_off = T.tw.size() / 2;
+  if (flags & SAR_STOLT_NUFFT) twiddles(T.tw, 2 * p->nz);   // the NUFFT Stolt fine grid
 
   // Stolt mirror classes: k_r^2, member columns and a superset of the in-band
   // k_z bins.  u(j) = (sqrt(k_z,j^2 + k_r^2)/2 - k_0)/dk is monotone in j; the
@@ -721,6 +723,7 @@ int plan_create_impl(sar_plan **out, const sar_geom_desc *g, const sar_image_des
   v.tw_x = (const float2 *)(base + o_tw);
   v.tw_y = (const float2 *)(base + o_tw) + T.tw_y_off;
   v.tw_z = (const float2 *)(base + o_tw) + T.tw_z_off;
+  v.tw_z2 = (const float2 *)(base + o_tw) + T.tw_z2_off;
   v.k0 = T.k0;
   v.dk = T.dk;
   v.inv_dk = 1.0 / T.dk;

@@ -93,6 +93,7 @@ struct SarDeviceView {
   const float2 *tw_x;   // [nx] exp(-2 pi i m/nx)
   const float2 *tw_y;   // [ny]
   const float2 *tw_z;   // [nz]
+  const float2 *tw_z2;  // [2 nz] (SAR_STOLT_NUFFT fine grid)
   double k0, dk, inv_dk;
   double kz_top, kz_step;  // k_z[nz-1] = 2 k_max and the k_z bin width (reading R5)
   double stolt_delta;   // decision guard band of the fast Stolt path (common.cuh)
