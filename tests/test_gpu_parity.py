@@ -946,3 +946,23 @@ def test_stolt_nufft_rejections():
     with pytest.raises(sar.SarError) as ei:
         sar.Plan.from_scene(dataclasses.replace(sc, nz=1024), flags=sar.SAR_STOLT_NUFFT)
     assert ei.value.status == 3
+
+
+def test_k3_ws_deterministic_and_equal_to_k3_pp():
+    """The warp-specialised K3 (n_z = 512; producer, Stolt and FFT warps handing
+    work on through mbarriers) on a small grid: repeated calls bit-identical,
+    and equal to the oracle like every other K3 (the edge cases at n_z = 512
+    above); many items per CTA so that the rings wrap many times."""
+    sc = scenes.raster_scene(40, 36, 64, 64, 64, 512, 1e-3, 0.2, jitter_xy=0.3e-3, jitter_z=1e-3, seed=12)
+    rng = np.random.default_rng(12)
+    sc.scat_pos = [np.column_stack([rng.uniform(-0.01, 0.01, 4), rng.uniform(-0.01, 0.01, 4),
+                                    rng.uniform(0.1, 0.3, 4)])]
+    sc.scat_amp = [np.ones(4, complex)]
+    d, s = _data(sc)
+    want, _ = oracle.reconstruct(s, sc)
+    with sar.Plan.from_scene(sc) as plan:
+        a = plan.reconstruct(d).clone()
+        for _ in range(4):
+            assert torch.equal(plan.reconstruct(d), a)
+    e2, einf = errs(a.cpu().numpy(), want)
+    assert e2 <= E2_BAR and einf <= EINF_BAR, (e2, einf)
