@@ -42,10 +42,12 @@ def smi():
 
 for rep in range(2):
     for spec in sys.argv[3:]:
-        tag, _, path = spec.partition(":")
+        tag, _, rest = spec.partition(":")
+        path, _, fl = rest.partition(":")
+        flags = int(fl) if fl else 0
         sarmod._lib = None
         sarmod.load_library(path or sarmod.LIB_PATH)
-        with sar.Plan.from_scene(sc, flags=sar.SAR_PROFILE_STAGES) as plan:
+        with sar.Plan.from_scene(sc, flags=sar.SAR_PROFILE_STAGES | flags) as plan:
             for _ in range(3):
                 plan.reconstruct(d, out)
             torch.cuda.synchronize()
