@@ -18,6 +18,25 @@ using sarfft::cadd;
 using sarfft::cmul;
 
 constexpr int KC = 16;  // k (or z) chunk: 16 complex64 = one 128-byte line
+
+// SAR_CHECKED builds (`build.py --variant=checked -DSAR_CHECKED`, testing only;
+// compute-sanitizer is closed on the GPU pool): every global store / bulk copy
+// of the path and the shared-memory indices of the warp-specialised kernels
+// are checked against their buffer and trap with a message when outside
+#ifdef SAR_CHECKED
+#define SAR_ASSERT(c)                                                                        \
+  do {                                                                                       \
+    if (!(c)) {                                                                              \
+      printf("SAR_CHECKED %s:%d block %d thread %d: %s\n", __FILE__, __LINE__, blockIdx.x,   \
+             threadIdx.x, #c);                                                               \
+      __trap();                                                                              \
+    }                                                                                        \
+  } while (0)
+#else
+#define SAR_ASSERT(c) ((void)0)
+#endif
+// p inside [base, base + n elements)
+#define SAR_IN(p, base, n) SAR_ASSERT((p) >= (base) && (p) < (base) + (n))
 constexpr double TWO_PI = 6.283185307179586476925286766559;
 constexpr double BAND_EPS = 1e-9;  // reading R9
 

@@ -108,6 +108,7 @@ __global__ void __launch_bounds__(nt_for(NX), minb_for(NX))
         const int h = vx >> v.slab_lg, al = vx & ((1 << v.slab_lg) - 1);
         v.slab_dst[h][(((size_t)blockIdx.y << v.slab_lg) + al) * v.nk + k] = tile[item];
       } else {
+        SAR_IN(out + (size_t)vx * v.nk + k, v.w0, v.w0_elems);
         out[(size_t)vx * v.nk + k] = tile[item];
       }
     }
@@ -152,6 +153,7 @@ __global__ void __launch_bounds__(nt_for(NX), minb_for(NX))
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           en[u] = q + u < q1 ? v.nn_ent[q + u] : SarNearEntry{0, 0.f};
+          SAR_ASSERT(en[u].row >= 0 && (size_t)en[u].row < v.raw_rows);
           val[u] = q + u < q1 ? __ldcs(s + (size_t)en[u].row * v.nk + k) : make_float2(0.f, 0.f);
         }
 #pragma unroll
@@ -179,7 +181,10 @@ __global__ void __launch_bounds__(nt_for(NX), minb_for(NX))
     const int item = tid + e * NT;
     if (ITEMS % NT != 0 && item >= ITEMS) continue;
     const int kk = item & (KC - 1), vx = item >> 4;
-    if (kbase + kk < v.nk) out[(size_t)vx * v.nk + kbase + kk] = tile[item];
+    if (kbase + kk < v.nk) {
+      SAR_IN(out + (size_t)vx * v.nk + kbase + kk, v.w0, v.w0_elems);
+      out[(size_t)vx * v.nk + kbase + kk] = tile[item];
+    }
   }
 }
 
@@ -414,6 +419,7 @@ __global__ void __launch_bounds__(K1_NT + 32, 1)
               const int h = m >> v.slab_lg, al = m & ((1 << v.slab_lg) - 1);
               __stcs(v.slab_dst[h] + (((size_t)vyl << v.slab_lg) + al) * v.nk + kc * C + c, x);
             } else {
+              SAR_IN(out + (size_t)m * v.nk + c, v.w0, v.w0_elems);
               st_mid(out + (size_t)m * v.nk + c, x);
             }
           }

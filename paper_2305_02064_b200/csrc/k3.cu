@@ -159,7 +159,10 @@ __global__ void __launch_bounds__(K3C_NT, 8) k3_class(const SarDeviceView v) {
           return col >= 0 ? dst + (size_t)col * NZ : nullptr;
         },
         [&](float2 *p, int m, float2 x) {
-          if (p) st_mid(p + m, x);
+          if (p) {
+            SAR_IN(p + m, v.w1, v.w1_elems);
+            st_mid(p + m, x);
+          }
         });
   } else {
     for (int i = tid; i < CC * NZ; i += K3C_NT) {
@@ -290,7 +293,10 @@ __device__ __forceinline__ void k3pp_consume(const SarDeviceView &v, int nitems_
             return col >= 0 ? dst + (size_t)col * NZ : nullptr;
           },
           [&](float2 *p, int m, float2 x) {
-            if (p) st_mid(p + m, x);
+            if (p) {
+            SAR_IN(p + m, v.w1, v.w1_elems);
+            st_mid(p + m, x);
+          }
           },
           1 + g);
     } else {
@@ -398,7 +404,11 @@ __global__ void __launch_bounds__(K3P_NG * K3P_G + 32, 1) k3_pp(const SarDeviceV
       if (lane == 0) sartma::mbar_arrive_expect_tx(&full[st], (uint32_t)nld * (uint32_t)nk * 8u);
       __syncwarp();
       const float2 *wf = v.w0 + (size_t)f * ncol * (size_t)nk;
-      if (ld) sartma::bulk_g2s(fin + lane * nk, wf + (size_t)h.colof[lane] * nk, (uint32_t)nk * 8u, &full[st]);
+      if (ld) {
+        SAR_ASSERT(h.colof[lane] >= 0 && h.colof[lane] < ncol);
+        SAR_IN(wf + (size_t)h.colof[lane] * nk + nk - 1, v.w0, v.w0_elems);
+        sartma::bulk_g2s(fin + lane * nk, wf + (size_t)h.colof[lane] * nk, (uint32_t)nk * 8u, &full[st]);
+      }
       cur = nxt;
     }
     return;
@@ -571,7 +581,11 @@ __global__ void __launch_bounds__(KW_NT, 1) k3_ws(const SarDeviceView v, int nit
       if (lane == 0) sartma::mbar_arrive_expect_tx(&full[st], (uint32_t)nld * (uint32_t)nk * 8u);
       __syncwarp();
       const float2 *wf = v.w0 + (size_t)f * ncol * (size_t)nk;
-      if (ld) sartma::bulk_g2s(fin + lane * nk, wf + (size_t)h.colof[lane] * nk, (uint32_t)nk * 8u, &full[st]);
+      if (ld) {
+        SAR_ASSERT(h.colof[lane] >= 0 && h.colof[lane] < ncol);
+        SAR_IN(wf + (size_t)h.colof[lane] * nk + nk - 1, v.w0, v.w0_elems);
+        sartma::bulk_g2s(fin + lane * nk, wf + (size_t)h.colof[lane] * nk, (uint32_t)nk * 8u, &full[st]);
+      }
       cur = nxt;
     }
     return;
@@ -629,6 +643,7 @@ __global__ void __launch_bounds__(KW_NT, 1) k3_ws(const SarDeviceView v, int nit
           const int sl = h.mslot[cl][m];
           float2 o = make_float2(0.f, 0.f);
           if (ok) o = cmac2(cmul2(wl, fin[sl * nk + i0]), wu, fin[sl * nk + i0 + 1]);
+          SAR_ASSERT(sl >= 0 && sl < KW_WF && j >= 0 && j < NZ);
           cols[sl * G::NZP + kw_pad(j)] = o;
         }
       }
@@ -697,6 +712,7 @@ __global__ void __launch_bounds__(KW_NT, 1) k3_ws(const SarDeviceView v, int nit
       float2 *dst = v.w1 + ((size_t)f * ncol + colof) * (size_t)NZ;
       sarfft2::static_for<0, H>([&](auto P) {
         constexpr int p = decltype(P)::value;
+        SAR_IN(dst + ip + 2 * sarfft2::freq_at(H, p) * 16, v.w1, v.w1_elems);
         st_mid(dst + ip + 2 * sarfft2::freq_at(H, p) * 16, g[p]);
       });
     }
@@ -822,6 +838,7 @@ __global__ void __launch_bounds__(K3N_NT, 3) k3_nufft(const SarDeviceView v) {
         if (posb[mid] < key) lo = mid + 1;
         else hi = mid;
       }
+      SAR_ASSERT(j < R + 4 * K3N_W + 8);
       cs[j] = lo;
     }
     __syncthreads();
@@ -834,6 +851,7 @@ __global__ void __launch_bounds__(K3N_NT, 3) k3_nufft(const SarDeviceView v) {
       // images p + kR inside [vlo, vhi]: the first is vlo + ((p - vlo) mod R)
       for (int lc = live ? vlo + ((p - vlo) % R + R) % R : vhi + 1; lc <= vhi; lc += R) {
         const int j = lc - vlo;
+        SAR_ASSERT(j >= 0 && j + 2 * K3N_W + 2 < ncs);
         const int lo = cs[j], n = cs[j + 2 * K3N_W + 2] - lo;
         const int a0 = lo + (n * qt) / 4, a1 = lo + (n * (qt + 1)) / 4;
         for (int i = a0; i < a1; ++i) {
@@ -854,6 +872,7 @@ __global__ void __launch_bounds__(K3N_NT, 3) k3_nufft(const SarDeviceView v) {
         acc[m].y += __shfl_xor_sync(0xffffffffu, acc[m].y, 2);
       }
       if (live && qt == 0) {
+        SAR_ASSERT(p >= 0 && p < R);
 #pragma unroll
         for (int m = 0; m < 4; ++m) grid[p * LDW + m] = acc[m];
       }
@@ -872,6 +891,7 @@ __global__ void __launch_bounds__(K3N_NT, 3) k3_nufft(const SarDeviceView v) {
         if (p && (n < NZ / 2 || n >= R - NZ / 2)) {
           const int qz = n < NZ / 2 ? n : n - R + NZ;
           const float d = __ldg(v.sn_dec + qz);
+          SAR_IN(p + qz, v.w1, v.w1_elems);
           st_mid(p + qz, make_float2(x.x * d, x.y * d));
         }
       });

@@ -141,6 +141,8 @@ __global__ void __launch_bounds__(K4bFft<NX>::NTC + 32)
             const int ix = (a - rx) & (NX - 1);
             const float mag = fast_abs(o) * sc;
             if constexpr (PEAK) pk = fmaxf(pk, mag);
+            SAR_ASSERT(v.img_elems == 0 || (rowp + ix >= reinterpret_cast<OT *>(img) &&
+                                             rowp + ix < reinterpret_cast<OT *>(img) + v.img_elems));
             if constexpr (CPLX) {
               __stcs(reinterpret_cast<float2 *>(rowp) + ix, make_float2(o.x * sc, o.y * sc));
             } else {
@@ -197,6 +199,7 @@ __global__ void __launch_bounds__(nt_for(NX), minb_for(NX))
     const int xs = (ix + rx) & (NX - 1);
     const float2 o = tile[xs * LD + zz];
     const size_t off = ((size_t)(f * v.nz_img + m) * v.ny + iy) * NX + ix;
+    SAR_ASSERT(v.img_elems == 0 || off < v.img_elems);
     const float mag = fast_abs(o) * sc;
     pk = fmaxf(pk, mag);
     if constexpr (CPLX) {

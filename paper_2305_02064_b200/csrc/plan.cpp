@@ -763,6 +763,10 @@ int plan_create_impl(sar_plan **out, const sar_geom_desc *g, const sar_image_des
   v.wh = p->d_wh;
   v.force_plain = (flags & SAR_FORCE_PLAIN) ? 1 : 0;
   v.w1 = p->d_w1;
+  v.w0_elems = n0;
+  v.w1_elems = n1;
+  v.raw_rows = (size_t)F * p->npair * P;
+  v.img_elems = slab_world > 0 ? 0 : (size_t)F * p->nz * p->ny * p->nx;
 
   p->num_sms = prop.multiProcessorCount;
   sar_build_tensor_maps(p);

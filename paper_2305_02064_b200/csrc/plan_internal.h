@@ -101,6 +101,7 @@ struct SarDeviceView {
   int force_plain;      // SAR_FORCE_PLAIN: the plain (non-TMA, non-persistent) kernels
   float img_scale;      // 1/(nx ny nz)
   unsigned *peak;       // [F] max |voxel| bits per frame (SAR_REPORT_PEAK) or nullptr
+  size_t w0_elems, w1_elems, raw_rows, img_elems;   // buffer sizes (SAR_CHECKED builds; img_elems 0: unchecked)
   float2 *w0;           // [F][ny][nx][nk]  planar lattice -> spectrum
   float2 *w1;           // [F][ny][nx][nz]  Stolt output -> partial inverse
 };
