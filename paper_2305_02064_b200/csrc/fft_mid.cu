@@ -186,10 +186,11 @@ __global__ void __launch_bounds__(mid2_ntc<N>() + 32)
           if constexpr (TST) {
             work[m * KC + c] = v;
           } else {
-            if (c < cmax && (DIR > 0 || (unsigned)((m + lbo) & (N - 1)) < span))
+            if (c < cmax && (DIR > 0 || (unsigned)((m + lbo) & (N - 1)) < span)) {
               SAR_ASSERT(SLAB || (base + (size_t)m * row + c >= data &&
                                   base + (size_t)m * row + c < data + (size_t)(nitems / nchunk / nx) * N * nx * inner));
               st_mid(base + (size_t)m * row + c, v);
+            }
           }
         });
     if constexpr (TST) {
