@@ -445,6 +445,7 @@ int sar_slab_launch(sar_plan *p, int stage, const void *d_in, void *d_out, void 
     vk.cls = p->d_slab_cls;
     vk.ncls = p->slab_ncls;
     vk.w0 = xs;
+    vk.w0_elems = (size_t)v.ny * nxl * v.nk;   // the received x-slab (SAR_CHECKED bounds)
     SAR_CHECK(launch_k3(vk, true, s, p->num_sms));
     // y-IFFT; exchange #2 takes block h = z-slots [h nz', (h+1) nz') of every
     // column: stored there by the y-IFFT's own epilogue when a 16-wide z chunk
@@ -491,6 +492,7 @@ int sar_slab_launch(sar_plan *p, int stage, const void *d_in, void *d_out, void 
   vk.z_off = r * nzl;
   vk.nz_img = v.nz;
   vk.w1 = zs;
+  vk.w1_elems = v.w0_elems;
   SAR_CHECK(launch_k4b(vk, d_image, (p->flags & SAR_OUTPUT_COMPLEX) != 0, s, p->tma_w1z ? &p->tm_w1z_rows : nullptr,
                        p->num_sms));
   return SAR_OK;
