@@ -136,14 +136,14 @@ __global__ void __launch_bounds__(mid2_ntc<N>() + 32)
 #pragma unroll
           for (int bx = 0; bx < NBOX; ++bx) {
             const bool live = lb >= 0 && (bx * ROWS <= lb || (bx + 1) * ROWS - 1 >= N - lb);
-            sartma::tma_load_3d(ring + (size_t)st * N * KC + bx * ROWS * KC, &tm, chunk * KC, a,
+            sartma::tma_load_3d_stream<2>(ring + (size_t)st * N * KC + bx * ROWS * KC, &tm, chunk * KC, a,
                                 live ? f * N + bx * ROWS : oob_row, &full[st]);
           }
         } else {
           sartma::mbar_arrive_expect_tx(&full[st], TILE_BYTES);
 #pragma unroll
           for (int bx = 0; bx < NBOX; ++bx)
-            sartma::tma_load_3d(ring + (size_t)st * N * KC + bx * ROWS * KC, &tm, chunk * KC, a,
+            sartma::tma_load_3d_stream<2>(ring + (size_t)st * N * KC + bx * ROWS * KC, &tm, chunk * KC, a,
                                 f * N + bx * ROWS, &full[st]);
         }
       }

@@ -285,7 +285,7 @@ __global__ void __launch_bounds__(K1_NT + 32, 1)
               ((long long)((f + v.f0) * v.nt + t) * v.nr + r) * v.P + (long long)iy * v.npx + j.b * br;
           unsigned char *sb = stages + st * STAGE;
           sartma::mbar_arrive_expect_tx(&full[st], tx_bytes);
-          sartma::tma_load_2d(sb, &tm_s, kc * C, (int)row, &full[st]);
+          sartma::tma_load_2d_stream<1>(sb, &tm_s, kc * C, (int)row, &full[st]);
           sartma::tma_load_2d(sb + K1_BOX_BYTES, &tm_ap, j.b * br, (f + v.f0) * v.npy + iy, &full[st]);
         }
       }

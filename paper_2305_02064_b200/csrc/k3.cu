@@ -407,7 +407,7 @@ __global__ void __launch_bounds__(K3P_NG * K3P_G + 32, 1) k3_pp(const SarDeviceV
       if (ld) {
         SAR_ASSERT(h.colof[lane] >= 0 && h.colof[lane] < ncol);
         SAR_IN(wf + (size_t)h.colof[lane] * nk + nk - 1, v.w0, v.w0_elems);
-        sartma::bulk_g2s(fin + lane * nk, wf + (size_t)h.colof[lane] * nk, (uint32_t)nk * 8u, &full[st]);
+        sartma::bulk_g2s_stream<4>(fin + lane * nk, wf + (size_t)h.colof[lane] * nk, (uint32_t)nk * 8u, &full[st]);
       }
       cur = nxt;
     }
@@ -584,7 +584,7 @@ __global__ void __launch_bounds__(KW_NT, 1) k3_ws(const SarDeviceView v, int nit
       if (ld) {
         SAR_ASSERT(h.colof[lane] >= 0 && h.colof[lane] < ncol);
         SAR_IN(wf + (size_t)h.colof[lane] * nk + nk - 1, v.w0, v.w0_elems);
-        sartma::bulk_g2s(fin + lane * nk, wf + (size_t)h.colof[lane] * nk, (uint32_t)nk * 8u, &full[st]);
+        sartma::bulk_g2s_stream<4>(fin + lane * nk, wf + (size_t)h.colof[lane] * nk, (uint32_t)nk * 8u, &full[st]);
       }
       cur = nxt;
     }

@@ -96,11 +96,11 @@ __global__ void __launch_bounds__(K4bFft<NX>::NTC + 32)
         const int zc = item % nzc, fy = item / nzc;  // fy = f*ny + y
         sartma::mbar_arrive_expect_tx(&full[st], TILE_BYTES);
         if constexpr (SLAB) {
-          sartma::tma_load_4d(ring + (size_t)st * NX * KC, &tm, zc * KC, 0, fy, 0, &full[st]);
+          sartma::tma_load_4d_stream<8>(ring + (size_t)st * NX * KC, &tm, zc * KC, 0, fy, 0, &full[st]);
         } else {
 #pragma unroll
           for (int bx = 0; bx < NBOX; ++bx)
-            sartma::tma_load_3d(ring + (size_t)st * NX * KC + bx * ROWS * KC, &tm, zc * KC, bx * ROWS, fy, &full[st]);
+            sartma::tma_load_3d_stream<8>(ring + (size_t)st * NX * KC + bx * ROWS * KC, &tm, zc * KC, bx * ROWS, fy, &full[st]);
         }
       }
     }

@@ -119,6 +119,80 @@ __device__ __forceinline__ void tma_load_4d(void *dst_smem, const void *tmap, in
       : "memory");
 }
 
+// L2 eviction-priority hints for the streamed reads (SAR_L2HINT bit mask, an
+// A/B build option: 1 = K1 raw samples, 2 = mid-axis FFT input (K2, K4a),
+// 4 = K3 columns, 8 = K4b tiles).  A read-once stream marked evict_first
+// leaves the lines the previous kernel wrote last (write-back, still in L2)
+// for the reader instead of pushing them out to HBM first.
+#ifndef SAR_L2HINT
+#define SAR_L2HINT 0
+#endif
+__device__ __forceinline__ uint64_t l2_evict_first() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ uint64_t l2_evict_last() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void bulk_g2s_hint(void *dst_smem, const void *src_gmem, uint32_t bytes, uint64_t *bar,
+                                              uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::
+          "r"(smem_u32(dst_smem)),
+      "l"(src_gmem), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d_hint(void *dst_smem, const void *tmap, int c0, int c1, uint64_t *bar,
+                                                 uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint "
+      "[%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(dst_smem)),
+      "l"(tmap), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d_hint(void *dst_smem, const void *tmap, int c0, int c1, int c2,
+                                                 uint64_t *bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint "
+      "[%0], [%1, {%2, %3, %4}], [%5], %6;" ::"r"(smem_u32(dst_smem)),
+      "l"(tmap), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_4d_hint(void *dst_smem, const void *tmap, int c0, int c1, int c2, int c3,
+                                                 uint64_t *bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint "
+      "[%0], [%1, {%2, %3, %4, %5}], [%6], %7;" ::"r"(smem_u32(dst_smem)),
+      "l"(tmap), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+
+// the streamed-read wrappers: hinted when the kernel's bit of SAR_L2HINT is set
+template <int BIT>
+__device__ __forceinline__ void bulk_g2s_stream(void *d, const void *src, uint32_t bytes, uint64_t *bar) {
+  if constexpr ((SAR_L2HINT & BIT) != 0) bulk_g2s_hint(d, src, bytes, bar, l2_evict_first());
+  else bulk_g2s(d, src, bytes, bar);
+}
+template <int BIT>
+__device__ __forceinline__ void tma_load_2d_stream(void *d, const void *tm, int c0, int c1, uint64_t *bar) {
+  if constexpr ((SAR_L2HINT & BIT) != 0) tma_load_2d_hint(d, tm, c0, c1, bar, l2_evict_first());
+  else tma_load_2d(d, tm, c0, c1, bar);
+}
+template <int BIT>
+__device__ __forceinline__ void tma_load_3d_stream(void *d, const void *tm, int c0, int c1, int c2, uint64_t *bar) {
+  if constexpr ((SAR_L2HINT & BIT) != 0) tma_load_3d_hint(d, tm, c0, c1, c2, bar, l2_evict_first());
+  else tma_load_3d(d, tm, c0, c1, c2, bar);
+}
+template <int BIT>
+__device__ __forceinline__ void tma_load_4d_stream(void *d, const void *tm, int c0, int c1, int c2, int c3,
+                                                   uint64_t *bar) {
+  if constexpr ((SAR_L2HINT & BIT) != 0) tma_load_4d_hint(d, tm, c0, c1, c2, c3, bar, l2_evict_first());
+  else tma_load_4d(d, tm, c0, c1, c2, c3, bar);
+}
+
 // TMA prefetch of a tensor box into L2 (no shared memory, no completion)
 __device__ __forceinline__ void tma_prefetch_2d(const void *tmap, int c0, int c1) {
   asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(tmap), "r"(c0), "r"(c1)
