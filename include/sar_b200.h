@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define SAR_B200_VERSION 5
+#define SAR_B200_VERSION 6
 
 typedef struct sar_plan sar_plan;       /* opaque */
 typedef struct CUstream_st *sar_stream; /* == cudaStream_t; NULL = legacy default stream */
@@ -330,6 +330,32 @@ int sar_debug_node_offsets(const sar_plan *p, int32_t *jx, int32_t *jy, int32_t 
  * Errors: INVALID_ARG, CUDA. */
 int sar_debug_stolt_index(sar_plan *p, const int32_t *d_cols, int32_t n, int32_t *d_i0,
                           float *d_tau, sar_stream stream);
+
+/* ---- back-projection baseline (BPA) -------------------------
+ *
+ * The paper's gold standard and comparison system,
+ * not a step of the reconstruction path: the matched filter of Eq. (9)
+ * with the exact round-trip distances of Eq. (2) and
+ * the ACTUAL element positions T_{t,p} = scan_xyz[p] + tx_xyz[t],
+ * R_{r,p} = scan_xyz[p] + rx_xyz[r] (the radar keeps its orientation):
+ *
+ *   o(v) = sum_{t,r,p,i} s[t,r,p,i] exp(+j k_i (|v - T_{t,p}| + |v - R_{r,p}|))
+ *
+ * (no normalisation, no compensation, no lattice: every voxel costs
+ * n_tx n_rx P n_k complex multiply-adds).  Of g only n_frames, n_tx, n_rx,
+ * tx_xyz, rx_xyz, npx, npy, scan_xyz, n_k, k and device are read (k uniform
+ * and ascending as for a plan; any positions).  frame: which frame of d_data.
+ * d_data: device, complex64 [F][n_tx][n_rx][npy*npx][n_k] (the layout of
+ * sar_reconstruct), read only.  h_voxels: HOST float64 [n_voxels][3] world
+ * positions (m), copied.  d_out: device complex64 [n_voxels], overwritten.
+ * ms_out: if not NULL receives the kernel's CUDA-event time (ms).  The call
+ * allocates and frees its own device tables and SYNCHRONISES `stream` before
+ * returning (a baseline, not a hot path).  n_voxels = 0 is a no-op.
+ * Distances and phase reduction in fp64, the k loop in fp32 (DESIGN.md
+ * section 10).  Errors: INVALID_ARG, GEOMETRY (k), UNSUPPORTED (not sm_100;
+ * one pose's n_tx*n_rx*n_k samples above 200 KB), OOM, CUDA. */
+int sar_bpa(const sar_geom_desc *g, int32_t frame, const void *d_data, const double *h_voxels,
+            int64_t n_voxels, void *d_out, sar_stream stream, float *ms_out);
 
 const char *sar_status_string(int status);
 const char *sar_last_error(void);

@@ -18,7 +18,7 @@ BUILD = os.path.join(HERE, "_build")
 LIB = os.path.join(HERE, "libsar_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-SOURCES = ["plan.cpp", "pipeline.cu", "k1.cu", "fft_mid.cu", "k3.cu", "k4.cu", "nufft.cu"]
+SOURCES = ["plan.cpp", "pipeline.cu", "k1.cu", "fft_mid.cu", "k3.cu", "k4.cu", "nufft.cu", "bpa.cu"]
 HEADERS = [os.path.join(CSRC, h) for h in ("plan_internal.h", "fft_tile.cuh", "fft_reg.cuh", "tma.cuh", "common.cuh")] + \
     [os.path.join(ROOT, "include", "sar_b200.h")]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-ffp-contract=off,-O2",

@@ -97,6 +97,7 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         "sar_slab_buffer_bytes": (C.c_int, [vp, C.POINTER(C.c_size_t), C.POINTER(C.c_size_t)]),
         "sar_slab_stage": (C.c_int, [vp, i32, vp, vp, vp, vp]),
         "sar_slab_stage_peers": (C.c_int, [vp, i32, vp, C.POINTER(vp), vp]),
+        "sar_bpa": (C.c_int, [C.POINTER(GeomDesc), i32, vp, vp, C.c_int64, vp, vp, C.POINTER(C.c_float)]),
         "sar_status_string": (C.c_char_p, [C.c_int]),
         "sar_last_error": (C.c_char_p, []),
         "sar_version": (C.c_int, []),
@@ -115,7 +116,7 @@ def exported_symbols():
             "sar_plan_get_axes", "sar_plan_workspace_bytes", "sar_plan_profile_read",
             "sar_plan_profile_reset", "sar_plan_launches_per_call", "sar_plan_peaks", "sar_debug_stage",
             "sar_debug_node_offsets", "sar_debug_stolt_index", "sar_plan_create_slab", "sar_slab_buffer_bytes",
-            "sar_slab_stage", "sar_slab_stage_peers", "sar_status_string",
+            "sar_slab_stage", "sar_slab_stage_peers", "sar_bpa", "sar_status_string",
             "sar_last_error", "sar_version"]
 
 
@@ -230,6 +231,39 @@ def describe_scene(sc, flags=0):
 def describe_stolt_ranges_scene(sc, flags=0):
     return describe_stolt_ranges(sc.tx, sc.rx, sc.scan, sc.npx, sc.npy, sc.x0, sc.y0, sc.dx, sc.dy, sc.z0, sc.k,
                                  sc.nx, sc.ny, sc.nz, sc.dz_img, sc.z_ref, flags=flags)
+
+
+def bpa(tx, rx, scan, npx, npy, k, data, voxels, frame=0, out=None, stream=None, device=0):
+    """Back-projection baseline (``sar_bpa``; the paper's comparison system,
+    P:199-200): o(v) = sum s exp(+j k (|v-T| + |v-R|)) at the world positions
+    ``voxels`` [V, 3] (host float64) from the device tensor ``data``
+    [F, n_tx, n_rx, P, n_k] complex64.  Returns (complex64 [V] device tensor,
+    kernel ms).  Synchronous."""
+    import torch
+    lib = load_library()
+    k = np.asarray(k, dtype=np.float64)
+    scan = np.asarray(scan, dtype=np.float64)
+    g, _, keep = _descriptors(tx, rx, scan, npx, npy, 0.0, 0.0, 1.0, 1.0, None, k, 2, 2, 2, 1.0, 1.0, None, device)
+    shape = (g.n_frames, g.n_tx, g.n_rx, g.npx * g.npy, g.n_k)
+    if not (isinstance(data, torch.Tensor) and data.is_cuda and data.dtype == torch.complex64
+            and tuple(data.shape) == shape and data.is_contiguous()):
+        raise ValueError(f"data must be a contiguous CUDA complex64 tensor of shape {shape}")
+    vox = np.ascontiguousarray(np.asarray(voxels, dtype=np.float64).reshape(-1, 3))
+    n = vox.shape[0]
+    if out is None:
+        out = torch.empty(n, dtype=torch.complex64, device=data.device)
+    elif not (out.is_cuda and out.dtype == torch.complex64 and out.numel() == n and out.is_contiguous()):
+        raise ValueError("out must be a contiguous CUDA complex64 tensor with one element per voxel")
+    ms = C.c_float(0.0)
+    _check(lib.sar_bpa(C.byref(g), C.c_int32(frame), C.c_void_p(data.data_ptr()), C.c_void_p(vox.ctypes.data),
+                       C.c_int64(n), C.c_void_p(out.data_ptr()), _stream_ptr(stream), C.byref(ms)))
+    del keep
+    return out, float(ms.value)
+
+
+def bpa_scene(sc, data, voxels, frame=0, **kw):
+    """``bpa`` for any object with the attributes of ``scenes.Scene``."""
+    return bpa(sc.tx, sc.rx, sc.scan, sc.npx, sc.npy, sc.k, data, voxels, frame=frame, **kw)
 
 
 class Plan:

@@ -41,7 +41,7 @@ def test_library_exports_every_declared_symbol():
     for d in declared:
         assert hasattr(lib, d)
     assert sorted(sarmod.exported_symbols()) == declared
-    assert lib.sar_version() == 5
+    assert lib.sar_version() == 6
 
 
 def test_library_has_no_unresolved_own_symbols():

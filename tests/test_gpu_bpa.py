@@ -1,0 +1,140 @@
+"""GPU parity of the back-projection baseline ``sar_bpa`` (the
+paper's gold standard) against ``oracle.bpa`` (fp64, pinned
+in tests/test_oracle_bpa.py) on the same seeded complex64 inputs, through the
+C ABI.  Bar: relative L2 <= 1e-4 and max normalised error <= 1e-3 on the
+COMPLEX back-projected values (fp64 distances and phase
+reduction, fp32 k loop re-seeded every 32 samples, fp64 running total)."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+import oracle  # noqa: E402
+import scenes  # noqa: E402
+import paper_2305_02064_b200 as sar  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+E2_BAR, EINF_BAR = 1e-4, 1e-3
+
+
+@pytest.fixture(scope="module", autouse=True)
+def built():
+    import __graft_entry__
+    __graft_entry__.build()
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def errs(got, want):
+    d = np.asarray(got, dtype=np.complex128) - want
+    return (np.linalg.norm(d) / max(np.linalg.norm(want), 1e-300),
+            np.abs(d).max() / max(np.abs(want).max(), 1e-300))
+
+
+def _voxels(sc, n, seed):
+    """n world positions: some on the image grid around the scatterers, the rest
+    uniform in the image volume."""
+    geo = oracle.rma.geometry_of(sc)
+    x0, y0, z0, dx, dy, dz = geo.axes
+    rng = np.random.default_rng(seed)
+    lo = np.array([x0, y0, z0])
+    hi = lo + np.array([sc.nx * dx, sc.ny * dy, sc.nz * dz])
+    v = rng.uniform(lo, hi, size=(n, 3))
+    q = sc.scat_pos[0]
+    m = min(len(q), n // 2)
+    if m:
+        v[:m] = q[:m] + rng.normal(0, 1e-3, size=(m, 3))
+    return v
+
+
+def _check(sc, s_np, d, vox, frame=0):
+    out, ms = sar.bpa_scene(sc, d, vox, frame=frame)
+    txw, rxw = scenes.element_positions(sc, frame)
+    want = oracle.bpa(s_np[frame], txw, rxw, sc.k, vox)
+    e2, einf = errs(out.cpu().numpy(), want)
+    assert e2 <= E2_BAR and einf <= EINF_BAR, (sc.name, e2, einf)
+    return e2, einf, ms
+
+
+@pytest.mark.parametrize("name,nvox", [("tiny", 300), ("small", 200)])
+def test_bpa_matches_oracle(name, nvox):
+    """Several CTAs of 128 voxels and a ragged tail; Tiny: n_k = 16 (one short
+    segment), Small: n_k = 64 (two re-seeded segments), several pose batches."""
+    sc = scenes.make_scene(name)
+    s = scenes.synthesize_cpu(sc)
+    _check(sc, s, torch.from_numpy(s).cuda(), _voxels(sc, nvox, 1))
+
+
+@pytest.mark.parametrize("kw", [
+    dict(npx=10, npy=7, n_k=37, n_tx=3),                 # 12 pairs, odd n_k with a ragged segment
+    dict(npx=9, npy=5, n_k=70, n_tx=1),                  # 4 pairs, three segments
+    dict(npx=12, npy=6, n_k=33, monostatic=True),        # 1 pair: receiver group padded
+    dict(npx=6, npy=4, n_k=2, n_tx=2),                   # minimum n_k
+    dict(npx=8, npy=8, n_k=20, n_tx=2, n_frames=3),      # a later frame of a batch
+])
+def test_bpa_edge_cases(kw):
+    kw = dict(kw)
+    npx, npy, n_k = kw.pop("npx"), kw.pop("npy"), kw.pop("n_k")
+    sc = scenes.raster_scene(npx, npy, 32, 32, n_k, 16, 2.5e-3, 0.2, jitter_xy=0.8e-3, jitter_z=2e-3, seed=21, **kw)
+    rng = np.random.default_rng(5)
+    F = sc.n_frames
+    sc.scat_pos = [rng.uniform([-0.02, -0.02, 0.18], [0.02, 0.02, 0.22], size=(4, 3)) for _ in range(F)]
+    sc.scat_amp = [np.ones(4, complex) for _ in range(F)]
+    s = scenes.synthesize_cpu(sc)
+    d = torch.from_numpy(s).cuda()
+    for frame, nv in ((F - 1, 131), (0, 1)):
+        _check(sc, s, d, _voxels(sc, nv, 7 + frame), frame=frame)
+
+
+def test_bpa_freehand_full_size_sampled_voxels():
+    """The Freehand configuration at full size (1.3e8 samples, n_k = 256, 65536
+    poses): 12 sampled voxels the oracle computes one by one."""
+    from scenes import gpu as sgpu
+    sc = scenes.make_scene("freehand")
+    sgpu.build()
+    d = sgpu.synthesize_gpu(sc)
+    _check(sc, d.cpu().numpy(), d, _voxels(sc, 12, 3))
+
+
+def test_bpa_peak_agrees_with_rma_image_small():
+    """The physics check the baseline exists for: on Small, the
+    back-projected magnitude on a box of image voxels around the strongest
+    scatterer peaks within one voxel of the RMA image's peak in that box."""
+    sc = scenes.make_scene("small")
+    s = scenes.synthesize_cpu(sc)
+    d = torch.from_numpy(s).cuda()
+    with sar.Plan.from_scene(sc) as plan:
+        img = plan.reconstruct(d)[0].cpu().numpy()
+        x0, y0, z0, dx, dy, dz = plan.axes()
+    q = sc.scat_pos[0][int(np.argmax(np.abs(sc.scat_amp[0])))]
+    c = np.rint([(q[2] - z0) / dz, (q[1] - y0) / dy, (q[0] - x0) / dx]).astype(int)
+    ms_, ys, xs = (np.arange(c[0] - 2, c[0] + 3) % sc.nz, np.arange(c[1] - 3, c[1] + 4) % sc.ny,
+                   np.arange(c[2] - 3, c[2] + 4) % sc.nx)
+    m, iy, ix = np.meshgrid(ms_, ys, xs, indexing="ij")
+    vox = np.stack([x0 + ix * dx, y0 + iy * dy, z0 + m * dz], axis=-1).reshape(-1, 3)
+    out, _ = sar.bpa_scene(sc, d, vox)
+    b = np.abs(out.cpu().numpy()).reshape(m.shape)
+    pb = np.unravel_index(np.argmax(b), b.shape)
+    pr = np.unravel_index(np.argmax(img[np.ix_(ms_, ys, xs)]), b.shape)
+    assert max(abs(int(u) - int(v)) for u, v in zip(pb, pr)) <= 1, (pb, pr)
+
+
+def test_bpa_deterministic_and_rejections():
+    sc = scenes.make_scene("tiny")
+    s = scenes.synthesize_cpu(sc)
+    d = torch.from_numpy(s).cuda()
+    vox = _voxels(sc, 200, 9)
+    a, _ = sar.bpa_scene(sc, d, vox)
+    b, _ = sar.bpa_scene(sc, d, vox)
+    assert torch.equal(torch.view_as_real(a), torch.view_as_real(b))
+    empty, ms = sar.bpa_scene(sc, d, np.zeros((0, 3)))
+    assert empty.numel() == 0 and ms == 0.0
+    with pytest.raises(sar.SarError) as ei:
+        sar.bpa_scene(sc, d, vox, frame=1)
+    assert ei.value.status == 1
+    kbad = sc.k.copy()
+    kbad[3] *= 1.0 + 1e-6
+    with pytest.raises(sar.SarError) as ei:
+        sar.bpa(sc.tx, sc.rx, sc.scan, sc.npx, sc.npy, kbad, d, vox)
+    assert ei.value.status == 2
