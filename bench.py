@@ -420,6 +420,97 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+# FP32 peak the ALU-bound lines report against:
+# 148 SMs x 128 FP32 lanes x 2 flop x 1.965 GHz
+FP32_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12
+
+
+def run_bpa(args):
+    """The GPU back-projection baseline (sar_bpa): a
+    step is one call over --bpa-voxels image voxels (default: a z-centred slab of
+    the config's image grid, at most 65536 voxels) against every sample of
+    frame 0.  Single GPU (a baseline, not the product path)."""
+    import torch
+    import scenes
+    import scenes.gpu
+    import paper_2305_02064_b200 as sar
+    from paper_2305_02064_b200 import build as sbuild
+
+    rank, world, local = _dist()
+    if rank != 0:
+        return
+    torch.cuda.set_device(local)
+    sbuild.build()
+    scenes.gpu.build()
+    sc = scenes.make_scene(args.config)
+    d = scenes.gpu.synthesize_gpu(sc)
+    with sar.Plan.from_scene(sc) as plan:
+        x0, y0, z0, dx, dy, dz = plan.axes()
+    nvox = args.bpa_voxels or min(sc.nx * sc.ny * sc.nz, 65536)
+    planes = max(1, min(sc.nz, nvox // (sc.nx * sc.ny)))
+    m0 = sc.nz // 2 - planes // 2
+    m, iy, ix = np.meshgrid(np.arange(m0, m0 + planes), np.arange(sc.ny), np.arange(sc.nx), indexing="ij")
+    vox = np.stack([x0 + ix * dx, y0 + iy * dy, z0 + m * dz], axis=-1).reshape(-1, 3)[:max(nvox, 1)]
+    nvox = vox.shape[0]
+    terms = nvox * sc.n_tx * sc.n_rx * sc.n_pos * sc.n_k
+    out = torch.empty(nvox, dtype=torch.complex64, device=d.device)
+    for _ in range(args.warmup):
+        sar.bpa_scene(sc, d, vox, out=out)
+    torch.cuda.synchronize()
+    kms = []
+    with ClockSampler(local) as clk:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(args.steps):
+            kms.append(sar.bpa_scene(sc, d, vox, out=out)[1])
+        e1.record()
+        torch.cuda.synchronize()
+    ms_step = e0.elapsed_time(e1) / args.steps
+    kern = float(np.mean(kms))
+    # e2e: host samples of the frame and host voxels in, host values out
+    h = d[:1].cpu().pin_memory()
+    sc1 = scenes.frame_subset(sc, 0, 1) if sc.n_frames > 1 else sc
+    t0 = time.perf_counter()
+    dd = h.to(d.device, non_blocking=True)
+    res = sar.bpa_scene(sc1, dd, vox)[0].cpu()
+    e2e_ms = (time.perf_counter() - t0) * 1e3
+    cpu = None
+    if not args.no_cpu_baseline:
+        import oracle
+        txw, rxw = scenes.element_positions(sc, 0)
+        s0 = d[0].cpu().numpy()
+        nv = max(1, min(nvox, int(2e9 // (terms // nvox))))   # ~2e9 terms: some 10-30 s of NumPy
+        t0 = time.perf_counter()
+        want = oracle.bpa(s0, txw, rxw, sc.k, vox[:nv])
+        dt = time.perf_counter() - t0
+        got = res[:nv].numpy().astype(np.complex128)
+        cpu = {"value": nv * (terms // nvox) / dt / 1e9, "unit": "Gterms/s", "kind": "oracle",
+               "sample": f"oracle.bpa on the first {nv} of the {nvox} voxels ({dt:.1f} s)",
+               "rel_l2_of_gpu_vs_oracle_on_sample": float(np.linalg.norm(got - want) / np.linalg.norm(want)),
+               **host_info()}
+    flops = 8.0 * terms   # one complex multiply-add per term
+    line = {
+        "metric": "Gterms/s (back-projection terms s*exp(jkR) accumulated per second; BPA baseline)",
+        "value": terms / (ms_step * 1e-3) / 1e9, "unit": "Gterms/s", "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32 (k loop), f64 (distances, phase reduction, totals)",
+        "data": "synthetic (seeded scenes, GPU-synthesised Eq. (9) echo)",
+        "config": {"workload": f"{args.config} BPA baseline, {nvox} voxels ({planes} central z planes)",
+                   "tx": sc.n_tx, "rx": sc.n_rx, "poses": sc.n_pos, "n_k": sc.n_k, "terms_per_step": terms,
+                   "l2": "samples re-read by every CTA from L2 (ALU bound)"},
+        "roofline": {"bound": "alu", "kernel": "k_bpa", "achieved": flops / (kern * 1e-3) / 1e12,
+                     "peak": FP32_PEAK_TFLOPS, "unit": "TFLOP/s",
+                     "frac": flops / (kern * 1e-3) / 1e12 / FP32_PEAK_TFLOPS, "traffic": None, "ms": kern,
+                     "alg_flops": flops, "peak_source": "148 SMs x 128 lanes x 2 x 1.965 GHz (DESIGN.md section 8)"},
+        "full_image_projection_s": (sc.nx * sc.ny * sc.nz / nvox) * kern * 1e-3,
+        "cpu_baseline": cpu,
+        "e2e": {"value": terms / (e2e_ms * 1e-3) / 1e9, "unit": "Gterms/s", "ms": e2e_ms,
+                "h2d_bytes_per_step": h.numel() * 8 + vox.nbytes, "d2h_bytes_per_step": nvox * 8},
+        "gpu_launches": args.steps, "clocks": clk.summary(),
+    }
+    print(json.dumps(line), flush=True)
+
+
 def run_slab(args):
     """One image split over the N ranks (single-image slab decomposition,
     sar_slab_stage + two NCCL all-to-alls): strong scaling of the Large
@@ -541,6 +632,10 @@ def main():
                     help="split ONE image over the ranks (slab decomposition, two all-to-alls; strong scaling)")
     ap.add_argument("--p2p", action="store_true",
                     help="with --slab: exchange by peer stores into IPC-mapped receive buffers instead of NCCL")
+    ap.add_argument("--bpa", action="store_true",
+                    help="time the GPU back-projection baseline (sar_bpa; the paper's comparison system, P:199-200) "
+                         "instead of the reconstruction path")
+    ap.add_argument("--bpa-voxels", type=int, default=0, help="with --bpa: voxels per step (default <= 65536)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -549,6 +644,8 @@ def main():
         print("warning: --warmup < 3 is below the timing rules", file=sys.stderr)
     if args.impl == "reference":
         run_reference(args)
+    elif args.bpa:
+        run_bpa(args)
     elif args.slab:
         run_slab(args)
     else:

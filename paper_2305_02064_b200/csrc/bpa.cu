@@ -10,17 +10,29 @@
 // timings and a physics check of the RMA image on configurations whose CPU
 // brute force would take hours.
 //
-// One thread per voxel, 128 voxels per CTA.  The CTA walks the poses in
-// batches: the batch's sample rows [pair][pose][k] and element positions are
-// staged in shared memory (every thread reads the same sample: broadcast
-// loads), then for each (t, group of 4 receivers, pose) a thread forms the
-// round-trip distance R in fp64, reduces the phases k_0 R and dk R to
-// fractions of a turn in fp64 (|k R| reaches ~10^3 rad), and runs the k loop
-// in paired fp32: acc += s_i * cur, cur *= step, re-seeding cur from the fp64
-// phase every BPA_SEG samples so the recurrence error stays ~1e-6.  The four
-// receivers are four independent chains (ILP); each k loop's fp32 sum is added
-// to the voxel's fp64 total, so the rounding of the long sum does not grow
-// with the number of terms.
+// One thread per BPA_NV = 2 voxels, 256 voxels per CTA; gridDim.y splits the
+// poses when there are few voxel CTAs (partial sums in fp64, reduced in a
+// fixed order: deterministic).  The CTA walks its poses in batches: the
+// batch's sample rows [pair][pose][k] (zero-padded to a multiple of 16) and
+// element positions are staged in shared memory; every lane reads the same
+// sample (broadcast loads), and a sample read once serves both voxels of the
+// thread -- with one voxel per thread the kernel is bound by the shared-memory
+// return path (a broadcast 8-byte load still fills 256 B of registers per
+// warp), not by the FP32 pipe.  For each (t, r, pose, voxel) a thread forms
+// the round-trip distance R in fp64, reduces the phases k_0 R and dk R to
+// fractions of a turn in fp64 (|k R| reaches ~10^3 rad), builds the phasors
+// w^e = exp(j e dk R), e = 1..8, in registers, and evaluates the k sum in
+// blocks of 16 samples centred on e = 0:
+//   sum_i s_i e^{j k_i R} = sum_a W_a sum_{e=-8..7} s_{16a+8+e} w^e,
+//   W_a = e^{j (k_0 + (16a+8) dk) R},  w^{-e} = conj(w^e).
+// With w^e = (c, d) and s = (x, y) the block sum needs no operand shuffles:
+// A += (c,c)*(x,y) for every e, Bp += (d,d)*(x,y) for e > 0, Bn likewise for
+// e < 0, and the sum is (A.x - (Bp-Bn).y, A.y + (Bp-Bn).x): two FFMA2 per
+// term.  Per block one complex multiply-add and one step of W_a (W_a is
+// re-seeded from the fp64 phase every BPA_RESEED blocks, so the recurrence
+// error stays ~1e-6).  Each (t, r, pose) fp32 sum is added to the voxel's
+// fp64 total, so the rounding of the long sum does not grow with the number
+// of terms.
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
@@ -33,18 +45,21 @@
 
 namespace {
 
-constexpr int BPA_NT = 128;   // voxels (threads) per CTA
-constexpr int BPA_SEG = 32;   // k samples per phasor re-seed
-constexpr int BPA_RG = 4;     // receivers per group (independent chains)
+constexpr int BPA_NT = 128;     // threads per CTA
+constexpr int BPA_NV = 2;       // voxels per thread (v, v + 128 of the CTA's 256)
+constexpr int BPA_NB = 16;      // k samples per block: e = -8 .. 7 around its centre
+constexpr int BPA_H = BPA_NB / 2;
+constexpr int BPA_RESEED = 8;   // blocks per exact re-seed of the block phasor
 
 struct BpaArgs {
   const float2 *s;      // frame base: [npair][P][nk]
   const double *txw;    // [nt][P][3] Tx world positions minus the origin
   const double *rxw;    // [nr][P][3]
   const double *vox;    // [V][3] voxels minus the origin
-  float2 *out;          // [V]
+  float2 *out;          // [V] (nsplit == 1)
+  double2 *part;        // [nsplit][V] partial sums (nsplit > 1)
   long long V;
-  int nt, nr, P, nk, PB;
+  int nt, nr, P, nk, nkp, PB, nsplit;
   double kt0, dkt;      // k_0 / 2 pi, dk / 2 pi (turns per metre)
 };
 
@@ -56,26 +71,39 @@ __device__ __forceinline__ float2 unit_phasor(double turns) {
   return r;
 }
 
-__global__ void __launch_bounds__(BPA_NT) k_bpa(const BpaArgs a) {
+__global__ void __launch_bounds__(BPA_NT, 3) k_bpa(const BpaArgs a) {
   extern __shared__ __align__(16) unsigned char smraw[];
   const int npair = a.nt * a.nr;
-  float2 *ss = reinterpret_cast<float2 *>(smraw);                                 // [npair][PB][nk]
-  double *pt = reinterpret_cast<double *>(smraw + (size_t)npair * a.PB * a.nk * sizeof(float2));  // [nt][PB][3]
-  double *prx = pt + (size_t)a.nt * a.PB * 3;                                      // [nr][PB][3]
+  float2 *ss = reinterpret_cast<float2 *>(smraw);                                  // [npair][PB][nkp]
+  double *pt = reinterpret_cast<double *>(smraw + (size_t)npair * a.PB * a.nkp * sizeof(float2));  // [nt][PB][3]
+  double *prx = pt + (size_t)a.nt * a.PB * 3;                                       // [nr][PB][3]
   const int tid = threadIdx.x;
-  long long v = (long long)blockIdx.x * BPA_NT + tid;
-  const bool live = v < a.V;
-  if (!live) v = a.V - 1;   // keeps the barriers uniform; its result is not stored
-  const double vx = a.vox[v * 3], vy = a.vox[v * 3 + 1], vz = a.vox[v * 3 + 2];
-  double tre = 0.0, tim = 0.0;
+  long long v[BPA_NV];
+  bool live[BPA_NV];
+  double vx[BPA_NV], vy[BPA_NV], vz[BPA_NV], tre[BPA_NV], tim[BPA_NV];
+#pragma unroll
+  for (int j = 0; j < BPA_NV; ++j) {
+    v[j] = ((long long)blockIdx.x * BPA_NV + j) * BPA_NT + tid;
+    live[j] = v[j] < a.V;
+    if (!live[j]) v[j] = a.V - 1;   // keeps the barriers uniform; its result is not stored
+    vx[j] = a.vox[v[j] * 3], vy[j] = a.vox[v[j] * 3 + 1], vz[j] = a.vox[v[j] * 3 + 2];
+    tre[j] = tim[j] = 0.0;
+  }
+  // this CTA's poses: split blockIdx.y of nsplit, in whole batches
+  const int nbatch = (a.P + a.PB - 1) / a.PB;
+  const int b_lo = (int)((long long)nbatch * blockIdx.y / a.nsplit);
+  const int b_hi = (int)((long long)nbatch * (blockIdx.y + 1) / a.nsplit);
 
-  for (int p0 = 0; p0 < a.P; p0 += a.PB) {
+  for (int bt = b_lo; bt < b_hi; ++bt) {
+    const int p0 = bt * a.PB;
     const int cnt = min(a.PB, a.P - p0);
     __syncthreads();   // the previous batch is consumed
-    const int per = cnt * a.nk;
-    for (int e = tid; e < npair * per; e += BPA_NT) {
-      const int pr = e / per, o = e - pr * per;
-      ss[(size_t)pr * a.PB * a.nk + o] = __ldg(a.s + ((size_t)pr * a.P + p0) * a.nk + o);
+    for (int e = tid; e < npair * cnt * a.nkp; e += BPA_NT) {
+      const int i = e % a.nkp, rowi = e / a.nkp;        // rowi = pr * cnt + pb
+      const int pr = rowi / cnt, pb = rowi - pr * cnt;
+      float2 x = make_float2(0.f, 0.f);
+      if (i < a.nk) x = __ldg(a.s + ((size_t)pr * a.P + p0 + pb) * a.nk + i);
+      ss[((size_t)pr * a.PB + pb) * a.nkp + i] = x;
     }
     for (int e = tid; e < a.nt * cnt * 3; e += BPA_NT) {
       const int t = e / (cnt * 3), o = e - t * cnt * 3;
@@ -88,58 +116,103 @@ __global__ void __launch_bounds__(BPA_NT) k_bpa(const BpaArgs a) {
     __syncthreads();
 
     for (int pb = 0; pb < cnt; ++pb) {
-      for (int r0 = 0; r0 < a.nr; r0 += BPA_RG) {
-        double RR[BPA_RG];
+      for (int r = 0; r < a.nr; ++r) {
+        const double *qr = prx + ((size_t)r * a.PB + pb) * 3;
+        double RR[BPA_NV];
 #pragma unroll
-        for (int j = 0; j < BPA_RG; ++j) {
-          const int r = min(r0 + j, a.nr - 1);
-          const double *q = prx + ((size_t)r * a.PB + pb) * 3;
-          const double dx = vx - q[0], dy = vy - q[1], dz = vz - q[2];
+        for (int j = 0; j < BPA_NV; ++j) {
+          const double dx = vx[j] - qr[0], dy = vy[j] - qr[1], dz = vz[j] - qr[2];
           RR[j] = sqrt(dx * dx + dy * dy + dz * dz);
         }
         for (int t = 0; t < a.nt; ++t) {
           const double *q = pt + ((size_t)t * a.PB + pb) * 3;
-          const double dx = vx - q[0], dy = vy - q[1], dz = vz - q[2];
-          const double RT = sqrt(dx * dx + dy * dy + dz * dz);
-          double ph0[BPA_RG], phd[BPA_RG];
-          float2 step[BPA_RG], acc[BPA_RG];
-          const float2 *row[BPA_RG];
+          // per voxel: cc[e-1] = (c,c), dd[e-1] = (d,d) of w^e = (c,d), e = 1..8
+          float2 cc[BPA_NV][BPA_H], dd[BPA_NV][BPA_H], Wstep[BPA_NV], Wa[BPA_NV], acc[BPA_NV];
+          double ph0[BPA_NV], phd[BPA_NV];
 #pragma unroll
-          for (int j = 0; j < BPA_RG; ++j) {
-            const double R = RT + RR[j];
+          for (int j = 0; j < BPA_NV; ++j) {
+            const double tx = vx[j] - q[0], ty = vy[j] - q[1], tz = vz[j] - q[2];
+            const double R = RR[j] + sqrt(tx * tx + ty * ty + tz * tz);
             ph0[j] = a.kt0 * R;
             ph0[j] -= rint(ph0[j]);
             phd[j] = a.dkt * R;
             phd[j] -= rint(phd[j]);
-            step[j] = unit_phasor(phd[j]);
+            const float2 w1 = unit_phasor(phd[j]);
+            float2 w = w1;
+#pragma unroll
+            for (int e = 0; e < BPA_H; ++e) {
+              cc[j][e] = make_float2(w.x, w.x);
+              dd[j][e] = make_float2(w.y, w.y);
+              if (e + 1 < BPA_H) w = sark::cmul2(w, w1);
+            }
+            Wstep[j] = unit_phasor((double)BPA_NB * phd[j]);   // w^16, from the fp64 phase
             acc[j] = make_float2(0.f, 0.f);
-            const int r = min(r0 + j, a.nr - 1);
-            row[j] = ss + ((size_t)(t * a.nr + r) * a.PB + pb) * a.nk;
+            Wa[j] = make_float2(1.f, 0.f);
           }
-          for (int i0 = 0; i0 < a.nk; i0 += BPA_SEG) {
-            float2 cur[BPA_RG];
+          const float2 *row = ss + ((size_t)(t * a.nr + r) * a.PB + pb) * a.nkp;
+          for (int blk = 0; blk * BPA_NB < a.nk; ++blk) {
+            if (blk % BPA_RESEED == 0) {
 #pragma unroll
-            for (int j = 0; j < BPA_RG; ++j) cur[j] = unit_phasor(ph0[j] + (double)i0 * phd[j]);
-            const int i1 = min(i0 + BPA_SEG, a.nk);
-            for (int i = i0; i < i1; ++i) {
+              for (int j = 0; j < BPA_NV; ++j)
+                Wa[j] = unit_phasor(ph0[j] + (double)(blk * BPA_NB + BPA_H) * phd[j]);
+            }
+            const float2 *rb = row + blk * BPA_NB + BPA_H;   // e = 0
+            float2 A0[BPA_NV], A1[BPA_NV], Bp[BPA_NV], Bn[BPA_NV];
+            const float2 s0 = rb[0], sm8 = rb[-BPA_H];
 #pragma unroll
-              for (int j = 0; j < BPA_RG; ++j) {
-                acc[j] = sark::cmac2(acc[j], row[j][i], cur[j]);
-                cur[j] = sark::cmul2(cur[j], step[j]);
+            for (int j = 0; j < BPA_NV; ++j) {
+              A0[j] = s0;                                              // e = 0: w^0 = 1
+              A1[j] = __fmul2_rn(cc[j][BPA_H - 1], sm8);               // e = -8
+              Bn[j] = __fmul2_rn(dd[j][BPA_H - 1], sm8);
+              Bp[j] = make_float2(0.f, 0.f);
+            }
+#pragma unroll
+            for (int e = 1; e < BPA_H; ++e) {
+              const float2 sp = rb[e], sn = rb[-e];
+#pragma unroll
+              for (int j = 0; j < BPA_NV; ++j) {
+                A0[j] = __ffma2_rn(cc[j][e - 1], sp, A0[j]);
+                A1[j] = __ffma2_rn(cc[j][e - 1], sn, A1[j]);
+                Bp[j] = __ffma2_rn(dd[j][e - 1], sp, Bp[j]);
+                Bn[j] = __ffma2_rn(dd[j][e - 1], sn, Bn[j]);
               }
             }
+#pragma unroll
+            for (int j = 0; j < BPA_NV; ++j) {
+              const float2 A = __fadd2_rn(A0[j], A1[j]);
+              const float bx = Bp[j].x - Bn[j].x, by = Bp[j].y - Bn[j].y;
+              acc[j] = sark::cmac2(acc[j], make_float2(A.x - by, A.y + bx), Wa[j]);
+              Wa[j] = sark::cmul2(Wa[j], Wstep[j]);
+            }
           }
 #pragma unroll
-          for (int j = 0; j < BPA_RG; ++j)
-            if (r0 + j < a.nr) {
-              tre += (double)acc[j].x;
-              tim += (double)acc[j].y;
-            }
+          for (int j = 0; j < BPA_NV; ++j) {
+            tre[j] += (double)acc[j].x;
+            tim[j] += (double)acc[j].y;
+          }
         }
       }
     }
   }
-  if (live) a.out[v] = make_float2((float)tre, (float)tim);
+#pragma unroll
+  for (int j = 0; j < BPA_NV; ++j)
+    if (live[j]) {
+      if (a.nsplit == 1) a.out[v[j]] = make_float2((float)tre[j], (float)tim[j]);
+      else a.part[(size_t)blockIdx.y * a.V + v[j]] = make_double2(tre[j], tim[j]);
+    }
+}
+
+// sum of the pose splits in split order
+__global__ void k_bpa_reduce(const double2 *__restrict__ part, float2 *__restrict__ out, long long V, int nsplit) {
+  const long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= V) return;
+  double re = 0.0, im = 0.0;
+  for (int sidx = 0; sidx < nsplit; ++sidx) {
+    const double2 x = part[(size_t)sidx * V + v];
+    re += x.x;
+    im += x.y;
+  }
+  out[v] = make_float2((float)re, (float)im);
 }
 
 int bfail(int status, const std::string &msg) {
@@ -181,9 +254,11 @@ extern "C" int sar_bpa(const sar_geom_desc *g, int32_t frame, const void *d_data
   for (int i = 0; i < nk; ++i)
     if (fabs(g->k[i] - (k0 + i * dk)) > 1e-9 * g->k[nk - 1]) return bfail(SAR_ERR_GEOMETRY, "k is not uniform");
 
-  // poses per batch: ~16 KB of samples, one pose at least
-  const size_t pose_bytes = (size_t)nt * nr * nk * sizeof(float2) + (size_t)(nt + nr) * 3 * sizeof(double);
-  int PB = (int)(16384 / pose_bytes);
+  // poses per batch: ~24 KB of staged samples (rows padded to whole blocks), one
+  // pose at least
+  const int nkp = (nk + BPA_NB - 1) / BPA_NB * BPA_NB;
+  const size_t pose_bytes = (size_t)nt * nr * nkp * sizeof(float2) + (size_t)(nt + nr) * 3 * sizeof(double);
+  int PB = (int)(24576 / pose_bytes);
   if (PB < 1) PB = 1;
   if (PB > P) PB = (int)P;
   const size_t smem = PB * pose_bytes;
@@ -223,9 +298,17 @@ extern "C" int sar_bpa(const sar_geom_desc *g, int32_t frame, const void *d_data
   for (long long v = 0; v < n_voxels; ++v)
     for (int d = 0; d < 3; ++d) vox[(size_t)v * 3 + d] = h_voxels[v * 3 + d] - c[d];
 
-  DevBuf dt, dr, dv;
+  // few voxel CTAs: split the pose batches over gridDim.y (~6 CTAs per SM wanted)
+  const long long nblk = (n_voxels + BPA_NT * BPA_NV - 1) / (BPA_NT * BPA_NV);
+  const long long nbatch = (P + PB - 1) / PB;
+  long long nsplit = (6LL * prop.multiProcessorCount + nblk - 1) / nblk;
+  if (nsplit > nbatch) nsplit = nbatch;
+  if (nsplit > 65535) nsplit = 65535;
+  if (nsplit < 1) nsplit = 1;
+  DevBuf dt, dr, dv, dp;
   if (cudaMalloc(&dt.p, txw.size() * 8) != cudaSuccess || cudaMalloc(&dr.p, rxw.size() * 8) != cudaSuccess ||
-      cudaMalloc(&dv.p, vox.size() * 8) != cudaSuccess) {
+      cudaMalloc(&dv.p, vox.size() * 8) != cudaSuccess ||
+      (nsplit > 1 && cudaMalloc(&dp.p, (size_t)nsplit * n_voxels * sizeof(double2)) != cudaSuccess)) {
     cudaGetLastError();
     return bfail(SAR_ERR_OOM, "device allocation of the BPA tables failed");
   }
@@ -246,7 +329,10 @@ extern "C" int sar_bpa(const sar_geom_desc *g, int32_t frame, const void *d_data
   a.nr = nr;
   a.P = (int)P;
   a.nk = nk;
+  a.nkp = nkp;
   a.PB = PB;
+  a.nsplit = (int)nsplit;
+  a.part = static_cast<double2 *>(dp.p);
   const double two_pi = 6.283185307179586476925286766559;
   a.kt0 = k0 / two_pi;
   a.dkt = dk / two_pi;
@@ -259,9 +345,12 @@ extern "C" int sar_bpa(const sar_geom_desc *g, int32_t frame, const void *d_data
     cudaEventCreate(&e1);
     cudaEventRecord(e0, s);
   }
-  const long long nblk = (n_voxels + BPA_NT - 1) / BPA_NT;
-  k_bpa<<<(unsigned)nblk, BPA_NT, smem, s>>>(a);
+  k_bpa<<<dim3((unsigned)nblk, (unsigned)nsplit), BPA_NT, smem, s>>>(a);
   e = cudaGetLastError();
+  if (e == cudaSuccess && nsplit > 1) {
+    k_bpa_reduce<<<(unsigned)((n_voxels + 255) / 256), 256, 0, s>>>(a.part, a.out, n_voxels, (int)nsplit);
+    e = cudaGetLastError();
+  }
   if (ms_out) cudaEventRecord(e1, s);
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
   if (ms_out) {
