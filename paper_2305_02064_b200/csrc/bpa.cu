@@ -46,7 +46,13 @@
 namespace {
 
 constexpr int BPA_NT = 128;     // threads per CTA
-constexpr int BPA_NV = 2;       // voxels per thread (v, v + 128 of the CTA's 256)
+#ifndef BPA_NV_
+#define BPA_NV_ 2
+#endif
+#ifndef BPA_MINB_
+#define BPA_MINB_ 3
+#endif
+constexpr int BPA_NV = BPA_NV_;   // voxels per thread (v, v + 128, ... of the CTA's 128 NV)
 constexpr int BPA_NB = 16;      // k samples per block: e = -8 .. 7 around its centre
 constexpr int BPA_H = BPA_NB / 2;
 constexpr int BPA_RESEED = 8;   // blocks per exact re-seed of the block phasor
@@ -71,7 +77,7 @@ __device__ __forceinline__ float2 unit_phasor(double turns) {
   return r;
 }
 
-__global__ void __launch_bounds__(BPA_NT, 3) k_bpa(const BpaArgs a) {
+__global__ void __launch_bounds__(BPA_NT, BPA_MINB_) k_bpa(const BpaArgs a) {
   extern __shared__ __align__(16) unsigned char smraw[];
   const int npair = a.nt * a.nr;
   float2 *ss = reinterpret_cast<float2 *>(smraw);                                  // [npair][PB][nkp]

@@ -193,3 +193,34 @@ def test_nearest_with_nufft_is_rejected():
     with pytest.raises(sar.SarError) as ei:
         sar.describe(**_args(), flags=sar.SAR_GRID_NEAREST | sar.SAR_GRID_NUFFT)
     assert ei.value.status == 1
+
+
+def test_bpa_host_side_validation():
+    """sar_bpa (the BPA baseline) checks its arguments on the host before it
+    touches a device: an empty voxel list is a no-op, NULL buffers, a frame out
+    of range and a non-uniform k are rejected with their status codes."""
+    import ctypes as C
+    lib = sar.load_library()
+    sc = scenes.make_scene("tiny")
+
+    def call(k=sc.k, frame=0, nvox=3, data=True, g_null=False):
+        g, _, keep = sarmod._descriptors(sc.tx, sc.rx, sc.scan, sc.npx, sc.npy, 0.0, 0.0, 1.0, 1.0, None, k,
+                                         2, 2, 2, 1.0, 1.0, None, 0)
+        vox = np.zeros((max(nvox, 1), 3))
+        dummy = np.zeros(4)
+        ms = C.c_float(-1.0)
+        st = lib.sar_bpa(None if g_null else C.byref(g), C.c_int32(frame),
+                         C.c_void_p(dummy.ctypes.data) if data else None, C.c_void_p(vox.ctypes.data),
+                         C.c_int64(nvox), C.c_void_p(dummy.ctypes.data), None, C.byref(ms))
+        del keep
+        return st, ms.value
+
+    assert call(nvox=0) == (0, 0.0)
+    assert call(g_null=True)[0] == 1
+    assert call(frame=1)[0] == 1 and call(frame=-1)[0] == 1
+    assert call(nvox=-1)[0] == 1
+    assert call(data=False)[0] == 1
+    kbad = sc.k.copy()
+    kbad[5] *= 1.0 + 1e-6
+    assert call(k=kbad)[0] == 2
+    assert b"uniform" in lib.sar_last_error()
