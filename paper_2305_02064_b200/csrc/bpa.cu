@@ -10,7 +10,7 @@
 // timings and a physics check of the RMA image on configurations whose CPU
 // brute force would take hours.
 //
-// One thread per BPA_NV = 2 voxels, 256 voxels per CTA; gridDim.y splits the
+// One thread per 2 voxels (4 when n_k >= 384), 256 (512) voxels per CTA; gridDim.y splits the
 // poses when there are few voxel CTAs (partial sums in fp64, reduced in a
 // fixed order: deterministic).  The CTA walks its poses in batches: the
 // batch's sample rows [pair][pose][k] (zero-padded to a multiple of 16) and
@@ -45,14 +45,10 @@
 
 namespace {
 
-constexpr int BPA_NT = 128;     // threads per CTA
-#ifndef BPA_NV_
-#define BPA_NV_ 2
-#endif
-#ifndef BPA_MINB_
-#define BPA_MINB_ 3
-#endif
-constexpr int BPA_NV = BPA_NV_;   // voxels per thread (v, v + 128, ... of the CTA's 128 NV)
+constexpr int BPA_NT = 128;     // threads per CTA; BPA_NV voxels per thread (v, v + 128, ...): 2, or 4
+                                // for long k rows (n_k >= 384: 216 registers, 8 warps per SM, half the
+                                // shared-memory reads per term; measured Large 0.55 vs 0.47 of the FP32
+                                // peak, Small 0.30 vs 0.35)
 constexpr int BPA_NB = 16;      // k samples per block: e = -8 .. 7 around its centre
 constexpr int BPA_H = BPA_NB / 2;
 constexpr int BPA_RESEED = 8;   // blocks per exact re-seed of the block phasor
@@ -77,7 +73,8 @@ __device__ __forceinline__ float2 unit_phasor(double turns) {
   return r;
 }
 
-__global__ void __launch_bounds__(BPA_NT, BPA_MINB_) k_bpa(const BpaArgs a) {
+template <int BPA_NV, int MINB>
+__global__ void __launch_bounds__(BPA_NT, MINB) k_bpa(const BpaArgs a) {
   extern __shared__ __align__(16) unsigned char smraw[];
   const int npair = a.nt * a.nr;
   float2 *ss = reinterpret_cast<float2 *>(smraw);                                  // [npair][PB][nkp]
@@ -305,7 +302,8 @@ extern "C" int sar_bpa(const sar_geom_desc *g, int32_t frame, const void *d_data
     for (int d = 0; d < 3; ++d) vox[(size_t)v * 3 + d] = h_voxels[v * 3 + d] - c[d];
 
   // few voxel CTAs: split the pose batches over gridDim.y (~6 CTAs per SM wanted)
-  const long long nblk = (n_voxels + BPA_NT * BPA_NV - 1) / (BPA_NT * BPA_NV);
+  const int NV = nk >= 384 ? 4 : 2;
+  const long long nblk = (n_voxels + BPA_NT * NV - 1) / (BPA_NT * NV);
   const long long nbatch = (P + PB - 1) / PB;
   long long nsplit = (6LL * prop.multiProcessorCount + nblk - 1) / nblk;
   if (nsplit > nbatch) nsplit = nbatch;
@@ -342,8 +340,9 @@ extern "C" int sar_bpa(const sar_geom_desc *g, int32_t frame, const void *d_data
   const double two_pi = 6.283185307179586476925286766559;
   a.kt0 = k0 / two_pi;
   a.dkt = dk / two_pi;
+  void (*kern)(const BpaArgs) = NV == 4 ? k_bpa<4, 2> : k_bpa<2, 3>;
   if (smem > 40 * 1024 &&
-      (e = cudaFuncSetAttribute(k_bpa, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess)
+      (e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess)
     return bcuda(e, "cudaFuncSetAttribute");
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (ms_out) {
@@ -351,7 +350,7 @@ extern "C" int sar_bpa(const sar_geom_desc *g, int32_t frame, const void *d_data
     cudaEventCreate(&e1);
     cudaEventRecord(e0, s);
   }
-  k_bpa<<<dim3((unsigned)nblk, (unsigned)nsplit), BPA_NT, smem, s>>>(a);
+  kern<<<dim3((unsigned)nblk, (unsigned)nsplit), BPA_NT, smem, s>>>(a);
   e = cudaGetLastError();
   if (e == cudaSuccess && nsplit > 1) {
     k_bpa_reduce<<<(unsigned)((n_voxels + 255) / 256), 256, 0, s>>>(a.part, a.out, n_voxels, (int)nsplit);

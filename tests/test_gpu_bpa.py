@@ -72,6 +72,7 @@ def test_bpa_matches_oracle(name, nvox):
     dict(npx=12, npy=6, n_k=33, monostatic=True),        # 1 pair: receiver group padded
     dict(npx=6, npy=4, n_k=2, n_tx=2),                   # minimum n_k
     dict(npx=8, npy=8, n_k=20, n_tx=2, n_frames=3),      # a later frame of a batch
+    dict(npx=6, npy=4, n_k=400, n_tx=2),                 # n_k >= 384: the 4-voxels-per-thread instance
 ])
 def test_bpa_edge_cases(kw):
     kw = dict(kw)
@@ -85,6 +86,18 @@ def test_bpa_edge_cases(kw):
     d = torch.from_numpy(s).cuda()
     for frame, nv in ((F - 1, 131), (0, 1)):
         _check(sc, s, d, _voxels(sc, nv, 7 + frame), frame=frame)
+
+
+def test_bpa_large_like_rows():
+    """Large's radar (3 Tx x 4 Rx, n_k = 512: the 4-voxels-per-thread instance, 32
+    blocks and 4 re-seeds per row) on a 48 x 40 raster, 700 voxels (two CTAs of
+    512 with a ragged tail, pose split)."""
+    sc = scenes.raster_scene(48, 40, 64, 64, 512, 32, 2.5e-3, 0.3, n_tx=3, jitter_xy=1.5e-3, jitter_z=4e-3, seed=33)
+    rng = np.random.default_rng(6)
+    sc.scat_pos = [rng.uniform([-0.03, -0.03, 0.27], [0.03, 0.03, 0.33], size=(30, 3))]
+    sc.scat_amp = [rng.rayleigh(1.0, 30).astype(complex)]
+    s = scenes.synthesize_cpu(sc)
+    _check(sc, s, torch.from_numpy(s).cuda(), _voxels(sc, 700, 4))
 
 
 def test_bpa_freehand_full_size_sampled_voxels():
