@@ -769,6 +769,9 @@ int plan_create_impl(sar_plan **out, const sar_geom_desc *g, const sar_image_des
   v.img_elems = slab_world > 0 ? 0 : (size_t)F * p->nz * p->ny * p->nx;
 
   p->num_sms = prop.multiProcessorCount;
+#ifdef SAR_SM_LIMIT   // A/B builds: persistent grids on fewer SMs (sustained-load power experiments)
+  if (p->num_sms > SAR_SM_LIMIT) p->num_sms = SAR_SM_LIMIT;
+#endif
   sar_build_tensor_maps(p);
   if (flags & SAR_CUDA_GRAPH) {
     if (cudaStreamCreateWithFlags(&p->cap_stream, cudaStreamNonBlocking) != cudaSuccess) {
