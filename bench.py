@@ -321,6 +321,14 @@ def run_ours(args):
     path_gbs = sc.alg_bytes() / (ms_step * 1e-3) / 1e9
     roof = {"bound": "hbm", "kernel": dom_name, "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
             "traffic": traffic, "alg_bytes": alg[dom], "ms": avg[dom], "peak_source": peak_src}
+    if dom == 0:
+        # K1: SURVEY 8(d) counts the raw samples it reads as algorithmic; the W0
+        # volume it writes is an intermediate (an implementation choice), kept
+        # as a second figure (round-1 verdict)
+        raw = sc.raw_bytes()
+        roof.update({"achieved": raw / (avg[dom] * 1e-3) / 1e9, "frac": raw / (avg[dom] * 1e-3) / 1e9 / peak,
+                     "alg_bytes": raw, "achieved_incl_intermediate_write": ach,
+                     "frac_incl_intermediate_write": ach / peak})
     if args.grid == "nufft" and dom == 0:
         # NUFFT spread (K1s) is FP32-FMA bound, not HBM bound: algorithmic
         # flops = samples x (2W+1)^2 taps x 4 (complex sample x real weight =
