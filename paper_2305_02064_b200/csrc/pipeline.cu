@@ -19,6 +19,7 @@
 // All transforms are the shared-memory Stockham FFT of fft_tile.cuh.  The
 // path is HBM-bound: every kernel streams its input
 // once with coalesced 128-byte row segments and keeps the transform on chip.
+#include <nvtx3/nvToolsExt.h>   // header-only NVTX v3: ranges cost a pointer test unless a tool is attached
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdlib.h>
@@ -73,6 +74,13 @@ int sar_launch_pipeline(sar_plan *p, const void *d_data, void *d_image, cudaStre
       return SAR_ERR_CUDA;                                                    \
     }                                                                         \
   } while (0)
+  // NVTX: one range per kernel launch of the path (ncu --nvtx / any NVTX tool
+  // can filter on them); popped on every exit of its scope
+  struct NvtxRange {
+    explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+  };
+  NvtxRange whole("sar_reconstruct: path");
   if (ev) SAR_CHECK(cudaEventRecord(ev[0], s));
   const CUtensorMap *tm_s = nullptr;
   if (p->tma_ap) {
@@ -83,18 +91,26 @@ int sar_launch_pipeline(sar_plan *p, const void *d_data, void *d_image, cudaStre
     // the spread (K1s) and the fine x/y FFTs + crop (x-FFT, K2n) replace K1
     // and K2; their times are reported in the K1 and K2 slots
     const CUtensorMap *tmf = p->tma_fine ? &p->tm_fine : nullptr;
-    SAR_CHECK(launch_nufft(v, data, s, tmf, p->num_sms, 1));
+    {
+      NvtxRange r("K1s NUFFT spread");
+      SAR_CHECK(launch_nufft(v, data, s, tmf, p->num_sms, 1));
+    }
     if (ev) SAR_CHECK(cudaEventRecord(ev[1], s));
+    NvtxRange r("fine x-FFT + K2n");
     SAR_CHECK(launch_nufft(v, data, s, tmf, p->num_sms, 2));
   } else {
-    SAR_CHECK(launch_k1(v, data, stop_stage != 1, s, tm_s, p->tma_ap ? &p->tm_ap : nullptr, p->k1_br,
-                        p->k1_regacc, p->num_sms));
+    {
+      NvtxRange r("K1 correct + x-FFT");
+      SAR_CHECK(launch_k1(v, data, stop_stage != 1, s, tm_s, p->tma_ap ? &p->tm_ap : nullptr, p->k1_br,
+                          p->k1_regacc, p->num_sms));
+    }
     if (ev) SAR_CHECK(cudaEventRecord(ev[1], s));
     if (stop_stage == 1) return SAR_OK;
     // debug stage 2 dumps the whole spectrum; otherwise rows of skipped
     // columns are not stored
     // (K2 keeps per-element stores: TMA stores of its live row boxes measured
     // slower, 0.366 vs 0.341 ms on Large; K4a below gains from them)
+    NvtxRange r("K2 y-FFT");
     SAR_CHECK(launch_mid<-1>(v.w0, v.tw_y, v.F, v.ny, v.nx, v.nk, s, p->tma_mid0 ? &p->tm_w0_mid : nullptr,
                              p->num_sms, nullptr, stop_stage == 2 ? nullptr : v.liveb));
   }
@@ -103,16 +119,23 @@ int sar_launch_pipeline(sar_plan *p, const void *d_data, void *d_image, cudaStre
   // skipped columns are not written by K3: zero them for the stage-3 dump
   if (stop_stage == 3 && v.liveb)
     SAR_CHECK(cudaMemsetAsync(v.w1, 0, (size_t)v.F * v.ny * v.nx * v.nz * sizeof(float2), s));
-  if (v.mode2d) {
-    SAR_CHECK(launch_k3_plane(v, s));
-  } else {
-    SAR_CHECK(launch_k3(v, stop_stage != 3, s, p->num_sms));
+  {
+    NvtxRange r("K3 filter + Stolt + z-IFFT");
+    if (v.mode2d) {
+      SAR_CHECK(launch_k3_plane(v, s));
+    } else {
+      SAR_CHECK(launch_k3(v, stop_stage != 3, s, p->num_sms));
+    }
   }
   if (ev) SAR_CHECK(cudaEventRecord(ev[3], s));
   if (stop_stage == 3) return SAR_OK;
-  SAR_CHECK(launch_mid<+1>(v.w1, v.tw_y, v.F, v.ny, v.nx, v.nz, s, p->tma_mid1 ? &p->tm_w1_mid : nullptr,
-                           p->num_sms, nullptr, v.liveb, p->tma_mid1 && K4A_ROWS == 32 ? &p->tm_w1_mid : nullptr));
+  {
+    NvtxRange r("K4a y-IFFT");
+    SAR_CHECK(launch_mid<+1>(v.w1, v.tw_y, v.F, v.ny, v.nx, v.nz, s, p->tma_mid1 ? &p->tm_w1_mid : nullptr,
+                             p->num_sms, nullptr, v.liveb, p->tma_mid1 && K4A_ROWS == 32 ? &p->tm_w1_mid : nullptr));
+  }
   if (ev) SAR_CHECK(cudaEventRecord(ev[4], s));
+  NvtxRange r4("K4b x-IFFT + magnitude");
   SAR_CHECK(launch_k4b(v, d_image, complex_out != 0, s, p->tma_rows1 ? &p->tm_w1_rows : nullptr, p->num_sms));
   if (ev) SAR_CHECK(cudaEventRecord(ev[5], s));
   return SAR_OK;
