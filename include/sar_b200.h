@@ -195,6 +195,7 @@ int sar_plan_create(sar_plan **out, const sar_geom_desc *g, const sar_image_desc
  * z_first+m*dz), see sar_plan_get_axes.  Enqueues 5 kernels (6 with
  * SAR_GRID_NUFFT) on `stream` and returns without synchronising; no allocation.  Not re-entrant per plan (the
  * workspace is shared): use one plan per concurrent stream.
+ * Each launch is wrapped in an NVTX range named after its stage (tools only).
  * Errors: INVALID_ARG (null pointers, a slab plan), CUDA. */
 int sar_reconstruct(sar_plan *p, const void *d_data, void *d_image, sar_stream stream);
 
